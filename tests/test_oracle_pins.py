@@ -1,0 +1,352 @@
+"""Pins of the fp64 oracle against what the paper and the mathematics fix (CPU only).
+
+Each test names the passage it pins.  None of them re-types the oracle's own
+formula: closed forms, invariants, brute force on tiny inputs, alternative
+routes (SVD vs Householder, explicit Eq. 2.5 vs Eq. 2.6) and published
+known-answer vectors.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import oracle as O
+from synth import planted_dense, make_input, CsrMatrix, random_factor
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def rng(seed=0):
+    return np.random.default_rng(seed)
+
+
+# ------------------------------------------------------------------ Gram (a1)
+def test_gram_closed_forms():
+    F = np.vstack([np.eye(2), np.zeros((1, 2))])
+    assert np.array_equal(O.gram(F), np.eye(2))
+    m = 17
+    assert O.gram(np.ones((m, 1))).tolist() == [[float(m)]]
+
+
+def test_gram_bruteforce_triple_loop():
+    F = rng(1).random((9, 4))
+    G = O.gram(F)
+    for a in range(4):
+        for b in range(4):
+            ref = 0.0
+            for i in range(9):
+                ref += F[i, a] * F[i, b]
+            assert abs(G[a, b] - ref) <= 1e-14 * max(1.0, abs(ref))
+    assert np.array_equal(G, G.T)
+
+
+# ------------------------------------------------------------------ exact product (a10)
+def test_ah_identity_and_planted_closed_form():
+    F = rng(2).random((12, 3))
+    assert np.array_equal(O.ah(np.eye(12), F), F)
+    _, H0 = planted_dense(40, 4, 0.0, rng(3))
+    A = H0 @ H0.T                                                     # planted A = H0 H0^T
+    # A H0 = H0 (H0^T H0): associativity closed form
+    assert np.allclose(O.ah(A, H0), H0 @ np.diag((H0 * H0).sum(0)), rtol=1e-13, atol=0)
+
+
+def test_ah_dense_equals_csr():
+    d = make_input("c2", n_override=1600)
+    A = d["A"]
+    F = random_factor(A.n, 5, 7)
+    assert np.allclose(O.ah(A, F), O.ah(A.to_dense(), F), rtol=1e-12, atol=1e-12)
+
+
+# ------------------------------------------------------------------ leverage scores (a3, Eq. 2.10)
+def test_scores_closed_forms():
+    F = np.vstack([np.eye(2), np.zeros((1, 2))])
+    assert np.allclose(O.leverage_scores(F), [1, 1, 0], atol=1e-15)
+    m = 23
+    assert np.allclose(O.leverage_scores(np.ones((m, 1))), 1.0 / m, rtol=1e-14)
+
+
+def test_scores_rank_sum_and_bounds():
+    for k in (1, 3, 8, 16):
+        F = rng(k).random((300, k))
+        l = O.leverage_scores(F)
+        assert abs(l.sum() - k) < 1e-10 * k                            # sum = rank
+        assert (l >= -1e-15).all() and (l <= 1 + 1e-12).all()
+
+
+def test_scores_basis_independent_svd_and_normal_equations():
+    F = rng(5).random((80, 6))
+    l = O.leverage_scores(F)
+    U, _, _ = np.linalg.svd(F, full_matrices=False)                   # P:285 SVD basis
+    assert np.allclose(l, (U * U).sum(1), rtol=1e-10, atol=1e-14)
+    Ginv = np.linalg.inv(F.T @ F)                                      # l_i = f_i G^-1 f_i^T (north star)
+    assert np.allclose(l, np.einsum("ij,jk,ik->i", F, Ginv, F), rtol=1e-9, atol=1e-13)
+
+
+def test_scores_planted_onehot_closed_form():
+    _, H0 = planted_dense(64, 4, 0.0, rng(6))
+    l = O.leverage_scores(H0)
+    g = (4 * np.arange(64)) // 64
+    col = H0[np.arange(64), g]
+    blk = np.array([np.sum(col[g == c] ** 2) for c in range(4)])
+    assert np.allclose(l, col ** 2 / blk[g], rtol=1e-12)               # orthogonal columns => G diagonal
+
+
+# ------------------------------------------------------------------ hybrid threshold (a4)
+def test_threshold_spec_example():
+    lev = np.zeros(12, dtype=np.float32)
+    lev[:2] = 1.0
+    pl = O.build_plan(lev, k=2, s=10, tau=0.4, seed=0, iteration=0, side=0)
+    assert pl["det_idx"].tolist() == [0, 1]
+    assert pl["theta"] == 2.0 and pl["xi"] == 0.0 and pl["s_R"] == 0
+    assert pl["uniq_idx"].tolist() == [0, 1] and pl["uniq_w"].tolist() == [1.0, 1.0]
+
+
+def test_threshold_bruteforce_and_accounting():
+    F = rng(7).random((500, 5)) ** 3
+    lev = O.leverage_scores(F).astype(np.float32)
+    s, tau, k = 60, 1.0 / 60, 5
+    th = O.hybrid_threshold(lev, k, s, tau)
+    brute = [i for i in range(500) if float(lev[i]) / k >= tau - 1e-18 and float(lev[i]) >= tau * k]
+    assert th["det_idx"].tolist() == brute
+    assert abs(th["theta"] + th["xi"] - k) < 1e-12
+    assert th["s_D"] + th["s_R"] == s
+    assert th["s_D"] <= s + 1                                          # tau >= 1/s => |I_D| <= s (up to fp rounding of sum l)
+    assert O.hybrid_threshold(lev, k, s, 1.0)["s_D"] == 0              # tau = 1: pure sampling
+
+
+# ------------------------------------------------------------------ Philox (a6, reading Z6)
+def test_philox_known_answer_vectors():
+    rows = [l.split() for l in open(os.path.join(GOLD, "philox4x32_10_kat.txt")) if l.strip() and l[0] != "#"]
+    for r in rows:
+        v = [int(x, 16) for x in r]
+        out = O.philox4x32_10(*[np.uint64(x) for x in v[:6]])
+        assert [int(o) for o in out] == v[6:10], r
+
+
+def test_mulhi64_exact_against_python_ints():
+    u = rng(8).integers(0, 2 ** 63, 1000, dtype=np.int64).astype(np.uint64) * np.uint64(2) + np.uint64(1)
+    for W in (1, 12345, 2 ** 40 * 7 + 3, 2 ** 46 - 1, 2 ** 63 + 5):
+        got = O.mulhi64(u, W)
+        ref = [(int(x) * W) >> 64 for x in u]
+        assert [int(g) for g in got] == ref
+
+
+# ------------------------------------------------------------------ inverse CDF (a5/a6)
+def test_draws_match_linear_scan_and_skip_zero_weight():
+    lev = np.array([0.0, 0.25, 0.0, 0.5, 0.125, 0.0, 0.125], dtype=np.float32)
+    det = np.zeros(7, bool)
+    w, P, W = O.fixed_point_mass(lev, det)
+    assert W == int(sum(math.floor(float(x) * 2 ** 40) for x in lev))
+    d = O.draw_indices(P, W, 500, seed=3, iteration=1, side=1)
+    u, _ = O.philox_u64(np.arange(500, dtype=np.uint64), 3, 0, 3)
+    for j in range(500):
+        t = (int(u[j]) * W) >> 64
+        acc, ref = 0, None
+        for i in range(7):                                           # brute-force linear scan
+            acc += int(w[i])
+            if acc > t:
+                ref = i
+                break
+        assert d[j] == ref
+    assert not np.isin(d, [0, 2, 5]).any()
+
+
+def test_draws_chi_square():
+    lev = (rng(9).random(40) ** 2).astype(np.float32)
+    w, P, W = O.fixed_point_mass(lev, np.zeros(40, bool))
+    N = 200_000
+    d = O.draw_indices(P, W, N, seed=11, iteration=0, side=0)
+    obs = np.bincount(d, minlength=40)
+    exp = N * w.astype(np.float64) / W
+    chi2 = ((obs - exp) ** 2 / exp).sum()
+    assert chi2 < 39 + 6 * math.sqrt(2 * 39)                           # 39 dof, ~6 sigma
+
+
+def test_plan_deterministic_and_disjoint():
+    F = rng(10).random((400, 4)) ** 4
+    lev = O.leverage_scores(F).astype(np.float32)
+    a = O.build_plan(lev, 4, 50, 1 / 50, 5, 2, 1)
+    b = O.build_plan(lev, 4, 50, 1 / 50, 5, 2, 1)
+    assert np.array_equal(a["uniq_idx"], b["uniq_idx"]) and np.array_equal(a["uniq_w"], b["uniq_w"])
+    assert not np.isin(a["draw_idx"], a["det_idx"]).any()
+    assert a["counts"].sum() == a["s_R"] and a["s_D"] + a["s_R"] == 50
+    c = O.build_plan(lev, 4, 50, 1 / 50, 5, 3, 1)                      # another iteration -> another stream
+    assert not np.array_equal(a["draw_idx"], c["draw_idx"])
+
+
+# ------------------------------------------------------------------ sampled products (a8/a9)
+def test_all_deterministic_reproduces_exact_product():
+    d = make_input("c2", n_override=1600)
+    A = d["A"]
+    F = random_factor(A.n, 4, 3)
+    lev = O.leverage_scores(F).astype(np.float32)
+    pl = O.build_plan(lev, 4, 10, tau=float(lev.min()) / 4 * 0.5, seed=0, iteration=0, side=0)
+    assert pl["s_D"] == A.n and pl["s_R"] == 0                         # S:91 full inclusion
+    G_s, Y_s = O.sampled_products(A, F, pl["uniq_idx"], pl["uniq_w"])
+    assert np.allclose(G_s, O.gram(F), rtol=1e-13)
+    assert np.allclose(Y_s, O.ah(A, F), rtol=1e-12, atol=1e-13)
+
+
+def test_sampled_product_unbiased():
+    """E[A^T S^T S F] = A^T F (Eq. 2.11 scaling); variance bound P:1706-1711."""
+    r = rng(12)
+    n, k = 300, 3
+    A = r.random((n, n))
+    A = (A + A.T) / 2
+    F = r.random((n, k)) ** 3
+    lev = O.leverage_scores(F).astype(np.float32)
+    exact = O.ah(A, F)
+    N, s = 400, 40
+    acc = np.zeros_like(exact)
+    for t in range(N):
+        pl = O.build_plan(lev, k, s, 1.0, seed=77, iteration=t, side=0)   # tau = 1: pure sampling
+        acc += O.sampled_products(A, F, pl["uniq_idx"], pl["uniq_w"])[1]
+    mean = acc / N
+    # Drineas-Kannan-Mahoney: E||A^T F - A^T S^T S F||_F^2 <= ||A||^2 ||F||^2 / (beta s), beta <= 1 here
+    bound = math.sqrt(O.frob_sq(A) * (F ** 2).sum() / s / N)
+    assert np.linalg.norm(mean - exact) < 4 * bound
+    # E ||S F||_F^2 = ||F||_F^2
+    sq = np.mean([float((O.build_plan(lev, k, s, 1.0, 9, t, 1)["uniq_w"][:, None]
+                         * F[O.build_plan(lev, k, s, 1.0, 9, t, 1)["uniq_idx"]] ** 2).sum()) for t in range(200)])
+    assert abs(sq - (F ** 2).sum()) < 0.1 * (F ** 2).sum()
+
+
+# ------------------------------------------------------------------ HALS (a11, Eq. 2.5/2.6, App. A)
+def test_hals_efficient_equals_explicit_eq25():
+    r = rng(13)
+    for trial in range(5):
+        n, k = 30, 5
+        A = r.random((n, n)); A = A + A.T
+        H = r.random((n, k)); W = r.random((n, k))
+        alpha = float(A.max()) * r.random()
+        X1 = O.hals_sweep(O.gram(H), A @ H, H, W, alpha)
+        X2 = O.hals_sweep_explicit(A, H, W, alpha)
+        assert np.allclose(X1, X2, rtol=1e-10, atol=1e-12)
+
+
+def test_hals_fixed_point_and_k1_closed_form():
+    r = rng(14)
+    H = r.random((25, 4))
+    A = H @ H.T
+    X = O.hals_sweep(O.gram(H), A @ H, H, H, alpha=1.7)
+    assert np.allclose(X, H, rtol=1e-10, atol=1e-12)
+    h = r.random((20, 1)); w = r.random((20, 1)) + 0.1
+    A = h @ h.T
+    X = O.hals_sweep(O.gram(h), A @ h, h, w, alpha=0.0)                # w <- h
+    assert np.allclose(X, h, rtol=1e-12)
+    a = 0.3
+    B = r.random((20, 20)); B = B + B.T
+    X = O.hals_sweep(O.gram(h), B @ h, h, w, alpha=a)
+    assert np.allclose(X[:, 0], np.maximum(0, (B @ h[:, 0] + a * h[:, 0]) / (h[:, 0] @ h[:, 0] + a)))
+
+
+def test_hals_monotone_surrogate_and_nonneg():
+    r = rng(15)
+    A = r.random((40, 40)); A = A + A.T
+    W = r.random((40, 4)); H = r.random((40, 4)); alpha = float(A.max())
+    f0 = O.surrogate_objective(A, W, H, alpha)
+    for _ in range(5):
+        W = O.hals_sweep(O.gram(H), A @ H, H, W, alpha)
+        f1 = O.surrogate_objective(A, W, H, alpha)
+        assert f1 <= f0 + 1e-9 * abs(f0) and (W >= 0).all()
+        H = O.hals_sweep(O.gram(W), A @ W, W, H, alpha)
+        f2 = O.surrogate_objective(A, W, H, alpha)
+        assert f2 <= f1 + 1e-9 * abs(f1) and (H >= 0).all()
+        f0 = f2
+
+
+def test_nls_bruteforce_spec_examples():
+    assert np.allclose(O.nls_bruteforce(np.eye(2), [1, -2]), [1, 0])
+    assert np.allclose(O.nls_bruteforce(2 * np.eye(2), [4, 6]), [2, 3])   # argmin x^T G x - 2 y^T x => x = G^-1 y
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_hals_sweeps_converge_to_bruteforce_nls(k):
+    """Iterated sweeps solve min_{x>=0} ||[F; sqrt(a) I] x - [a_r; sqrt(a) f_r]|| per row (App. G)."""
+    r = rng(20 + k)
+    n = 12
+    A = r.standard_normal((n, n)); A = A + A.T
+    F = r.random((n, k)); X = r.random((n, k)); alpha = 0.5
+    G, Y = O.gram(F), A @ F
+    for _ in range(3000):
+        X = O.hals_sweep(G, Y, F, X, alpha)
+    for i in range(n):
+        ref = O.nls_bruteforce(G + alpha * np.eye(k), Y[i] + alpha * F[i])
+        assert np.allclose(X[i], ref, atol=1e-9)
+
+
+# ------------------------------------------------------------------ range finder (a12)
+def test_omega_gaussian_moments():
+    Om = O.gaussian_omega(4000, 10, seed=3).astype(np.float64)
+    assert abs(Om.mean()) < 5 / math.sqrt(Om.size)
+    assert abs(Om.var() - 1) < 6 * math.sqrt(2 / Om.size)
+    assert Om.dtype == np.float64 and np.array_equal(O.gaussian_omega(4000, 10, 3), O.gaussian_omega(4000, 10, 3))
+
+
+def test_rangefinder_exact_rank_capture_and_identity():
+    r = rng(30)
+    n, rank, l = 120, 6, 9
+    B = r.standard_normal((n, rank))
+    A = B @ np.diag(np.arange(1, rank + 1.0)) @ B.T                   # exact rank 6
+    U, lam, Q = O.rangefinder(A, l, 1, seed=1)
+    assert np.allclose(U @ np.diag(lam) @ U.T, A, atol=1e-9 * np.abs(A).max())
+    assert np.allclose(Q.T @ Q, np.eye(l), atol=1e-12)
+    U, lam, Q = O.rangefinder(np.eye(50), 7, 1, seed=2)                # residual^2 = n - l
+    assert abs(np.linalg.norm(np.eye(50) - Q @ Q.T @ np.eye(50)) ** 2 - (50 - 7)) < 1e-9
+
+
+def test_apx_evd_spec_examples_and_2mu_bound():
+    D = np.diag([5.0, 1.0] + [0.0] * 30)
+    U, lam, _ = O.rangefinder(D, 4, 1, seed=4)
+    assert abs(lam[0] - 5.0) < 1e-12
+    N = np.diag([-7.0, 2.0] + [0.1] * 30)                              # negative dominant eigenvalue
+    U, lam, _ = O.rangefinder(N, 4, 2, seed=4)
+    assert abs(lam[0] + 7.0) < 1e-9
+    r = rng(31)
+    X = r.random((80, 80)); A = X + X.T
+    U, lam, Q = O.rangefinder(A, 6, 0, seed=5)
+    mu = np.linalg.norm(A - Q @ (Q.T @ A))
+    assert np.linalg.norm(A - U @ np.diag(lam) @ U.T) <= 2 * mu + 1e-9
+    # residual trick ||A - Q Q^T A||^2 = ||A||^2 - ||Q^T A||^2
+    assert abs(mu ** 2 - (np.linalg.norm(A) ** 2 - np.linalg.norm(Q.T @ A) ** 2)) < 1e-8 * np.linalg.norm(A) ** 2
+
+
+def test_lai_apply_equals_materialized():
+    r = rng(32)
+    U = np.linalg.qr(r.standard_normal((60, 8)))[0]
+    lam = r.standard_normal(8)
+    F = r.random((60, 3))
+    assert np.allclose(O.lai_apply(U, lam, F), (U @ np.diag(lam) @ U.T) @ F, rtol=1e-12, atol=1e-13)
+
+
+# ------------------------------------------------------------------ residual (a15) and end to end
+def test_fast_residual_identity():
+    r = rng(33)
+    A = r.random((50, 50)); A = A + A.T
+    W = r.random((50, 4)); H = r.random((50, 4))
+    direct = np.linalg.norm(A - W @ H.T) / np.linalg.norm(A)
+    assert abs(O.residual_fast(A, W, H) - direct) < 1e-12
+    assert abs(O.residual(A, H) - np.linalg.norm(A - H @ H.T) / np.linalg.norm(A)) < 1e-13
+    assert O.residual(H @ H.T, H) < 1e-15
+
+
+def test_planted_recovery_exact_and_lvs():
+    d = make_input("c1", noise=False)
+    A, H0 = d["A"], d["H0"]
+    alpha = d["alpha"]
+    W, H, _ = O.iterate(A, H0, H0, alpha, 150, "exact")
+    assert O.residual(A, H) < 1e-3                                     # north star: near-zero residual
+    W, H, tr = O.iterate(A, H0, H0, alpha, 150, "lvs", s=200, tau=1 / 200, seed=0)
+    assert O.residual(A, H) < 1e-3
+    assert all(t["s_D"] + t["s_R"] == 200 or t["s_R"] == 0 for t in tr)
+
+
+def test_lai_iterate_on_low_rank_matches_exact():
+    d = make_input("c1", noise=False)
+    A, H0, alpha = d["A"], d["H0"], d["alpha"]
+    U, lam, _ = O.rangefinder(A, 12, 1, seed=0)                         # A has rank 8 <= l: LAI is exact
+    _, H1, _ = O.iterate(A, H0, H0, alpha, 5, "exact")
+    _, H2, _ = O.iterate(A, H0, H0, alpha, 5, "lai", U=U, lam=lam)
+    assert np.allclose(H1, H2, rtol=1e-6, atol=1e-9)
