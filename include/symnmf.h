@@ -1,0 +1,227 @@
+/*
+ * symnmf.h -- C ABI of the B200 (sm_100a) hot path of randomized SymNMF
+ *             (Hayashi, Aggarwal, Kannan, Ballard, "Randomized Algorithms for
+ *              Symmetric Nonnegative Matrix Factorization", arXiv 2402.08134).
+ *
+ * Citations: P:<n> = line n of the paper's LaTeX source; Z<n> =
+ * reading n of the ambiguity ledger in DESIGN.md.
+ *
+ * Conventions (all functions):
+ *  - Matrices are row-major (C order).  Every float/double/int pointer in an
+ *    argument list is a CUDA DEVICE pointer unless its name ends in `_host`.
+ *  - The caller owns every buffer, including the workspace `ws`.  The library
+ *    never allocates device memory and keeps no global mutable state; calls
+ *    on different streams with different workspaces are independent.
+ *  - Workspace query: call with ws == NULL; *ws_bytes receives the size,
+ *    nothing is enqueued, SYMNMF_OK is returned.  A later call whose
+ *    *ws_bytes is smaller returns SYMNMF_ERR_WORKSPACE.  The workspace must be
+ *    256-byte aligned.  Its first 256 bytes hold a device status word (see
+ *    symnmf_status_read) that kernels set on device-side failure; kernels
+ *    downstream of a failure become no-ops.
+ *  - Asynchrony: every function except symnmf_iterate, symnmf_solver_stats
+ *    and symnmf_status_read only enqueues work on `st` (no host sync) and is
+ *    CUDA-graph capturable.
+ *  - Errors never cross the ABI as exceptions; every entry point returns a
+ *    symnmf_status.  SYMNMF_ERR_ARG is returned synchronously, before any work
+ *    is enqueued, for null pointers, n < 1, k < 1 or k > 64, s < 1,
+ *    tau outside (0, 1], alpha < 0, l > n or l > 96, a CSR/3XTF32 mismatch.
+ *  - Floating point: inputs fp32; Grams, theta/xi, sampling weights and
+ *    residual reductions fp64 (Z27).  No fast-math.
+ */
+#ifndef SYMNMF_H_
+#define SYMNMF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SYMNMF_OK = 0,
+  SYMNMF_ERR_ARG = 1,          /* invalid argument (synchronous)                         */
+  SYMNMF_ERR_NOT_PD = 2,       /* Cholesky of a k x k / l x l Gram failed after 1 jitter  */
+  SYMNMF_ERR_WORKSPACE = 3,    /* *ws_bytes smaller than required                        */
+  SYMNMF_ERR_CUDA = 4,         /* CUDA launch / runtime error                            */
+  SYMNMF_ERR_UNSUPPORTED = 5,  /* device is not sm_100 or mode not built                 */
+  SYMNMF_ERR_CAPACITY = 6      /* plan capacity smaller than s_D or |U| (device side)    */
+} symnmf_status;
+
+enum { SYMNMF_DENSE = 0, SYMNMF_CSR = 1 };        /* symnmf_matrix.kind              */
+enum { SYMNMF_FP32 = 0, SYMNMF_3XTF32 = 1 };      /* precision of a dense product     */
+enum { SYMNMF_EXACT = 0, SYMNMF_LVS = 1, SYMNMF_LAI = 2 };  /* symnmf_iterate mode     */
+
+/* Symmetric n x n input A (Eq. 2.2).  The caller guarantees
+ * A = A^T.  DENSE: val is n x lda fp32 (lda >= n, lda % 4 == 0 for 3XTF32).
+ * CSR: both triangles stored ("row/column slicing ... because the
+ * matrix is symmetric"), rowptr int64 [n+1], colidx int32 [nnz] sorted and
+ * unique within a row, val fp32 [nnz]. */
+typedef struct {
+  int32_t kind;
+  int32_t reserved;
+  int64_t n;
+  const float* val;
+  int64_t lda;
+  const int64_t* rowptr;
+  const int32_t* colidx;
+  int64_t nnz;
+} symnmf_matrix;
+
+/* Device-resident hybrid sampling plan S_H = diag(S_D, S_R) (Eq. 4.1-4.2,
+ * P:722-741), written by symnmf_hybrid_sample and read by symnmf_sampled_ah.
+ *   det_idx  int32 [cap]  I_D = {i : l_i >= tau k} in increasing order (Z1)
+ *   draw_idx int32 [s]    the s_R i.i.d. draws in draw order (Z4, Z6)
+ *   uniq_idx int32 [cap]  U = I_D u {drawn rows}, increasing
+ *   uniq_w   fp64  [cap]  omega_i: 1 on I_D, c_i * (W / (s_R * w_i)) on drawn rows (Z5)
+ *   counts   int64 [4]    s_D, s_R, |U|, W (integer mass of I_R, Z3)
+ *   mass     fp64  [2]    theta = sum_{I_D} l_i, xi = k - theta
+ * cap >= min(n, s) is required; SYMNMF_ERR_CAPACITY is raised on device if
+ * s_D or |U| exceeds cap (possible only for tau < 1/s, Z2). */
+typedef struct {
+  int64_t cap;
+  int32_t* det_idx;
+  int32_t* draw_idx;
+  int32_t* uniq_idx;
+  double* uniq_w;
+  int64_t* counts;
+  double* mass;
+} symnmf_plan;
+
+/* Per half-iteration statistics recorded by the solver (E7). */
+typedef struct {
+  int64_t s_d;
+  int64_t s_r;
+  int64_t n_uniq;
+  double theta;
+} symnmf_half_stats;
+
+/* Library version (major*10000 + minor*100 + patch).  Host only. */
+int32_t symnmf_version(void);
+
+/* Sync `st`, then copy the device status word of `ws` to *status_host. */
+symnmf_status symnmf_status_read(const void* ws, int32_t* status_host, cudaStream_t st);
+
+/* (a1) G = F^T F ("G_H := H^T H").  F n x k fp32,
+ * G k x k fp64 (exactly symmetric).  fp32 products, per-tile fp32 partial
+ * sums flushed to fp64, fixed-order (deterministic) fp64 combine. */
+symnmf_status symnmf_gram(const float* F, int64_t n, int32_t k, double* G,
+                          void* ws, size_t* ws_bytes, cudaStream_t st);
+
+/* (a10) Y = A F ("the product XH"), F and Y n x k fp32.
+ * DENSE: precision SYMNMF_FP32 (SIMT fp32, chunked accumulation) or
+ * SYMNMF_3XTF32 (tcgen05 tensor cores, split a = a_hi + a_lo).  CSR: fp32
+ * SpMM; precision must be SYMNMF_FP32. */
+symnmf_status symnmf_ah(const symnmf_matrix* A, const float* F, int32_t k, float* Y,
+                        int32_t precision, void* ws, size_t* ws_bytes, cudaStream_t st);
+
+/* (a1-a3) Leverage scores l_i = f_i (F^T F)^{-1} f_i^T (Eq. 2.10 P:280-286,
+ * Alg. LvS-SymNMF) by CholeskyQR: fp64 Gram,
+ * fp64 Cholesky F^T F = R^T R (one jitter retry of 1e-12 tr(G)/k, then
+ * SYMNMF_ERR_NOT_PD on the device status word), l_i = ||f_i R^{-1}||^2.
+ * lev fp32 [n]; G_out (nullable) receives F^T F. */
+symnmf_status symnmf_leverage_scores(const float* F, int64_t n, int32_t k, float* lev,
+                                     double* G_out, void* ws, size_t* ws_bytes, cudaStream_t st);
+
+/* (a4-a7) Hybrid deterministic + random leverage-score sampling plan
+ * (Eq. 2.11).  I_D = {i : (double)lev_i >= tau*k} (Z1),
+ * s_R = max(0, s - s_D) (Z2; 0 if the remaining mass is 0), integer mass
+ * w_i = floor(lev_i 2^40) on I_R and its inclusive prefix P (Z3, Z6), draw j
+ * = first i with P_i > floor(u_j W / 2^64), u_j from Philox4x32-10 with
+ * counter (j, 0, 2*iteration + side, 0) and key (seed lo, seed hi) (Z6).
+ * Bit-exact given lev and (seed, iteration, side). */
+symnmf_status symnmf_hybrid_sample(const float* lev, int64_t n, int32_t k, int64_t s, double tau,
+                                   uint64_t seed, uint32_t iteration, uint32_t side,
+                                   const symnmf_plan* plan, void* ws, size_t* ws_bytes, cudaStream_t st);
+
+/* (a8, a9) Sampled products of Alg. LvS-SymNMF:
+ * Y_s = (S A)^T (S F) = sum_{i in U} omega_i A[i,:]^T f_i   (n x k fp32, Z28)
+ * G_s = F^T S^T S F  = sum_{i in U} omega_i f_i^T f_i      (k x k fp64, nullable)
+ * The alpha terms are not sampled. */
+symnmf_status symnmf_sampled_ah(const symnmf_matrix* A, const float* F, int32_t k,
+                                const symnmf_plan* plan, float* Y, double* G_s,
+                                void* ws, size_t* ws_bytes, cudaStream_t st);
+
+/* (a12) Alg. RRF + Alg. Apx-EVD on dense symmetric A:
+ * Omega n x l Gaussian (Philox counter (e/2, 0, 0, 1), Box-Muller, Z18),
+ * Y = A Omega, Q = orth(Y); q times {Q = orth(A Q); Q = orth(A Q)} (Z16),
+ * T = sym(Q^T A Q), T = V Lambda V^T (Jacobi, fp64), U = Q V, ordered by
+ * |lambda| descending (Z17).  orth = CholeskyQR2 with fp64 Gram/Cholesky.
+ * U n x l fp32, lambda fp64 [l].  2q + 2 applications of A. */
+symnmf_status symnmf_rangefinder(const symnmf_matrix* A, int32_t l, int32_t q, uint64_t seed,
+                                 int32_t precision, float* U, double* lambda,
+                                 void* ws, size_t* ws_bytes, cudaStream_t st);
+
+/* (a12) The Gaussian test matrix Omega alone (n x l fp32), for parity tests. */
+symnmf_status symnmf_gaussian(int64_t n, int32_t l, uint64_t seed, float* Omega, cudaStream_t st);
+
+/* (a13) LAI product Y = U (Lambda (U^T F)), U n x l fp32,
+ * lambda fp64 [l], F and Y n x k fp32. */
+symnmf_status symnmf_lai_ah(const float* U, const double* lambda, int64_t n, int32_t l,
+                            const float* F, int32_t k, float* Y,
+                            void* ws, size_t* ws_bytes, cudaStream_t st);
+
+/* (a11) One efficient symmetric HALS sweep (Eq. 2.6, App. G
+ * P:1649-1653) of Update(G + alpha I, Y + alpha F^T):
+ * for every row r, for i = 0..k-1 in order (Gauss-Seidel, Z9)
+ *   X[r,i] <- max(0, (Y[r,i] + alpha F[r,i] - sum_{j != i} X[r,j] G[j,i]) / (G[i,i] + alpha))
+ * (a column with G[i,i] + alpha == 0 is left unchanged).  G fp64 k x k
+ * WITHOUT alpha I; Y, F, X n x k fp32; X updated in place.  G_new
+ * (nullable) receives X^T X of the updated X (the next half's Gram). */
+symnmf_status symnmf_hals_sweep(const double* G, const float* Y, const float* F, float* X,
+                                int64_t n, int32_t k, double alpha, double* G_new,
+                                void* ws, size_t* ws_bytes, cudaStream_t st);
+
+/* (a15) Normalised residual ||A - H H^T||_F / ||A||_F in fp64 (P:101-103,
+ * P:1530-1532).  DENSE: direct sum of (A_ij - h_i.h_j)^2; CSR: the trace
+ * identity ||A||^2 - 2 tr(H^T A H) + ||H^T H||^2.
+ * out fp64 device [4] = {residual, ||A||_F^2, tr(H^T A H), ||H^T H||_F^2}. */
+symnmf_status symnmf_residual(const symnmf_matrix* A, const float* H, int32_t k, double* out,
+                              void* ws, size_t* ws_bytes, cudaStream_t st);
+
+/* (a14) Iteration driver of Alg. LvS-SymNMF, LAI-SymNMF
+ * or exact HALS: per iteration t the W-half (side 0, F = H) then
+ * the H-half (side 1, F = W) (Z11-Z13); iteration index first_iter + t keys
+ * the sampler so a resumed run is bit-reproducible.  W, H n x k fp32 in/out.
+ *   EXACT: G = F^T F, Y = A F (precision as in symnmf_ah)
+ *   LVS  : scores of F, hybrid plan (s, tau, seed), G_s, Y_s
+ *   LAI  : G = F^T F, Y = U (Lambda (U^T F)) (U, lambda, l from symnmf_rangefinder; A may be NULL
+ *          unless resid_host is given)
+ * then X <- sweep(G, Y, F, X, alpha).  The per-iteration body is captured
+ * once as a CUDA graph and replayed.  stats_host (nullable, 2*iters
+ * entries) receives the per-half plan statistics (LVS); resid_host
+ * (nullable, iters entries) receives ||A - H H^T||/||A|| after every
+ * iteration (one extra exact product per iteration).  Synchronises `st` and
+ * returns the device status. */
+symnmf_status symnmf_iterate(const symnmf_matrix* A, int64_t n, float* W, float* H, int32_t k, double alpha,
+                             int32_t mode, int32_t precision, int64_t s, double tau, uint64_t seed,
+                             int32_t first_iter, int32_t iters,
+                             const float* U, const double* lambda, int32_t l,
+                             symnmf_half_stats* stats_host, double* resid_host,
+                             void* ws, size_t* ws_bytes, cudaStream_t st);
+
+/* Reusable solver handle (caller-owned state; the library still holds no
+ * global state): symnmf_solver_create captures the iteration graph once,
+ * symnmf_solver_run enqueues `iters` iterations without a host sync (the
+ * device iteration counter continues from the previous run), and
+ * symnmf_solver_stats syncs and copies the recorded statistics.  The
+ * arguments have the meaning of symnmf_iterate's; `max_iters` bounds the
+ * total number of iterations whose statistics are recorded. */
+typedef struct symnmf_solver symnmf_solver;
+symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_matrix* A, int64_t n, float* W, float* H,
+                                   int32_t k, double alpha, int32_t mode, int32_t precision, int64_t s,
+                                   double tau, uint64_t seed, int32_t first_iter, int32_t max_iters,
+                                   const float* U, const double* lambda, int32_t l, int32_t with_residual,
+                                   void* ws, size_t* ws_bytes, cudaStream_t st);
+symnmf_status symnmf_solver_run(symnmf_solver* solver, int32_t iters, cudaStream_t st);
+symnmf_status symnmf_solver_stats(symnmf_solver* solver, int32_t* iters_done_host,
+                                  symnmf_half_stats* stats_host, double* resid_host, cudaStream_t st);
+symnmf_status symnmf_solver_destroy(symnmf_solver* solver);
+/* Kernel and memset node counts of the captured per-iteration graph (host only). */
+symnmf_status symnmf_solver_graph_nodes(const symnmf_solver* solver, int32_t* kernels_host, int32_t* memsets_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SYMNMF_H_ */

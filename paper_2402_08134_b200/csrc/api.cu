@@ -1,0 +1,636 @@
+// The C ABI of libsymnmf (include/symnmf.h): argument validation, workspace
+// carving, kernel sequencing, and the CUDA-graph iteration driver.
+#include <new>
+#include "kernels.cuh"
+
+using namespace symnmf;
+
+namespace {
+
+bool device_ok() {
+  int dev = 0, major = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return false;
+  return major == 10;
+}
+
+bool bad_k(int k) { return k < 1 || k > kMaxK; }
+
+bool bad_matrix(const symnmf_matrix* A) {
+  if (!A || A->n < 1 || !A->val) return true;
+  if (A->kind == SYMNMF_DENSE) return A->lda < A->n;
+  if (A->kind == SYMNMF_CSR) return !A->rowptr || (!A->colidx && A->nnz > 0) || A->nnz < 0;
+  return true;
+}
+
+// Workspace protocol: query (ws == NULL) or check size/alignment.
+symnmf_status ws_protocol(void* ws, size_t* ws_bytes, size_t need, bool* query) {
+  *query = false;
+  if (!ws_bytes) return SYMNMF_ERR_ARG;
+  if (!ws) { *ws_bytes = need; *query = true; return SYMNMF_OK; }
+  if (*ws_bytes < need) return SYMNMF_ERR_WORKSPACE;
+  if (reinterpret_cast<uintptr_t>(ws) % 256) return SYMNMF_ERR_ARG;
+  return SYMNMF_OK;
+}
+
+symnmf_status finish() {
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) { (void)cudaGetLastError(); return SYMNMF_ERR_CUDA; }
+  return SYMNMF_OK;
+}
+
+__global__ void set_i32(int32_t* p, int32_t v) { *p = v; }
+__global__ void bump_iter(int32_t* it) { *it += 1; }
+__global__ void record_stats(const int32_t* iter_dev, int32_t first, int32_t max_iters, int side,
+                             const int64_t* counts, const double* mass, symnmf_half_stats* stats) {
+  const int t = *iter_dev - first;
+  if (t < 0 || t >= max_iters) return;
+  symnmf_half_stats h;
+  h.s_d = counts[0]; h.s_r = counts[1]; h.n_uniq = counts[2]; h.theta = mass[0];
+  stats[2 * t + side] = h;
+}
+__global__ void record_resid(const int32_t* iter_dev, int32_t first, int32_t max_iters, const double* rout,
+                             double* resid) {
+  const int t = *iter_dev - first;
+  if (t < 0 || t >= max_iters) return;
+  resid[t] = rout[0];
+}
+
+// Dense or CSR exact product into Y (n x k, ld k).
+bool enqueue_product(const symnmf_matrix& A, const float* F, int k, float* Y, int precision, void* tcs,
+                     size_t tcs_bytes, const int32_t* status, cudaStream_t st) {
+  if (A.kind == SYMNMF_CSR) { launch_spmm_csr(A, F, k, Y, status, st); return true; }
+  if (precision == SYMNMF_3XTF32)
+    return launch_dense_ah_tc(A.val, A.lda, A.n, F, k, k, Y, k, tcs, tcs_bytes, status, st);
+  launch_dense_ah_simt(A.val, A.lda, A.n, F, k, k, Y, k, status, st);
+  return true;
+}
+
+void enqueue_gram(const float* F, int64_t n, int k, double* partial, int grid, double* G, const int32_t* status,
+                  cudaStream_t st) {
+  launch_cross_gram(F, k, k, F, k, k, true, n, nullptr, nullptr, nullptr, partial, grid, G, k, status, st);
+}
+
+}  // namespace
+
+extern "C" int32_t symnmf_version(void) { return 100; }   // 0.1.0
+
+extern "C" symnmf_status symnmf_status_read(const void* ws, int32_t* status_host, cudaStream_t st) {
+  if (!ws || !status_host) return SYMNMF_ERR_ARG;
+  SYMNMF_CUDA_TRY(cudaMemcpyAsync(status_host, ws, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  SYMNMF_CUDA_TRY(cudaStreamSynchronize(st));
+  return SYMNMF_OK;
+}
+
+// ---------------------------------------------------------------- (a1)
+extern "C" symnmf_status symnmf_gram(const float* F, int64_t n, int32_t k, double* G, void* ws, size_t* ws_bytes,
+                                     cudaStream_t st) {
+  if (!F || !G || n < 1 || bad_k(k)) return SYMNMF_ERR_ARG;
+  const int grid = gram_grid(n);
+  Carver c(nullptr);
+  c.take<double>(gram_partial_doubles(k, k, true, grid));
+  bool q;
+  symnmf_status s = ws_protocol(ws, ws_bytes, c.bytes(), &q);
+  if (s != SYMNMF_OK || q) return s;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  double* part = w.take<double>(gram_partial_doubles(k, k, true, grid));
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
+  enqueue_gram(F, n, k, part, grid, G, ws_status(ws), st);
+  return finish();
+}
+
+// ---------------------------------------------------------------- (a10)
+extern "C" symnmf_status symnmf_ah(const symnmf_matrix* A, const float* F, int32_t k, float* Y, int32_t precision,
+                                   void* ws, size_t* ws_bytes, cudaStream_t st) {
+  if (bad_matrix(A) || !F || !Y || bad_k(k)) return SYMNMF_ERR_ARG;
+  if (precision != SYMNMF_FP32 && precision != SYMNMF_3XTF32) return SYMNMF_ERR_ARG;
+  if (A->kind == SYMNMF_CSR && precision != SYMNMF_FP32) return SYMNMF_ERR_ARG;
+  const size_t tcs = (A->kind == SYMNMF_DENSE && precision == SYMNMF_3XTF32) ? dense_ah_tc_scratch(A->n, k) : 0;
+  Carver c(nullptr);
+  c.take<char>(tcs);
+  bool q;
+  symnmf_status s = ws_protocol(ws, ws_bytes, c.bytes(), &q);
+  if (s != SYMNMF_OK || q) return s;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  void* scratch = w.take<char>(tcs);
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
+  if (!enqueue_product(*A, F, k, Y, precision, scratch, tcs, ws_status(ws), st)) return SYMNMF_ERR_UNSUPPORTED;
+  return finish();
+}
+
+// ---------------------------------------------------------------- (a1)-(a3)
+extern "C" symnmf_status symnmf_leverage_scores(const float* F, int64_t n, int32_t k, float* lev, double* G_out,
+                                                void* ws, size_t* ws_bytes, cudaStream_t st) {
+  if (!F || !lev || n < 1 || bad_k(k)) return SYMNMF_ERR_ARG;
+  const int grid = gram_grid(n), kp = kpad(k);
+  auto layout = [&](Carver& c, double** part, double** G, float** R) {
+    *part = c.take<double>(gram_partial_doubles(k, k, true, grid));
+    *G = c.take<double>((size_t)k * k);
+    *R = c.take<float>((size_t)kp * kp);
+  };
+  double *part, *G;
+  float* R;
+  Carver c(nullptr);
+  layout(c, &part, &G, &R);
+  bool q;
+  symnmf_status s = ws_protocol(ws, ws_bytes, c.bytes(), &q);
+  if (s != SYMNMF_OK || q) return s;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  layout(w, &part, &G, &R);
+  if (G_out) G = G_out;
+  int32_t* status = ws_status(ws);
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
+  enqueue_gram(F, n, k, part, grid, G, status, st);
+  launch_chol_inv(G, k, R, kp, kp, nullptr, 0, status, st);
+  launch_leverage(F, n, k, R, lev, status, st);
+  return finish();
+}
+
+// ---------------------------------------------------------------- (a4)-(a7)
+static void sampler_layout(Carver& c, int64_t n, SamplerWs* sw) {
+  const int64_t nb = samp_blocks(n);
+  sw->bw = c.take<uint64_t>(nb);
+  sw->bd = c.take<uint32_t>(nb);
+  sw->bt = c.take<double>(nb);
+  sw->bu = c.take<uint32_t>(nb);
+  sw->P = c.take<uint64_t>(n);
+  sw->cnt = c.take<int32_t>(n);
+}
+
+static bool bad_plan(const symnmf_plan* p) {
+  return !p || p->cap < 1 || !p->det_idx || !p->draw_idx || !p->uniq_idx || !p->uniq_w || !p->counts || !p->mass;
+}
+
+extern "C" symnmf_status symnmf_hybrid_sample(const float* lev, int64_t n, int32_t k, int64_t s, double tau,
+                                              uint64_t seed, uint32_t iteration, uint32_t side,
+                                              const symnmf_plan* plan, void* ws, size_t* ws_bytes, cudaStream_t st) {
+  if (!lev || n < 1 || bad_k(k) || s < 1 || !(tau > 0.0 && tau <= 1.0) || side > 1 || bad_plan(plan))
+    return SYMNMF_ERR_ARG;
+  SamplerWs sw;
+  Carver c(nullptr);
+  sampler_layout(c, n, &sw);
+  bool q;
+  symnmf_status r = ws_protocol(ws, ws_bytes, c.bytes(), &q);
+  if (r != SYMNMF_OK || q) return r;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  sampler_layout(w, n, &sw);
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(sw.cnt, 0, sizeof(int32_t) * n, st));
+  const double T = tau * (double)k;   // reading Z1: threshold on p_i = l_i / k
+  launch_hybrid_sample(lev, n, k, s, T, seed, nullptr, iteration, side, *plan, sw, ws_status(ws), st);
+  return finish();
+}
+
+// ---------------------------------------------------------------- (a8), (a9)
+extern "C" symnmf_status symnmf_sampled_ah(const symnmf_matrix* A, const float* F, int32_t k, const symnmf_plan* plan,
+                                           float* Y, double* G_s, void* ws, size_t* ws_bytes, cudaStream_t st) {
+  if (bad_matrix(A) || !F || !Y || bad_k(k) || bad_plan(plan)) return SYMNMF_ERR_ARG;
+  const int grid = gram_grid(std::min<int64_t>(plan->cap, A->n));
+  Carver c(nullptr);
+  c.take<double>(gram_partial_doubles(k, k, true, grid));
+  bool q;
+  symnmf_status r = ws_protocol(ws, ws_bytes, c.bytes(), &q);
+  if (r != SYMNMF_OK || q) return r;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  double* part = w.take<double>(gram_partial_doubles(k, k, true, grid));
+  int32_t* status = ws_status(ws);
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
+  const int64_t cap = std::min<int64_t>(plan->cap, A->n);
+  if (A->kind == SYMNMF_CSR)
+    launch_sampled_csr(*A, F, k, plan->uniq_idx, plan->uniq_w, plan->counts + 2, cap, Y, status, st);
+  else
+    launch_sampled_dense(A->val, A->lda, A->n, F, k, plan->uniq_idx, plan->uniq_w, plan->counts + 2, cap, Y, status, st);
+  if (G_s)
+    launch_cross_gram(F, k, k, F, k, k, true, cap, plan->counts + 2, plan->uniq_idx, plan->uniq_w, part, grid, G_s, k,
+                      status, st);
+  return finish();
+}
+
+// ---------------------------------------------------------------- (a12)
+extern "C" symnmf_status symnmf_gaussian(int64_t n, int32_t l, uint64_t seed, float* Omega, cudaStream_t st) {
+  if (n < 1 || l < 1 || !Omega) return SYMNMF_ERR_ARG;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  launch_gaussian(n, l, seed, Omega, st);
+  return finish();
+}
+
+namespace {
+struct RfLayout {
+  float *Om, *Yb, *Q1, *Q;
+  double *Gl, *R64, *part, *T, *V;
+  void* tcs;
+  size_t tcs_bytes;
+  int grid;
+};
+void rf_layout(Carver& c, int64_t n, int l, int precision, RfLayout* L) {
+  L->grid = gram_grid(n);
+  L->Om = c.take<float>((size_t)n * l);
+  L->Yb = c.take<float>((size_t)n * l);
+  L->Q1 = c.take<float>((size_t)n * l);
+  L->Q = c.take<float>((size_t)n * l);
+  L->Gl = c.take<double>((size_t)l * l);
+  L->R64 = c.take<double>((size_t)l * l);
+  L->T = c.take<double>((size_t)l * l);
+  L->V = c.take<double>((size_t)l * l);
+  L->part = c.take<double>(gram_partial_doubles(l, l, false, L->grid));
+  L->tcs_bytes = precision == SYMNMF_3XTF32 ? dense_ah_tc_scratch(n, l) : 0;
+  L->tcs = c.take<char>(L->tcs_bytes);
+}
+// orth(Yb) -> Q by CholeskyQR2 with fp64 Gram, Cholesky and row apply.
+void enqueue_orth(const RfLayout& L, int64_t n, int l, const float* Yin, float* Qout, int32_t* status, cudaStream_t st) {
+  launch_cross_gram(Yin, l, l, Yin, l, l, true, n, nullptr, nullptr, nullptr, L.part, L.grid, L.Gl, l, status, st);
+  launch_chol_inv(L.Gl, l, nullptr, 0, 0, L.R64, l, status, st);
+  launch_rowapply64(Yin, l, n, l, L.R64, l, L.Q1, l, status, st);
+  launch_cross_gram(L.Q1, l, l, L.Q1, l, l, true, n, nullptr, nullptr, nullptr, L.part, L.grid, L.Gl, l, status, st);
+  launch_chol_inv(L.Gl, l, nullptr, 0, 0, L.R64, l, status, st);
+  launch_rowapply64(L.Q1, l, n, l, L.R64, l, Qout, l, status, st);
+}
+bool enqueue_dense_apply(const symnmf_matrix& A, const float* X, int l, float* Y, int precision, const RfLayout& L,
+                         const int32_t* status, cudaStream_t st) {
+  if (precision == SYMNMF_3XTF32)
+    return launch_dense_ah_tc(A.val, A.lda, A.n, X, l, l, Y, l, L.tcs, L.tcs_bytes, status, st);
+  launch_dense_ah_simt(A.val, A.lda, A.n, X, l, l, Y, l, status, st);
+  return true;
+}
+}  // namespace
+
+extern "C" symnmf_status symnmf_rangefinder(const symnmf_matrix* A, int32_t l, int32_t q, uint64_t seed,
+                                            int32_t precision, float* U, double* lambda, void* ws, size_t* ws_bytes,
+                                            cudaStream_t st) {
+  if (bad_matrix(A) || A->kind != SYMNMF_DENSE || l < 1 || l > kMaxL || l > A->n || q < 0 || !U || !lambda)
+    return SYMNMF_ERR_ARG;
+  if (precision != SYMNMF_FP32 && precision != SYMNMF_3XTF32) return SYMNMF_ERR_ARG;
+  const int64_t n = A->n;
+  RfLayout L;
+  Carver c(nullptr);
+  rf_layout(c, n, l, precision, &L);
+  bool qq;
+  symnmf_status r = ws_protocol(ws, ws_bytes, c.bytes(), &qq);
+  if (r != SYMNMF_OK || qq) return r;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  rf_layout(w, n, l, precision, &L);
+  int32_t* status = ws_status(ws);
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
+  launch_gaussian(n, l, seed, L.Om, st);                                   // Alg. RRF line "Draw Omega"
+  if (!enqueue_dense_apply(*A, L.Om, l, L.Yb, precision, L, status, st)) return SYMNMF_ERR_UNSUPPORTED;
+  enqueue_orth(L, n, l, L.Yb, L.Q, status, st);
+  for (int t = 0; t < q; ++t) {                                             // (A A^T)^q with re-orthonormalisation
+    for (int h = 0; h < 2; ++h) {
+      enqueue_dense_apply(*A, L.Q, l, L.Yb, precision, L, status, st);
+      enqueue_orth(L, n, l, L.Yb, L.Q, status, st);
+    }
+  }
+  enqueue_dense_apply(*A, L.Q, l, L.Yb, precision, L, status, st);        // Z = A Q
+  launch_cross_gram(L.Q, l, l, L.Yb, l, l, false, n, nullptr, nullptr, nullptr, L.part, L.grid, L.T, l, status, st);
+  launch_symmetrize(L.T, l, st);                                            // T = Q^T A Q
+  launch_jacobi_evd(L.T, l, L.V, lambda, status, st);                       // T = V Lambda V^T
+  launch_rowapply64(L.Q, l, n, l, L.V, l, U, l, status, st);                // U = Q V
+  return finish();
+}
+
+// ---------------------------------------------------------------- (a13)
+extern "C" symnmf_status symnmf_lai_ah(const float* U, const double* lambda, int64_t n, int32_t l, const float* F,
+                                       int32_t k, float* Y, void* ws, size_t* ws_bytes, cudaStream_t st) {
+  if (!U || !lambda || !F || !Y || n < 1 || l < 1 || l > kMaxL || bad_k(k)) return SYMNMF_ERR_ARG;
+  const int grid = gram_grid(n);
+  auto layout = [&](Carver& c, double** part, double** Z, float** M) {
+    *part = c.take<double>(gram_partial_doubles(l, k, false, grid));
+    *Z = c.take<double>((size_t)l * k);
+    *M = c.take<float>((size_t)l * k);
+  };
+  double *part, *Z;
+  float* M;
+  Carver c(nullptr);
+  layout(c, &part, &Z, &M);
+  bool q;
+  symnmf_status r = ws_protocol(ws, ws_bytes, c.bytes(), &q);
+  if (r != SYMNMF_OK || q) return r;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  layout(w, &part, &Z, &M);
+  int32_t* status = ws_status(ws);
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
+  launch_cross_gram(U, l, l, F, k, k, false, n, nullptr, nullptr, nullptr, part, grid, Z, k, status, st);
+  launch_scale_rows(Z, l, k, lambda, M, status, st);
+  launch_rowapply32(U, l, n, l, M, k, Y, k, status, st);
+  return finish();
+}
+
+// ---------------------------------------------------------------- (a11)
+extern "C" symnmf_status symnmf_hals_sweep(const double* G, const float* Y, const float* F, float* X, int64_t n,
+                                           int32_t k, double alpha, double* G_new, void* ws, size_t* ws_bytes,
+                                           cudaStream_t st) {
+  if (!G || !Y || !F || !X || n < 1 || bad_k(k) || !(alpha >= 0.0)) return SYMNMF_ERR_ARG;
+  const int grid = gram_grid(n);
+  Carver c(nullptr);
+  c.take<double>(gram_partial_doubles(k, k, true, grid));
+  bool q;
+  symnmf_status r = ws_protocol(ws, ws_bytes, c.bytes(), &q);
+  if (r != SYMNMF_OK || q) return r;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  double* part = w.take<double>(gram_partial_doubles(k, k, true, grid));
+  int32_t* status = ws_status(ws);
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
+  launch_hals_sweep(G, Y, F, X, n, k, alpha, status, st);
+  if (G_new) enqueue_gram(X, n, k, part, grid, G_new, status, st);
+  return finish();
+}
+
+// ---------------------------------------------------------------- (a15)
+extern "C" symnmf_status symnmf_residual(const symnmf_matrix* A, const float* H, int32_t k, double* out, void* ws,
+                                         size_t* ws_bytes, cudaStream_t st) {
+  if (bad_matrix(A) || !H || !out || bad_k(k)) return SYMNMF_ERR_ARG;
+  const int64_t n = A->n;
+  const int rgrid = residual_grid(n), ggrid = gram_grid(n);
+  const bool csr = A->kind == SYMNMF_CSR;
+  auto layout = [&](Carver& c, double** rp, float** AH, double** G, double** gp) {
+    *rp = c.take<double>((size_t)2 * rgrid);
+    *AH = c.take<float>(csr ? (size_t)n * k : 0);
+    *G = c.take<double>(csr ? (size_t)k * k : 0);
+    *gp = c.take<double>(csr ? gram_partial_doubles(k, k, true, ggrid) : 0);
+  };
+  double *rp, *G, *gp;
+  float* AH;
+  Carver c(nullptr);
+  layout(c, &rp, &AH, &G, &gp);
+  bool q;
+  symnmf_status r = ws_protocol(ws, ws_bytes, c.bytes(), &q);
+  if (r != SYMNMF_OK || q) return r;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  layout(w, &rp, &AH, &G, &gp);
+  int32_t* status = ws_status(ws);
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
+  if (csr) {
+    launch_spmm_csr(*A, H, k, AH, status, st);
+    enqueue_gram(H, n, k, gp, ggrid, G, status, st);
+  }
+  launch_residual(*A, H, k, AH, G, rp, rgrid, out, status, st);
+  return finish();
+}
+
+// ---------------------------------------------------------------- (a14) solver
+struct symnmf_solver {
+  symnmf_matrix A;
+  bool hasA;
+  int64_t n;
+  float *W, *H;
+  int k;
+  double alpha;
+  int mode, precision;
+  int64_t s;
+  double T;
+  uint64_t seed;
+  int32_t first_iter, max_iters;
+  const float* U;
+  const double* lam;
+  int l;
+  int with_resid;
+  // workspace carve
+  int32_t* status;
+  int32_t* iter_dev;
+  int ggrid, rgrid;
+  double *G, *Gs, *gpart;
+  float* Rinv32;
+  float* lev;
+  SamplerWs sw;
+  symnmf_plan plan;
+  float* Y;
+  symnmf_half_stats* stats;
+  double *resid, *rpart, *rout, *GH;
+  double *Zpart, *Z;
+  float* M32;
+  void* tcs;
+  size_t tcs_bytes;
+  cudaGraph_t graph;
+  cudaGraphExec_t exec;
+  int32_t iters_done;
+};
+
+namespace {
+
+void solver_layout(symnmf_solver& S, Carver& c) {
+  const int64_t n = S.n;
+  const int k = S.k, kp = kpad(k);
+  S.status = reinterpret_cast<int32_t*>(c.base);   // header
+  S.iter_dev = c.take<int32_t>(4);
+  S.ggrid = gram_grid(n);
+  S.G = c.take<double>((size_t)k * k);
+  S.Gs = c.take<double>((size_t)k * k);
+  S.GH = c.take<double>((size_t)k * k);
+  S.gpart = c.take<double>(gram_partial_doubles(k, k, true, S.ggrid));
+  S.Y = c.take<float>((size_t)n * k);
+  S.stats = c.take<symnmf_half_stats>((size_t)2 * S.max_iters);
+  S.resid = c.take<double>((size_t)S.max_iters);
+  S.rgrid = residual_grid(n);
+  S.rpart = c.take<double>((size_t)2 * S.rgrid);
+  S.rout = c.take<double>(4);
+  if (S.mode == SYMNMF_LVS) {
+    S.Rinv32 = c.take<float>((size_t)kp * kp);
+    S.lev = c.take<float>(n);
+    sampler_layout(c, n, &S.sw);
+    S.plan.cap = n;
+    S.plan.det_idx = c.take<int32_t>(n);
+    S.plan.draw_idx = c.take<int32_t>(S.s);
+    S.plan.uniq_idx = c.take<int32_t>(n);
+    S.plan.uniq_w = c.take<double>(n);
+    S.plan.counts = c.take<int64_t>(4);
+    S.plan.mass = c.take<double>(2);
+  }
+  if (S.mode == SYMNMF_LAI) {
+    S.Zpart = c.take<double>(gram_partial_doubles(S.l, k, false, S.ggrid));
+    S.Z = c.take<double>((size_t)S.l * k);
+    S.M32 = c.take<float>((size_t)S.l * k);
+  }
+  S.tcs_bytes = (S.hasA && S.A.kind == SYMNMF_DENSE && S.precision == SYMNMF_3XTF32) ? dense_ah_tc_scratch(n, k) : 0;
+  S.tcs = c.take<char>(S.tcs_bytes);
+}
+
+bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
+  const int64_t n = S.n;
+  const int k = S.k;
+  float* F = side == 0 ? S.H : S.W;   // W-half: H fixed (Alg. LvS-SymNMF)
+  float* X = side == 0 ? S.W : S.H;   // H-half: W fixed (lines 690-696)
+  int32_t* status = S.status;
+  enqueue_gram(F, n, k, S.gpart, S.ggrid, S.G, status, st);
+  if (S.mode == SYMNMF_EXACT) {
+    if (!enqueue_product(S.A, F, k, S.Y, S.precision, S.tcs, S.tcs_bytes, status, st)) return false;
+    launch_hals_sweep(S.G, S.Y, F, X, n, k, S.alpha, status, st);
+  } else if (S.mode == SYMNMF_LVS) {
+    const int kp = kpad(k);
+    launch_chol_inv(S.G, k, S.Rinv32, kp, kp, nullptr, 0, status, st);
+    launch_leverage(F, n, k, S.Rinv32, S.lev, status, st);
+    launch_hybrid_sample(S.lev, n, k, S.s, S.T, S.seed, S.iter_dev, 0, (uint32_t)side, S.plan, S.sw, status, st);
+    launch_cross_gram(F, k, k, F, k, k, true, S.plan.cap, S.plan.counts + 2, S.plan.uniq_idx, S.plan.uniq_w, S.gpart,
+                      S.ggrid, S.Gs, k, status, st);
+    if (S.A.kind == SYMNMF_CSR)
+      launch_sampled_csr(S.A, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap, S.Y, status, st);
+    else
+      launch_sampled_dense(S.A.val, S.A.lda, n, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap,
+                           S.Y, status, st);
+    launch_hals_sweep(S.Gs, S.Y, F, X, n, k, S.alpha, status, st);
+    record_stats<<<1, 1, 0, st>>>(S.iter_dev, S.first_iter, S.max_iters, side, S.plan.counts, S.plan.mass, S.stats);
+  } else {
+    launch_cross_gram(S.U, S.l, S.l, F, k, k, false, n, nullptr, nullptr, nullptr, S.Zpart, S.ggrid, S.Z, k, status,
+                      st);
+    launch_scale_rows(S.Z, S.l, k, S.lam, S.M32, status, st);
+    launch_rowapply32(S.U, S.l, n, S.l, S.M32, k, S.Y, k, status, st);
+    launch_hals_sweep(S.G, S.Y, F, X, n, k, S.alpha, status, st);
+  }
+  return true;
+}
+
+bool enqueue_iteration(symnmf_solver& S, cudaStream_t st) {
+  if (!enqueue_half(S, 0, st) || !enqueue_half(S, 1, st)) return false;
+  if (S.with_resid) {
+    if (S.A.kind == SYMNMF_CSR) {
+      launch_spmm_csr(S.A, S.H, S.k, S.Y, S.status, st);
+      enqueue_gram(S.H, S.n, S.k, S.gpart, S.ggrid, S.GH, S.status, st);
+    }
+    launch_residual(S.A, S.H, S.k, S.Y, S.GH, S.rpart, S.rgrid, S.rout, S.status, st);
+    record_resid<<<1, 1, 0, st>>>(S.iter_dev, S.first_iter, S.max_iters, S.rout, S.resid);
+  }
+  bump_iter<<<1, 1, 0, st>>>(S.iter_dev);
+  return true;
+}
+
+}  // namespace
+
+extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_matrix* A, int64_t n, float* W,
+                                              float* H, int32_t k, double alpha, int32_t mode, int32_t precision,
+                                              int64_t s, double tau, uint64_t seed, int32_t first_iter,
+                                              int32_t max_iters, const float* U, const double* lambda, int32_t l,
+                                              int32_t with_residual, void* ws, size_t* ws_bytes, cudaStream_t st) {
+  if (n < 1 || !W || !H || bad_k(k) || !(alpha >= 0.0) || max_iters < 1 || first_iter < 0) return SYMNMF_ERR_ARG;
+  if (mode != SYMNMF_EXACT && mode != SYMNMF_LVS && mode != SYMNMF_LAI) return SYMNMF_ERR_ARG;
+  if (precision != SYMNMF_FP32 && precision != SYMNMF_3XTF32) return SYMNMF_ERR_ARG;
+  const bool needA = mode != SYMNMF_LAI || with_residual;
+  if (needA && (bad_matrix(A) || A->n != n)) return SYMNMF_ERR_ARG;
+  if (A && !bad_matrix(A) && A->kind == SYMNMF_CSR && precision != SYMNMF_FP32) return SYMNMF_ERR_ARG;
+  if (mode == SYMNMF_LVS && (s < 1 || !(tau > 0.0 && tau <= 1.0))) return SYMNMF_ERR_ARG;
+  if (mode == SYMNMF_LAI && (!U || !lambda || l < 1 || l > kMaxL || l > n)) return SYMNMF_ERR_ARG;
+  symnmf_solver S{};
+  S.hasA = A && !bad_matrix(A);
+  if (S.hasA) S.A = *A;
+  S.n = n; S.W = W; S.H = H; S.k = k; S.alpha = alpha; S.mode = mode; S.precision = precision;
+  S.s = mode == SYMNMF_LVS ? s : 0;
+  S.T = tau * (double)k;   // reading Z1
+  S.seed = seed; S.first_iter = first_iter; S.max_iters = max_iters;
+  S.U = U; S.lam = lambda; S.l = l; S.with_resid = with_residual ? 1 : 0;
+  Carver c(nullptr);
+  solver_layout(S, c);
+  bool q;
+  symnmf_status r = ws_protocol(ws, ws_bytes, c.bytes(), &q);
+  if (r != SYMNMF_OK || q) return r;
+  if (!out) return SYMNMF_ERR_ARG;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  solver_layout(S, w);
+  S.status = ws_status(ws);
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, kWsHeader, st));
+  if (mode == SYMNMF_LVS) SYMNMF_CUDA_TRY(cudaMemsetAsync(S.sw.cnt, 0, sizeof(int32_t) * n, st));
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(S.stats, 0, sizeof(symnmf_half_stats) * 2 * max_iters, st));
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(S.resid, 0, sizeof(double) * max_iters, st));
+  set_i32<<<1, 1, 0, st>>>(S.iter_dev, first_iter);
+  if (finish() != SYMNMF_OK) return SYMNMF_ERR_CUDA;
+  // Capture one iteration on a private stream (the caller's may be the legacy default stream).
+  cudaStream_t cs;
+  SYMNMF_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+    cudaStreamDestroy(cs);
+    return SYMNMF_ERR_CUDA;
+  }
+  const bool ok = enqueue_iteration(S, cs);
+  cudaGraph_t g = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(cs, &g);
+  cudaStreamDestroy(cs);
+  if (!ok) { if (g) cudaGraphDestroy(g); return SYMNMF_ERR_UNSUPPORTED; }
+  if (ce != cudaSuccess || !g) { (void)cudaGetLastError(); return SYMNMF_ERR_CUDA; }
+  cudaGraphExec_t ex;
+  if (cudaGraphInstantiate(&ex, g, 0) != cudaSuccess) {
+    (void)cudaGetLastError();
+    cudaGraphDestroy(g);
+    return SYMNMF_ERR_CUDA;
+  }
+  S.graph = g;
+  S.exec = ex;
+  S.iters_done = 0;
+  symnmf_solver* p = new (std::nothrow) symnmf_solver(S);
+  if (!p) { cudaGraphExecDestroy(ex); cudaGraphDestroy(g); return SYMNMF_ERR_ARG; }
+  *out = p;
+  return SYMNMF_OK;
+}
+
+extern "C" symnmf_status symnmf_solver_run(symnmf_solver* S, int32_t iters, cudaStream_t st) {
+  if (!S || iters < 0) return SYMNMF_ERR_ARG;
+  for (int t = 0; t < iters; ++t) SYMNMF_CUDA_TRY(cudaGraphLaunch(S->exec, st));
+  S->iters_done += iters;
+  return SYMNMF_OK;
+}
+
+extern "C" symnmf_status symnmf_solver_stats(symnmf_solver* S, int32_t* iters_done_host, symnmf_half_stats* stats_host,
+                                             double* resid_host, cudaStream_t st) {
+  if (!S) return SYMNMF_ERR_ARG;
+  const int32_t m = std::min(S->iters_done, S->max_iters);
+  int32_t status = 0;
+  SYMNMF_CUDA_TRY(cudaMemcpyAsync(&status, S->status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  if (stats_host && m > 0)
+    SYMNMF_CUDA_TRY(cudaMemcpyAsync(stats_host, S->stats, sizeof(symnmf_half_stats) * 2 * m, cudaMemcpyDeviceToHost, st));
+  if (resid_host && m > 0)
+    SYMNMF_CUDA_TRY(cudaMemcpyAsync(resid_host, S->resid, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
+  SYMNMF_CUDA_TRY(cudaStreamSynchronize(st));
+  if (iters_done_host) *iters_done_host = S->iters_done;
+  return (symnmf_status)status;
+}
+
+extern "C" symnmf_status symnmf_solver_destroy(symnmf_solver* S) {
+  if (!S) return SYMNMF_ERR_ARG;
+  cudaGraphExecDestroy(S->exec);
+  cudaGraphDestroy(S->graph);
+  delete S;
+  return SYMNMF_OK;
+}
+
+extern "C" symnmf_status symnmf_solver_graph_nodes(const symnmf_solver* S, int32_t* kernels_host,
+                                                   int32_t* memsets_host) {
+  if (!S || !S->graph) return SYMNMF_ERR_ARG;
+  size_t nn = 0;
+  SYMNMF_CUDA_TRY(cudaGraphGetNodes(S->graph, nullptr, &nn));
+  cudaGraphNode_t* nodes = new (std::nothrow) cudaGraphNode_t[nn ? nn : 1];
+  if (!nodes) return SYMNMF_ERR_ARG;
+  if (cudaGraphGetNodes(S->graph, nodes, &nn) != cudaSuccess) { delete[] nodes; return SYMNMF_ERR_CUDA; }
+  int32_t kc = 0, mc = 0;
+  for (size_t i = 0; i < nn; ++i) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(nodes[i], &t) != cudaSuccess) continue;
+    if (t == cudaGraphNodeTypeKernel) ++kc;
+    if (t == cudaGraphNodeTypeMemset) ++mc;
+  }
+  delete[] nodes;
+  if (kernels_host) *kernels_host = kc;
+  if (memsets_host) *memsets_host = mc;
+  return SYMNMF_OK;
+}
+
+extern "C" symnmf_status symnmf_iterate(const symnmf_matrix* A, int64_t n, float* W, float* H, int32_t k, double alpha,
+                                        int32_t mode, int32_t precision, int64_t s, double tau, uint64_t seed,
+                                        int32_t first_iter, int32_t iters, const float* U, const double* lambda,
+                                        int32_t l, symnmf_half_stats* stats_host, double* resid_host, void* ws,
+                                        size_t* ws_bytes, cudaStream_t st) {
+  if (iters < 1) return SYMNMF_ERR_ARG;
+  symnmf_solver* S = nullptr;
+  symnmf_status r = symnmf_solver_create(&S, A, n, W, H, k, alpha, mode, precision, s, tau, seed, first_iter, iters, U,
+                                         lambda, l, resid_host ? 1 : 0, ws, ws_bytes, st);
+  if (r != SYMNMF_OK || !ws) return r;
+  r = symnmf_solver_run(S, iters, st);
+  if (r == SYMNMF_OK) r = symnmf_solver_stats(S, nullptr, stats_host, resid_host, st);
+  symnmf_solver_destroy(S);
+  return r;
+}

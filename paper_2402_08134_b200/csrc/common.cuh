@@ -1,0 +1,127 @@
+// Shared device/host helpers of libsymnmf (sm_100a).  No arithmetic of the
+// method lives here except the Philox4x32-10 generator (reading Z6).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+#include <algorithm>
+#include "symnmf.h"
+
+namespace symnmf {
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+constexpr int kMaxK = 64;       // factor width supported by every kernel
+constexpr int kMaxL = 96;       // range-finder sketch width (Jacobi smem bound)
+constexpr int kWsHeader = 256;  // bytes reserved at the head of every workspace
+
+// ---------------------------------------------------------------- status word
+// Workspace header: int32 status at offset 0; the rest is scratch.
+__device__ __forceinline__ bool dev_failed(const int32_t* status) {
+  return *(volatile const int32_t*)status != 0;
+}
+__device__ __forceinline__ void dev_fail(int32_t* status, int32_t code) {
+  atomicCAS(status, 0, code);
+}
+
+// ---------------------------------------------------------------- Philox4x32-10
+// Salmon et al. SC'11; key bumped by the Weyl constants before rounds 2..10.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) { k.x += 0x9E3779B9u; k.y += 0xBB67AE85u; }
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+  }
+  return c;
+}
+
+// ---------------------------------------------------------------- warp helpers
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan of one value per thread (blockDim.x multiple of 32,
+// <= 1024).  `sh` needs 33 entries.  Returns the exclusive prefix; *total gets the sum.
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T* sh, T* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  T inc = warp_incl_scan(v, lane);
+  if (lane == 31) sh[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    T w = lane < nw ? sh[lane] : T(0);
+    T wi = warp_incl_scan(w, lane);
+    if (lane < nw) sh[lane] = wi - w;
+    if (lane == 31) sh[32] = wi;  // lane 31 holds the block total (nw <= 32)
+  }
+  __syncthreads();
+  T res = sh[wid] + inc - v;
+  if (total) *total = sh[32];
+  __syncthreads();
+  return res;
+}
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  T r = T(0);
+  if (wid == 0) {
+    r = lane < nw ? sh[lane] : T(0);
+    r = warp_sum(r);
+  }
+  __syncthreads();
+  return r;  // valid in warp 0 (all lanes)
+}
+
+inline int kpad(int k) {  // padded factor width used to pick a kernel instance
+  return k <= 8 ? 8 : k <= 16 ? 16 : k <= 32 ? 32 : 64;
+}
+
+// ---------------------------------------------------------------- workspace carving
+struct Carver {
+  char* base;
+  size_t off;
+  explicit Carver(void* b) : base(static_cast<char*>(b)), off(kWsHeader) {}
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+  size_t bytes() const { return (off + 255) & ~size_t(255); }
+};
+
+inline int32_t* ws_status(void* ws) { return static_cast<int32_t*>(ws); }
+
+}  // namespace symnmf
+
+#define SYMNMF_CUDA_TRY(expr)                                   \
+  do {                                                          \
+    cudaError_t e_ = (expr);                                    \
+    if (e_ != cudaSuccess) return SYMNMF_ERR_CUDA;              \
+  } while (0)
+#define SYMNMF_LAUNCH_CHECK()                                   \
+  do {                                                          \
+    if (cudaPeekAtLastError() != cudaSuccess) {                 \
+      (void)cudaGetLastError();                                 \
+      return SYMNMF_ERR_CUDA;                                   \
+    }                                                           \
+  } while (0)

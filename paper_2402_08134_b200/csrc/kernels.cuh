@@ -1,0 +1,79 @@
+// Host-side launchers of the libsymnmf kernels (internal; the ABI is in api.cu).
+#pragma once
+#include "common.cuh"
+
+namespace symnmf {
+
+// ---------------------------------------------------------------- gram.cu
+// Grid used for a cross Gram over `rows_cap` rows (fixes the partial-buffer size).
+int gram_grid(int64_t rows_cap);
+size_t gram_partial_doubles(int ka, int kb, bool sym, int grid);
+// out[a*ldo + b] = sum_r w_r A[g(r), a] B[g(r), b]  (a < ka, b < kb), fp64; rows r < nrows
+// (or < *nrows_dev if non-null); g(r) = gather ? gather[r] : r; w_r = wts ? wts[r] : 1.
+// sym => A == B and ka == kb: only the upper 4x4 blocks are computed, output mirrored.
+void launch_cross_gram(const float* A, int64_t lda, int ka, const float* B, int64_t ldb, int kb, bool sym,
+                       int64_t nrows, const int64_t* nrows_dev, const int32_t* gather, const double* wts,
+                       double* partial, int grid, double* out, int ldo, const int32_t* status, cudaStream_t st);
+// One-CTA fp64 Cholesky G = R^T R (upper) with one jitter retry, then R^{-1}.
+// Writes R^{-1} as fp32 (ld ldr32, zero padded to padk) and/or fp64 (ld ldr64).
+void launch_chol_inv(const double* G, int k, float* Rinv32, int ldr32, int padk32, double* Rinv64, int ldr64,
+                     int32_t* status, cudaStream_t st);
+
+// ---------------------------------------------------------------- leverage.cu
+void launch_leverage(const float* F, int64_t n, int k, const float* Rinv32, float* lev,
+                     const int32_t* status, cudaStream_t st);
+
+// ---------------------------------------------------------------- sampler.cu
+constexpr int kSampBlock = 1024;  // elements per block of the sampler passes
+inline int64_t samp_blocks(int64_t n) { return (n + kSampBlock - 1) / kSampBlock; }
+struct SamplerWs {
+  uint64_t* bw;      // [nb] block mass, then exclusive offsets
+  uint32_t* bd;      // [nb] block det counts, then offsets
+  double* bt;        // [nb] block theta
+  uint32_t* bu;      // [nb] block unique counts, then offsets
+  uint64_t* P;       // [n] inclusive prefix of w
+  int32_t* cnt;      // [n] draw multiplicities (kept zero between calls)
+};
+// Philox stream = 2 * it + side with it = *iter_dev if iter_dev else iteration.
+void launch_hybrid_sample(const float* lev, int64_t n, int k, int64_t s, double T, uint64_t seed,
+                          const int32_t* iter_dev, uint32_t iteration, uint32_t side, const symnmf_plan& plan,
+                          const SamplerWs& w, int32_t* status, cudaStream_t st);
+
+// ---------------------------------------------------------------- spmm.cu / dense.cu
+void launch_spmm_csr(const symnmf_matrix& A, const float* F, int k, float* Y, const int32_t* status, cudaStream_t st);
+void launch_sampled_csr(const symnmf_matrix& A, const float* F, int k, const int32_t* uniq, const double* w,
+                        const int64_t* n_uniq_dev, int64_t cap, float* Y, const int32_t* status, cudaStream_t st);
+void launch_dense_ah_simt(const float* A, int64_t lda, int64_t n, const float* F, int64_t ldf, int k, float* Y,
+                          int64_t ldy, const int32_t* status, cudaStream_t st);
+void launch_sampled_dense(const float* A, int64_t lda, int64_t n, const float* F, int k, const int32_t* uniq,
+                          const double* w, const int64_t* n_uniq_dev, int64_t cap, float* Y, const int32_t* status,
+                          cudaStream_t st);
+// tcgen05 3xTF32 dense product (tc_gemm.cu); returns false if unavailable for the shape.
+bool launch_dense_ah_tc(const float* A, int64_t lda, int64_t n, const float* F, int64_t ldf, int k, float* Y,
+                        int64_t ldy, void* scratch, size_t scratch_bytes, const int32_t* status, cudaStream_t st);
+size_t dense_ah_tc_scratch(int64_t n, int k);
+
+// ---------------------------------------------------------------- hals.cu
+void launch_hals_sweep(const double* G, const float* Y, const float* F, float* X, int64_t n, int k, double alpha,
+                       const int32_t* status, cudaStream_t st);
+
+// ---------------------------------------------------------------- lai.cu
+void launch_gaussian(int64_t n, int l, uint64_t seed, float* Omega, cudaStream_t st);
+// Y[r, :kb] = sum_a X[r, a] M[a, :]  (row apply of a small ka x kb matrix M), fp32 or fp64 M.
+void launch_rowapply32(const float* X, int64_t ldx, int64_t n, int ka, const float* M, int kb, float* Y, int64_t ldy,
+                       const int32_t* status, cudaStream_t st);
+void launch_rowapply64(const float* X, int64_t ldx, int64_t n, int ka, const double* M, int kb, float* Y,
+                       int64_t ldy, const int32_t* status, cudaStream_t st);
+// M32[a, b] = lambda[a] * Z[a, b] (fp64 in, fp32 out)
+void launch_scale_rows(const double* Z, int l, int k, const double* lambda, float* M32, const int32_t* status,
+                       cudaStream_t st);
+// One-CTA Jacobi EVD of symmetric T (l x l fp64); sorts by |lambda| desc; V (ld l) fp64.
+void launch_jacobi_evd(double* T, int l, double* V, double* lambda, int32_t* status, cudaStream_t st);
+void launch_symmetrize(double* T, int l, cudaStream_t st);
+
+// ---------------------------------------------------------------- residual.cu
+void launch_residual(const symnmf_matrix& A, const float* H, int k, const float* AH, const double* G,
+                     double* partial, int grid, double* out, const int32_t* status, cudaStream_t st);
+int residual_grid(int64_t n);
+
+}  // namespace symnmf

@@ -1,0 +1,167 @@
+// (a10) Exact CSR product Y = A F and (a9) the sampled CSR product
+// Y_s = sum_{i in U} omega_i A[i,:]^T f_i (by symmetry
+// row i of A equals column i).
+//
+// Exact: a group of k/4 lanes owns one row; each lane keeps a float4 slice of
+// the output row and streams the row's (col, val) pairs with 4-way unrolled
+// independent gathers of F rows (128-bit loads).  Sampled: one warp per
+// sampled row; groups of k/4 lanes scatter-add omega_i a_ic f_i into row c of
+// Y_s with 128-bit vector atomics (red.global.add.v4.f32).
+#include "kernels.cuh"
+
+namespace symnmf {
+
+template <int LPR>   // lanes per row = k / 4
+__global__ void __launch_bounds__(256) spmm_csr_v4(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                                   const float* __restrict__ val, int64_t n,
+                                                   const float4* __restrict__ F4, float4* __restrict__ Y4,
+                                                   const int32_t* __restrict__ status) {
+  if (dev_failed(status)) return;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int li = threadIdx.x % LPR;
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / LPR;
+  for (int64_t r = gtid / LPR; r < n; r += ngroups) {
+    const int64_t e0 = rowptr[r], e1 = rowptr[r + 1];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int64_t e = e0;
+    for (; e + 4 <= e1; e += 4) {
+      int c[4];
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { c[u] = __ldg(col + e + u); v[u] = __ldg(val + e + u); }
+      float4 f[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) f[u] = __ldg(F4 + (int64_t)c[u] * LPR + li);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc.x = fmaf(v[u], f[u].x, acc.x); acc.y = fmaf(v[u], f[u].y, acc.y);
+        acc.z = fmaf(v[u], f[u].z, acc.z); acc.w = fmaf(v[u], f[u].w, acc.w);
+      }
+    }
+    for (; e < e1; ++e) {
+      const int c = __ldg(col + e);
+      const float v = __ldg(val + e);
+      const float4 f = __ldg(F4 + (int64_t)c * LPR + li);
+      acc.x = fmaf(v, f.x, acc.x); acc.y = fmaf(v, f.y, acc.y);
+      acc.z = fmaf(v, f.z, acc.z); acc.w = fmaf(v, f.w, acc.w);
+    }
+    Y4[r * LPR + li] = acc;
+  }
+}
+
+// Generic k (k % 4 != 0): one warp per row, lane j owns columns j and j + 32.
+__global__ void __launch_bounds__(256) spmm_csr_scalar(const int64_t* __restrict__ rowptr,
+                                                       const int32_t* __restrict__ col, const float* __restrict__ val,
+                                                       int64_t n, const float* __restrict__ F, int k,
+                                                       float* __restrict__ Y, const int32_t* __restrict__ status) {
+  if (dev_failed(status)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+    float a0 = 0.f, a1 = 0.f;
+    for (int64_t e = rowptr[r]; e < rowptr[r + 1]; ++e) {
+      const int64_t c = __ldg(col + e);
+      const float v = __ldg(val + e);
+      if (lane < k) a0 = fmaf(v, __ldg(F + c * k + lane), a0);
+      if (lane + 32 < k) a1 = fmaf(v, __ldg(F + c * k + lane + 32), a1);
+    }
+    if (lane < k) Y[r * k + lane] = a0;
+    if (lane + 32 < k) Y[r * k + lane + 32] = a1;
+  }
+}
+
+static int grid_for(int64_t work_threads) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((work_threads + 255) / 256, 148 * 16));
+}
+
+void launch_spmm_csr(const symnmf_matrix& A, const float* F, int k, float* Y, const int32_t* status, cudaStream_t st) {
+  const int64_t n = A.n;
+  if (k % 4 == 0) {
+    const int lpr = k / 4;
+    const int grid = grid_for(n * lpr);
+    const float4* F4 = reinterpret_cast<const float4*>(F);
+    float4* Y4 = reinterpret_cast<float4*>(Y);
+    switch (lpr) {
+      case 1: spmm_csr_v4<1><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, n, F4, Y4, status); return;
+      case 2: spmm_csr_v4<2><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, n, F4, Y4, status); return;
+      case 4: spmm_csr_v4<4><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, n, F4, Y4, status); return;
+      case 8: spmm_csr_v4<8><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, n, F4, Y4, status); return;
+      case 16: spmm_csr_v4<16><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, n, F4, Y4, status); return;
+      default: break;
+    }
+  }
+  spmm_csr_scalar<<<grid_for(n * 32), 256, 0, st>>>(A.rowptr, A.colidx, A.val, n, F, k, Y, status);
+}
+
+// ---------------------------------------------------------------- sampled (scatter) product
+template <int LPR>
+__global__ void __launch_bounds__(256) sampled_csr_v4(const int64_t* __restrict__ rowptr,
+                                                      const int32_t* __restrict__ col, const float* __restrict__ val,
+                                                      const float4* __restrict__ F4, const int32_t* __restrict__ uniq,
+                                                      const double* __restrict__ w,
+                                                      const int64_t* __restrict__ n_uniq_dev, float4* __restrict__ Y4,
+                                                      const int32_t* __restrict__ status) {
+  if (dev_failed(status)) return;
+  constexpr int NPW = 32 / LPR;   // nonzeros per warp step
+  const int lane = threadIdx.x & 31, sub = lane / LPR, li = lane % LPR;
+  const int64_t nu = *n_uniq_dev;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < nu; u += nw) {
+    const int64_t i = uniq[u];
+    const float om = (float)w[u];
+    float4 f = __ldg(F4 + i * LPR + li);
+    f.x *= om; f.y *= om; f.z *= om; f.w *= om;
+    const int64_t e1 = rowptr[i + 1];
+    for (int64_t e = rowptr[i] + sub; e < e1; e += NPW) {
+      const int64_t c = __ldg(col + e);
+      const float a = __ldg(val + e);
+      atomicAdd(Y4 + c * LPR + li, make_float4(a * f.x, a * f.y, a * f.z, a * f.w));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) sampled_csr_scalar(const int64_t* __restrict__ rowptr,
+                                                          const int32_t* __restrict__ col,
+                                                          const float* __restrict__ val, const float* __restrict__ F,
+                                                          int k, const int32_t* __restrict__ uniq,
+                                                          const double* __restrict__ w,
+                                                          const int64_t* __restrict__ n_uniq_dev,
+                                                          float* __restrict__ Y, const int32_t* __restrict__ status) {
+  if (dev_failed(status)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t nu = *n_uniq_dev;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < nu; u += nw) {
+    const int64_t i = uniq[u];
+    const float om = (float)w[u];
+    const float f0 = lane < k ? om * F[i * k + lane] : 0.f;
+    const float f1 = lane + 32 < k ? om * F[i * k + lane + 32] : 0.f;
+    for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+      const int64_t c = __ldg(col + e);
+      const float a = __ldg(val + e);
+      if (lane < k) atomicAdd(Y + c * k + lane, a * f0);
+      if (lane + 32 < k) atomicAdd(Y + c * k + lane + 32, a * f1);
+    }
+  }
+}
+
+void launch_sampled_csr(const symnmf_matrix& A, const float* F, int k, const int32_t* uniq, const double* w,
+                        const int64_t* n_uniq_dev, int64_t cap, float* Y, const int32_t* status, cudaStream_t st) {
+  cudaMemsetAsync(Y, 0, sizeof(float) * (size_t)A.n * k, st);
+  const int grid = grid_for(std::max<int64_t>(cap, 1) * 32);
+  if (k % 4 == 0) {
+    const float4* F4 = reinterpret_cast<const float4*>(F);
+    float4* Y4 = reinterpret_cast<float4*>(Y);
+    switch (k / 4) {
+      case 1: sampled_csr_v4<1><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
+      case 2: sampled_csr_v4<2><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
+      case 4: sampled_csr_v4<4><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
+      case 8: sampled_csr_v4<8><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
+      case 16: sampled_csr_v4<16><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
+      default: break;
+    }
+  }
+  sampled_csr_scalar<<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, F, k, uniq, w, n_uniq_dev, Y, status);
+}
+
+}  // namespace symnmf

@@ -1,0 +1,353 @@
+"""GPU parity: every C-ABI operation vs the fp64 oracle on the same seeded inputs.
+
+Tolerances (north star): products / Grams / sampled products
+1e-5 relative Frobenius (fp32 path); scores 1e-5 relative 2-norm (Z21);
+plans bit-exact given the same fp32 score vector and (seed, iteration, side);
+normalised residual after 10 iterations 1e-4 relative.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from synth import make_input, random_factor, planted_dense
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2402_08134_b200 import symnmf as S  # noqa: E402
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def cu(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def sym_dense(n, seed):
+    r = np.random.default_rng(seed)
+    X = r.random((n, n))
+    return ((X + X.T) / 2).astype(np.float32)
+
+
+@pytest.fixture(scope="module")
+def c1():
+    return make_input("c1")
+
+
+@pytest.fixture(scope="module")
+def c2small():
+    return make_input("c2", n_override=20_000)
+
+
+# ------------------------------------------------------------------ (a1) Gram
+@pytest.mark.parametrize("n,k", [(1, 1), (7, 3), (1000, 8), (1003, 16), (40_000, 32), (5_001, 64), (100_003, 5)])
+def test_gram(n, k):
+    F = random_factor(n, k, 1)
+    G = S.gram(cu(F)).cpu().numpy()
+    ref = O.gram(F)
+    assert rel(G, ref) < 1e-6
+    assert np.array_equal(G, G.T)
+
+
+# ------------------------------------------------------------------ (a10) exact product
+@pytest.mark.parametrize("n,k", [(1000, 8), (1003, 5), (257, 16), (2048, 32), (300, 64), (5, 1)])
+def test_ah_dense_fp32(n, k):
+    A = sym_dense(n, n + k)
+    F = random_factor(n, k, 2)
+    Y = S.ah(S.DeviceMatrix.from_host(A), cu(F)).cpu().numpy()
+    assert rel(Y, O.ah(A, F)) < 1e-5
+
+
+@pytest.mark.parametrize("k", [1, 3, 8, 16, 32, 64])
+def test_ah_csr(c2small, k):
+    A = c2small["A"]
+    F = random_factor(A.n, k, 3)
+    Y = S.ah(S.DeviceMatrix.from_host(A), cu(F)).cpu().numpy()
+    assert rel(Y, O.ah(A, F)) < 1e-5
+
+
+def test_ah_dense_equals_csr_storage(c2small):
+    sub = make_input("c2", n_override=3_200)["A"]
+    F = random_factor(sub.n, 8, 4)
+    Yc = S.ah(S.DeviceMatrix.from_host(sub), cu(F)).cpu().numpy()
+    Yd = S.ah(S.DeviceMatrix.from_host(sub.to_dense()), cu(F)).cpu().numpy()
+    assert rel(Yc, Yd) < 1e-6
+
+
+# ------------------------------------------------------------------ (a3) scores
+@pytest.mark.parametrize("n,k", [(7, 3), (1000, 8), (1003, 16), (50_000, 32), (4_099, 64), (100_000, 1)])
+def test_leverage_scores(n, k):
+    F = random_factor(n, k, 5)
+    lev, G = S.leverage_scores(cu(F), return_gram=True)
+    lev = lev.cpu().numpy()
+    ref = O.leverage_scores(F)
+    assert rel(lev, ref) < 1e-5                                    # Z21 norm-wise
+    big = ref >= k / n
+    assert np.max(np.abs(lev[big] - ref[big]) / ref[big]) < 1e-4
+    assert abs(lev.astype(np.float64).sum() - k) < 1e-4 * k        # sum = rank
+    assert rel(G.cpu().numpy(), O.gram(F)) < 1e-6
+
+
+def test_leverage_scores_closed_forms():
+    F = np.zeros((5, 2), np.float32); F[0, 0] = 1; F[1, 1] = 1   # [I2; 0] -> (1, 1, 0, ...)
+    lev = S.leverage_scores(cu(F)).cpu().numpy()
+    assert np.allclose(lev, [1, 1, 0, 0, 0], atol=1e-6)
+    lev = S.leverage_scores(cu(np.ones((64, 1), np.float32))).cpu().numpy()
+    assert np.allclose(lev, 1 / 64, rtol=1e-6)
+
+
+def test_leverage_rank_deficient_uses_jitter():
+    F = random_factor(500, 4, 6)
+    F[:, 3] = 0.0                                                 # zero column: G singular -> one jitter retry
+    lev = S.leverage_scores(cu(F)).cpu().numpy()
+    assert abs(lev.sum() - 3) < 1e-3
+
+
+def test_leverage_not_pd_reported():
+    F = np.zeros((100, 3), np.float32)                            # tr(G) = 0: no jitter possible
+    with pytest.raises(S.A.SymNMFError) as e:
+        S.leverage_scores(cu(F))
+    assert e.value.code == S.A.ERR_NOT_PD
+
+
+# ------------------------------------------------------------------ (a4-a7) plan, bit-exact
+def _scores(n, k, seed, power=3):
+    F = random_factor(n, k, seed) ** power
+    return O.leverage_scores(F).astype(np.float32)
+
+
+@pytest.mark.parametrize("n,k,s,tau,seed,it,side", [
+    (1000, 8, 200, 1 / 200, 0, 0, 0),
+    (1000, 8, 200, 1 / 200, 0, 7, 1),
+    (100_000, 16, 2000, 1 / 2000, 3, 2, 0),
+    (100_000, 16, 2000, 1.0, 3, 2, 1),       # tau = 1: pure i.i.d. sampling
+    (7, 3, 5, 1 / 5, 1, 0, 0),
+    (1, 1, 1, 1.0, 0, 0, 0),
+    (2_000_000, 32, 20_000, 1 / 20_000, 0, 1, 1),
+    ((1 << 20) + 17, 4, 30_000, 1 / 30_000, 9, 5, 0),
+])
+def test_hybrid_plan_bit_exact(n, k, s, tau, seed, it, side):
+    lev = _scores(n, k, seed + 11)
+    g = S.hybrid_sample(cu(lev), k, s, tau, seed, it, side).to_host()
+    o = O.build_plan(lev, k, s, tau, seed, it, side)
+    assert g["s_D"] == o["s_D"] and g["s_R"] == o["s_R"] and g["n_uniq"] == o["n_uniq"] and g["W"] == o["W"]
+    assert np.array_equal(g["det_idx"], o["det_idx"])
+    assert np.array_equal(g["draw_idx"], o["draw_idx"])
+    assert np.array_equal(g["uniq_idx"], o["uniq_idx"])
+    assert np.array_equal(g["uniq_w"], o["uniq_w"])                 # IEEE fp64, fixed op order
+    assert abs(g["theta"] - o["theta"]) <= 1e-12 * max(1.0, o["theta"])
+    assert abs(g["theta"] + g["xi"] - k) < 1e-12 * k
+
+
+def test_hybrid_plan_all_deterministic_and_zero_mass():
+    lev = _scores(3000, 4, 21)
+    tau = float(lev.min()) / 4 * 0.5                              # every row in I_D, needs cap = n
+    g = S.hybrid_sample(cu(lev), 4, 10, tau, 0, 0, 0).to_host()
+    assert g["s_D"] == 3000 and g["s_R"] == 0 and np.array_equal(g["uniq_idx"], np.arange(3000))
+    lev = np.zeros(12, np.float32); lev[:2] = 1.0                 # W = 0 -> s_R = 0
+    g = S.hybrid_sample(cu(lev), 2, 10, 0.4, 0, 0, 0).to_host()
+    assert g["det_idx"].tolist() == [0, 1] and g["s_R"] == 0 and g["theta"] == 2.0
+
+
+def test_hybrid_capacity_error():
+    lev = _scores(3000, 4, 22)
+    with pytest.raises(S.A.SymNMFError) as e:
+        S.hybrid_sample(cu(lev), 4, 10, float(lev.min()) / 8, 0, 0, 0, cap=100)
+    assert e.value.code == S.A.ERR_CAPACITY
+
+
+# ------------------------------------------------------------------ (a8, a9) sampled products
+def _plan_for(F, k, s, tau, seed=0, it=0, side=0):
+    """Both sides sample from the same score vector, computed by the oracle (fp32-rounded)."""
+    lev = O.leverage_scores(F).astype(np.float32)
+    plan = S.hybrid_sample(cu(lev), k, s, tau, seed, it, side)
+    return plan, O.build_plan(lev, k, s, tau, seed, it, side)
+
+
+def test_sampled_dense(c1):
+    A, cfg = c1["A"], c1["cfg"]
+    F = c1["H0"]
+    plan, o = _plan_for(F, cfg.k, cfg.s, cfg.tau)
+    Y, Gs = S.sampled_ah(S.DeviceMatrix.from_host(A), cu(F), plan)
+    Gr, Yr = O.sampled_products(A, F, o["uniq_idx"], o["uniq_w"])
+    assert rel(Y.cpu().numpy(), Yr) < 1e-5 and rel(Gs.cpu().numpy(), Gr) < 1e-6
+
+
+@pytest.mark.parametrize("k", [3, 16, 32])
+def test_sampled_csr(c2small, k):
+    A = c2small["A"]
+    F = random_factor(A.n, k, 9) ** 2
+    plan, o = _plan_for(F, k, 1000, 1 / 1000, seed=5, it=3, side=1)
+    Y, Gs = S.sampled_ah(S.DeviceMatrix.from_host(A), cu(F), plan)
+    Gr, Yr = O.sampled_products(A, F, o["uniq_idx"], o["uniq_w"])
+    assert rel(Y.cpu().numpy(), Yr) < 1e-5 and rel(Gs.cpu().numpy(), Gr) < 1e-6
+
+
+def test_sampled_all_rows_equals_exact(c2small):
+    A = make_input("c2", n_override=4_000)["A"]
+    F = random_factor(A.n, 8, 10)
+    lev = S.leverage_scores(cu(F))
+    tau = float(lev.min().item()) / 8 * 0.5
+    plan = S.hybrid_sample(lev, 8, 10, tau, 0, 0, 0)
+    M = S.DeviceMatrix.from_host(A)
+    Y, Gs = S.sampled_ah(M, cu(F), plan)
+    assert rel(Y.cpu().numpy(), S.ah(M, cu(F)).cpu().numpy()) < 1e-6
+    assert rel(Gs.cpu().numpy(), O.gram(F)) < 1e-6
+
+
+# ------------------------------------------------------------------ (a11) HALS sweep
+@pytest.mark.parametrize("n,k", [(1000, 8), (1001, 5), (20_000, 16), (3_000, 32), (777, 64)])
+def test_hals_sweep(n, k):
+    r = np.random.default_rng(n + k)
+    A = sym_dense(min(n, 1500), 7) if n <= 1500 else None
+    F = random_factor(n, k, 11)
+    X = random_factor(n, k, 12)
+    G = O.gram(F)
+    Y = (A @ F.astype(np.float64)).astype(np.float32) if A is not None else \
+        (F.astype(np.float64) @ G + r.random((n, k))).astype(np.float32)
+    alpha = 0.7
+    Xg, Gn = S.hals_sweep(cu(G), cu(Y), cu(F), cu(X), alpha, return_gram=True)
+    Xr = O.hals_sweep(G, Y, F, X, alpha)
+    assert rel(Xg.cpu().numpy(), Xr) < 1e-5
+    assert rel(Gn.cpu().numpy(), O.gram(Xr)) < 1e-5
+
+
+def test_hals_fixed_point():
+    H = random_factor(500, 6, 13)
+    A = (H.astype(np.float64) @ H.T).astype(np.float32)
+    G = O.gram(H)
+    Y = (A.astype(np.float64) @ H).astype(np.float32)
+    X = S.hals_sweep(cu(G), cu(Y), cu(H), cu(H.copy()), 1.3).cpu().numpy()
+    assert rel(X, H) < 1e-5
+
+
+# ------------------------------------------------------------------ (a12, a13) LAI
+def test_gaussian_omega_matches_oracle():
+    Om = S.gaussian(1001, 13, seed=5).cpu().numpy()
+    ref = O.gaussian_omega(1001, 13, seed=5)
+    assert np.max(np.abs(Om - ref)) <= 2e-6 * max(1.0, np.abs(ref).max())
+    assert np.mean(Om == ref) > 0.999
+
+
+def test_lai_apply():
+    r = np.random.default_rng(3)
+    U = np.linalg.qr(r.standard_normal((3000, 20)))[0].astype(np.float32)
+    lam = r.standard_normal(20) * 10
+    F = random_factor(3000, 16, 14)
+    Y = S.lai_ah(cu(U), cu(lam), cu(F)).cpu().numpy()
+    assert rel(Y, O.lai_apply(U, lam, F)) < 1e-5
+
+
+def test_rangefinder_low_rank_exact():
+    r = np.random.default_rng(4)
+    n, rank, l = 1200, 10, 16
+    B = r.standard_normal((n, rank))
+    A = (B @ np.diag(np.linspace(1, 10, rank)) @ B.T).astype(np.float32)
+    U, lam = S.rangefinder(S.DeviceMatrix.from_host(A), l, 2, seed=1)
+    U, lam = U.cpu().numpy().astype(np.float64), lam.cpu().numpy()
+    assert np.allclose(U.T @ U, np.eye(l), atol=1e-5)
+    Ar = U @ np.diag(lam) @ U.T
+    assert rel(Ar, A) < 1e-5                                        # exact-rank capture
+    Uo, lo, _ = O.rangefinder(A, l, 2, seed=1)
+    assert np.allclose(np.sort(np.abs(lam))[-rank:], np.sort(np.abs(lo))[-rank:], rtol=1e-5)
+
+
+def test_rangefinder_gaussian_kernel_operator():
+    d = make_input("c3", n_override=2_000)
+    A = d["A"]
+    l = 40
+    U, lam = S.rangefinder(S.DeviceMatrix.from_host(A), l, 2, seed=0)
+    Uo, lo, _ = O.rangefinder(A, l, 2, seed=0)
+    P = random_factor(A.shape[0], 8, 15)
+    Yg = O.lai_apply(U.cpu().numpy(), lam.cpu().numpy(), P)
+    Yo = O.lai_apply(Uo, lo, P)
+    # both approximate A to the same accuracy; the operators agree to the tail mass
+    assert rel(Yg, Yo) < 2e-4
+    assert abs(np.abs(lam.cpu().numpy()[0]) - np.abs(lo[0])) < 1e-5 * abs(lo[0])
+
+
+# ------------------------------------------------------------------ (a15) residual
+def test_residual_dense_and_csr(c1, c2small):
+    A, H = c1["A"], c1["H0"]
+    out = S.residual(S.DeviceMatrix.from_host(A), cu(H)).cpu().numpy()
+    assert abs(out[0] - O.residual(A, H)) < 1e-9
+    B = c2small["A"]
+    Hb = random_factor(B.n, 16, 16) * 0.05
+    out = S.residual(S.DeviceMatrix.from_host(B), cu(Hb)).cpu().numpy()
+    assert abs(out[0] - O.residual(B, Hb)) < 1e-7
+
+
+# ------------------------------------------------------------------ (a14) iterate
+def _run(d, mode, iters, **kw):
+    A, H0, alpha = d["A"], d["H0"], d["alpha"]
+    M = S.DeviceMatrix.from_host(A)
+    W, H = cu(H0), cu(H0)
+    out = S.iterate(M, W, H, alpha, iters, mode=mode, **kw)
+    return W.cpu().numpy(), H.cpu().numpy(), out
+
+
+def test_iterate_exact_c1(c1):
+    _, Hg, out = _run(c1, "exact", 10, with_residual=True)
+    _, Hr, _ = O.iterate(c1["A"], c1["H0"], c1["H0"], c1["alpha"], 10, "exact")
+    rg, ro = O.residual(c1["A"], Hg), O.residual(c1["A"], Hr)
+    assert abs(rg - ro) <= 1e-4 * ro
+    assert abs(out["residual"][-1] - rg) < 1e-6
+
+
+def test_iterate_lvs_c1(c1):
+    cfg = c1["cfg"]
+    _, Hg, out = _run(c1, "lvs", 10, s=cfg.s, tau=cfg.tau, seed=0)
+    _, Hr, tr = O.iterate(c1["A"], c1["H0"], c1["H0"], c1["alpha"], 10, "lvs", s=cfg.s, tau=cfg.tau, seed=0)
+    for g, o in zip(out["halves"], tr):
+        assert (g["s_D"], g["s_R"], g["n_uniq"]) == (o["s_D"], o["s_R"], o["n_uniq"])
+    rg, ro = O.residual(c1["A"], Hg), O.residual(c1["A"], Hr)
+    assert abs(rg - ro) <= 1e-4 * ro
+
+
+def test_iterate_exact_and_lvs_c2():
+    d = make_input("c2")
+    cfg = d["cfg"]
+    for mode, kw in (("exact", {}), ("lvs", dict(s=cfg.s, tau=cfg.tau, seed=0))):
+        _, Hg, out = _run(d, mode, 10, **kw)
+        _, Hr, _ = O.iterate(d["A"], d["H0"], d["H0"], d["alpha"], 10, mode, **kw)
+        rg, ro = O.residual(d["A"], Hg), O.residual(d["A"], Hr)
+        assert abs(rg - ro) <= 1e-4 * ro, (mode, rg, ro)
+
+
+def test_iterate_lai_c1(c1):
+    A = c1["A"]
+    M = S.DeviceMatrix.from_host(A)
+    U, lam = S.rangefinder(M, 12, 2, seed=0)
+    W, H = cu(c1["H0"]), cu(c1["H0"])
+    S.iterate(M, W, H, c1["alpha"], 10, mode="lai", U=U, lam=lam)
+    _, Hr, _ = O.iterate(A, c1["H0"], c1["H0"], c1["alpha"], 10, "lai", U=U.cpu().numpy(), lam=lam.cpu().numpy())
+    rg, ro = O.residual(A, H.cpu().numpy()), O.residual(A, Hr)
+    assert abs(rg - ro) <= 1e-4 * ro
+
+
+def test_solver_first_iter_keys_the_sampler(c1):
+    """A resumed run (first_iter = 3) draws from the Philox streams of iteration 3 (bit-reproducible resume)."""
+    cfg = c1["cfg"]
+    M = S.DeviceMatrix.from_host(c1["A"])
+    W, H = cu(c1["H0"]), cu(c1["H0"])
+    sv = S.Solver(M, W, H, c1["alpha"], mode="lvs", s=cfg.s, tau=cfg.tau, seed=0, first_iter=3, max_iters=2)
+    sv.run(1)
+    st = sv.stats()
+    assert st["status"] == 0 and st["iters"] == 1
+    lev = O.leverage_scores(c1["H0"]).astype(np.float32)
+    o = O.build_plan(lev, cfg.k, cfg.s, cfg.tau, 0, 3, 0)           # side 0 samples rows of H0 at it = 3
+    g = st["halves"][0]
+    assert (g["s_D"], g["s_R"], g["n_uniq"]) == (o["s_D"], o["s_R"], o["n_uniq"])
+    sv.run(1)
+    assert sv.stats()["iters"] == 2
+    sv.close()
