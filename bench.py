@@ -26,6 +26,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "SymNMF iters/sec (exact & LvS); A·H / sampled SpMM HBM GB/s vs B200 peak"
 UNIT = "iters/s"
+SLEEP_CYCLES = 400_000   # ~0.2 ms: hides host enqueue latency from the device-side event timing
 
 
 def parse():
@@ -220,6 +221,7 @@ def run_ours(args, ws, rank, local, pg):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for e0, e1 in evs:
         flush.zero_()
+        torch.cuda._sleep(SLEEP_CYCLES)   # keep the GPU busy while the host enqueues the step
         e0.record(stream)
         solver.run(1)
         e1.record(stream)
@@ -252,6 +254,7 @@ def run_ours(args, ws, rank, local, pg):
     ex_ms = []
     for _ in range(ex_steps):
         flush.zero_()
+        torch.cuda._sleep(SLEEP_CYCLES)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream); sx.run(1); e1.record(stream)
         e1.synchronize()
@@ -267,6 +270,7 @@ def run_ours(args, ws, rank, local, pg):
         acc = 0.0
         for _ in range(reps):
             flush.zero_()
+            torch.cuda._sleep(SLEEP_CYCLES)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream); fn(); e1.record(stream)
             e1.synchronize()

@@ -337,6 +337,12 @@ def residual(A, H) -> float:
     A64 = as_f64(A)
     H = np.asarray(H, dtype=np.float64)
     n = H.shape[0]
+    if sp.issparse(A64):
+        # sparse A: the exact identity ||A - H H^T||^2 = ||A||^2 - 2 tr(H^T A H) + ||H^T H||^2
+        a2 = frob_sq(A64)
+        G = H.T @ H
+        r2 = a2 - 2.0 * float((H * (A64 @ H)).sum()) + float((G * G).sum())
+        return math.sqrt(max(r2, 0.0)) / math.sqrt(a2)
     num = 0.0
     for r0 in range(0, n, 2048):
         r1 = min(n, r0 + 2048)

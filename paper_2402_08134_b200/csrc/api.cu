@@ -241,12 +241,17 @@ void rf_layout(Carver& c, int64_t n, int l, int precision, RfLayout* L) {
   L->tcs_bytes = precision == SYMNMF_3XTF32 ? dense_ah_tc_scratch(n, l) : 0;
   L->tcs = c.take<char>(L->tcs_bytes);
 }
-// orth(Yb) -> Q by CholeskyQR2 with fp64 Gram, Cholesky and row apply.
+// orth(Yb) -> Q by shifted CholeskyQR2 with fp64 Gram, Cholesky and row apply: the
+// first pass factors G + 1e-14 tr(G) I (span(Q1) = span(Y) is unchanged; a sketch
+// that is rank deficient to fp32 precision, e.g. an exact low-rank A, stays
+// factorable), the second pass restores orthonormality.
 void enqueue_orth(const RfLayout& L, int64_t n, int l, const float* Yin, float* Qout, int32_t* status, cudaStream_t st) {
-  launch_cross_gram(Yin, l, l, Yin, l, l, true, n, nullptr, nullptr, nullptr, L.part, L.grid, L.Gl, l, status, st);
-  launch_chol_inv(L.Gl, l, nullptr, 0, 0, L.R64, l, status, st);
+  launch_cross_gram(Yin, l, l, Yin, l, l, true, n, nullptr, nullptr, nullptr, L.part, L.grid, L.Gl, l, status, st,
+                    true);
+  launch_chol_inv(L.Gl, l, nullptr, 0, 0, L.R64, l, status, st, 1e-14);
   launch_rowapply64(Yin, l, n, l, L.R64, l, L.Q1, l, status, st);
-  launch_cross_gram(L.Q1, l, l, L.Q1, l, l, true, n, nullptr, nullptr, nullptr, L.part, L.grid, L.Gl, l, status, st);
+  launch_cross_gram(L.Q1, l, l, L.Q1, l, l, true, n, nullptr, nullptr, nullptr, L.part, L.grid, L.Gl, l, status, st,
+                    true);
   launch_chol_inv(L.Gl, l, nullptr, 0, 0, L.R64, l, status, st);
   launch_rowapply64(L.Q1, l, n, l, L.R64, l, Qout, l, status, st);
 }
@@ -287,7 +292,8 @@ extern "C" symnmf_status symnmf_rangefinder(const symnmf_matrix* A, int32_t l, i
     }
   }
   enqueue_dense_apply(*A, L.Q, l, L.Yb, precision, L, status, st);        // Z = A Q
-  launch_cross_gram(L.Q, l, l, L.Yb, l, l, false, n, nullptr, nullptr, nullptr, L.part, L.grid, L.T, l, status, st);
+  launch_cross_gram(L.Q, l, l, L.Yb, l, l, false, n, nullptr, nullptr, nullptr, L.part, L.grid, L.T, l, status, st,
+                    true);
   launch_symmetrize(L.T, l, st);                                            // T = Q^T A Q
   launch_jacobi_evd(L.T, l, L.V, lambda, status, st);                       // T = V Lambda V^T
   launch_rowapply64(L.Q, l, n, l, L.V, l, U, l, status, st);                // U = Q V

@@ -22,7 +22,7 @@ __device__ __forceinline__ void pair_to_blocks(int p, int nba, int nbb, int sym,
   ai = a; bi = a + rem;
 }
 
-template <int PPT>
+template <int PPT, bool F64P>
 __global__ void __launch_bounds__(GT) cross_gram_partial(
     const float* __restrict__ A, int64_t lda, int ka, const float* __restrict__ B, int64_t ldb, int kb, int sym,
     int64_t nrows, const int64_t* __restrict__ nrows_dev, const int32_t* __restrict__ gather,
@@ -101,12 +101,22 @@ __global__ void __launch_bounds__(GT) cross_gram_partial(
         const float w = sw[r];
         const float4 a4 = *reinterpret_cast<const float4*>(sa + r * sta + 4 * ai[q]);
         const float4 b4 = *reinterpret_cast<const float4*>(sb + r * stb + 4 * bi[q]);
-        const float a[4] = {a4.x * w, a4.y * w, a4.z * w, a4.w * w};
-        const float b[4] = {b4.x, b4.y, b4.z, b4.w};
+        if constexpr (F64P) {   // exact products (fp32 inputs), fp64 sums: Grams whose small
+                                // eigenvalues matter (CholeskyQR of the range finder's sketches)
+          const double a[4] = {(double)a4.x * w, (double)a4.y * w, (double)a4.z * w, (double)a4.w * w};
+          const double b[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[q][i * 4 + j] = fmaf(a[i], b[j], acc[q][i * 4 + j]);
+            for (int j = 0; j < 4; ++j) acc64[q][i * 4 + j] = fma(a[i], b[j], acc64[q][i * 4 + j]);
+        } else {
+          const float a[4] = {a4.x * w, a4.y * w, a4.z * w, a4.w * w};
+          const float b[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[q][i * 4 + j] = fmaf(a[i], b[j], acc[q][i * 4 + j]);
+        }
       }
     }
     since_flush += rows_per_tile;
@@ -186,7 +196,8 @@ size_t gram_partial_doubles(int ka, int kb, bool sym, int grid) {
 
 void launch_cross_gram(const float* A, int64_t lda, int ka, const float* B, int64_t ldb, int kb, bool sym,
                        int64_t nrows, const int64_t* nrows_dev, const int32_t* gather, const double* wts,
-                       double* partial, int grid, double* out, int ldo, const int32_t* status, cudaStream_t st) {
+                       double* partial, int grid, double* out, int ldo, const int32_t* status, cudaStream_t st,
+                       bool fp64_products) {
   const int nba = (ka + 3) / 4, nbb = (kb + 3) / 4;
   const int pairs = sym ? nba * (nba + 1) / 2 : nba * nbb;
   const int sta = nba * 4 + 4, stb = nbb * 4 + 4;
@@ -195,15 +206,18 @@ void launch_cross_gram(const float* A, int64_t lda, int ka, const float* B, int6
   size_t red = RG > 1 ? sizeof(double) * RG * pairs * 16 : 0;
   size_t smem = std::max(tile, red);
   const int ppt = (pairs + GT - 1) / GT;
+#define SYMNMF_GRAM_LAUNCH(P, D)                                                                          \
+  do {                                                                                                    \
+    cudaFuncSetAttribute(cross_gram_partial<P, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    cross_gram_partial<P, D><<<grid, GT, smem, st>>>(A, lda, ka, B, ldb, kb, sym, nrows, nrows_dev, gather, \
+                                                     wts, partial, status);                               \
+  } while (0)
   if (ppt <= 1) {
-    cudaFuncSetAttribute(cross_gram_partial<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cross_gram_partial<1><<<grid, GT, smem, st>>>(A, lda, ka, B, ldb, kb, sym, nrows, nrows_dev, gather, wts,
-                                                  partial, status);
+    if (fp64_products) SYMNMF_GRAM_LAUNCH(1, true); else SYMNMF_GRAM_LAUNCH(1, false);
   } else {
-    cudaFuncSetAttribute(cross_gram_partial<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cross_gram_partial<2><<<grid, GT, smem, st>>>(A, lda, ka, B, ldb, kb, sym, nrows, nrows_dev, gather, wts,
-                                                  partial, status);
+    if (fp64_products) SYMNMF_GRAM_LAUNCH(2, true); else SYMNMF_GRAM_LAUNCH(2, false);
   }
+#undef SYMNMF_GRAM_LAUNCH
   cross_gram_finalize<<<1, 256, 0, st>>>(partial, grid, ka, kb, sym, out, ldo, status);
 }
 
@@ -211,8 +225,11 @@ void launch_cross_gram(const float* A, int64_t lda, int ka, const float* B, int6
 // One CTA.  G = R^T R with R upper (right-looking, fp64).  A non-positive or
 // non-finite pivot triggers one retry with G + (1e-12 tr(G)/k) I;
 // a second failure sets SYMNMF_ERR_NOT_PD.  Then R^{-1} column by column.
+// shift_rel > 0 factors G + shift_rel tr(G) I from the start (the shifted
+// first pass of the range finder's CholeskyQR2, which must survive a
+// numerically rank-deficient sketch A Omega).
 __global__ void chol_inv_kernel(const double* __restrict__ G, int k, float* __restrict__ R32, int ldr32, int padk32,
-                                double* __restrict__ R64, int ldr64, int32_t* __restrict__ status) {
+                                double* __restrict__ R64, int ldr64, double shift_rel, int32_t* __restrict__ status) {
   extern __shared__ double smd[];
   __shared__ int fail;
   __shared__ double jitter;
@@ -224,11 +241,11 @@ __global__ void chol_inv_kernel(const double* __restrict__ G, int k, float* __re
   for (int attempt = 0; attempt < 2; ++attempt) {
     if (tid == 0) {
       fail = 0;
-      if (attempt == 0) jitter = 0.0;
-      else {
-        double tr = 0.0;
-        for (int i = 0; i < k; ++i) tr += G[i * k + i];
-        jitter = 1e-12 * tr / k;
+      double tr = 0.0;
+      for (int i = 0; i < k; ++i) tr += G[i * k + i];
+      jitter = shift_rel * tr;
+      if (attempt == 1) {
+        jitter += 1e-12 * tr / k;
         if (!(jitter > 0.0)) fail = 2;
       }
     }
@@ -289,10 +306,10 @@ __global__ void chol_inv_kernel(const double* __restrict__ G, int k, float* __re
 }
 
 void launch_chol_inv(const double* G, int k, float* Rinv32, int ldr32, int padk32, double* Rinv64, int ldr64,
-                     int32_t* status, cudaStream_t st) {
+                     int32_t* status, cudaStream_t st, double shift_rel) {
   const size_t smem = sizeof(double) * 2 * k * (k + 1);
   cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  chol_inv_kernel<<<1, 256, smem, st>>>(G, k, Rinv32, ldr32, padk32, Rinv64, ldr64, status);
+  chol_inv_kernel<<<1, 256, smem, st>>>(G, k, Rinv32, ldr32, padk32, Rinv64, ldr64, shift_rel, status);
 }
 
 }  // namespace symnmf

@@ -13,11 +13,12 @@ size_t gram_partial_doubles(int ka, int kb, bool sym, int grid);
 // sym => A == B and ka == kb: only the upper 4x4 blocks are computed, output mirrored.
 void launch_cross_gram(const float* A, int64_t lda, int ka, const float* B, int64_t ldb, int kb, bool sym,
                        int64_t nrows, const int64_t* nrows_dev, const int32_t* gather, const double* wts,
-                       double* partial, int grid, double* out, int ldo, const int32_t* status, cudaStream_t st);
+                       double* partial, int grid, double* out, int ldo, const int32_t* status, cudaStream_t st,
+                       bool fp64_products = false);
 // One-CTA fp64 Cholesky G = R^T R (upper) with one jitter retry, then R^{-1}.
 // Writes R^{-1} as fp32 (ld ldr32, zero padded to padk) and/or fp64 (ld ldr64).
 void launch_chol_inv(const double* G, int k, float* Rinv32, int ldr32, int padk32, double* Rinv64, int ldr64,
-                     int32_t* status, cudaStream_t st);
+                     int32_t* status, cudaStream_t st, double shift_rel = 0.0);
 
 // ---------------------------------------------------------------- leverage.cu
 void launch_leverage(const float* F, int64_t n, int k, const float* Rinv32, float* lev,

@@ -1,13 +1,302 @@
-// tcgen05 3xTF32 dense product (placeholder until the tensor-core kernel lands).
+// (a10)/(a12) Dense Y = A X on the 5th-generation tensor cores in 3xTF32
+// (precision SYMNMF_3XTF32): A n x n fp32 (the data matrix, streamed once from
+// HBM), X n x k fp32 (the factor F, or Omega / Q in the range finder).
+//
+//   Y = A_hi X_hi + A_hi X_lo + A_lo X_hi,   v_hi = v with the low 13 mantissa
+//   bits cleared (exactly representable in tf32), v_lo = v - v_hi (exact).
+//
+// Per CTA (one 128-row tile of A and one K range, split-K over gridDim.y):
+//   warp 0      TMA producer: A tile [128 x 32] fp32 (128B swizzle), X_hi^T / X_lo^T tiles
+//               [NP x 32] (pre-split and transposed once per product, K-major)
+//   warps 4..7  split the A tile in shared memory (hi in place, lo in a second buffer),
+//               fence.proxy.async, arrive; afterwards the epilogue (tcgen05.ld -> fp32 red.add)
+//   warp 1      one elected thread issues 3 x 4 tcgen05.mma.kind::tf32 (M=128, N=NP, K=8)
+//               per stage into a TMEM accumulator and commits the stage back to the producer
+//   warp 2      TMEM allocation / deallocation
+// Pipeline: 4 smem stages with full (TMA tx) / conv (128 arrivals) / empty (MMA commit) mbarriers.
+#include <cstdio>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include "kernels.cuh"
 
 namespace symnmf {
 
-size_t dense_ah_tc_scratch(int64_t, int) { return 0; }
+constexpr int TC_BM = 128;
+constexpr int TC_BK = 32;          // fp32 elements per 128-byte row
+template <int NP> constexpr int tc_stages() { return NP <= 80 ? 4 : 3; }
+constexpr int TC_THREADS = 256;
 
-bool launch_dense_ah_tc(const float*, int64_t, int64_t, const float*, int64_t, int, float*, int64_t, void*, size_t,
-                        const int32_t*, cudaStream_t) {
-  return false;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// Bounded wait: a pipeline that cannot make progress for ~10 s traps (a device
+// error the host sees) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok = 0;
+  uint64_t spins = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (!ok && ++spins > (1ull << 27)) {
+      printf("symnmf tc_gemm: mbarrier wait timeout block (%d,%d) thread %d bar %u parity %u\n", blockIdx.x,
+             blockIdx.y, threadIdx.x, a, parity);
+      __trap();
+    }
+  }
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major operand, 128-byte swizzle: rows of 128 B, 8-row core groups 1024 B apart.
+__device__ __forceinline__ uint64_t smem_desc_k128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);          // start address
+  d |= (uint64_t)1 << 16;                           // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;                 // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                           // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                           // SWIZZLE_128B
+  return d;
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+          tmem_d),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int NP>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    tc_gemm_3xtf32(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBhi,
+                   const __grid_constant__ CUtensorMap mapBlo, int64_t n, int kb_per_split, int64_t nkb_total,
+                   float* __restrict__ Y, int64_t ldy, int k, const int32_t* __restrict__ status) {
+  constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;   // 16 KB
+  constexpr uint32_t B_BYTES = NP * TC_BK * 4;      // NP x 128 B
+  constexpr uint32_t STAGE = 2 * A_BYTES + 2 * B_BYTES;
+  constexpr uint32_t TMEM_COLS = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : 256;
+  constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + tc_stages<NP>() * STAGE);
+  uint64_t* conv = full + tc_stages<NP>();
+  uint64_t* empty = conv + tc_stages<NP>();
+  uint64_t* tmem_full = empty + tc_stages<NP>();
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  if (dev_failed(status)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m0 = (int64_t)blockIdx.x * TC_BM;
+  const int64_t kb0 = (int64_t)blockIdx.y * kb_per_split;
+  const int nkb = (int)min64(kb_per_split, nkb_total - kb0);
+  if (nkb <= 0) return;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < tc_stages<NP>(); ++s) { mbar_init(full + s, 1); mbar_init(conv + s, 128); mbar_init(empty + s, 1); }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % tc_stages<NP>();
+        if (i >= tc_stages<NP>()) mbar_wait(empty + s, ((i / tc_stages<NP>()) - 1) & 1);
+        unsigned char* st = sm + s * STAGE;
+        const int kx = (int)((kb0 + i) * TC_BK);
+        mbar_expect_tx(full + s, A_BYTES + 2 * B_BYTES);
+        tma_load_2d(&mapA, full + s, st, kx, (int)m0);
+        tma_load_2d(&mapBhi, full + s, st + 2 * A_BYTES, kx, 0);
+        tma_load_2d(&mapBlo, full + s, st + 2 * A_BYTES + B_BYTES, kx, 0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % tc_stages<NP>();
+        mbar_wait(conv + s, (i / tc_stages<NP>()) & 1);
+        tc_fence_after();
+        const uint32_t a_hi = smem_u32(sm + s * STAGE), a_lo = a_hi + A_BYTES;
+        const uint32_t b_hi = a_hi + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < TC_BK / 8; ++kk) {
+          const uint32_t off = kk * 32;   // 8 tf32 = 32 bytes along the swizzled row
+          const uint32_t acc0 = (i | kk) ? 1u : 0u;
+          mma_tf32(tmem, smem_desc_k128(a_hi + off), smem_desc_k128(b_hi + off), IDESC, acc0);
+          mma_tf32(tmem, smem_desc_k128(a_hi + off), smem_desc_k128(b_lo + off), IDESC, 1u);
+          mma_tf32(tmem, smem_desc_k128(a_lo + off), smem_desc_k128(b_hi + off), IDESC, 1u);
+        }
+        mma_commit(empty + s);
+      }
+      mma_commit(tmem_full);
+    }
+  } else if (warp >= 4) {
+    const int t = threadIdx.x - 128;   // 0..127
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % tc_stages<NP>();
+      mbar_wait(full + s, (i / tc_stages<NP>()) & 1);
+      uint4* a = reinterpret_cast<uint4*>(sm + s * STAGE);
+      uint4* lo = reinterpret_cast<uint4*>(sm + s * STAGE + A_BYTES);
+#pragma unroll 4
+      for (int e = t; e < (int)(A_BYTES / 16); e += 128) {
+        const uint4 v = a[e];
+        uint4 h, l;
+        h.x = v.x & 0xFFFFE000u; h.y = v.y & 0xFFFFE000u; h.z = v.z & 0xFFFFE000u; h.w = v.w & 0xFFFFE000u;
+        l.x = __float_as_uint(__uint_as_float(v.x) - __uint_as_float(h.x));
+        l.y = __float_as_uint(__uint_as_float(v.y) - __uint_as_float(h.y));
+        l.z = __float_as_uint(__uint_as_float(v.z) - __uint_as_float(h.z));
+        l.w = __float_as_uint(__uint_as_float(v.w) - __uint_as_float(h.w));
+        a[e] = h;
+        lo[e] = l;
+      }
+      fence_proxy_async();
+      mbar_arrive(conv + s);
+    }
+    // epilogue: TMEM lane = tile row, column = output column
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int wq = warp & 3;
+    const int64_t row = m0 + wq * 32 + lane;
+#pragma unroll
+    for (int c0 = 0; c0 < NP; c0 += 16) {
+      uint32_t r[16];
+      const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)c0;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < n) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (c0 + j < k) atomicAdd(Y + row * ldy + c0 + j, __uint_as_float(r[j]));
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+  }
+}
+
+// X (n x k, ldx) -> X_hi^T, X_lo^T (NP x ldk, K contiguous, zero padded)
+__global__ void split_transpose(const float* __restrict__ X, int64_t ldx, int64_t n, int k, int NP, int64_t ldk,
+                                float* __restrict__ hiT, float* __restrict__ loT) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ldk) return;
+  for (int c = 0; c < NP; ++c) {
+    float v = (j < n && c < k) ? X[j * ldx + c] : 0.f;
+    const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    hiT[(int64_t)c * ldk + j] = h;
+    loT[(int64_t)c * ldk + j] = v - h;
+  }
+}
+
+// ---------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                     uint32_t box_inner, uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int np_for(int k) { return k <= 16 ? 16 : k <= 32 ? 32 : k <= 64 ? 64 : k <= 80 ? 80 : 96; }
+static int64_t ldk_for(int64_t n) { return (n + 31) / 32 * 32; }
+
+size_t dense_ah_tc_scratch(int64_t n, int k) { return sizeof(float) * 2 * (size_t)np_for(k) * ldk_for(n) + 1024; }
+
+template <int NP>
+static bool launch_tc_t(const float* A, int64_t lda, int64_t n, const float* X, int64_t ldx, int k, float* Y,
+                        int64_t ldy, void* scratch, const int32_t* status, cudaStream_t st) {
+  const int64_t ldk = ldk_for(n);
+  float* hiT = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(scratch) + 255) & ~uintptr_t(255));
+  float* loT = hiT + (size_t)NP * ldk;
+  CUtensorMap mA, mH, mL;
+  if (!make_map(&mA, A, (uint64_t)n, (uint64_t)n, (uint64_t)lda * 4, TC_BK, TC_BM)) return false;
+  if (!make_map(&mH, hiT, (uint64_t)ldk, (uint64_t)NP, (uint64_t)ldk * 4, TC_BK, NP)) return false;
+  if (!make_map(&mL, loT, (uint64_t)ldk, (uint64_t)NP, (uint64_t)ldk * 4, TC_BK, NP)) return false;
+  split_transpose<<<(unsigned)((ldk + 255) / 256), 256, 0, st>>>(X, ldx, n, k, NP, ldk, hiT, loT);
+  cudaMemset2DAsync(Y, sizeof(float) * ldy, 0, sizeof(float) * k, n, st);
+  const int64_t mt = (n + TC_BM - 1) / TC_BM;
+  const int64_t nkb = (n + TC_BK - 1) / TC_BK;
+  int64_t splits = std::max<int64_t>(1, (148 * 4 + mt - 1) / mt);
+  splits = std::min<int64_t>(splits, nkb);
+  const int kps = (int)((nkb + splits - 1) / splits);
+  splits = (nkb + kps - 1) / kps;
+  constexpr size_t STAGE = 2 * TC_BM * TC_BK * 4 + 2 * NP * TC_BK * 4;
+  const size_t smem = 1024 + tc_stages<NP>() * STAGE + (3 * tc_stages<NP>() + 1) * 8 + 16;
+  cudaFuncSetAttribute(tc_gemm_3xtf32<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  tc_gemm_3xtf32<NP><<<dim3((unsigned)mt, (unsigned)splits), TC_THREADS, smem, st>>>(mA, mH, mL, n, kps, nkb, Y, ldy,
+                                                                                     k, status);
+  return true;
+}
+
+bool launch_dense_ah_tc(const float* A, int64_t lda, int64_t n, const float* X, int64_t ldx, int k, float* Y,
+                        int64_t ldy, void* scratch, size_t scratch_bytes, const int32_t* status, cudaStream_t st) {
+  if (lda % 4 != 0 || (reinterpret_cast<uintptr_t>(A) & 15) || k > 96) return false;
+  if (!scratch || scratch_bytes < dense_ah_tc_scratch(n, k)) return false;
+  switch (np_for(k)) {
+    case 16: return launch_tc_t<16>(A, lda, n, X, ldx, k, Y, ldy, scratch, status, st);
+    case 32: return launch_tc_t<32>(A, lda, n, X, ldx, k, Y, ldy, scratch, status, st);
+    case 64: return launch_tc_t<64>(A, lda, n, X, ldx, k, Y, ldy, scratch, status, st);
+    case 80: return launch_tc_t<80>(A, lda, n, X, ldx, k, Y, ldy, scratch, status, st);
+    default: return launch_tc_t<96>(A, lda, n, X, ldx, k, Y, ldy, scratch, status, st);
+  }
 }
 
 }  // namespace symnmf

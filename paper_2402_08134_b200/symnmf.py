@@ -161,6 +161,22 @@ class SamplingPlan:
                 "theta": float(m[0]), "xi": float(m[1])}
 
 
+def plan_from_arrays(uniq_idx, uniq_w, s_D=0, s_R=0, W=0, det_idx=None, draw_idx=None, device="cuda"):
+    """A SamplingPlan holding caller-given index sets and weights (e.g. a replayed plan)."""
+    uniq_idx = np.asarray(uniq_idx, dtype=np.int32)
+    nu = uniq_idx.size
+    det = np.asarray(det_idx if det_idx is not None else [], dtype=np.int32)
+    drw = np.asarray(draw_idx if draw_idx is not None else [], dtype=np.int32)
+    cap = max(nu, det.size, 1)
+    pad = lambda a, m, dt: torch.from_numpy(np.concatenate([a, np.zeros(m - a.size, dtype=dt)])).to(device)
+    W = int(W)
+    return SamplingPlan(pad(det, cap, np.int32), pad(drw, max(drw.size, 1), np.int32), pad(uniq_idx, cap, np.int32),
+                        pad(np.asarray(uniq_w, dtype=np.float64), cap, np.float64),
+                        torch.tensor([s_D, s_R, nu, W - (1 << 64) if W >= (1 << 63) else W], dtype=torch.int64,
+                                     device=device),
+                        torch.zeros(2, dtype=torch.float64, device=device), cap)
+
+
 def new_plan(n: int, s: int, cap=None, device="cuda") -> SamplingPlan:
     cap = int(cap or n)
     return SamplingPlan(torch.empty(cap, dtype=torch.int32, device=device),

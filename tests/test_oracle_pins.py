@@ -330,6 +330,10 @@ def test_fast_residual_identity():
     assert abs(O.residual_fast(A, W, H) - direct) < 1e-12
     assert abs(O.residual(A, H) - np.linalg.norm(A - H @ H.T) / np.linalg.norm(A)) < 1e-13
     assert O.residual(H @ H.T, H) < 1e-15
+    B = make_input("c2", n_override=1600)["A"]                         # sparse path (trace identity) = direct
+    Hb = r.random((1600, 4)) * 0.05
+    direct = np.linalg.norm(B.to_dense().astype(np.float64) - Hb @ Hb.T) / np.linalg.norm(B.to_dense())
+    assert abs(O.residual(B, Hb) - direct) < 1e-12
 
 
 def test_planted_recovery_exact_and_lvs():
