@@ -332,7 +332,8 @@ def test_fast_residual_identity():
     assert O.residual(H @ H.T, H) < 1e-15
     B = make_input("c2", n_override=1600)["A"]                         # sparse path (trace identity) = direct
     Hb = r.random((1600, 4)) * 0.05
-    direct = np.linalg.norm(B.to_dense().astype(np.float64) - Hb @ Hb.T) / np.linalg.norm(B.to_dense())
+    Bd = B.to_dense().astype(np.float64)
+    direct = np.linalg.norm(Bd - Hb @ Hb.T) / np.linalg.norm(Bd)
     assert abs(O.residual(B, Hb) - direct) < 1e-12
 
 
