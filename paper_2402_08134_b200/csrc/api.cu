@@ -402,6 +402,10 @@ struct symnmf_solver {
   // workspace carve
   int32_t* status;
   int32_t* iter_dev;
+  unsigned int* counter;   // last-CTA counter of the fused kernels (kept zero between launches)
+  double* Gacc;            // zeroed fp64 Gram accumulator of the fused kernels
+  double* Gbuf[2];         // Gbuf[side]: F^T F of the fixed factor of half `side`
+  float* AHres;            // A H for the residual (CSR), separate from the sampled Y
   int ggrid, rgrid;
   double *G, *Gs, *gpart;
   float* Rinv32;
@@ -427,6 +431,11 @@ void solver_layout(symnmf_solver& S, Carver& c) {
   const int k = S.k, kp = kpad(k);
   S.status = reinterpret_cast<int32_t*>(c.base);   // header
   S.iter_dev = c.take<int32_t>(4);
+  S.counter = c.take<unsigned int>(4);
+  S.Gacc = c.take<double>((size_t)kGramReplicas * k * k);
+  S.Gbuf[0] = c.take<double>((size_t)k * k);
+  S.Gbuf[1] = c.take<double>((size_t)k * k);
+  S.AHres = c.take<float>((S.with_resid && S.hasA && S.A.kind == SYMNMF_CSR) ? (size_t)n * k : 0);
   S.ggrid = gram_grid(n);
   S.G = c.take<double>((size_t)k * k);
   S.Gs = c.take<double>((size_t)k * k);
@@ -439,7 +448,7 @@ void solver_layout(symnmf_solver& S, Carver& c) {
   S.rpart = c.take<double>((size_t)2 * S.rgrid);
   S.rout = c.take<double>(4);
   if (S.mode == SYMNMF_LVS) {
-    S.Rinv32 = c.take<float>((size_t)kp * kp);
+    S.Rinv32 = c.take<float>((size_t)kp * kp + kp);   // R (upper) | 1 / diag(R)
     S.lev = c.take<float>(n);
     sampler_layout(c, n, &S.sw);
     S.plan.cap = n;
@@ -465,30 +474,37 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
   float* F = side == 0 ? S.H : S.W;   // W-half: H fixed (Alg. LvS-SymNMF)
   float* X = side == 0 ? S.W : S.H;   // H-half: W fixed (lines 690-696)
   int32_t* status = S.status;
-  enqueue_gram(F, n, k, S.gpart, S.ggrid, S.G, status, st);
+  // F^T F of the fixed factor was produced by the previous sweep (fused Gram of its output),
+  // or at solver creation for the first half; the sweep below produces X^T X for the next half.
+  const double* Gf = S.Gbuf[side];
+  double* Gnext = S.Gbuf[side ^ 1];
+  const bool lvs = S.mode == SYMNMF_LVS;
   if (S.mode == SYMNMF_EXACT) {
     if (!enqueue_product(S.A, F, k, S.Y, S.precision, S.tcs, S.tcs_bytes, status, st)) return false;
-    launch_hals_sweep(S.G, S.Y, F, X, n, k, S.alpha, status, st);
-  } else if (S.mode == SYMNMF_LVS) {
-    const int kp = kpad(k);
-    launch_chol_inv(S.G, k, S.Rinv32, kp, kp, nullptr, 0, status, st);
-    launch_leverage(F, n, k, S.Rinv32, S.lev, status, st);
-    launch_hybrid_sample(S.lev, n, k, S.s, S.T, S.seed, S.iter_dev, 0, (uint32_t)side, S.plan, S.sw, status, st);
-    launch_cross_gram(F, k, k, F, k, k, true, S.plan.cap, S.plan.counts + 2, S.plan.uniq_idx, S.plan.uniq_w, S.gpart,
-                      S.ggrid, S.Gs, k, status, st);
+    launch_sweep_fused(Gf, S.alpha, S.Y, F, X, n, k, false, S.Gacc, Gnext, nullptr, S.counter, status, st);
+  } else if (lvs) {
+    // scores of F from R^{-1} (computed with F^T F) fused with sampler pass S1/S2
+    launch_leverage_fused(F, n, k, S.Rinv32, S.lev, S.T, S.sw, S.s, S.plan, S.counter, status, st);
+    launch_samp_prefix(S.lev, n, S.T, S.sw, S.plan, status, st);
+    launch_samp_draws(S.sw, n, S.s, S.seed, S.iter_dev, 0, (uint32_t)side, S.plan, status, st);
+    launch_uniq_count_fused(S.lev, n, S.T, S.sw, S.plan, S.iter_dev, S.first_iter, S.max_iters, side, S.stats,
+                            S.counter, status, st);
+    launch_samp_uniq_write(S.lev, n, S.T, S.sw, S.plan, status, st);
+    launch_sampled_gram_fused(F, k, S.plan, S.Gacc, S.Gs, S.counter, status, st);
     if (S.A.kind == SYMNMF_CSR)
-      launch_sampled_csr(S.A, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap, S.Y, status, st);
+      launch_sampled_csr_nozero(S.A, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap, S.Y,
+                                status, st);
     else
       launch_sampled_dense(S.A.val, S.A.lda, n, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap,
                            S.Y, status, st);
-    launch_hals_sweep(S.Gs, S.Y, F, X, n, k, S.alpha, status, st);
-    record_stats<<<1, 1, 0, st>>>(S.iter_dev, S.first_iter, S.max_iters, side, S.plan.counts, S.plan.mass, S.stats);
+    // Update(G_s + alpha I, Y_s + alpha F^T); Y re-zeroed for the next scatter; X^T X and its R^{-1}
+    launch_sweep_fused(S.Gs, S.alpha, S.Y, F, X, n, k, true, S.Gacc, Gnext, S.Rinv32, S.counter, status, st);
   } else {
     launch_cross_gram(S.U, S.l, S.l, F, k, k, false, n, nullptr, nullptr, nullptr, S.Zpart, S.ggrid, S.Z, k, status,
                       st);
     launch_scale_rows(S.Z, S.l, k, S.lam, S.M32, status, st);
     launch_rowapply32(S.U, S.l, n, S.l, S.M32, k, S.Y, k, status, st);
-    launch_hals_sweep(S.G, S.Y, F, X, n, k, S.alpha, status, st);
+    launch_sweep_fused(Gf, S.alpha, S.Y, F, X, n, k, false, S.Gacc, Gnext, nullptr, S.counter, status, st);
   }
   return true;
 }
@@ -496,11 +512,9 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
 bool enqueue_iteration(symnmf_solver& S, cudaStream_t st) {
   if (!enqueue_half(S, 0, st) || !enqueue_half(S, 1, st)) return false;
   if (S.with_resid) {
-    if (S.A.kind == SYMNMF_CSR) {
-      launch_spmm_csr(S.A, S.H, S.k, S.Y, S.status, st);
-      enqueue_gram(S.H, S.n, S.k, S.gpart, S.ggrid, S.GH, S.status, st);
-    }
-    launch_residual(S.A, S.H, S.k, S.Y, S.GH, S.rpart, S.rgrid, S.rout, S.status, st);
+    if (S.A.kind == SYMNMF_CSR) launch_spmm_csr(S.A, S.H, S.k, S.AHres, S.status, st);
+    // Gbuf[0] now holds H^T H of the updated H (fused Gram of the H-half sweep)
+    launch_residual(S.A, S.H, S.k, S.AHres, S.Gbuf[0], S.rpart, S.rgrid, S.rout, S.status, st);
     record_resid<<<1, 1, 0, st>>>(S.iter_dev, S.first_iter, S.max_iters, S.rout, S.resid);
   }
   bump_iter<<<1, 1, 0, st>>>(S.iter_dev);
@@ -544,7 +558,13 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
   if (mode == SYMNMF_LVS) SYMNMF_CUDA_TRY(cudaMemsetAsync(S.sw.cnt, 0, sizeof(int32_t) * n, st));
   SYMNMF_CUDA_TRY(cudaMemsetAsync(S.stats, 0, sizeof(symnmf_half_stats) * 2 * max_iters, st));
   SYMNMF_CUDA_TRY(cudaMemsetAsync(S.resid, 0, sizeof(double) * max_iters, st));
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(S.counter, 0, sizeof(unsigned int) * 4, st));
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Gacc, 0, sizeof(double) * kGramReplicas * k * k, st));
+  if (mode == SYMNMF_LVS) SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Y, 0, sizeof(float) * n * k, st));
   set_i32<<<1, 1, 0, st>>>(S.iter_dev, first_iter);
+  // H^T H (and its CholeskyQR factor for LvS) for the first W-half; later halves get
+  // theirs from the fused Gram of the preceding sweep.
+  launch_gram_fused(H, n, k, S.Gacc, S.Gbuf[0], mode == SYMNMF_LVS ? S.Rinv32 : nullptr, S.counter, S.status, st);
   if (finish() != SYMNMF_OK) return SYMNMF_ERR_CUDA;
   // Capture one iteration on a private stream (the caller's may be the legacy default stream).
   cudaStream_t cs;

@@ -10,6 +10,7 @@
 namespace symnmf {
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
 
 constexpr int kMaxK = 64;       // factor width supported by every kernel
 constexpr int kMaxL = 96;       // range-finder sketch width (Jacobi smem bound)

@@ -1,0 +1,748 @@
+// Fused kernels of the per-iteration hot loop (solver path):
+//
+//  gram_fused       G = F^T F (+ CholeskyQR factor R^{-1}) in ONE launch: per-CTA 4x4
+//                   register-blocked partial Grams, fp64 red.add into a global accumulator,
+//                   the last CTA to finish copies G out, re-zeroes the accumulator and (if
+//                   asked) runs the one-warp fp64 Cholesky + triangular inverse.
+//  sweep_fused      the HALS sweep (Eq. 2.6) of 256-row tiles staged with
+//                   vectorised loads, fused with the Gram of the UPDATED factor (the next
+//                   half's F^T F, P:420 / P:690) and its Cholesky in the last CTA; in LvS
+//                   mode it also re-zeroes Y for the next sampled scatter.
+//  leverage_fused   scores l_i = ||f_i R^{-1}||^2 fused with pass S1 of the
+//                   sampler (integer mass / I_D counts per 1024-row block) and, in the last
+//                   CTA, the block scan S2 (W, s_D, s_R, theta, xi, Z1-Z3).
+//  uniq_count_fused pass S5 + block scan S6 of the plan compaction, and the per-half
+//                   statistics record (s_D, s_R, |U|, theta).
+//  sampled_gram_fused  G_s = sum_{i in U} omega_i f_i^T f_i over the compact plan.
+// The "last CTA" pattern uses a per-call-site counter in the workspace that the last CTA
+// resets, so the kernels are CUDA-graph replay safe.
+#include "kernels.cuh"
+
+
+namespace symnmf {
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ bool arrive_last(unsigned int* counter) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x * gridDim.y - 1;
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    if (threadIdx.x == 0) *counter = 0;
+  }
+  return last;
+}
+
+// One warp: fp64 Cholesky a = R^T R (upper, in place, ld = k + 1) of G + jitter I with one
+// retry, then x = R^{-1}.  Returns nonzero on failure.
+__device__ int warp_chol_inv(double* a, double* x, const double* G, int k, double shift_rel, bool inverse = true) {
+  const int lane = threadIdx.x & 31, ld = k + 1;
+  // G -> shared memory once (independent loads), trace from shared memory
+  for (int e = lane; e < k * k; e += 32) {
+    const int i = e / k, c = e - i * k;
+    x[i * ld + c] = G[e];
+  }
+  __syncwarp();
+  double tr = 0.0;
+  for (int i = 0; i < k; ++i) tr += x[i * ld + i];
+  int fail = 1;
+  for (int attempt = 0; attempt < 2 && fail; ++attempt) {
+    double jitter = shift_rel * tr + (attempt ? 1e-12 * tr / k : 0.0);
+    if (attempt && !(jitter > 0.0)) break;
+    for (int e = lane; e < k * ld; e += 32) {
+      const int i = e / ld, c = e - i * ld;
+      if (c < k) a[e] = x[e] + (i == c ? jitter : 0.0);
+    }
+    __syncwarp();
+    fail = 0;
+    for (int j = 0; j < k; ++j) {
+      const double d = a[j * ld + j];
+      if (!(d > 0.0) || !isfinite(d)) { fail = 1; break; }
+      const double r = sqrt(d), rinv = 1.0 / r;
+      __syncwarp();
+      for (int c = j + 1 + lane; c < k; c += 32) a[j * ld + c] *= rinv;
+      if (lane == 0) a[j * ld + j] = r;
+      __syncwarp();
+      for (int i = j + 1 + lane; i < k; i += 32) {      // lane-parallel rows of the trailing update
+        const double aji = a[j * ld + i];
+        for (int c = i; c < k; ++c) a[i * ld + c] = fma(-aji, a[j * ld + c], a[i * ld + c]);
+      }
+      __syncwarp();
+    }
+    __syncwarp();
+  }
+  if (fail) return 1;
+  if (!inverse) return 0;
+  for (int c = lane; c < k; c += 32) {
+    x[c * ld + c] = 1.0 / a[c * ld + c];
+    for (int i = c - 1; i >= 0; --i) {
+      double s = 0.0;
+      for (int j = i + 1; j <= c; ++j) s = fma(a[i * ld + j], x[j * ld + c], s);
+      x[i * ld + c] = -s / a[i * ld + i];
+    }
+    for (int i = c + 1; i < k; ++i) x[i * ld + c] = 0.0;
+  }
+  __syncwarp();
+  return 0;
+}
+
+// 1/sqrt(d) in fp64 without the long-latency fp64 sqrt and divide sequences: fp32 MUFU
+// estimate refined by two Newton steps (relative error ~1e-16 for normal d).
+__device__ __forceinline__ double rsqrt_fp64(double d) {
+  if (!(d > 1e-30 && d < 1e30)) return 1.0 / sqrt(d);   // outside the fp32 estimate's safe range
+  double y = (double)rsqrtf((float)d);
+  const double h = 0.5 * d;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+
+// One warp, k <= KP <= 32: fp64 Cholesky G + jitter I = R^T R held in registers, lane c owning
+// column c (R[i][c], i <= c).  Step j broadcasts R[j][i] from lane i with compile-time shuffle
+// sources, so there is no shared memory traffic and no barrier.  Padding columns c >= k carry
+// the identity.  Writes R (fp32, KP x KP upper, zero padded) and rd = 1 / diag(R).
+template <int KP>
+__device__ int warp_chol_col(const double* G, int k, double shift_rel, float* R32, float* rd32) {
+  static_assert(KP <= 32, "one column per lane");
+  const int lane = threadIdx.x & 31;
+  double a[KP], b[KP];
+#pragma unroll
+  for (int i = 0; i < KP; ++i) a[i] = (lane < k && i < k) ? G[i * k + lane] : (i == lane ? 1.0 : 0.0);
+  double dl = 0.0;
+#pragma unroll
+  for (int i = 0; i < KP; ++i)
+    if (i == lane) dl = a[i];
+  const double tr = warp_sum(lane < k ? dl : 0.0);
+  int fail = 1;
+  double myr = 1.0;
+  for (int attempt = 0; attempt < 2 && fail; ++attempt) {
+    const double jitter = shift_rel * tr + (attempt ? 1e-12 * tr / k : 0.0);
+    if (attempt && !(jitter > 0.0)) break;
+#pragma unroll
+    for (int i = 0; i < KP; ++i) b[i] = a[i] + ((i == lane && lane < k) ? jitter : 0.0);
+    fail = 0;
+#pragma unroll
+    for (int j = 0; j < KP; ++j) {
+      const double d = __shfl_sync(0xffffffffu, b[j], j);
+      if (!(d > 0.0) || !isfinite(d)) { fail = 1; break; }
+      const double rinv = rsqrt_fp64(d), r = d * rinv;
+      if (lane == j) { b[j] = r; myr = r; }
+      else if (lane > j) b[j] *= rinv;                    // R[j][lane]
+#pragma unroll
+      for (int i = j + 1; i < KP; ++i) {
+        const double rji = __shfl_sync(0xffffffffu, b[j], i);   // R[j][i] from lane i
+        if (lane >= i) b[i] = fma(-rji, b[j], b[i]);            // A[i][lane] -= R[j][i] R[j][lane]
+      }
+    }
+  }
+  if (fail) return 1;
+  if (lane < KP) {
+#pragma unroll
+    for (int i = 0; i < KP; ++i) R32[i * KP + lane] = (i <= lane && lane < k) ? (float)b[i] : 0.f;
+    rd32[lane] = lane < k ? (float)(1.0 / myr) : 0.f;
+  }
+  return 0;
+}
+
+// Per-thread share of a k x k Gram accumulated from row tiles in shared memory:
+// one upper 4x4 block (ai <= bi) per thread, row groups g = t / pairs.
+struct GramThread {
+  int ai, bi, g, RG, p;
+  bool active;
+  float acc[16];
+  double acc64[16];
+  int since;
+  __device__ void init(int t, int nthreads, int nb) {
+    const int pairs = nb * (nb + 1) / 2;
+    RG = nthreads / pairs;
+    g = t / pairs;
+    p = t - g * pairs;
+    active = g < RG;
+    int a = 0, rem = p;
+    while (rem >= nb - a) { rem -= nb - a; ++a; }
+    ai = a; bi = a + rem;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) { acc[e] = 0.f; acc64[e] = 0.0; }
+    since = 0;
+  }
+  // rows r of s (row stride `stride` floats, 16B aligned), optional fp32 row weights w
+  __device__ void accumulate(const float* s, int stride, int rows, const float* w) {
+    if (!active) return;
+    for (int r = g; r < rows; r += RG) {
+      const float4 a4 = *reinterpret_cast<const float4*>(s + r * stride + 4 * ai);
+      const float4 b4 = *reinterpret_cast<const float4*>(s + r * stride + 4 * bi);
+      const float wr = w ? w[r] : 1.f;
+      const float a[4] = {a4.x * wr, a4.y * wr, a4.z * wr, a4.w * wr};
+      const float b[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i * 4 + j] = fmaf(a[i], b[j], acc[i * 4 + j]);
+    }
+    since += (rows + RG - 1) / RG;
+    if (since >= 64) flush();
+  }
+  __device__ void flush() {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) { acc64[e] += (double)acc[e]; acc[e] = 0.f; }
+    since = 0;
+  }
+  // CTA-cooperative commit: reduce the row groups in shared memory (fixed order), then one
+  // fp64 red.add per Gram entry and CTA into replica blockIdx % kGramReplicas of the global
+  // accumulator (k x k upper triangle per replica): bounded same-address contention.
+  // `red` needs RG * pairs * 16 doubles (<= 32 KB); all threads of the CTA must call.
+  __device__ void commit(double* Gacc, int k, double* red) {
+    flush();
+    const int nb = (k + 3) >> 2, pairs = nb * (nb + 1) / 2, P16 = pairs * 16;
+    __syncthreads();
+    if (active) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) red[g * P16 + p * 16 + e] = acc64[e];
+    }
+    __syncthreads();
+    double* rep = Gacc + (size_t)(blockIdx.x % kGramReplicas) * k * k;
+    for (int idx = threadIdx.x; idx < P16; idx += blockDim.x) {
+      double s = 0.0;
+      for (int gg = 0; gg < RG; ++gg) s += red[gg * P16 + idx];
+      const int pp = idx >> 4, i = (idx >> 2) & 3, j = idx & 3;
+      int a0 = 0, rem = pp;
+      while (rem >= nb - a0) { rem -= nb - a0; ++a0; }
+      const int a = 4 * a0 + i, b = 4 * (a0 + rem) + j;
+      if (a < k && b < k && a <= b && s != 0.0) atomicAdd(rep + a * k + b, s);
+    }
+  }
+};
+
+// Last CTA: G_out (mirrored, fp64) <- sum of the accumulator replicas, replicas <- 0;
+// optional Cholesky -> R^{-1} fp32 (KP x KP).
+// Rf32 (nullable): CholeskyQR factor of G, R upper (KP x KP fp32) followed by 1 / diag(R) (KP).
+template <int KP>
+__device__ void finalize_gram(double* Gacc, double* Gout, int k, float* Rf32, double* sm_a, double* sm_x,
+                              int32_t* status) {
+  const int kk = k * k;
+  for (int e = threadIdx.x; e < kk; e += blockDim.x) {
+    const int a = e / k, b = e - a * k;
+    if (a > b) continue;
+    double v[kGramReplicas];
+#pragma unroll
+    for (int r = 0; r < kGramReplicas; ++r) v[r] = __ldcg(Gacc + (size_t)r * kk + e);
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < kGramReplicas; ++r) s += v[r];
+    Gout[a * k + b] = s;
+    Gout[b * k + a] = s;
+#pragma unroll
+    for (int r = 0; r < kGramReplicas; ++r) Gacc[(size_t)r * kk + e] = 0.0;
+  }
+  __syncthreads();
+  if (!Rf32) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int fail;
+    if constexpr (KP <= 32) {
+      fail = warp_chol_col<KP>(Gout, k, 0.0, Rf32, Rf32 + KP * KP);
+    } else {
+      fail = warp_chol_inv(sm_a, sm_x, Gout, k, 0.0, /*inverse=*/false);
+      if (!fail) {
+        for (int e = threadIdx.x; e < KP * KP; e += 32) {
+          const int i = e / KP, c = e - i * KP;
+          Rf32[e] = (i <= c && c < k) ? (float)sm_a[i * (k + 1) + c] : 0.f;
+        }
+        for (int c = threadIdx.x; c < KP; c += 32) Rf32[KP * KP + c] = c < k ? (float)(1.0 / sm_a[c * (k + 1) + c]) : 0.f;
+      }
+    }
+    if (fail && threadIdx.x == 0) dev_fail(status, SYMNMF_ERR_NOT_PD);
+  }
+}
+
+// ---------------------------------------------------------------- gram_fused
+constexpr int FT = 256;         // threads per CTA
+constexpr size_t kRedBytes = sizeof(double) * 256 * 16;   // commit reduction scratch
+constexpr int FROWS = 256;      // rows per staged tile
+
+template <int KP>
+__global__ void __launch_bounds__(FT) gram_fused(const float* __restrict__ F, int64_t n, int k, double* Gacc,
+                                                 double* Gout, float* Rinv32, unsigned int* counter,
+                                                 int32_t* status) {
+  constexpr int ST = KP + 4;
+  extern __shared__ __align__(16) unsigned char smf[];
+  float* s = reinterpret_cast<float*>(smf);
+  if (dev_failed(status)) return;
+  GramThread gt;
+  gt.init(threadIdx.x, FT, (k + 3) / 4);
+  const int64_t tiles = (n + FROWS - 1) / FROWS;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int64_t r0 = t * FROWS;
+    const int rows = (int)min64(FROWS, n - r0);
+    __syncthreads();
+    if (k == KP) {
+      const float4* src = reinterpret_cast<const float4*>(F + r0 * k);
+      constexpr int Q = FROWS * KP / 4 / FT;   // float4 per thread
+      float4 v[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int e = threadIdx.x + q * FT;
+        v[q] = (e < rows * (KP / 4)) ? __ldg(src + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int e = threadIdx.x + q * FT, r = e / (KP / 4), c = e - r * (KP / 4);
+        *reinterpret_cast<float4*>(s + r * ST + 4 * c) = v[q];
+      }
+    } else {
+      for (int e = threadIdx.x; e < FROWS * KP; e += FT) {
+        const int r = e / KP, c = e - r * KP;
+        s[r * ST + c] = (r < rows && c < k) ? F[(r0 + r) * k + c] : 0.f;
+      }
+    }
+    __syncthreads();
+    gt.accumulate(s, ST, rows, nullptr);
+  }
+  gt.commit(Gacc, k, reinterpret_cast<double*>(smf));
+  if (arrive_last(counter)) {
+    double* sa = reinterpret_cast<double*>(smf);
+    finalize_gram<KP>(Gacc, Gout, k, Rinv32, sa, sa + k * (k + 1), status);
+  }
+}
+
+// ---------------------------------------------------------------- sweep_fused
+template <int KP>
+__global__ void __launch_bounds__(FT) sweep_fused(const double* __restrict__ G, double alpha, float* __restrict__ Y,
+                                                  const float* __restrict__ F, float* __restrict__ X, int64_t n, int k,
+                                                  int zeroY, double* Gacc, double* Gout, float* Rinv32,
+                                                  unsigned int* counter, int32_t* status) {
+  constexpr int ST = KP + 4;
+  constexpr int Q = KP / 4;       // float4 per lane per array (32-row warp tile)
+  __shared__ __align__(16) float sG[KP * KP];     // sG[i*KP + j] = G[j][i], 0 on the diagonal
+  __shared__ float sInv[KP];
+  __shared__ int sOk[KP];
+  extern __shared__ __align__(16) unsigned char smw[];
+  float* sX = reinterpret_cast<float*>(smw);        // [256][ST] updated rows (tile)
+  float* sB = sX + FROWS * ST;                       // [256][ST] Y + alpha F
+  if (dev_failed(status)) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int e = tid; e < KP * KP; e += FT) {
+    const int i = e / KP, j = e - i * KP;
+    sG[e] = (i < k && j < k && i != j) ? (float)G[j * k + i] : 0.f;
+  }
+  for (int i = tid; i < KP; i += FT) {
+    const double den = i < k ? G[i * k + i] + alpha : 0.0;
+    sOk[i] = den > 0.0;
+    sInv[i] = den > 0.0 ? (float)(1.0 / den) : 0.f;
+  }
+  GramThread gt;
+  gt.init(tid, FT, (k + 3) / 4);
+  const float a32 = (float)alpha;
+  __syncthreads();
+  const int64_t tiles = (n + FROWS - 1) / FROWS;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int64_t r0 = t * FROWS + wid * 32;          // this warp's 32 rows
+    const int cnt = (int)max64(0, min64(32, n - r0));
+    float* wX = sX + wid * 32 * ST;
+    float* wB = sB + wid * 32 * ST;
+    if (k == KP) {
+      const float4* Y4 = reinterpret_cast<const float4*>(Y + r0 * k);
+      const float4* F4 = reinterpret_cast<const float4*>(F + r0 * k);
+      const float4* X4 = reinterpret_cast<const float4*>(X + r0 * k);
+      float4 vy[Q], vf[Q], vx[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int e = lane + 32 * q;
+        const bool ok = e < cnt * Q;
+        vy[q] = ok ? __ldcs(Y4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+        vf[q] = ok ? __ldg(F4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+        vx[q] = ok ? X4[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int e = lane + 32 * q, r = e / Q, c = e - r * Q;
+        float4 b;
+        b.x = fmaf(a32, vf[q].x, vy[q].x); b.y = fmaf(a32, vf[q].y, vy[q].y);
+        b.z = fmaf(a32, vf[q].z, vy[q].z); b.w = fmaf(a32, vf[q].w, vy[q].w);
+        *reinterpret_cast<float4*>(wB + r * ST + 4 * c) = b;
+        *reinterpret_cast<float4*>(wX + r * ST + 4 * c) = vx[q];
+      }
+    } else {
+      for (int e = lane; e < 32 * KP; e += 32) {
+        const int r = e / KP, c = e - r * KP;
+        const bool ok = r < cnt && c < k;
+        const int64_t gidx = (r0 + r) * k + c;
+        wB[r * ST + c] = ok ? fmaf(a32, F[gidx], Y[gidx]) : 0.f;
+        wX[r * ST + c] = ok ? X[gidx] : 0.f;
+      }
+    }
+    __syncwarp();
+    if (lane < cnt) {
+      float x[KP], b[KP];
+#pragma unroll
+      for (int j = 0; j < KP; j += 4) {
+        const float4 xv = *reinterpret_cast<const float4*>(wX + lane * ST + j);
+        const float4 bv = *reinterpret_cast<const float4*>(wB + lane * ST + j);
+        x[j] = xv.x; x[j + 1] = xv.y; x[j + 2] = xv.z; x[j + 3] = xv.w;
+        b[j] = bv.x; b[j + 1] = bv.y; b[j + 2] = bv.z; b[j + 3] = bv.w;
+      }
+#pragma unroll
+      for (int i = 0; i < KP; ++i) {
+        if (i < k) {
+          // four independent partial sums: the column update is a short dependency chain
+          float s0 = b[i], s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+          for (int j = 0; j < KP; j += 4) {
+            const float4 g = *reinterpret_cast<const float4*>(sG + i * KP + j);
+            s0 = fmaf(-x[j], g.x, s0);
+            s1 = fmaf(-x[j + 1], g.y, s1);
+            s2 = fmaf(-x[j + 2], g.z, s2);
+            s3 = fmaf(-x[j + 3], g.w, s3);
+          }
+          const float s = (s0 + s1) + (s2 + s3);
+          if (sOk[i]) x[i] = fmaxf(0.f, s * sInv[i]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < KP; j += 4)
+        *reinterpret_cast<float4*>(wX + lane * ST + j) = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < KP; j += 4)
+        *reinterpret_cast<float4*>(wX + lane * ST + j) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncwarp();
+    if (k == KP) {
+      float4* X4 = reinterpret_cast<float4*>(X + r0 * k);
+      float4* Y4 = reinterpret_cast<float4*>(Y + r0 * k);
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int e = lane + 32 * q, r = e / Q, c = e - r * Q;
+        if (e < cnt * Q) {
+          X4[e] = *reinterpret_cast<const float4*>(wX + r * ST + 4 * c);
+          if (zeroY) __stcs(Y4 + e, make_float4(0.f, 0.f, 0.f, 0.f));
+        }
+      }
+    } else {
+      for (int e = lane; e < cnt * k; e += 32) {
+        const int r = e / k, c = e - r * k;
+        X[(r0 + r) * k + c] = wX[r * ST + c];
+        if (zeroY) Y[(r0 + r) * k + c] = 0.f;
+      }
+    }
+    __syncthreads();
+    if (Gacc) gt.accumulate(sX, ST, (int)min64(FROWS, n - t * FROWS), nullptr);
+    __syncthreads();
+  }
+  if (!Gacc) return;
+  gt.commit(Gacc, k, reinterpret_cast<double*>(smw));
+  if (arrive_last(counter)) {
+    double* sa = reinterpret_cast<double*>(smw);
+    finalize_gram<KP>(Gacc, Gout, k, Rinv32, sa, sa + k * (k + 1), status);
+  }
+}
+
+// ---------------------------------------------------------------- leverage_fused (+ S1, S2)
+constexpr double kTwo40f = 1099511627776.0;
+
+template <int KP>
+__global__ void __launch_bounds__(FT) leverage_fused(const float* __restrict__ F, int64_t n, int k,
+                                                     const float* __restrict__ Rinv, float* __restrict__ lev,
+                                                     double T, uint64_t* __restrict__ bw, uint32_t* __restrict__ bd,
+                                                     double* __restrict__ bt, int64_t s, int64_t cap,
+                                                     int64_t* __restrict__ counts, double* __restrict__ mass,
+                                                     unsigned int* counter, int32_t* status) {
+  constexpr int ST = KP + 4;
+  __shared__ __align__(16) float sR[KP * KP];
+  __shared__ float sRd[KP];
+  __shared__ uint64_t shw[33];
+  __shared__ uint32_t shd[33];
+  __shared__ double sht[33];
+  extern __shared__ __align__(16) unsigned char sml[];
+  float* sF = reinterpret_cast<float*>(sml);          // [256][ST]
+  if (dev_failed(status)) return;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < KP * KP + KP; e += FT) {   // Rf = [R (KP x KP upper) | 1 / diag(R)]
+    if (e < KP * KP) sR[e] = Rinv[e]; else sRd[e - KP * KP] = Rinv[e];
+  }
+  const int64_t b = blockIdx.x;                       // sampler block: rows [1024 b, 1024 b + 1024)
+  uint64_t sw = 0;
+  uint32_t sd = 0;
+  double stt = 0.0;
+  constexpr int Q = FROWS * KP / 4 / FT;   // float4 per thread per 256-row sub-tile
+  float4 v[Q];                              // next sub-tile, loaded while the current one computes
+  auto load_sub = [&](int sub) {
+    const int64_t r0 = b * kSampBlock + sub * FROWS;
+    const int rows = (int)max64(0, min64(FROWS, n - r0));
+    const float4* src = reinterpret_cast<const float4*>(F + r0 * k);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int e = tid + q * FT;
+      v[q] = (e < rows * (KP / 4)) ? __ldg(src + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  if (k == KP) load_sub(0);
+  for (int sub = 0; sub < kSampBlock / FROWS; ++sub) {
+    const int64_t r0 = b * kSampBlock + sub * FROWS;
+    const int rows = (int)max64(0, min64(FROWS, n - r0));
+    __syncthreads();
+    if (rows > 0) {
+      if (k == KP) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int e = tid + q * FT, r = e / (KP / 4), c = e - r * (KP / 4);
+          *reinterpret_cast<float4*>(sF + r * ST + 4 * c) = v[q];
+        }
+        if (sub + 1 < kSampBlock / FROWS) load_sub(sub + 1);
+      } else {
+        for (int e = tid; e < FROWS * KP; e += FT) {
+          const int r = e / KP, c = e - r * KP;
+          sF[r * ST + c] = (r < rows && c < k) ? F[(r0 + r) * k + c] : 0.f;
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < rows) {
+      float f[KP];
+#pragma unroll
+      for (int a = 0; a < KP; a += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(sF + tid * ST + a);
+        f[a] = v.x; f[a + 1] = v.y; f[a + 2] = v.z; f[a + 3] = v.w;
+      }
+      // q = f R^{-1} by forward substitution q R = f (R upper, rd = 1 / diag R), l = ||q||^2
+      float l = 0.f;
+#pragma unroll
+      for (int a = 0; a < KP; ++a) {
+        const float q = f[a] * sRd[a];
+        l = fmaf(q, q, l);
+#pragma unroll
+        for (int c = a + 1; c < KP; ++c) f[c] = fmaf(-q, sR[a * KP + c], f[c]);
+      }
+      lev[r0 + tid] = l;
+      const double ld = (double)l;
+      const bool det = ld >= T;                                     // reading Z1
+      sw += det ? 0ull : (uint64_t)__double2ull_rd(ld * kTwo40f);  // reading Z6
+      sd += det ? 1u : 0u;
+      stt += det ? ld : 0.0;
+    }
+  }
+  sw = block_sum(sw, shw);
+  sd = block_sum(sd, shd);
+  stt = block_sum(stt, sht);
+  if (tid == 0) { bw[b] = sw; bd[b] = sd; bt[b] = stt; }
+  if (!arrive_last(counter)) return;
+  // S2: exclusive scan of the block sums, totals into the plan
+  const int64_t nb = gridDim.x;
+  uint64_t cw = 0;
+  uint32_t cd = 0;
+  double theta = 0.0;
+  for (int64_t base = 0; base < nb; base += FT) {
+    const int64_t i = base + tid;
+    const uint64_t vw = i < nb ? __ldcg(bw + i) : 0ull;
+    const uint32_t vd = i < nb ? __ldcg(bd + i) : 0u;
+    const double vt = i < nb ? __ldcg(bt + i) : 0.0;
+    uint64_t tw; uint32_t td;
+    const uint64_t ew = block_excl_scan(vw, shw, &tw);
+    const uint32_t ed = block_excl_scan(vd, shd, &td);
+    const double st_ = block_sum(vt, sht);
+    if (i < nb) { bw[i] = cw + ew; bd[i] = cd + ed; }
+    cw += tw; cd += td;
+    theta += st_;
+  }
+  if (tid == 0) {
+    const int64_t sD = (int64_t)cd;
+    const int64_t sR_ = (cw == 0ull) ? 0 : (s > sD ? s - sD : 0);   // reading Z2
+    counts[0] = sD;
+    counts[1] = sR_;
+    counts[3] = (int64_t)cw;
+    mass[0] = theta;
+    mass[1] = (double)k - theta;
+    if (sD > cap) dev_fail(status, SYMNMF_ERR_CAPACITY);
+  }
+}
+
+// ---------------------------------------------------------------- uniq_count_fused (S5 + S6 + stats)
+__global__ void __launch_bounds__(256) uniq_count_fused(const float* __restrict__ lev, int64_t n, double T,
+                                                        const int32_t* __restrict__ cnt, uint32_t* __restrict__ bu,
+                                                        int64_t cap, int64_t* __restrict__ counts,
+                                                        const double* __restrict__ mass, const int32_t* iter_dev,
+                                                        int32_t first_iter, int32_t max_iters, int side,
+                                                        symnmf_half_stats* stats, unsigned int* counter,
+                                                        int32_t* status) {
+  __shared__ uint32_t sh[33];
+  if (dev_failed(status)) return;
+  const int64_t i0 = (int64_t)blockIdx.x * kSampBlock + threadIdx.x * 4;
+  uint32_t c = 0;
+  if (i0 + 3 < n) {
+    const float4 l4 = *reinterpret_cast<const float4*>(lev + i0);
+    const int4 c4 = *reinterpret_cast<const int4*>(cnt + i0);
+    c = ((double)l4.x >= T || c4.x > 0) + ((double)l4.y >= T || c4.y > 0) + ((double)l4.z >= T || c4.z > 0) +
+        ((double)l4.w >= T || c4.w > 0);
+  } else {
+    for (int e = 0; e < 4; ++e)
+      if (i0 + e < n) c += ((double)lev[i0 + e] >= T || cnt[i0 + e] > 0) ? 1u : 0u;
+  }
+  c = block_sum(c, sh);
+  if (threadIdx.x == 0) bu[blockIdx.x] = c;
+  if (!arrive_last(counter)) return;
+  const int64_t nb = gridDim.x;
+  uint32_t run = 0;
+  for (int64_t base = 0; base < nb; base += 256) {
+    const int64_t i = base + threadIdx.x;
+    const uint32_t v = i < nb ? __ldcg(bu + i) : 0u;
+    uint32_t tot;
+    const uint32_t e = block_excl_scan(v, sh, &tot);
+    if (i < nb) bu[i] = run + e;
+    run += tot;
+  }
+  if (threadIdx.x == 0) {
+    counts[2] = (int64_t)run;
+    if ((int64_t)run > cap) dev_fail(status, SYMNMF_ERR_CAPACITY);
+    if (stats) {
+      const int t = *iter_dev - first_iter;
+      if (t >= 0 && t < max_iters) {
+        symnmf_half_stats h;
+        h.s_d = counts[0]; h.s_r = counts[1]; h.n_uniq = (int64_t)run; h.theta = mass[0];
+        stats[2 * t + side] = h;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- sampled_gram_fused
+template <int KP>
+__global__ void __launch_bounds__(FT) sampled_gram_fused(const float* __restrict__ F, int k,
+                                                         const int32_t* __restrict__ uniq,
+                                                         const double* __restrict__ w,
+                                                         const int64_t* __restrict__ n_uniq_dev, double* Gacc,
+                                                         double* Gout, unsigned int* counter, int32_t* status) {
+  constexpr int ST = KP + 4;
+  constexpr int ROWS = 64;
+  __shared__ __align__(16) float s[ROWS * ST];
+  extern __shared__ double red[];   // 32 KB: row-group reduction of the commit
+  __shared__ float sw[ROWS];
+  __shared__ int64_t srow[ROWS];
+  if (dev_failed(status)) return;
+  const int64_t nu = *n_uniq_dev;
+  GramThread gt;
+  gt.init(threadIdx.x, FT, (k + 3) / 4);
+  for (int64_t r0 = (int64_t)blockIdx.x * ROWS; r0 < nu; r0 += (int64_t)gridDim.x * ROWS) {
+    const int rows = (int)min64(ROWS, nu - r0);
+    __syncthreads();
+    if (threadIdx.x < ROWS) {
+      const bool ok = threadIdx.x < rows;
+      srow[threadIdx.x] = ok ? (int64_t)uniq[r0 + threadIdx.x] : 0;
+      sw[threadIdx.x] = ok ? (float)w[r0 + threadIdx.x] : 0.f;
+    }
+    __syncthreads();
+    if (k == KP) {       // gathered rows: one float4 per (row, 4 columns), all loads in flight
+      constexpr int NV = ROWS * KP / 4, Q = (NV + FT - 1) / FT;
+      float4 v[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int e = threadIdx.x + q * FT, r = e / (KP / 4), c = e - r * (KP / 4);
+        v[q] = (e < NV && r < rows) ? __ldg(reinterpret_cast<const float4*>(F + srow[r] * k) + c)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int e = threadIdx.x + q * FT, r = e / (KP / 4), c = e - r * (KP / 4);
+        if (e < NV) *reinterpret_cast<float4*>(s + r * ST + 4 * c) = v[q];
+      }
+    } else {
+      for (int e = threadIdx.x; e < ROWS * KP; e += FT) {
+        const int r = e / KP, c = e - r * KP;
+        s[r * ST + c] = (r < rows && c < k) ? __ldg(F + srow[r] * k + c) : 0.f;
+      }
+    }
+    __syncthreads();
+    gt.accumulate(s, ST, rows, sw);
+  }
+  gt.commit(Gacc, k, red);
+  if (arrive_last(counter)) finalize_gram<KP>(Gacc, Gout, k, nullptr, nullptr, nullptr, status);
+}
+
+// ---------------------------------------------------------------- launchers
+static int fused_grid(int64_t tiles, int per_sm) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * per_sm));
+}
+
+template <int KP>
+static void gram_fused_t(const float* F, int64_t n, int k, double* Gacc, double* Gout, float* Rinv32,
+                         unsigned int* counter, int32_t* status, cudaStream_t st) {
+  const size_t smem = std::max({sizeof(float) * FROWS * (KP + 4), sizeof(double) * 2 * k * (k + 1), kRedBytes});
+  cudaFuncSetAttribute(gram_fused<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  gram_fused<KP><<<fused_grid((n + FROWS - 1) / FROWS, 2), FT, smem, st>>>(F, n, k, Gacc, Gout, Rinv32, counter,
+                                                                            status);
+}
+
+void launch_gram_fused(const float* F, int64_t n, int k, double* Gacc, double* Gout, float* Rinv32,
+                       unsigned int* counter, int32_t* status, cudaStream_t st) {
+  switch (kpad(k)) {
+    case 8: gram_fused_t<8>(F, n, k, Gacc, Gout, Rinv32, counter, status, st); break;
+    case 16: gram_fused_t<16>(F, n, k, Gacc, Gout, Rinv32, counter, status, st); break;
+    case 32: gram_fused_t<32>(F, n, k, Gacc, Gout, Rinv32, counter, status, st); break;
+    default: gram_fused_t<64>(F, n, k, Gacc, Gout, Rinv32, counter, status, st); break;
+  }
+}
+
+template <int KP>
+static void sweep_fused_t(const double* G, double alpha, float* Y, const float* F, float* X, int64_t n, int k,
+                          bool zeroY, double* Gacc, double* Gout, float* Rinv32, unsigned int* counter,
+                          int32_t* status, cudaStream_t st) {
+  const size_t smem = std::max({sizeof(float) * 2 * FROWS * (KP + 4), sizeof(double) * 2 * k * (k + 1), kRedBytes});
+  cudaFuncSetAttribute(sweep_fused<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  sweep_fused<KP><<<fused_grid((n + FROWS - 1) / FROWS, KP <= 32 ? 2 : 1), FT, smem, st>>>(
+      G, alpha, Y, F, X, n, k, zeroY ? 1 : 0, Gacc, Gout, Rinv32, counter, status);
+}
+
+void launch_sweep_fused(const double* G, double alpha, float* Y, const float* F, float* X, int64_t n, int k,
+                        bool zeroY, double* Gacc, double* Gout, float* Rinv32, unsigned int* counter,
+                        int32_t* status, cudaStream_t st) {
+  switch (kpad(k)) {
+    case 8: sweep_fused_t<8>(G, alpha, Y, F, X, n, k, zeroY, Gacc, Gout, Rinv32, counter, status, st); break;
+    case 16: sweep_fused_t<16>(G, alpha, Y, F, X, n, k, zeroY, Gacc, Gout, Rinv32, counter, status, st); break;
+    case 32: sweep_fused_t<32>(G, alpha, Y, F, X, n, k, zeroY, Gacc, Gout, Rinv32, counter, status, st); break;
+    default: sweep_fused_t<64>(G, alpha, Y, F, X, n, k, zeroY, Gacc, Gout, Rinv32, counter, status, st); break;
+  }
+}
+
+template <int KP>
+static void leverage_fused_t(const float* F, int64_t n, int k, const float* Rinv, float* lev, double T,
+                             const SamplerWs& w, int64_t s, const symnmf_plan& plan, unsigned int* counter,
+                             int32_t* status, cudaStream_t st) {
+  const size_t smem = sizeof(float) * FROWS * (KP + 4);
+  cudaFuncSetAttribute(leverage_fused<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  leverage_fused<KP><<<(unsigned)samp_blocks(n), FT, smem, st>>>(F, n, k, Rinv, lev, T, w.bw, w.bd, w.bt, s,
+                                                                 plan.cap, plan.counts, plan.mass, counter, status);
+}
+
+void launch_leverage_fused(const float* F, int64_t n, int k, const float* Rinv, float* lev, double T,
+                           const SamplerWs& w, int64_t s, const symnmf_plan& plan, unsigned int* counter,
+                           int32_t* status, cudaStream_t st) {
+  switch (kpad(k)) {
+    case 8: leverage_fused_t<8>(F, n, k, Rinv, lev, T, w, s, plan, counter, status, st); break;
+    case 16: leverage_fused_t<16>(F, n, k, Rinv, lev, T, w, s, plan, counter, status, st); break;
+    case 32: leverage_fused_t<32>(F, n, k, Rinv, lev, T, w, s, plan, counter, status, st); break;
+    default: leverage_fused_t<64>(F, n, k, Rinv, lev, T, w, s, plan, counter, status, st); break;
+  }
+}
+
+void launch_uniq_count_fused(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
+                             const int32_t* iter_dev, int32_t first_iter, int32_t max_iters, int side,
+                             symnmf_half_stats* stats, unsigned int* counter, int32_t* status, cudaStream_t st) {
+  uniq_count_fused<<<(unsigned)samp_blocks(n), 256, 0, st>>>(lev, n, T, w.cnt, w.bu, plan.cap, plan.counts,
+                                                             plan.mass, iter_dev, first_iter, max_iters, side, stats,
+                                                             counter, status);
+}
+
+void launch_sampled_gram_fused(const float* F, int k, const symnmf_plan& plan, double* Gacc, double* Gout,
+                               unsigned int* counter, int32_t* status, cudaStream_t st) {
+  const int grid = fused_grid((plan.cap + 63) / 64, 1);
+  switch (kpad(k)) {
+    case 8: sampled_gram_fused<8><<<grid, FT, kRedBytes, st>>>(F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
+    case 16: sampled_gram_fused<16><<<grid, FT, kRedBytes, st>>>(F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
+    case 32: sampled_gram_fused<32><<<grid, FT, kRedBytes, st>>>(F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
+    default: sampled_gram_fused<64><<<grid, FT, kRedBytes, st>>>(F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
+  }
+}
+
+}  // namespace symnmf

@@ -72,6 +72,34 @@ void launch_scale_rows(const double* Z, int l, int k, const double* lambda, floa
 void launch_jacobi_evd(double* T, int l, double* V, double* lambda, int32_t* status, cudaStream_t st);
 void launch_symmetrize(double* T, int l, cudaStream_t st);
 
+// ---------------------------------------------------------------- fused.cu (solver hot loop)
+// Gacc: zeroed kGramReplicas x k x k fp64 accumulator (left zeroed); counter: zeroed uint (left zeroed).
+constexpr int kGramReplicas = 16;
+void launch_gram_fused(const float* F, int64_t n, int k, double* Gacc, double* Gout, float* Rinv32,
+                       unsigned int* counter, int32_t* status, cudaStream_t st);
+void launch_sweep_fused(const double* G, double alpha, float* Y, const float* F, float* X, int64_t n, int k,
+                        bool zeroY, double* Gacc, double* Gout, float* Rinv32, unsigned int* counter,
+                        int32_t* status, cudaStream_t st);
+void launch_leverage_fused(const float* F, int64_t n, int k, const float* Rinv, float* lev, double T,
+                           const SamplerWs& w, int64_t s, const symnmf_plan& plan, unsigned int* counter,
+                           int32_t* status, cudaStream_t st);
+void launch_uniq_count_fused(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
+                             const int32_t* iter_dev, int32_t first_iter, int32_t max_iters, int side,
+                             symnmf_half_stats* stats, unsigned int* counter, int32_t* status, cudaStream_t st);
+void launch_sampled_gram_fused(const float* F, int k, const symnmf_plan& plan, double* Gacc, double* Gout,
+                               unsigned int* counter, int32_t* status, cudaStream_t st);
+// sampler.cu passes used by the fused path
+void launch_samp_prefix(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
+                        int32_t* status, cudaStream_t st);
+void launch_samp_draws(const SamplerWs& w, int64_t n, int64_t s, uint64_t seed, const int32_t* iter_dev,
+                       uint32_t iteration, uint32_t side, const symnmf_plan& plan, int32_t* status, cudaStream_t st);
+void launch_samp_uniq_write(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
+                            int32_t* status, cudaStream_t st);
+// sampled CSR scatter into a Y the caller has zeroed
+void launch_sampled_csr_nozero(const symnmf_matrix& A, const float* F, int k, const int32_t* uniq, const double* w,
+                               const int64_t* n_uniq_dev, int64_t cap, float* Y, const int32_t* status,
+                               cudaStream_t st);
+
 // ---------------------------------------------------------------- residual.cu
 void launch_residual(const symnmf_matrix& A, const float* H, int k, const float* AH, const double* G,
                      double* partial, int grid, double* out, const int32_t* status, cudaStream_t st);

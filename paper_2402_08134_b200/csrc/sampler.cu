@@ -141,6 +141,41 @@ __global__ void samp_draws(const uint64_t* __restrict__ P, int64_t n, uint64_t s
   atomicAdd(cnt + lo, 1);
 }
 
+// Same draws; the search first locates the 1024-row block in the exclusive block offsets
+// bw (staged in shared memory), then searches the block's slice of P (10 dependent loads).
+// The index found is the same first i with P_i > t.
+__global__ void samp_draws_2level(const uint64_t* __restrict__ P, const uint64_t* __restrict__ bw, int64_t nb,
+                                  int64_t n, uint64_t seed, const int32_t* __restrict__ iter_dev, uint32_t iteration,
+                                  uint32_t side, const int64_t* __restrict__ counts, int32_t* __restrict__ draw_idx,
+                                  int32_t* __restrict__ cnt, const int32_t* __restrict__ status) {
+  extern __shared__ uint64_t sbw[];
+  if (dev_failed(status)) return;
+  const int64_t sR = counts[1];
+  if ((int64_t)blockIdx.x * blockDim.x >= sR) return;
+  for (int64_t i = threadIdx.x; i < nb; i += blockDim.x) sbw[i] = bw[i];
+  __syncthreads();
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= sR) return;
+  const uint64_t W = (uint64_t)counts[3];
+  const uint32_t it = iter_dev ? (uint32_t)*iter_dev : iteration;
+  const uint4 x = philox4x32_10(make_uint4((uint32_t)j, (uint32_t)((uint64_t)j >> 32), 2u * it + side, 0u),
+                                make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+  const uint64_t u = ((uint64_t)x.y << 32) | (uint64_t)x.x;
+  const uint64_t t = __umul64hi(u, W);
+  int64_t bl = 0, bh = nb - 1;          // largest b with bw[b] <= t (bw[0] = 0 <= t)
+  while (bl < bh) {
+    const int64_t mid = (bl + bh + 1) >> 1;
+    if (sbw[mid] <= t) bl = mid; else bh = mid - 1;
+  }
+  int64_t lo = bl * kSampBlock, hi = min64(n, lo + kSampBlock) - 1;   // P[hi] > t
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (P[mid] > t) hi = mid; else lo = mid + 1;
+  }
+  draw_idx[j] = (int32_t)lo;
+  atomicAdd(cnt + lo, 1);
+}
+
 __global__ void __launch_bounds__(ST) samp_uniq_counts(const float* __restrict__ lev, int64_t n, double T,
                                                        const int32_t* __restrict__ cnt, uint32_t* __restrict__ bu,
                                                        const int32_t* __restrict__ status) {
@@ -220,6 +255,30 @@ __global__ void __launch_bounds__(ST) samp_uniq_write(const float* __restrict__ 
   }
 }
 
+void launch_samp_prefix(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
+                        int32_t* status, cudaStream_t st) {
+  samp_prefix<<<(unsigned)samp_blocks(n), ST, 0, st>>>(lev, n, T, w.bw, w.bd, w.P, plan.det_idx, plan.cap, status);
+}
+
+void launch_samp_draws(const SamplerWs& w, int64_t n, int64_t s, uint64_t seed, const int32_t* iter_dev,
+                       uint32_t iteration, uint32_t side, const symnmf_plan& plan, int32_t* status, cudaStream_t st) {
+  const int64_t dblocks = std::max<int64_t>(1, (s + 255) / 256);
+  const int64_t nb = samp_blocks(n);
+  if (nb <= 6144) {
+    samp_draws_2level<<<(unsigned)dblocks, 256, sizeof(uint64_t) * nb, st>>>(
+        w.P, w.bw, nb, n, seed, iter_dev, iteration, side, plan.counts, plan.draw_idx, w.cnt, status);
+    return;
+  }
+  samp_draws<<<(unsigned)dblocks, 256, 0, st>>>(w.P, n, seed, iter_dev, iteration, side, plan.counts, plan.draw_idx,
+                                                w.cnt, status);
+}
+
+void launch_samp_uniq_write(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
+                            int32_t* status, cudaStream_t st) {
+  samp_uniq_write<<<(unsigned)samp_blocks(n), ST, 0, st>>>(lev, n, T, w.cnt, w.bu, plan.counts, plan.uniq_idx,
+                                                           plan.uniq_w, plan.cap, status);
+}
+
 void launch_hybrid_sample(const float* lev, int64_t n, int k, int64_t s, double T, uint64_t seed,
                           const int32_t* iter_dev, uint32_t iteration, uint32_t side, const symnmf_plan& plan,
                           const SamplerWs& w, int32_t* status, cudaStream_t st) {
@@ -227,9 +286,7 @@ void launch_hybrid_sample(const float* lev, int64_t n, int k, int64_t s, double 
   samp_block_sums<<<(unsigned)nb, ST, 0, st>>>(lev, n, T, w.bw, w.bd, w.bt, status);
   samp_scan_blocks<<<1, 1024, 0, st>>>(nb, w.bw, w.bd, w.bt, s, k, plan.cap, plan.counts, plan.mass, status);
   samp_prefix<<<(unsigned)nb, ST, 0, st>>>(lev, n, T, w.bw, w.bd, w.P, plan.det_idx, plan.cap, status);
-  const int64_t dblocks = std::max<int64_t>(1, (s + 255) / 256);
-  samp_draws<<<(unsigned)dblocks, 256, 0, st>>>(w.P, n, seed, iter_dev, iteration, side, plan.counts, plan.draw_idx,
-                                                w.cnt, status);
+  launch_samp_draws(w, n, s, seed, iter_dev, iteration, side, plan, status, st);
   samp_uniq_counts<<<(unsigned)nb, ST, 0, st>>>(lev, n, T, w.cnt, w.bu, status);
   samp_scan_uniq<<<1, 1024, 0, st>>>(nb, w.bu, plan.cap, plan.counts, status);
   samp_uniq_write<<<(unsigned)nb, ST, 0, st>>>(lev, n, T, w.cnt, w.bu, plan.counts, plan.uniq_idx, plan.uniq_w,

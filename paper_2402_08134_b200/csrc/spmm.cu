@@ -148,6 +148,12 @@ __global__ void __launch_bounds__(256) sampled_csr_scalar(const int64_t* __restr
 void launch_sampled_csr(const symnmf_matrix& A, const float* F, int k, const int32_t* uniq, const double* w,
                         const int64_t* n_uniq_dev, int64_t cap, float* Y, const int32_t* status, cudaStream_t st) {
   cudaMemsetAsync(Y, 0, sizeof(float) * (size_t)A.n * k, st);
+  launch_sampled_csr_nozero(A, F, k, uniq, w, n_uniq_dev, cap, Y, status, st);
+}
+
+void launch_sampled_csr_nozero(const symnmf_matrix& A, const float* F, int k, const int32_t* uniq, const double* w,
+                               const int64_t* n_uniq_dev, int64_t cap, float* Y, const int32_t* status,
+                               cudaStream_t st) {
   const int grid = grid_for(std::max<int64_t>(cap, 1) * 32);
   if (k % 4 == 0) {
     const float4* F4 = reinterpret_cast<const float4*>(F);
