@@ -40,7 +40,11 @@ symnmf_status finish() {
 }
 
 __global__ void set_i32(int32_t* p, int32_t v) { *p = v; }
-__global__ void bump_iter(int32_t* it) { *it += 1; }
+__global__ void bump_iter(int32_t* it) {
+  pdl_trigger();
+  pdl_wait();
+  *it += 1;
+}
 __global__ void record_stats(const int32_t* iter_dev, int32_t first, int32_t max_iters, int side,
                              const int64_t* counts, const double* mass, symnmf_half_stats* stats) {
   const int t = *iter_dev - first;
@@ -51,6 +55,8 @@ __global__ void record_stats(const int32_t* iter_dev, int32_t first, int32_t max
 }
 __global__ void record_resid(const int32_t* iter_dev, int32_t first, int32_t max_iters, const double* rout,
                              double* resid) {
+  pdl_trigger();
+  pdl_wait();
   const int t = *iter_dev - first;
   if (t < 0 || t >= max_iters) return;
   resid[t] = rout[0];
@@ -515,9 +521,9 @@ bool enqueue_iteration(symnmf_solver& S, cudaStream_t st) {
     if (S.A.kind == SYMNMF_CSR) launch_spmm_csr(S.A, S.H, S.k, S.AHres, S.status, st);
     // Gbuf[0] now holds H^T H of the updated H (fused Gram of the H-half sweep)
     launch_residual(S.A, S.H, S.k, S.AHres, S.Gbuf[0], S.rpart, S.rgrid, S.rout, S.status, st);
-    record_resid<<<1, 1, 0, st>>>(S.iter_dev, S.first_iter, S.max_iters, S.rout, S.resid);
+    launch_pdl(record_resid, 1, 1, 0, st, S.iter_dev, S.first_iter, S.max_iters, S.rout, S.resid);
   }
-  bump_iter<<<1, 1, 0, st>>>(S.iter_dev);
+  launch_pdl(bump_iter, 1, 1, 0, st, S.iter_dev);
   return true;
 }
 

@@ -5,6 +5,7 @@
 #include <stdint.h>
 #include <stddef.h>
 #include <algorithm>
+#include <utility>
 #include "symnmf.h"
 
 namespace symnmf {
@@ -16,9 +17,36 @@ constexpr int kMaxK = 64;       // factor width supported by every kernel
 constexpr int kMaxL = 96;       // range-finder sketch width (Jacobi smem bound)
 constexpr int kWsHeader = 256;  // bytes reserved at the head of every workspace
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Kernels launched with launch_pdl() may start while their predecessor drains: they let
+// their own dependents launch at once (launch_dependents) and wait for the predecessor's
+// completion and memory flush (griddepcontrol.wait) before touching its outputs.  Both
+// are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 // ---------------------------------------------------------------- status word
-// Workspace header: int32 status at offset 0; the rest is scratch.
+// Workspace header: int32 status at offset 0; the rest is scratch.  Every kernel checks
+// it first, so this is also where a PDL-launched kernel waits for its predecessor.
 __device__ __forceinline__ bool dev_failed(const int32_t* status) {
+  pdl_trigger();
+  pdl_wait();
   return *(volatile const int32_t*)status != 0;
 }
 __device__ __forceinline__ void dev_fail(int32_t* status, int32_t code) {

@@ -103,6 +103,28 @@ __device__ __forceinline__ double rsqrt_fp64(double d) {
 // column c (R[i][c], i <= c).  Step j broadcasts R[j][i] from lane i with compile-time shuffle
 // sources, so there is no shared memory traffic and no barrier.  Padding columns c >= k carry
 // the identity.  Writes R (fp32, KP x KP upper, zero padded) and rd = 1 / diag(R).
+// One factorisation pass over b (fully unrolled: every register index is a compile-time
+// constant, no break, so b stays in registers).  Returns nonzero if a pivot was not positive.
+template <int KP>
+__device__ __forceinline__ int chol_col_pass(double (&b)[KP], int lane, double& myr) {
+  int fail = 0;
+#pragma unroll
+  for (int j = 0; j < KP; ++j) {
+    const double d = __shfl_sync(0xffffffffu, b[j], j);
+    fail |= (!(d > 0.0) || !isfinite(d)) ? 1 : 0;
+    const double dd = fail ? 1.0 : d;
+    const double rinv = rsqrt_fp64(dd), r = dd * rinv;
+    if (lane == j) { b[j] = r; myr = r; }
+    else if (lane > j) b[j] *= rinv;                          // R[j][lane]
+#pragma unroll
+    for (int i = j + 1; i < KP; ++i) {
+      const double rji = __shfl_sync(0xffffffffu, b[j], i);   // R[j][i] from lane i
+      if (lane >= i) b[i] = fma(-rji, b[j], b[i]);            // A[i][lane] -= R[j][i] R[j][lane]
+    }
+  }
+  return fail;
+}
+
 template <int KP>
 __device__ int warp_chol_col(const double* G, int k, double shift_rel, float* R32, float* rd32) {
   static_assert(KP <= 32, "one column per lane");
@@ -115,27 +137,17 @@ __device__ int warp_chol_col(const double* G, int k, double shift_rel, float* R3
   for (int i = 0; i < KP; ++i)
     if (i == lane) dl = a[i];
   const double tr = warp_sum(lane < k ? dl : 0.0);
-  int fail = 1;
   double myr = 1.0;
-  for (int attempt = 0; attempt < 2 && fail; ++attempt) {
-    const double jitter = shift_rel * tr + (attempt ? 1e-12 * tr / k : 0.0);
-    if (attempt && !(jitter > 0.0)) break;
+  double jitter = shift_rel * tr;
+#pragma unroll
+  for (int i = 0; i < KP; ++i) b[i] = a[i] + ((i == lane && lane < k) ? jitter : 0.0);
+  int fail = chol_col_pass<KP>(b, lane, myr);
+  if (fail) {                                   // one retry with 1e-12 tr(G)/k on the diagonal
+    jitter += 1e-12 * tr / k;
+    if (!(jitter > 0.0)) return 1;
 #pragma unroll
     for (int i = 0; i < KP; ++i) b[i] = a[i] + ((i == lane && lane < k) ? jitter : 0.0);
-    fail = 0;
-#pragma unroll
-    for (int j = 0; j < KP; ++j) {
-      const double d = __shfl_sync(0xffffffffu, b[j], j);
-      if (!(d > 0.0) || !isfinite(d)) { fail = 1; break; }
-      const double rinv = rsqrt_fp64(d), r = d * rinv;
-      if (lane == j) { b[j] = r; myr = r; }
-      else if (lane > j) b[j] *= rinv;                    // R[j][lane]
-#pragma unroll
-      for (int i = j + 1; i < KP; ++i) {
-        const double rji = __shfl_sync(0xffffffffu, b[j], i);   // R[j][i] from lane i
-        if (lane >= i) b[i] = fma(-rji, b[j], b[i]);            // A[i][lane] -= R[j][i] R[j][lane]
-      }
-    }
+    fail = chol_col_pass<KP>(b, lane, myr);
   }
   if (fail) return 1;
   if (lane < KP) {
@@ -729,7 +741,7 @@ void launch_leverage_fused(const float* F, int64_t n, int k, const float* Rinv, 
 void launch_uniq_count_fused(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
                              const int32_t* iter_dev, int32_t first_iter, int32_t max_iters, int side,
                              symnmf_half_stats* stats, unsigned int* counter, int32_t* status, cudaStream_t st) {
-  uniq_count_fused<<<(unsigned)samp_blocks(n), 256, 0, st>>>(lev, n, T, w.cnt, w.bu, plan.cap, plan.counts,
+  launch_pdl(uniq_count_fused, (unsigned)samp_blocks(n), 256, 0, st, lev, n, T, w.cnt, w.bu, plan.cap, plan.counts,
                                                              plan.mass, iter_dev, first_iter, max_iters, side, stats,
                                                              counter, status);
 }
@@ -738,10 +750,10 @@ void launch_sampled_gram_fused(const float* F, int k, const symnmf_plan& plan, d
                                unsigned int* counter, int32_t* status, cudaStream_t st) {
   const int grid = fused_grid((plan.cap + 63) / 64, 1);
   switch (kpad(k)) {
-    case 8: sampled_gram_fused<8><<<grid, FT, kRedBytes, st>>>(F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
-    case 16: sampled_gram_fused<16><<<grid, FT, kRedBytes, st>>>(F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
-    case 32: sampled_gram_fused<32><<<grid, FT, kRedBytes, st>>>(F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
-    default: sampled_gram_fused<64><<<grid, FT, kRedBytes, st>>>(F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
+    case 8: launch_pdl(sampled_gram_fused<8>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
+    case 16: launch_pdl(sampled_gram_fused<16>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
+    case 32: launch_pdl(sampled_gram_fused<32>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
+    default: launch_pdl(sampled_gram_fused<64>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
   }
 }
 

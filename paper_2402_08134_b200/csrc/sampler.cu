@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(ST) samp_uniq_write(const float* __restrict__ 
 
 void launch_samp_prefix(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
                         int32_t* status, cudaStream_t st) {
-  samp_prefix<<<(unsigned)samp_blocks(n), ST, 0, st>>>(lev, n, T, w.bw, w.bd, w.P, plan.det_idx, plan.cap, status);
+  launch_pdl(samp_prefix, (unsigned)samp_blocks(n), ST, 0, st, lev, n, T, w.bw, w.bd, w.P, plan.det_idx, plan.cap, status);
 }
 
 void launch_samp_draws(const SamplerWs& w, int64_t n, int64_t s, uint64_t seed, const int32_t* iter_dev,
@@ -265,17 +265,17 @@ void launch_samp_draws(const SamplerWs& w, int64_t n, int64_t s, uint64_t seed, 
   const int64_t dblocks = std::max<int64_t>(1, (s + 255) / 256);
   const int64_t nb = samp_blocks(n);
   if (nb <= 6144) {
-    samp_draws_2level<<<(unsigned)dblocks, 256, sizeof(uint64_t) * nb, st>>>(
+    launch_pdl(samp_draws_2level, (unsigned)dblocks, 256, sizeof(uint64_t) * nb, st, 
         w.P, w.bw, nb, n, seed, iter_dev, iteration, side, plan.counts, plan.draw_idx, w.cnt, status);
     return;
   }
-  samp_draws<<<(unsigned)dblocks, 256, 0, st>>>(w.P, n, seed, iter_dev, iteration, side, plan.counts, plan.draw_idx,
+  launch_pdl(samp_draws, (unsigned)dblocks, 256, 0, st, w.P, n, seed, iter_dev, iteration, side, plan.counts, plan.draw_idx,
                                                 w.cnt, status);
 }
 
 void launch_samp_uniq_write(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
                             int32_t* status, cudaStream_t st) {
-  samp_uniq_write<<<(unsigned)samp_blocks(n), ST, 0, st>>>(lev, n, T, w.cnt, w.bu, plan.counts, plan.uniq_idx,
+  launch_pdl(samp_uniq_write, (unsigned)samp_blocks(n), ST, 0, st, lev, n, T, w.cnt, w.bu, plan.counts, plan.uniq_idx,
                                                            plan.uniq_w, plan.cap, status);
 }
 

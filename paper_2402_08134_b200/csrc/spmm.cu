@@ -82,15 +82,15 @@ void launch_spmm_csr(const symnmf_matrix& A, const float* F, int k, float* Y, co
     const float4* F4 = reinterpret_cast<const float4*>(F);
     float4* Y4 = reinterpret_cast<float4*>(Y);
     switch (lpr) {
-      case 1: spmm_csr_v4<1><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, n, F4, Y4, status); return;
-      case 2: spmm_csr_v4<2><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, n, F4, Y4, status); return;
-      case 4: spmm_csr_v4<4><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, n, F4, Y4, status); return;
-      case 8: spmm_csr_v4<8><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, n, F4, Y4, status); return;
-      case 16: spmm_csr_v4<16><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, n, F4, Y4, status); return;
+      case 1: launch_pdl(spmm_csr_v4<1>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, n, F4, Y4, status); return;
+      case 2: launch_pdl(spmm_csr_v4<2>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, n, F4, Y4, status); return;
+      case 4: launch_pdl(spmm_csr_v4<4>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, n, F4, Y4, status); return;
+      case 8: launch_pdl(spmm_csr_v4<8>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, n, F4, Y4, status); return;
+      case 16: launch_pdl(spmm_csr_v4<16>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, n, F4, Y4, status); return;
       default: break;
     }
   }
-  spmm_csr_scalar<<<grid_for(n * 32), 256, 0, st>>>(A.rowptr, A.colidx, A.val, n, F, k, Y, status);
+  launch_pdl(spmm_csr_scalar, grid_for(n * 32), 256, 0, st, A.rowptr, A.colidx, A.val, n, F, k, Y, status);
 }
 
 // ---------------------------------------------------------------- sampled (scatter) product
@@ -159,15 +159,15 @@ void launch_sampled_csr_nozero(const symnmf_matrix& A, const float* F, int k, co
     const float4* F4 = reinterpret_cast<const float4*>(F);
     float4* Y4 = reinterpret_cast<float4*>(Y);
     switch (k / 4) {
-      case 1: sampled_csr_v4<1><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
-      case 2: sampled_csr_v4<2><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
-      case 4: sampled_csr_v4<4><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
-      case 8: sampled_csr_v4<8><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
-      case 16: sampled_csr_v4<16><<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
+      case 1: launch_pdl(sampled_csr_v4<1>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
+      case 2: launch_pdl(sampled_csr_v4<2>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
+      case 4: launch_pdl(sampled_csr_v4<4>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
+      case 8: launch_pdl(sampled_csr_v4<8>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
+      case 16: launch_pdl(sampled_csr_v4<16>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
       default: break;
     }
   }
-  sampled_csr_scalar<<<grid, 256, 0, st>>>(A.rowptr, A.colidx, A.val, F, k, uniq, w, n_uniq_dev, Y, status);
+  launch_pdl(sampled_csr_scalar, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F, k, uniq, w, n_uniq_dev, Y, status);
 }
 
 }  // namespace symnmf
