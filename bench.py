@@ -1,19 +1,21 @@
 #!/usr/bin/env python
 """Benchmark of the randomized-SymNMF hot path on B200 (BASELINE.json metric).
 
-python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--mode lvs] [--impl ours|reference]
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--mode lvs|exact|lai]
+                [--impl ours|reference]
 
-A step is one full LvS-HALS iteration (W-half + H-half: Gram, CholeskyQR
-scores, hybrid plan, sampled Gram, sampled product, HALS sweep) of config
-`--config` (default configs[1] = c2), replayed from the solver's captured
-CUDA graph with inputs resident in HBM.  L2 is flushed (256 MiB write)
-before every timed step.  N > 1 runs N independent replicas (DESIGN.md §7:
-the single-GPU north star does not shard; weak scaling, no collective on
-the data path), timed on the device as the max over ranks.
+A step is one full iteration (W-half + H-half) of the solver of config
+`--config` (default configs[1] = c2, mode LvS: CholeskyQR scores, hybrid plan,
+sampled Gram, sampled product, HALS sweep with the next Gram fused), replayed
+from the solver's captured CUDA graph with inputs resident in HBM.  L2 is
+flushed (256 MiB write) before every timed step.  N > 1 runs N independent
+replicas (the single-GPU north star does not shard; weak
+scaling, no collective on the data path), timed on the device as the max over
+ranks.  Only tests/, smoke() and this file's cpu_baseline / reference legs
+import oracle/.
 """
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -26,7 +28,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "SymNMF iters/sec (exact & LvS); A·H / sampled SpMM HBM GB/s vs B200 peak"
 UNIT = "iters/s"
-SLEEP_CYCLES = 400_000   # ~0.2 ms: hides host enqueue latency from the device-side event timing
+SLEEP_CYCLES = 400_000   # ~0.2 ms: keeps the GPU busy while the host enqueues, so events time the device
+TF32_OVER_BF16 = 0.5     # nominal dense tf32 / bf16 ratio (B200_PROFILING.md: 1.1 vs 2.25 PFLOP/s)
 
 
 def parse():
@@ -35,12 +38,16 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2")
-    ap.add_argument("--mode", default="lvs", choices=["lvs", "exact"])
+    ap.add_argument("--mode", default=None, choices=[None, "lvs", "exact", "lai"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--profile-only", action="store_true", help="warmup + timed loop only (for ncu)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.mode is None:
+        a.mode = "lai" if a.config == "c5" else "lvs"
+    return a
 
 
 def peaks():
@@ -48,7 +55,7 @@ def peaks():
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return json.load(f), "measured"
     except Exception:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
 # ------------------------------------------------------------------ clocks
@@ -65,8 +72,7 @@ class ClockSampler:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self.proc = None
 
@@ -85,13 +91,14 @@ class ClockSampler:
             self.proc.wait(2)
         except Exception:
             self.proc.kill()
-        rows = self.rows
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
         def num(x):
             try:
                 return float(x)
             except ValueError:
                 return None
+        rows = self.rows
         load = [r for r in rows if (num(r[2]) or 0) > 0] or rows
         sm = [num(r[0]) for r in load if num(r[0]) is not None]
         mx = [num(r[1]) for r in rows if num(r[1]) is not None]
@@ -108,84 +115,103 @@ def dist_setup(args):
     pg = None
     if ws > 1:
         import torch.distributed as dist
-        backend = "nccl" if args.impl == "ours" else "gloo"
         if args.impl == "ours":
             import torch
             torch.cuda.set_device(local)
-        dist.init_process_group(backend)
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
         pg = dist
     return ws, rank, local, pg
 
 
-# ------------------------------------------------------------------ algorithmic bytes
-def kernel_bytes(name, n, k, nnz_u=0, n_u=0, nnz=0):
-    if name == "sampled_ah_csr":          # 8 nnz_U + 16|U| + 4|U|k gathered + 4nk output write
-        return 8 * nnz_u + 16 * n_u + 4 * n_u * k + 4 * n * k
-    if name == "hals_sweep":              # read Y, X, F + write X
-        return 16 * n * k
-    if name == "gram":
-        return 4 * n * k
+def max_over_ranks(pg, value, dev):
+    if not pg:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=dev)
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ algorithmic bytes per launch
+def kernel_cost(name, n, k, nnz=0, nnz_u=0, n_u=0, l=0, zeroY=False):
+    """(algorithmic bytes, flops) one launch must move / compute (SURVEY §8(d) per-unit figures)."""
+    if name == "spmm_csr":
+        return 8 * nnz + 8 * (n + 1) + 8 * n * k, 2 * nnz * k
+    if name in ("gemm_3xtf32", "gemm_fp32"):
+        return 4 * n * n + 8 * n * k, 2 * n * n * k
+    if name == "sampled_ah_csr":
+        return 8 * nnz_u + 16 * n_u + 4 * n_u * k + 4 * n * k, 2 * nnz_u * k
+    if name == "sampled_ah_dense":
+        return 4 * n_u * n + 4 * n_u * k + 4 * n * k, 2 * n * n_u * k
+    if name == "hals_sweep":
+        return (20 if zeroY else 16) * n * k, 2 * n * k * k
     if name == "leverage":
-        return 4 * n * k + 4 * n
-    if name == "spmm_csr":                # 8 nnz + 8(n+1) + 4nk (F once) + 4nk (Y)
-        return 8 * nnz + 8 * (n + 1) + 8 * n * k
-    if name == "hybrid_sample":           # lev read x3, P u64 write+searches, counts, plan
-        return 4 * n * 3 + 8 * n + 4 * n * 2
-    raise KeyError(name)
+        return 4 * n * k + 4 * n, n * k * k
+    if name == "sampled_gram":
+        return n_u * (4 * k + 12), n_u * k * k
+    if name == "samp_prefix":
+        return 4 * n + 8 * n, 0
+    if name in ("samp_uniq_count", "samp_uniq_write"):
+        return 8 * n, 0
+    if name == "lai_utf":
+        return 4 * n * l + 4 * n * k, 2 * n * l * k
+    if name == "lai_uz":
+        return 4 * n * l + 4 * n * k, 2 * n * l * k
+    return None, None
 
 
 # ------------------------------------------------------------------ reference arm: the oracle on host cores
-def run_reference(args, rank, ws):
+def oracle_steps(args, d, steps, warmup, budget_s=None):
     import numpy as np
     import oracle as O
+    cfg = d["cfg"]
+    A, alpha = d["A"], d["alpha"]
+    kw = {}
+    if args.mode == "lvs":
+        kw = dict(s=cfg.s, tau=cfg.tau, seed=cfg.seed)
+    elif args.mode == "lai":
+        U, lam, _ = O.rangefinder(A, cfg.l, cfg.q, seed=cfg.seed)
+        kw = dict(U=U, lam=lam)
+    W = H = d["H0"].astype(np.float64)
+    it = 0
+    for _ in range(warmup):
+        W, H, _ = O.iterate(A, W, H, alpha, 1, args.mode, first_iter=it, **kw)
+        it += 1
+    t0 = time.perf_counter()
+    done = 0
+    while done < steps:
+        W, H, _ = O.iterate(A, W, H, alpha, 1, args.mode, first_iter=it, **kw)
+        it += 1
+        done += 1
+        if budget_s is not None and time.perf_counter() - t0 > budget_s:
+            break
+    return done, time.perf_counter() - t0
+
+
+def run_reference(args, rank, ws):
     from synth import make_input
     if rank != 0:
         return None
     d = make_input(args.config)
     cfg = d["cfg"]
-    A, H0, alpha = d["A"], d["H0"], d["alpha"]
-    kw = dict(s=cfg.s, tau=cfg.tau, seed=0) if args.mode == "lvs" else {}
-    W, H = H0.astype(np.float64), H0.astype(np.float64)
-    it = 0
-    for _ in range(args.warmup):
-        W, H, _ = O.iterate(A, W, H, alpha, 1, args.mode, first_iter=it, **kw)
-        it += 1
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        W, H, _ = O.iterate(A, W, H, alpha, 1, args.mode, first_iter=it, **kw)
-        it += 1
-    dt = time.perf_counter() - t0
-    v = args.steps / dt
-    cores = os.cpu_count()
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+    done, dt = oracle_steps(args, d, args.steps, args.warmup)
+    v = done / dt
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": done,
+            "warmup": args.warmup, "ms_per_step": 1e3 * dt / done, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "n": d["n"], "k": cfg.k, "mode": args.mode,
-                       "s": cfg.s, "tau": cfg.tau},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"{args.steps} full oracle {args.mode} iterations of {args.config}"},
+                       "s": cfg.s if args.mode == "lvs" else None, "tau": cfg.tau if args.mode == "lvs" else None},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+                             "sample": f"{done} full oracle {args.mode} iterations of {args.config}"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    return line
 
 
-def cpu_baseline(args, budget_s=15.0):
-    import numpy as np
-    import oracle as O
-    from synth import make_input
-    d = make_input(args.config)
-    cfg = d["cfg"]
-    kw = dict(s=cfg.s, tau=cfg.tau, seed=0) if args.mode == "lvs" else {}
-    W = H = d["H0"].astype(np.float64)
-    t0 = time.perf_counter()
-    done = 0
-    while True:
-        W, H, _ = O.iterate(d["A"], W, H, d["alpha"], 1, args.mode, first_iter=done, **kw)
-        done += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
+def cpu_baseline(args, d):
+    steps = 10 ** 6
+    done, dt = oracle_steps(args, d, steps, 0, budget_s=args.cpu_budget)
     return {"value": done / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-            "sample": f"first {done} oracle {args.mode} iterations of {args.config} (full n), ~{budget_s:.0f} s budget"}
+            "sample": f"first {done} oracle {args.mode} iterations of {args.config} (full n), "
+                      f"~{args.cpu_budget:.0f} s budget"}
 
 
 # ------------------------------------------------------------------ our arm
@@ -201,13 +227,26 @@ def run_ours(args, ws, rank, local, pg):
     cfg = d["cfg"]
     A, H0, alpha = d["A"], d["H0"], d["alpha"]
     n, k = d["n"], cfg.k
+    dense = not hasattr(A, "rowptr")
+    precision = "3xtf32" if dense and n % 4 == 0 else "fp32"
     M = S.DeviceMatrix.from_host(A)
     W = torch.from_numpy(H0).to(dev)
     H = torch.from_numpy(H0).to(dev)
-    lvs = args.mode == "lvs"
-    kw = dict(s=cfg.s, tau=cfg.tau, seed=cfg.seed) if lvs else {}
+    kw = {}
+    extra = {}
+    if args.mode == "lvs":
+        kw = dict(s=cfg.s, tau=cfg.tau, seed=cfg.seed)
+    elif args.mode == "lai":
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        U, lam = S.rangefinder(M, cfg.l, cfg.q, cfg.seed, precision=precision)
+        e1.record()
+        torch.cuda.synchronize()
+        extra["rangefinder_ms"] = e0.elapsed_time(e1)
+        kw = dict(U=U, lam=lam)
     total = args.warmup + args.steps
-    solver = S.Solver(M, W, H, alpha, mode=args.mode, max_iters=total, **kw)
+    solver = S.Solver(M, W, H, alpha, mode=args.mode, precision=precision, max_iters=total, **kw)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MiB > 126 MB L2
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -221,15 +260,14 @@ def run_ours(args, ws, rank, local, pg):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for e0, e1 in evs:
         flush.zero_()
-        torch.cuda._sleep(SLEEP_CYCLES)   # keep the GPU busy while the host enqueues the step
+        torch.cuda._sleep(SLEEP_CYCLES)
         e0.record(stream)
         solver.run(1)
         e1.record(stream)
     torch.cuda.synchronize()
     if pg:
         pg.barrier()
-    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
-    t_ms = sum(step_ms)
+    t_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
     st = solver.stats()
     if st["status"] != 0:
         raise RuntimeError(f"device status {st['status']}")
@@ -237,148 +275,136 @@ def run_ours(args, ws, rank, local, pg):
     if args.profile_only:
         clocks.stop()
         return None
-    t_max = t_ms
-    if pg:
-        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-        pg.all_reduce(tt, op=pg.ReduceOp.MAX)
-        t_max = float(tt.item())
+    t_max = max_over_ranks(pg, t_ms, dev)
     value = ws * args.steps / (t_max / 1e3)
 
-    # exact-product iterations (the "exact" half of the metric), same protocol
-    ex_steps = max(3, min(args.steps, 30))
-    W2 = torch.from_numpy(H0).to(dev)
-    H2 = torch.from_numpy(H0).to(dev)
-    sx = S.Solver(M, W2, H2, alpha, mode="exact", max_iters=args.warmup + ex_steps)
-    sx.run(args.warmup)
-    torch.cuda.synchronize()
-    ex_ms = []
-    for _ in range(ex_steps):
-        flush.zero_()
-        torch.cuda._sleep(SLEEP_CYCLES)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream); sx.run(1); e1.record(stream)
-        e1.synchronize()
-        ex_ms.append(e0.elapsed_time(e1))
-    exact_ips = ex_steps / (sum(ex_ms) / 1e3)
-
-    # per-kernel phase timing on the same inputs (eager ABI calls, CUDA events on this stream)
-    F = H.clone()
-    X = W.clone()
-    reps = 20
-    def timeit(fn):
-        fn(); torch.cuda.synchronize()
+    # the other half of the metric: exact-product iterations (LvS configs) with the same protocol
+    if args.mode == "lvs":
+        ex_steps = max(3, min(args.steps, 30))
+        W2, H2 = torch.from_numpy(H0).to(dev), torch.from_numpy(H0).to(dev)
+        sx = S.Solver(M, W2, H2, alpha, mode="exact", precision=precision, max_iters=args.warmup + ex_steps)
+        sx.run(args.warmup)
+        torch.cuda.synchronize()
         acc = 0.0
-        for _ in range(reps):
+        for _ in range(ex_steps):
             flush.zero_()
             torch.cuda._sleep(SLEEP_CYCLES)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream); fn(); e1.record(stream)
+            e0.record(stream); sx.run(1); e1.record(stream)
             e1.synchronize()
             acc += e0.elapsed_time(e1)
-        return acc / reps
-    lev = S.leverage_scores(F)
-    phases = {"gram": timeit(lambda: S.gram(F)), "leverage": timeit(lambda: S.leverage_scores(F, check=False))}
-    if lvs:
-        plan = S.hybrid_sample(lev, k, cfg.s, cfg.tau, 0, 0, 0)
-        phases["hybrid_sample"] = timeit(lambda: S.hybrid_sample(lev, k, cfg.s, cfg.tau, 0, 0, 0, plan=plan,
-                                                                 check=False))
-        Y, Gs = S.sampled_ah(M, F, plan)
-        phases["sampled_ah_csr" if M.kind == 1 else "sampled_ah_dense"] = timeit(lambda: S.sampled_ah(M, F, plan))
-        ph = plan.to_host()
-        rp = A.rowptr if hasattr(A, "rowptr") else None
-        nnz_u = int(sum(rp[i + 1] - rp[i] for i in ph["uniq_idx"])) if rp is not None else 0
-        n_u = ph["n_uniq"]
-    else:
-        Y = S.ah(M, F)
-        phases["spmm_csr"] = timeit(lambda: S.ah(M, F, out=Y))
-        nnz_u = n_u = 0
-    G = S.gram(F)
-    phases["hals_sweep"] = timeit(lambda: S.hals_sweep(G, Y, F, X, alpha))
-    dom = max(phases, key=phases.get)
+        extra["exact_iters_per_s"] = ws * ex_steps / (max_over_ranks(pg, acc, dev) / 1e3)
+        extra["exact_precision"] = precision
+        sx.close()
+
+    # per-kernel device times of the same kernels (eager evented iterations)
+    prof = solver.profile(iters=5)
+    per = {}
+    for name, ms in prof:
+        per.setdefault(name, []).append(ms)
+    share = {nm: sum(v) for nm, v in per.items()}
+    iter_ms = sum(share.values())
+    dom = max((nm for nm in share if nm != "bump_iter"), key=share.get)
+    dom_ms = statistics.mean(per[dom])
+    nnz = A.nnz if not dense else n * n
+    nnz_u = n_u = 0
+    if args.mode == "lvs":
+        halves = st["halves"][2 * args.warmup:] or st["halves"]
+        n_u = int(round(statistics.mean(h["n_uniq"] for h in halves)))
+        if not dense:   # nnz of a representative plan: the final H's own plan
+            lev = S.leverage_scores(H)
+            ph = S.hybrid_sample(lev, k, cfg.s, cfg.tau, cfg.seed, total, 0).to_host()
+            nnz_u = int(np.sum(A.rowptr[ph["uniq_idx"] + 1] - A.rowptr[ph["uniq_idx"]]))
+    by, fl = kernel_cost(dom, n, k, nnz=nnz, nnz_u=nnz_u, n_u=n_u, l=cfg.l, zeroY=args.mode == "lvs")
     pk, which = peaks()
-    nnz = A.nnz if hasattr(A, "nnz") else n * n
-    try:
-        algo = kernel_bytes(dom, n, k, nnz_u=nnz_u, n_u=n_u, nnz=nnz)
-    except KeyError:
-        algo = None
-    achieved = algo / (phases[dom] * 1e-3) / 1e9 if algo else None
-    traffic = None
+    roof = {"bound": "hbm", "kernel": dom, "achieved": None, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": None,
+            "traffic": None, "algorithmic_bytes": by, "kernel_ms": dom_ms, "share_of_step": share[dom] / iter_ms,
+            "peak_source": f"{which} (MEASURED_PEAKS.json hbm_gbs: copy bandwidth)"}
+    if by:
+        roof["achieved"] = by / (dom_ms * 1e-3) / 1e9
+        roof["frac"] = roof["achieved"] / pk["hbm_gbs"]
+    if dom in ("gemm_3xtf32",) and fl:
+        tf32 = pk.get("bf16_tflops", 1590.0) * TF32_OVER_BF16 / 3.0
+        roof["tensor_3xtf32_tflops"] = {"achieved": fl / (dom_ms * 1e-3) / 1e12, "peak": tf32,
+                                        "frac": fl / (dom_ms * 1e-3) / 1e12 / tf32}
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(args.config, {}).get(dom)
+            roof["traffic"] = json.load(open(tpath)).get(args.config, {}).get(dom)
         except Exception:
-            traffic = None
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": (achieved / pk["hbm_gbs"]) if achieved else None, "traffic": traffic,
-                "algorithmic_bytes": algo, "kernel_ms": phases[dom], "peak_source": which,
-                "phases_ms": {kk: round(v, 5) for kk, v in phases.items()}}
+            pass
+    kernels = {}
+    for nm, v in per.items():
+        b_, _ = kernel_cost(nm, n, k, nnz=nnz, nnz_u=nnz_u, n_u=n_u, l=cfg.l, zeroY=args.mode == "lvs")
+        kernels[nm] = {"ms": round(statistics.mean(v), 5), "launches_per_step": len(v),
+                       "gbs": round(b_ / (statistics.mean(v) * 1e-3) / 1e9, 1) if b_ else None}
 
-    # end to end through the public API: pinned host inputs in, result out, every step
+    # end to end through the public API: pinned host inputs in, factors out, every step
     e2e = None
     if not args.no_e2e:
-        if hasattr(A, "rowptr"):
+        if not dense:
             host_in = [torch.from_numpy(A.rowptr).pin_memory(), torch.from_numpy(A.colidx).pin_memory(),
                        torch.from_numpy(A.val).pin_memory()]
             dev_in = [M.rowptr, M.colidx, M.val]
         else:
             host_in = [torch.from_numpy(A).pin_memory()]
             dev_in = [M.dense]
-        hW = torch.from_numpy(H0).pin_memory(); hH = torch.from_numpy(H0).pin_memory()
-        oW = torch.empty_like(hW).pin_memory(); oH = torch.empty_like(hH).pin_memory()
-        W3 = torch.empty_like(W); H3 = torch.empty_like(H)
-        s3 = S.Solver(M, W3, H3, alpha, mode=args.mode, max_iters=args.warmup + args.steps, **kw)
+        hW, hH = torch.from_numpy(H0).pin_memory(), torch.from_numpy(H0).pin_memory()
+        oW, oH = torch.empty_like(hW).pin_memory(), torch.empty_like(hH).pin_memory()
+        W3, H3 = torch.empty_like(W), torch.empty_like(H)
+        e2e_steps = max(3, min(args.steps, 30))
+        s3 = S.Solver(M, W3, H3, alpha, mode=args.mode, precision=precision, max_iters=args.warmup + e2e_steps, **kw)
+
         def e2e_step():
             for h, dd in zip(host_in, dev_in):
                 dd.copy_(h, non_blocking=True)
-            W3.copy_(hW, non_blocking=True); H3.copy_(hH, non_blocking=True)
+            W3.copy_(hW, non_blocking=True)
+            H3.copy_(hH, non_blocking=True)
             s3.run(1)
-            oW.copy_(W3, non_blocking=True); oH.copy_(H3, non_blocking=True)
-        for _ in range(args.warmup):
+            oW.copy_(W3, non_blocking=True)
+            oH.copy_(H3, non_blocking=True)
+        for _ in range(min(args.warmup, 2)):
             e2e_step()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(e2e_steps):
             e2e_step()
         e1.record(stream)
         torch.cuda.synchronize()
-        te = e0.elapsed_time(e1)
-        if pg:
-            tt = torch.tensor([te], dtype=torch.float64, device=dev)
-            pg.all_reduce(tt, op=pg.ReduceOp.MAX)
-            te = float(tt.item())
+        te = max_over_ranks(pg, e0.elapsed_time(e1), dev)
         h2d = sum(t.numel() * t.element_size() for t in host_in) + 2 * hW.numel() * 4
-        e2e = {"value": ws * args.steps / (te / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": 2 * hW.numel() * 4}
+        e2e = {"value": ws * e2e_steps / (te / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(2 * hW.numel() * 4), "steps": e2e_steps,
+               "inputs": "A + W + H copied H2D from pinned memory, W + H copied D2H, every step"}
+        s3.close()
     clk = clocks.stop()
     halves = st["halves"][2 * args.warmup:]
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.config, "n": n, "nnz": int(nnz), "k": k, "mode": args.mode,
-                       "s": cfg.s if lvs else None, "tau": cfg.tau if lvs else None,
+                       "precision": precision, "s": cfg.s if args.mode == "lvs" else None,
+                       "tau": cfg.tau if args.mode == "lvs" else None, "l": cfg.l or None, "q": cfg.q or None,
                        "l2": "flushed (256 MiB write) before every timed step", "parallelism": f"replicas{ws}",
-                       "graph": "per-iteration CUDA graph replay"},
-            "exact_iters_per_s": exact_ips * ws,
-            "lvs_stats_mean": {"s_D": statistics.mean(h["s_D"] for h in halves) if halves else None,
-                               "n_uniq": statistics.mean(h["n_uniq"] for h in halves) if halves else None},
-            "roofline": roofline, "clocks": clk, "e2e": e2e,
+                       "graph": "per-iteration CUDA graph replay (PDL edges)"},
+            **extra,
+            "lvs_stats_mean": ({"s_D": statistics.mean(h["s_D"] for h in halves),
+                                "n_uniq": statistics.mean(h["n_uniq"] for h in halves), "nnz_U": nnz_u}
+                               if args.mode == "lvs" and halves else None),
+            "roofline": roof, "kernels": kernels, "clocks": clk, "e2e": e2e,
             "gpu_launches": kernels_per_iter * args.steps, "kernels_per_step": kernels_per_iter,
             "memsets_per_step": memsets_per_iter}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args)
-    solver.close(); sx.close()
+        line["cpu_baseline"] = cpu_baseline(args, d)
+    solver.close()
     return line if rank == 0 else None
 
 
 def main():
     args = parse()
     ws, rank, local, pg = dist_setup(args)
-    if args.impl == "reference":
-        line = run_reference(args, rank, ws)
-    else:
-        line = run_ours(args, ws, rank, local, pg)
+    line = run_reference(args, rank, ws) if args.impl == "reference" else run_ours(args, ws, rank, local, pg)
     if line is not None and rank == 0:
         print(json.dumps(line), flush=True)
     if pg:

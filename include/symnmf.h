@@ -218,6 +218,12 @@ symnmf_status symnmf_solver_run(symnmf_solver* solver, int32_t iters, cudaStream
 symnmf_status symnmf_solver_stats(symnmf_solver* solver, int32_t* iters_done_host,
                                   symnmf_half_stats* stats_host, double* resid_host, cudaStream_t st);
 symnmf_status symnmf_solver_destroy(symnmf_solver* solver);
+/* Per-kernel device timing (host only, synchronising): runs `iters` iterations EAGERLY (not
+ * from the graph; W and H advance exactly as with symnmf_solver_run) with a CUDA event after
+ * every launch site, and returns for each site of one iteration (in launch order) its name
+ * (names_host[i], NUL terminated) and mean duration in ms (ms_host[i]); *count_host <= cap. */
+symnmf_status symnmf_solver_profile(symnmf_solver* solver, int32_t iters, int32_t cap, char (*names_host)[48],
+                                    float* ms_host, int32_t* count_host, cudaStream_t st);
 /* Kernel and memset node counts of the captured per-iteration graph (host only). */
 symnmf_status symnmf_solver_graph_nodes(const symnmf_solver* solver, int32_t* kernels_host, int32_t* memsets_host);
 

@@ -60,6 +60,7 @@ SIGNATURES = {
     "symnmf_solver_stats": (I32, [P, C.POINTER(I32), C.POINTER(HalfStats), C.POINTER(F64), P]),
     "symnmf_solver_destroy": (I32, [P]),
     "symnmf_solver_graph_nodes": (I32, [P, C.POINTER(I32), C.POINTER(I32)]),
+    "symnmf_solver_profile": (I32, [P, I32, I32, C.c_void_p, C.POINTER(C.c_float), C.POINTER(I32), P]),
 }
 
 _lib = None

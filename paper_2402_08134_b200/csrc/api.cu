@@ -1,6 +1,8 @@
 // The C ABI of libsymnmf (include/symnmf.h): argument validation, workspace
 // carving, kernel sequencing, and the CUDA-graph iteration driver.
+#include <cstdio>
 #include <new>
+#include <vector>
 #include "kernels.cuh"
 
 using namespace symnmf;
@@ -428,9 +430,28 @@ struct symnmf_solver {
   cudaGraph_t graph;
   cudaGraphExec_t exec;
   int32_t iters_done;
+  // profiling (symnmf_solver_profile): an event after every launch site of an eager iteration
+  struct Prof {
+    static constexpr int kMax = 64;
+    cudaEvent_t ev[kMax + 1];
+    const char* name[kMax];
+    int n;
+  }* prof;
 };
 
 namespace {
+
+// Profiling hook: records an event after the launch site just enqueued (no-op unless profiling).
+void mark(symnmf_solver& S, cudaStream_t st, const char* name) {
+  if (!S.prof || S.prof->n >= symnmf_solver::Prof::kMax) return;
+  S.prof->name[S.prof->n] = name;
+  cudaEventRecord(S.prof->ev[++S.prof->n], st);
+}
+
+__global__ void spin_kernel(long long cycles) {
+  const long long t0 = clock64();
+  while (clock64() - t0 < cycles) {}
+}
 
 void solver_layout(symnmf_solver& S, Carver& c) {
   const int64_t n = S.n;
@@ -487,30 +508,43 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
   const bool lvs = S.mode == SYMNMF_LVS;
   if (S.mode == SYMNMF_EXACT) {
     if (!enqueue_product(S.A, F, k, S.Y, S.precision, S.tcs, S.tcs_bytes, status, st)) return false;
+    mark(S, st, S.A.kind == SYMNMF_CSR ? "spmm_csr" : (S.precision == SYMNMF_3XTF32 ? "gemm_3xtf32" : "gemm_fp32"));
     launch_sweep_fused(Gf, S.alpha, S.Y, F, X, n, k, false, S.Gacc, Gnext, nullptr, S.counter, status, st);
+    mark(S, st, "hals_sweep");
   } else if (lvs) {
     // scores of F from R^{-1} (computed with F^T F) fused with sampler pass S1/S2
     launch_leverage_fused(F, n, k, S.Rinv32, S.lev, S.T, S.sw, S.s, S.plan, S.counter, status, st);
+    mark(S, st, "leverage");
     launch_samp_prefix(S.lev, n, S.T, S.sw, S.plan, status, st);
+    mark(S, st, "samp_prefix");
     launch_samp_draws(S.sw, n, S.s, S.seed, S.iter_dev, 0, (uint32_t)side, S.plan, status, st);
+    mark(S, st, "samp_draws");
     launch_uniq_count_fused(S.lev, n, S.T, S.sw, S.plan, S.iter_dev, S.first_iter, S.max_iters, side, S.stats,
                             S.counter, status, st);
+    mark(S, st, "samp_uniq_count");
     launch_samp_uniq_write(S.lev, n, S.T, S.sw, S.plan, status, st);
+    mark(S, st, "samp_uniq_write");
     launch_sampled_gram_fused(F, k, S.plan, S.Gacc, S.Gs, S.counter, status, st);
+    mark(S, st, "sampled_gram");
     if (S.A.kind == SYMNMF_CSR)
       launch_sampled_csr_nozero(S.A, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap, S.Y,
                                 status, st);
     else
       launch_sampled_dense(S.A.val, S.A.lda, n, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap,
                            S.Y, status, st);
+    mark(S, st, S.A.kind == SYMNMF_CSR ? "sampled_ah_csr" : "sampled_ah_dense");
     // Update(G_s + alpha I, Y_s + alpha F^T); Y re-zeroed for the next scatter; X^T X and its R^{-1}
     launch_sweep_fused(S.Gs, S.alpha, S.Y, F, X, n, k, true, S.Gacc, Gnext, S.Rinv32, S.counter, status, st);
+    mark(S, st, "hals_sweep");
   } else {
     launch_cross_gram(S.U, S.l, S.l, F, k, k, false, n, nullptr, nullptr, nullptr, S.Zpart, S.ggrid, S.Z, k, status,
                       st);
+    mark(S, st, "lai_utf");
     launch_scale_rows(S.Z, S.l, k, S.lam, S.M32, status, st);
     launch_rowapply32(S.U, S.l, n, S.l, S.M32, k, S.Y, k, status, st);
+    mark(S, st, "lai_uz");
     launch_sweep_fused(Gf, S.alpha, S.Y, F, X, n, k, false, S.Gacc, Gnext, nullptr, S.counter, status, st);
+    mark(S, st, "hals_sweep");
   }
   return true;
 }
@@ -522,8 +556,10 @@ bool enqueue_iteration(symnmf_solver& S, cudaStream_t st) {
     // Gbuf[0] now holds H^T H of the updated H (fused Gram of the H-half sweep)
     launch_residual(S.A, S.H, S.k, S.AHres, S.Gbuf[0], S.rpart, S.rgrid, S.rout, S.status, st);
     launch_pdl(record_resid, 1, 1, 0, st, S.iter_dev, S.first_iter, S.max_iters, S.rout, S.resid);
+    mark(S, st, "residual");
   }
   launch_pdl(bump_iter, 1, 1, 0, st, S.iter_dev);
+  mark(S, st, "bump_iter");
   return true;
 }
 
@@ -628,6 +664,44 @@ extern "C" symnmf_status symnmf_solver_destroy(symnmf_solver* S) {
   cudaGraphDestroy(S->graph);
   delete S;
   return SYMNMF_OK;
+}
+
+extern "C" symnmf_status symnmf_solver_profile(symnmf_solver* S, int32_t iters, int32_t cap,
+                                               char (*names_host)[48], float* ms_host, int32_t* count_host,
+                                               cudaStream_t st) {
+  if (!S || iters < 1 || cap < 1 || !names_host || !ms_host || !count_host) return SYMNMF_ERR_ARG;
+  symnmf_solver::Prof prof;
+  prof.n = 0;
+  for (int i = 0; i <= symnmf_solver::Prof::kMax; ++i) SYMNMF_CUDA_TRY(cudaEventCreate(&prof.ev[i]));
+  std::vector<double> acc;
+  int sites = 0;
+  for (int it = 0; it < iters; ++it) {
+    // keep the device busy while the host enqueues the instrumented iteration
+    spin_kernel<<<1, 1, 0, st>>>(200000);
+    prof.n = 0;
+    cudaEventRecord(prof.ev[0], st);
+    S->prof = &prof;
+    const bool ok = enqueue_iteration(*S, st);
+    S->prof = nullptr;
+    if (!ok) break;
+    SYMNMF_CUDA_TRY(cudaStreamSynchronize(st));
+    sites = prof.n;
+    acc.resize(sites, 0.0);
+    for (int i = 0; i < sites; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, prof.ev[i], prof.ev[i + 1]);
+      acc[i] += ms;
+    }
+  }
+  S->iters_done += iters;
+  const int m = std::min(sites, (int)cap);
+  for (int i = 0; i < m; ++i) {
+    std::snprintf(names_host[i], 48, "%s", prof.name[i]);
+    ms_host[i] = (float)(acc[i] / iters);
+  }
+  *count_host = m;
+  for (int i = 0; i <= symnmf_solver::Prof::kMax; ++i) cudaEventDestroy(prof.ev[i]);
+  return finish();
 }
 
 extern "C" symnmf_status symnmf_solver_graph_nodes(const symnmf_solver* S, int32_t* kernels_host,

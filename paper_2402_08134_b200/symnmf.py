@@ -296,6 +296,21 @@ class Solver:
                   for i in range(2 * k)]
         return {"status": code, "iters": done.value, "halves": halves, "residual": [rs[i] for i in range(k)]}
 
+    def profile(self, iters=5):
+        """Per launch site of one iteration: [(name, mean ms)], from eager evented iterations."""
+        cap = 64
+        names = C.create_string_buffer(48 * cap)
+        ms = (C.c_float * cap)()
+        cnt = C.c_int32(0)
+        A.check("symnmf_solver_profile", lib().symnmf_solver_profile(self.h, int(iters), cap, names, ms,
+                                                                     C.byref(cnt), _stream()))
+        raw = names.raw
+        out = []
+        for i in range(cnt.value):
+            nm = raw[48 * i:48 * (i + 1)].split(b"\0", 1)[0].decode()
+            out.append((nm, float(ms[i])))
+        return out
+
     def graph_nodes(self):
         kc, mc = C.c_int32(0), C.c_int32(0)
         A.check("symnmf_solver_graph_nodes", lib().symnmf_solver_graph_nodes(self.h, C.byref(kc), C.byref(mc)))
