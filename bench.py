@@ -143,6 +143,10 @@ def kernel_cost(name, n, k, nnz=0, nnz_u=0, n_u=0, l=0, zeroY=False):
         return 8 * nnz_u + 16 * n_u + 4 * n_u * k + 4 * n * k, 2 * nnz_u * k
     if name == "sampled_ah_dense":
         return 4 * n_u * n + 4 * n_u * k + 4 * n * k, 2 * n * n_u * k
+    if name == "csr_tile_exact":   # spmm + sweep fused: Y never leaves the SM, F counted once
+        return 8 * nnz + 8 * (n + 1) + 12 * n * k, 2 * nnz * k + 2 * n * k * k
+    if name == "csr_tile_lvs":     # sampled product (SURVEY §8(d) N8 bytes) + sweep, fused
+        return 8 * nnz_u + 16 * n_u + 4 * n_u * k + 12 * n * k, 2 * nnz_u * k + 2 * n * k * k
     if name == "hals_sweep":
         return (20 if zeroY else 16) * n * k, 2 * n * k * k
     if name == "leverage":

@@ -421,6 +421,9 @@ struct symnmf_solver {
   SamplerWs sw;
   symnmf_plan plan;
   float* Y;
+  bool tile;               // CSR with kpad(k) == k: product fused into the sweep (csr_tile_sweep)
+  float* Fs;               // LvS tile path: compact omega-scaled sampled rows (cap x k)
+  uint2* tab;              // LvS tile path: U membership table, ceil(n/32) words
   symnmf_half_stats* stats;
   double *resid, *rpart, *rout, *GH;
   double *Zpart, *Z;
@@ -468,7 +471,8 @@ void solver_layout(symnmf_solver& S, Carver& c) {
   S.Gs = c.take<double>((size_t)k * k);
   S.GH = c.take<double>((size_t)k * k);
   S.gpart = c.take<double>(gram_partial_doubles(k, k, true, S.ggrid));
-  S.Y = c.take<float>((size_t)n * k);
+  S.tile = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode != SYMNMF_LAI;
+  S.Y = c.take<float>(S.tile ? 0 : (size_t)n * k);
   S.stats = c.take<symnmf_half_stats>((size_t)2 * S.max_iters);
   S.resid = c.take<double>((size_t)S.max_iters);
   S.rgrid = residual_grid(n);
@@ -485,6 +489,8 @@ void solver_layout(symnmf_solver& S, Carver& c) {
     S.plan.uniq_w = c.take<double>(n);
     S.plan.counts = c.take<int64_t>(4);
     S.plan.mass = c.take<double>(2);
+    S.Fs = c.take<float>(S.tile ? (size_t)S.plan.cap * k : 0);
+    S.tab = c.take<uint2>(S.tile ? (size_t)(n + 31) / 32 : 0);
   }
   if (S.mode == SYMNMF_LAI) {
     S.Zpart = c.take<double>(gram_partial_doubles(S.l, k, false, S.ggrid));
@@ -506,7 +512,11 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
   const double* Gf = S.Gbuf[side];
   double* Gnext = S.Gbuf[side ^ 1];
   const bool lvs = S.mode == SYMNMF_LVS;
-  if (S.mode == SYMNMF_EXACT) {
+  if (S.mode == SYMNMF_EXACT && S.tile) {
+    launch_csr_tile_sweep(S.A, F, nullptr, nullptr, Gf, S.alpha, X, n, k, S.Gacc, Gnext, nullptr, S.counter, status,
+                          st);
+    mark(S, st, "csr_tile_exact");
+  } else if (S.mode == SYMNMF_EXACT) {
     if (!enqueue_product(S.A, F, k, S.Y, S.precision, S.tcs, S.tcs_bytes, status, st)) return false;
     mark(S, st, S.A.kind == SYMNMF_CSR ? "spmm_csr" : (S.precision == SYMNMF_3XTF32 ? "gemm_3xtf32" : "gemm_fp32"));
     launch_sweep_fused(Gf, S.alpha, S.Y, F, X, n, k, false, S.Gacc, Gnext, nullptr, S.counter, status, st);
@@ -522,10 +532,17 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     launch_uniq_count_fused(S.lev, n, S.T, S.sw, S.plan, S.iter_dev, S.first_iter, S.max_iters, side, S.stats,
                             S.counter, status, st);
     mark(S, st, "samp_uniq_count");
-    launch_samp_uniq_write(S.lev, n, S.T, S.sw, S.plan, status, st);
+    launch_samp_uniq_write(S.lev, n, S.T, S.sw, S.plan, status, st, S.tab);
     mark(S, st, "samp_uniq_write");
-    launch_sampled_gram_fused(F, k, S.plan, S.Gacc, S.Gs, S.counter, status, st);
+    launch_sampled_gram_fused(F, k, S.plan, S.Gacc, S.Gs, S.counter, status, st, S.Fs);
     mark(S, st, "sampled_gram");
+    if (S.tile) {
+      // pull-form Y_s fused with Update(G_s + alpha I, Y_s + alpha F^T), X^T X and its R
+      launch_csr_tile_sweep(S.A, F, S.Fs, S.tab, S.Gs, S.alpha, X, n, k, S.Gacc, Gnext, S.Rinv32, S.counter, status,
+                            st);
+      mark(S, st, "csr_tile_lvs");
+      return true;
+    }
     if (S.A.kind == SYMNMF_CSR)
       launch_sampled_csr_nozero(S.A, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap, S.Y,
                                 status, st);
@@ -602,7 +619,7 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
   SYMNMF_CUDA_TRY(cudaMemsetAsync(S.resid, 0, sizeof(double) * max_iters, st));
   SYMNMF_CUDA_TRY(cudaMemsetAsync(S.counter, 0, sizeof(unsigned int) * 4, st));
   SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Gacc, 0, sizeof(double) * kGramReplicas * k * k, st));
-  if (mode == SYMNMF_LVS) SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Y, 0, sizeof(float) * n * k, st));
+  if (mode == SYMNMF_LVS && !S.tile) SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Y, 0, sizeof(float) * n * k, st));
   set_i32<<<1, 1, 0, st>>>(S.iter_dev, first_iter);
   // H^T H (and its CholeskyQR factor for LvS) for the first W-half; later halves get
   // theirs from the fused Gram of the preceding sweep.

@@ -129,24 +129,21 @@ template <int KP>
 __device__ int warp_chol_col(const double* G, int k, double shift_rel, float* R32, float* rd32) {
   static_assert(KP <= 32, "one column per lane");
   const int lane = threadIdx.x & 31;
-  double a[KP], b[KP];
-#pragma unroll
-  for (int i = 0; i < KP; ++i) a[i] = (lane < k && i < k) ? G[i * k + lane] : (i == lane ? 1.0 : 0.0);
-  double dl = 0.0;
-#pragma unroll
-  for (int i = 0; i < KP; ++i)
-    if (i == lane) dl = a[i];
-  const double tr = warp_sum(lane < k ? dl : 0.0);
+  double b[KP];   // column `lane` of G (re-read from G for the retry: keeps register use at KP doubles)
+  const double dl = lane < k ? G[lane * k + lane] : 0.0;
+  const double tr = warp_sum(dl);
   double myr = 1.0;
   double jitter = shift_rel * tr;
 #pragma unroll
-  for (int i = 0; i < KP; ++i) b[i] = a[i] + ((i == lane && lane < k) ? jitter : 0.0);
+  for (int i = 0; i < KP; ++i)
+    b[i] = ((lane < k && i < k) ? G[i * k + lane] : (i == lane ? 1.0 : 0.0)) + ((i == lane && lane < k) ? jitter : 0.0);
   int fail = chol_col_pass<KP>(b, lane, myr);
   if (fail) {                                   // one retry with 1e-12 tr(G)/k on the diagonal
     jitter += 1e-12 * tr / k;
     if (!(jitter > 0.0)) return 1;
 #pragma unroll
-    for (int i = 0; i < KP; ++i) b[i] = a[i] + ((i == lane && lane < k) ? jitter : 0.0);
+    for (int i = 0; i < KP; ++i)
+      b[i] = ((lane < k && i < k) ? G[i * k + lane] : (i == lane ? 1.0 : 0.0)) + ((i == lane && lane < k) ? jitter : 0.0);
     fail = chol_col_pass<KP>(b, lane, myr);
   }
   if (fail) return 1;
@@ -625,7 +622,8 @@ __global__ void __launch_bounds__(FT) sampled_gram_fused(const float* __restrict
                                                          const int32_t* __restrict__ uniq,
                                                          const double* __restrict__ w,
                                                          const int64_t* __restrict__ n_uniq_dev, double* Gacc,
-                                                         double* Gout, unsigned int* counter, int32_t* status) {
+                                                         double* Gout, float* __restrict__ Fs, unsigned int* counter,
+                                                         int32_t* status) {
   constexpr int ST = KP + 4;
   constexpr int ROWS = 64;
   __shared__ __align__(16) float s[ROWS * ST];
@@ -666,10 +664,305 @@ __global__ void __launch_bounds__(FT) sampled_gram_fused(const float* __restrict
       }
     }
     __syncthreads();
+    if (Fs) {   // compact omega-scaled rows (|U| x KP) for the pull-form sampled product
+      for (int e = threadIdx.x; e < rows * (KP / 4); e += FT) {
+        const int r = e / (KP / 4), c = e - r * (KP / 4);
+        float4 v = *reinterpret_cast<const float4*>(s + r * ST + 4 * c);
+        const float om = sw[r];
+        v.x *= om; v.y *= om; v.z *= om; v.w *= om;
+        reinterpret_cast<float4*>(Fs)[(r0 + r) * (KP / 4) + c] = v;
+      }
+    }
     gt.accumulate(s, ST, rows, sw);
   }
   gt.commit(Gacc, k, red);
   if (arrive_last(counter)) finalize_gram<KP>(Gacc, Gout, k, nullptr, nullptr, nullptr, status);
+}
+
+// ---------------------------------------------------------------- csr_tile_sweep
+// One 256-row tile of the fixed-factor product, computed in shared memory, then swept.
+//   SAMPLED = false: y_c = sum_e A[c, col_e] F[col_e, :]  (Y = A F), the tile's nonzeros
+//                    split into equal slices (one per lane group), partial row sums flushed to
+//                    shared memory at row boundaries -- hub rows do not serialise one warp.
+//   SAMPLED = true:  y_c = sum_{i in U} omega_i A[i, c] f_i = sum_{i in row c, i in U} A[c, i] Fs[u(i)]
+//                    (Y_s = (SA)^T(SF); row c of A = column c): the tile's
+//                    column indices are streamed with coalesced 128-bit loads and tested against
+//                    the U membership table; hits gather the compact omega-scaled row Fs[u].
+// Then thread r sweeps row r (Eq. 2.6) with G (+alpha I) and b = y + alpha f_r, writes
+// X, and the tile's updated rows are accumulated into X^T X (fp32 per tile, fp64 in shared memory).
+constexpr int TR = 256;          // rows per tile = threads per CTA
+constexpr int TCU = 4;           // int4 column-index loads per thread per round (sampled)
+
+template <int KP>
+struct GramTile {   // per-thread upper 4x4 block (ai <= bi) of the tile Gram; row groups g
+  int ai, bi, g, RG;
+  bool active;
+  __device__ void init(int t) {
+    constexpr int nb = KP / 4, pairs = nb * (nb + 1) / 2;
+    RG = TR / pairs;
+    g = t / pairs;
+    const int p = t - g * pairs;
+    active = g < RG;
+    int a = 0, rem = p;
+    while (rem >= nb - a) { rem -= nb - a; ++a; }
+    ai = a; bi = a + rem;
+  }
+  __device__ void tile(const float* s, int rows, double* gacc) const {
+    constexpr int ST = KP + 4;
+    if (!active) return;
+    float acc[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+    for (int r = g; r < rows; r += RG) {
+      const float4 a4 = *reinterpret_cast<const float4*>(s + r * ST + 4 * ai);
+      const float4 b4 = *reinterpret_cast<const float4*>(s + r * ST + 4 * bi);
+      const float a[4] = {a4.x, a4.y, a4.z, a4.w}, b[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i * 4 + j] = fmaf(a[i], b[j], acc[i * 4 + j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (acc[i * 4 + j] != 0.f) atomicAdd(gacc + (4 * ai + i) * KP + 4 * bi + j, (double)acc[i * 4 + j]);
+  }
+};
+
+__device__ __forceinline__ int tile_row_of(const int* sOff, int rows, int e) {   // sOff[r] <= e < sOff[r+1]
+  int lo = 0, hi = rows - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (sOff[mid] <= e) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <int KP>
+__device__ __forceinline__ void sadd4(float* p, float s, float4 f) {
+  atomicAdd(p, s * f.x); atomicAdd(p + 1, s * f.y); atomicAdd(p + 2, s * f.z); atomicAdd(p + 3, s * f.w);
+}
+
+template <int KP, bool SAMPLED>
+__global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
+    const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, const float* __restrict__ val, int64_t n,
+    const float* __restrict__ F, const float* __restrict__ Fs, const uint2* __restrict__ tab,
+    const double* __restrict__ G, double alpha, float* __restrict__ X, double* Gacc, double* Gout, float* Rf32,
+    unsigned int* counter, int32_t* status) {
+  constexpr int ST = KP + 4, LPR = KP / 4, NG = 32 / LPR;
+  __shared__ __align__(16) float sG[KP * KP];     // sG[i*KP + j] = G[j][i], 0 on the diagonal
+  __shared__ float sInv[KP];
+  __shared__ int sOk[KP];
+  __shared__ int sOff[TR + 1];
+  extern __shared__ __align__(16) unsigned char smt[];
+  float* sY = reinterpret_cast<float*>(smt);                          // [TR][ST]
+  double* gacc = reinterpret_cast<double*>(smt + sizeof(float) * TR * ST);   // [KP][KP]
+  int* hl = reinterpret_cast<int*>(gacc + KP * KP);                  // per warp: 32 x {row, u, a}
+  if (dev_failed(status)) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, grp = lane / LPR, li = lane % LPR;
+  int* wl = hl + wid * 96;
+  for (int e = tid; e < KP * KP; e += TR) {
+    const int i = e / KP, j = e - i * KP;
+    sG[e] = (i != j) ? (float)G[j * KP + i] : 0.f;
+    gacc[e] = 0.0;
+  }
+  for (int i = tid; i < KP; i += TR) {
+    const double den = G[i * KP + i] + alpha;
+    sOk[i] = den > 0.0;
+    sInv[i] = den > 0.0 ? (float)(1.0 / den) : 0.f;
+  }
+  GramTile<KP> gt;
+  gt.init(tid);
+  const float a32 = (float)alpha;
+  const float4* F4 = reinterpret_cast<const float4*>(F);
+  const float4* Fs4 = reinterpret_cast<const float4*>(Fs);
+  const int64_t tiles = (n + TR - 1) / TR;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int64_t r0 = t * TR;
+    const int rows = (int)min64(TR, n - r0);
+    const int64_t eb = rowptr[r0];
+    __syncthreads();   // previous tile's Gram reads of sY are done
+    {
+      const int64_t ep = rowptr[r0 + min(tid, rows)];
+      sOff[tid] = (int)(ep - eb);
+      if (tid == 0) sOff[TR] = (int)(rowptr[r0 + rows] - eb);
+#pragma unroll
+      for (int c = 0; c < KP; c += 4) *reinterpret_cast<float4*>(sY + tid * ST + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+    const int total = sOff[TR];
+    if (!SAMPLED) {
+      // ---- exact: nnz-balanced slices, one per lane group
+      constexpr int NSL = (TR / 32) * NG;
+      const int L = (total + NSL - 1) / NSL;
+      const int s0 = min(total, (wid * NG + grp) * L), s1 = min(total, s0 + L);
+      if (s0 < s1) {
+        int row = tile_row_of(sOff, rows, s0);
+        int rend = sOff[row + 1];
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        bool dirty = false;
+        for (int e = s0; e < s1; e += 4) {
+          int cc[4];
+          float aa[4];
+          float4 ff[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const bool ok = e + u < s1;
+            cc[u] = ok ? __ldg(col + eb + e + u) : 0;
+            aa[u] = ok ? __ldg(val + eb + e + u) : 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) ff[u] = (e + u < s1) ? __ldg(F4 + (int64_t)cc[u] * LPR + li) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (e + u < s1) {
+              while (e + u >= rend) {
+                if (dirty) { float* p = sY + row * ST + 4 * li; atomicAdd(p, acc.x); atomicAdd(p + 1, acc.y); atomicAdd(p + 2, acc.z); atomicAdd(p + 3, acc.w); }
+                acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                dirty = false;
+                ++row;
+                rend = sOff[row + 1];
+              }
+              acc.x = fmaf(aa[u], ff[u].x, acc.x); acc.y = fmaf(aa[u], ff[u].y, acc.y);
+              acc.z = fmaf(aa[u], ff[u].z, acc.z); acc.w = fmaf(aa[u], ff[u].w, acc.w);
+              dirty = true;
+            }
+          }
+        }
+        if (dirty) { float* p = sY + row * ST + 4 * li; atomicAdd(p, acc.x); atomicAdd(p + 1, acc.y); atomicAdd(p + 2, acc.z); atomicAdd(p + 3, acc.w); }
+      }
+    } else {
+      // ---- sampled (pull): stream the tile's column indices, test membership in U
+      const int ea = (int)(eb & 3);                 // eb - ea is 16-byte aligned
+      const int32_t* cbase = col + (eb - ea);
+      const int span = total + ea;
+      for (int base = 0; base < span; base += TR * 4 * TCU) {
+        int cv[4 * TCU];
+#pragma unroll
+        for (int j = 0; j < TCU; ++j) {
+          const int q = base + 4 * (tid + TR * j);
+          if (q + 3 < span) {
+            const int4 v = __ldg(reinterpret_cast<const int4*>(cbase + q));
+            cv[4 * j] = v.x; cv[4 * j + 1] = v.y; cv[4 * j + 2] = v.z; cv[4 * j + 3] = v.w;
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) cv[4 * j + c] = (q + c < span) ? __ldg(cbase + q + c) : -1;
+          }
+        }
+        uint2 tv[4 * TCU];
+#pragma unroll
+        for (int j = 0; j < 4 * TCU; ++j) {
+          const int q = base + 4 * (tid + TR * (j >> 2)) + (j & 3);
+          if (q < ea) cv[j] = -1;
+          tv[j] = cv[j] >= 0 ? __ldg(tab + (cv[j] >> 5)) : make_uint2(0u, 0u);
+        }
+#pragma unroll
+        for (int j = 0; j < 4 * TCU; ++j) {
+          const int q = base + 4 * (tid + TR * (j >> 2)) + (j & 3);
+          const int c = cv[j];
+          const uint32_t bit = c >= 0 ? (tv[j].x >> (c & 31)) & 1u : 0u;
+          const uint32_t m = __ballot_sync(0xffffffffu, bit);
+          if (m == 0u) continue;
+          if (bit) {
+            const int rk = __popc(m & ((1u << lane) - 1u));
+            const int e = q - ea;                    // offset in the tile's nonzeros
+            wl[3 * rk] = tile_row_of(sOff, rows, e);
+            wl[3 * rk + 1] = (int)(tv[j].y + __popc(tv[j].x & ((1u << (c & 31)) - 1u)));
+            wl[3 * rk + 2] = __float_as_int(__ldg(val + eb + e));
+          }
+          __syncwarp();
+          const int nh = __popc(m);
+          for (int h = grp; h < nh; h += NG) {
+            const int row = wl[3 * h], u = wl[3 * h + 1];
+            const float a = __int_as_float(wl[3 * h + 2]);
+            sadd4<KP>(sY + row * ST + 4 * li, a, __ldg(Fs4 + (int64_t)u * LPR + li));
+          }
+          __syncwarp();
+        }
+      }
+    }
+    __syncthreads();
+    // ---- HALS sweep of row tid: b = y + alpha f, Gauss-Seidel over the KP columns
+    if (tid < rows) {
+      const int64_t r = r0 + tid;
+      float x[KP], b[KP];
+      const float4* X4 = reinterpret_cast<const float4*>(X + r * KP);
+#pragma unroll
+      for (int j = 0; j < KP; j += 4) {
+        const float4 xv = X4[j / 4];
+        const float4 fv = __ldg(F4 + r * LPR + j / 4);
+        const float4 yv = *reinterpret_cast<const float4*>(sY + tid * ST + j);
+        x[j] = xv.x; x[j + 1] = xv.y; x[j + 2] = xv.z; x[j + 3] = xv.w;
+        b[j] = fmaf(a32, fv.x, yv.x); b[j + 1] = fmaf(a32, fv.y, yv.y);
+        b[j + 2] = fmaf(a32, fv.z, yv.z); b[j + 3] = fmaf(a32, fv.w, yv.w);
+      }
+#pragma unroll
+      for (int i = 0; i < KP; ++i) {
+        float s0 = b[i], s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+        for (int j = 0; j < KP; j += 4) {
+          const float4 g = *reinterpret_cast<const float4*>(sG + i * KP + j);
+          s0 = fmaf(-x[j], g.x, s0);
+          s1 = fmaf(-x[j + 1], g.y, s1);
+          s2 = fmaf(-x[j + 2], g.z, s2);
+          s3 = fmaf(-x[j + 3], g.w, s3);
+        }
+        const float s = (s0 + s1) + (s2 + s3);
+        if (sOk[i]) x[i] = fmaxf(0.f, s * sInv[i]);
+      }
+      float4* Xw = reinterpret_cast<float4*>(X + r * KP);
+#pragma unroll
+      for (int j = 0; j < KP; j += 4) {
+        const float4 v = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
+        Xw[j / 4] = v;
+        *reinterpret_cast<float4*>(sY + tid * ST + j) = v;
+      }
+    }
+    __syncthreads();
+    gt.tile(sY, rows, gacc);
+  }
+  // ---- commit the CTA's X^T X into a replica of the global accumulator; last CTA finalizes
+  __syncthreads();
+  double* rep = Gacc + (size_t)(blockIdx.x % kGramReplicas) * KP * KP;
+  for (int e = tid; e < KP * KP; e += TR) {
+    const int a = e / KP, b = e - a * KP;
+    if (a <= b && gacc[e] != 0.0) atomicAdd(rep + e, gacc[e]);
+  }
+  if (arrive_last(counter)) {
+    double* sa = reinterpret_cast<double*>(smt);
+    finalize_gram<KP>(Gacc, Gout, KP, Rf32, sa, sa + KP * (KP + 1), status);
+  }
+}
+
+template <int KP>
+static void csr_tile_sweep_t(const symnmf_matrix& A, const float* F, const float* Fs, const uint2* tab,
+                             const double* G, double alpha, float* X, int64_t n, double* Gacc, double* Gout,
+                             float* Rf32, unsigned int* counter, int32_t* status, cudaStream_t st) {
+  const size_t smem = std::max(sizeof(float) * TR * (KP + 4) + sizeof(double) * KP * KP + sizeof(int) * 8 * 96,
+                               sizeof(double) * 2 * KP * (KP + 1));
+  const int64_t tiles = (n + TR - 1) / TR;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 2));
+  if (Fs) {
+    cudaFuncSetAttribute(csr_tile_sweep<KP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch_pdl(csr_tile_sweep<KP, true>, grid, TR, smem, st, A.rowptr, A.colidx, A.val, n, F, Fs, tab, G, alpha, X,
+               Gacc, Gout, Rf32, counter, status);
+  } else {
+    cudaFuncSetAttribute(csr_tile_sweep<KP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch_pdl(csr_tile_sweep<KP, false>, grid, TR, smem, st, A.rowptr, A.colidx, A.val, n, F, Fs, tab, G, alpha, X,
+               Gacc, Gout, Rf32, counter, status);
+  }
+}
+
+void launch_csr_tile_sweep(const symnmf_matrix& A, const float* F, const float* Fs, const uint2* tab,
+                           const double* G, double alpha, float* X, int64_t n, int k, double* Gacc, double* Gout,
+                           float* Rf32, unsigned int* counter, int32_t* status, cudaStream_t st) {
+  switch (k) {
+    case 8: csr_tile_sweep_t<8>(A, F, Fs, tab, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
+    case 16: csr_tile_sweep_t<16>(A, F, Fs, tab, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
+    case 32: csr_tile_sweep_t<32>(A, F, Fs, tab, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
+    default: csr_tile_sweep_t<64>(A, F, Fs, tab, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
+  }
 }
 
 // ---------------------------------------------------------------- launchers
@@ -747,13 +1040,14 @@ void launch_uniq_count_fused(const float* lev, int64_t n, double T, const Sample
 }
 
 void launch_sampled_gram_fused(const float* F, int k, const symnmf_plan& plan, double* Gacc, double* Gout,
-                               unsigned int* counter, int32_t* status, cudaStream_t st) {
+                               unsigned int* counter, int32_t* status, cudaStream_t st, float* Fs) {
   const int grid = fused_grid((plan.cap + 63) / 64, 1);
+  if (Fs && kpad(k) != k) Fs = nullptr;   // the compact table needs float4 rows
   switch (kpad(k)) {
-    case 8: launch_pdl(sampled_gram_fused<8>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
-    case 16: launch_pdl(sampled_gram_fused<16>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
-    case 32: launch_pdl(sampled_gram_fused<32>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
-    default: launch_pdl(sampled_gram_fused<64>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
+    case 8: launch_pdl(sampled_gram_fused<8>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, Fs, counter, status); break;
+    case 16: launch_pdl(sampled_gram_fused<16>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, Fs, counter, status); break;
+    case 32: launch_pdl(sampled_gram_fused<32>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, Fs, counter, status); break;
+    default: launch_pdl(sampled_gram_fused<64>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, Fs, counter, status); break;
   }
 }
 

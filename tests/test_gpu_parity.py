@@ -449,3 +449,74 @@ def test_iterate_exact_3xtf32_c1():
     _, Hr, _ = O.iterate(d["A"], d["H0"], d["H0"], d["alpha"], 10, "exact")
     rg, ro = O.residual(d["A"], Hg), O.residual(d["A"], Hr)
     assert abs(rg - ro) <= 1e-4 * ro
+
+
+# ------------------------------------------------------------------ CSR tile path (product fused into the sweep)
+def _csr_case(cfgname, n, k, seed=7):
+    from synth.configs import init_factor, mean_entry
+    d = make_input(cfgname, n_override=n)
+    A = d["A"]
+    H0 = init_factor(n, k, mean_entry(A), np.random.default_rng(seed))
+    return A, H0, d["alpha"]
+
+
+@pytest.mark.parametrize("cfgname,n,k", [("c2", 20_000, 16), ("c2", 20_000, 8), ("c4", 40_000, 32),
+                                         ("c4", 40_000, 64), ("c4", 40_001, 16), ("c2", 300, 32)])
+def test_csr_tile_exact_one_iteration(cfgname, n, k):
+    """Solver EXACT on CSR (A F computed per 256-row tile with nnz-balanced slices, fused with
+    the sweep and the next Gram): W and H after one iteration vs the oracle's fp64 iteration.
+    Covers ragged last tiles (n % 256 != 0), hub rows (power-law c4 recipe) and k = 8..64."""
+    A, H0, alpha = _csr_case(cfgname, n, k)
+    M = S.DeviceMatrix.from_host(A)
+    W, H = cu(H0), cu(H0)
+    sv = S.Solver(M, W, H, alpha, mode="exact", max_iters=1)
+    sv.run(1)
+    assert sv.stats()["status"] == 0
+    sv.close()
+    Wr, Hr, _ = O.iterate(A, H0, H0, alpha, 1, "exact")
+    assert rel(W.cpu().numpy(), Wr) < 1e-5
+    assert rel(H.cpu().numpy(), Hr) < 1e-5
+
+
+@pytest.mark.parametrize("cfgname,n,k,s", [("c4", 40_000, 32, 800), ("c2", 20_001, 16, 400), ("c4", 40_000, 8, 2000)])
+def test_csr_tile_lvs_equals_scatter_composition(cfgname, n, k, s):
+    """Solver LvS on CSR (pull-form Y_s through the symmetric structure with the U membership
+    table, fused with the sweep) equals the ABI composition with the scatter-form Y_s."""
+    A, H0, alpha = _csr_case(cfgname, n, k)
+    tau = 1.0 / s
+    M = S.DeviceMatrix.from_host(A)
+    W1, H1 = cu(H0), cu(H0)
+    sv = S.Solver(M, W1, H1, alpha, mode="lvs", s=s, tau=tau, seed=3, max_iters=1)
+    sv.run(1)
+    st = sv.stats()
+    assert st["status"] == 0
+    sv.close()
+    W2, H2 = cu(H0), cu(H0)
+    for side in (0, 1):
+        F, X = (H2, W2) if side == 0 else (W2, H2)
+        lev = S.leverage_scores(F)
+        plan = S.hybrid_sample(lev, k, s, tau, 3, 0, side)
+        ph = plan.to_host()
+        assert (ph["s_D"], ph["s_R"], ph["n_uniq"]) == (st["halves"][side]["s_D"], st["halves"][side]["s_R"],
+                                                         st["halves"][side]["n_uniq"])
+        Y, Gs = S.sampled_ah(M, F, plan)
+        S.hals_sweep(Gs, Y, F, X, alpha)
+    assert rel(W1.cpu().numpy(), W2.cpu().numpy()) < 1e-5
+    assert rel(H1.cpu().numpy(), H2.cpu().numpy()) < 1e-5
+
+
+def test_csr_tile_lvs_replayed_plan_vs_oracle():
+    """One LvS half through the solver vs the oracle's sampled products + sweep fed the plan the
+    GPU drew (the same plan is recomputed by the ABI sampler from the same device scores)."""
+    A, H0, alpha = _csr_case("c4", 30_000, 32)
+    s, tau = 600, 1.0 / 600
+    M = S.DeviceMatrix.from_host(A)
+    W, H = cu(H0), cu(H0)
+    sv = S.Solver(M, W, H, alpha, mode="lvs", s=s, tau=tau, seed=5, max_iters=1)
+    sv.run(1)
+    sv.close()
+    lev = S.leverage_scores(cu(H0))
+    ph = S.hybrid_sample(lev, 32, s, tau, 5, 0, 0).to_host()
+    Gs, Ys = O.sampled_products(A, H0, ph["uniq_idx"], ph["uniq_w"])
+    Wr = O.hals_sweep(Gs, Ys, H0, H0, alpha)
+    assert rel(W.cpu().numpy(), Wr) < 1e-5
