@@ -107,81 +107,147 @@ void launch_dense_ah_simt(const float* A, int64_t lda, int64_t n, const float* F
 }
 
 // ---------------------------------------------------------------- sampled dense
-// Thread = output row c (a column of A[U,:]); the CTA walks the sampled rows
-// U in chunks of 32, staging omega_u F[U_u, :] in shared memory, reading
-// A[U_u, c0 .. c0+127] coalesced.  gridDim.y splits U (atomics into zeroed Y).
-template <int KP>
-__global__ void __launch_bounds__(128) sampled_dense_kernel(const float* __restrict__ A, int64_t lda, int64_t n,
-                                                            const float* __restrict__ F, int k,
-                                                            const int32_t* __restrict__ uniq,
-                                                            const double* __restrict__ w,
-                                                            const int64_t* __restrict__ n_uniq_dev,
-                                                            float* __restrict__ Y, const int32_t* __restrict__ status) {
-  __shared__ __align__(16) float sFw[32][KP];
-  __shared__ int64_t sRow[32];
+// Y_s[c, :] = sum_u A[U_u, c] (omega_u F[U_u, :])  (A[U,:]^T = A[:,U] by symmetry, Z28).
+// CTA tile: 128 output rows c x KP columns; thread = 4 rows c (one float4 of each gathered row of
+// A) x JB columns.  The gathered 32 x 128 slab of A is staged through shared memory with cp.async
+// (double buffered: the next slab is in flight while the current one is consumed); omega F[U]
+// rows are scaled once while staged.  fp32 FMAs, flushed into fp64 registers every stage (16-32 sampled
+// rows).  gridDim.y splits U (fp32 atomics into a zeroed Y) so that ~4 CTAs run per SM.
+constexpr int SDC = 128;   // output rows per CTA
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool ok) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  const int sz = ok ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int KP, int JB, int SDU>   // SDU sampled rows per stage
+__global__ void __launch_bounds__(32 * (KP / JB)) sampled_dense_v2(const float* __restrict__ A, int64_t lda, int64_t n,
+                                                                  const float* __restrict__ F, int k,
+                                                                  const int32_t* __restrict__ uniq,
+                                                                  const double* __restrict__ w,
+                                                                  const int64_t* __restrict__ n_uniq_dev,
+                                                                  float* __restrict__ Y, int vec,
+                                                                  const int32_t* __restrict__ status) {
+  constexpr int NT = 32 * (KP / JB);
+  __shared__ __align__(16) float sA[2][SDU][SDC];
+  __shared__ __align__(16) float sF[2][SDU][KP];
+  __shared__ int64_t sRow[2][SDU];
   if (dev_failed(status)) return;
-  const int tid = threadIdx.x;
-  const int64_t c = (int64_t)blockIdx.x * 128 + tid;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * SDC;
   const int64_t nu = *n_uniq_dev;
-  const int64_t per = (nu + gridDim.y - 1) / gridDim.y;
-  const int64_t u0 = (int64_t)blockIdx.y * per, u1 = min(nu, u0 + per);
-  float acc[KP];
-  double acc64[KP];
+  const int64_t per = ((nu + gridDim.y - 1) / gridDim.y + SDU - 1) / SDU * SDU;
+  const int64_t u0 = (int64_t)blockIdx.y * per, u1 = min64(nu, u0 + per);
+  if (u0 >= u1) return;
+  const int nst = (int)((u1 - u0 + SDU - 1) / SDU);
+  // stage s: row indices + scaled F rows (plain loads) and the A slab (cp.async)
+  auto stage_rows = [&](int s, int buf) {
+    const int64_t ub = u0 + (int64_t)s * SDU;
+    if (tid < SDU) sRow[buf][tid] = (ub + tid < u1) ? (int64_t)uniq[ub + tid] : -1;
+  };
+  auto stage_data = [&](int s, int buf) {
+    const int64_t ub = u0 + (int64_t)s * SDU;
+    for (int e = tid; e < SDU * (SDC / 4); e += NT) {
+      const int r = e / (SDC / 4), q = e - r * (SDC / 4);
+      const int64_t row = sRow[buf][r];
+      const int64_t c = c0 + 4 * q;
+      float* dst = &sA[buf][r][4 * q];
+      if (vec) {
+        const bool ok = row >= 0 && c < n;   // n % 4 == 0 and 16B-aligned rows: whole float4 in range
+        cp_async16(dst, ok ? (const void*)(A + row * lda + c) : (const void*)A, ok);
+      } else {
 #pragma unroll
-  for (int j = 0; j < KP; ++j) { acc[j] = 0.f; acc64[j] = 0.0; }
-  for (int64_t ub = u0; ub < u1; ub += 32) {
-    const int cnt = (int)min64(32, u1 - ub);
-    __syncthreads();
-    if (tid < 32) sRow[tid] = tid < cnt ? (int64_t)uniq[ub + tid] : 0;
-    __syncthreads();
-    for (int e = tid; e < 32 * KP; e += 128) {
+        for (int t = 0; t < 4; ++t) dst[t] = (row >= 0 && c + t < n) ? __ldg(A + row * lda + c + t) : 0.f;
+      }
+    }
+    for (int e = tid; e < SDU * KP; e += NT) {
       const int r = e / KP, j = e - r * KP;
-      sFw[r][j] = (r < cnt && j < k) ? (float)w[ub + r] * F[sRow[r] * k + j] : 0.f;
+      const int64_t row = sRow[buf][r];
+      sF[buf][r][j] = (row >= 0 && j < k) ? (float)w[ub + r] * __ldg(F + row * k + j) : 0.f;
+    }
+    cp_async_commit();
+  };
+  float acc[4][JB];
+  double acc64[4][JB];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < JB; ++j) { acc[i][j] = 0.f; acc64[i][j] = 0.0; }
+  stage_rows(0, 0);
+  __syncthreads();
+  stage_data(0, 0);
+  for (int s = 0; s < nst; ++s) {
+    const int buf = s & 1;
+    if (s + 1 < nst) {
+      stage_rows(s + 1, buf ^ 1);
+      __syncthreads();
+      stage_data(s + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
-    if (c < n) {
-      float a[32];
+#pragma unroll 8
+    for (int r = 0; r < SDU; ++r) {
+      const float4 a = *reinterpret_cast<const float4*>(&sA[buf][r][4 * tx]);
+      float f[JB];
 #pragma unroll
-      for (int r = 0; r < 32; ++r) a[r] = r < cnt ? __ldg(A + sRow[r] * lda + c) : 0.f;
+      for (int j = 0; j < JB; j += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(&sF[buf][r][ty * JB + j]);
+        f[j] = v.x; f[j + 1] = v.y; f[j + 2] = v.z; f[j + 3] = v.w;
+      }
+      const float av[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
-      for (int r = 0; r < 32; ++r)
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < KP; ++j) acc[j] = fmaf(a[r], sFw[r][j], acc[j]);
-#pragma unroll
-      for (int j = 0; j < KP; ++j) { acc64[j] += (double)acc[j]; acc[j] = 0.f; }
+        for (int j = 0; j < JB; ++j) acc[i][j] = fmaf(av[i], f[j], acc[i][j]);
     }
-  }
-  if (c < n) {
-    const bool atomic = gridDim.y > 1;
 #pragma unroll
-    for (int j = 0; j < KP; ++j) {
-      if (j >= k) break;
-      const float v = (float)acc64[j];
-      if (atomic) atomicAdd(Y + c * k + j, v);
-      else Y[c * k + j] = v;
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < JB; ++j) { acc64[i][j] += (double)acc[i][j]; acc[i][j] = 0.f; }
+    __syncthreads();   // buffer `buf` is refilled by the next iteration's stage_data
+  }
+  const bool atomic = gridDim.y > 1;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t c = c0 + 4 * tx + i;
+    if (c >= n) continue;
+#pragma unroll
+    for (int j = 0; j < JB; ++j) {
+      const int jj = ty * JB + j;
+      if (jj >= k) continue;
+      const float v = (float)acc64[i][j];
+      if (atomic) atomicAdd(Y + c * k + jj, v);
+      else Y[c * k + jj] = v;
     }
   }
 }
 
-template <int KP>
+template <int KP, int JB, int SDU = (KP == 64 ? 16 : 32)>
 static void launch_sd_t(const float* A, int64_t lda, int64_t n, const float* F, int k, const int32_t* uniq,
                         const double* w, const int64_t* nu, int64_t cap, float* Y, const int32_t* status,
                         cudaStream_t st) {
-  const int64_t cb = (n + 127) / 128;
-  int64_t splits = std::max<int64_t>(1, std::min<int64_t>((148 * 8 + cb - 1) / cb, (cap + 127) / 128));
+  const int64_t cb = (n + SDC - 1) / SDC;
+  int64_t splits = std::max<int64_t>(1, std::min<int64_t>((148 * 4 + cb - 1) / cb, (cap + 4 * SDU - 1) / (4 * SDU)));
   if (splits > 1) cudaMemsetAsync(Y, 0, sizeof(float) * n * k, st);
-  sampled_dense_kernel<KP><<<dim3((unsigned)cb, (unsigned)splits), 128, 0, st>>>(A, lda, n, F, k, uniq, w, nu, Y,
-                                                                                 status);
+  const int vec = (lda % 4 == 0 && n % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) ? 1 : 0;
+  sampled_dense_v2<KP, JB, SDU><<<dim3((unsigned)cb, (unsigned)splits), 32 * (KP / JB), 0, st>>>(A, lda, n, F, k, uniq, w,
+                                                                                          nu, Y, vec, status);
 }
 
 void launch_sampled_dense(const float* A, int64_t lda, int64_t n, const float* F, int k, const int32_t* uniq,
                           const double* w, const int64_t* n_uniq_dev, int64_t cap, float* Y, const int32_t* status,
                           cudaStream_t st) {
   switch (kpad(k)) {
-    case 8: launch_sd_t<8>(A, lda, n, F, k, uniq, w, n_uniq_dev, cap, Y, status, st); break;
-    case 16: launch_sd_t<16>(A, lda, n, F, k, uniq, w, n_uniq_dev, cap, Y, status, st); break;
-    case 32: launch_sd_t<32>(A, lda, n, F, k, uniq, w, n_uniq_dev, cap, Y, status, st); break;
-    default: launch_sd_t<64>(A, lda, n, F, k, uniq, w, n_uniq_dev, cap, Y, status, st); break;
+    case 8: launch_sd_t<8, 4>(A, lda, n, F, k, uniq, w, n_uniq_dev, cap, Y, status, st); break;
+    case 16: launch_sd_t<16, 4>(A, lda, n, F, k, uniq, w, n_uniq_dev, cap, Y, status, st); break;
+    case 32: launch_sd_t<32, 4>(A, lda, n, F, k, uniq, w, n_uniq_dev, cap, Y, status, st); break;
+    default: launch_sd_t<64, 8>(A, lda, n, F, k, uniq, w, n_uniq_dev, cap, Y, status, st); break;
   }
 }
 

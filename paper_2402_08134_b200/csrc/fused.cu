@@ -681,54 +681,24 @@ __global__ void __launch_bounds__(FT) sampled_gram_fused(const float* __restrict
 
 // ---------------------------------------------------------------- csr_tile_sweep
 // One 256-row tile of the fixed-factor product, computed in shared memory, then swept.
-//   SAMPLED = false: y_c = sum_e A[c, col_e] F[col_e, :]  (Y = A F), the tile's nonzeros
-//                    split into equal slices (one per lane group), partial row sums flushed to
-//                    shared memory at row boundaries -- hub rows do not serialise one warp.
+//   SAMPLED = false: y_c = sum_e A[c, col_e] F[col_e, :]  (Y = A F).  The tile's nonzeros
+//                    are split into 32 equal slices, one per lane group; a group accumulates a row
+//                    in registers and stores it once (rows interior to its slice are its own), the
+//                    first / last row of a slice go to carry slots that are combined in slice order
+//                    afterwards -- no atomics, deterministic, and hub rows are spread over groups.
 //   SAMPLED = true:  y_c = sum_{i in U} omega_i A[i, c] f_i = sum_{i in row c, i in U} A[c, i] Fs[u(i)]
-//                    (Y_s = (SA)^T(SF); row c of A = column c): the tile's
-//                    column indices are streamed with coalesced 128-bit loads and tested against
-//                    the U membership table; hits gather the compact omega-scaled row Fs[u].
+//                    (Y_s = (SA)^T(SF); row c of A = column c).  Each warp
+//                    streams an equal slice of the tile's column indices (coalesced 128-bit loads),
+//                    tests them against the U membership table, compacts the hits in nonzero order,
+//                    loads their values, and reduces runs of equal rows across its lane groups with a
+//                    segmented shuffle scan (boundary rows again through carries).
 // Then thread r sweeps row r (Eq. 2.6) with G (+alpha I) and b = y + alpha f_r, writes
-// X, and the tile's updated rows are accumulated into X^T X (fp32 per tile, fp64 in shared memory).
+// X, and the updated rows of the tile are accumulated into X^T X (fp32 per tile, fp64 registers
+// across tiles), committed once per CTA; the last CTA forms X^T X and its Cholesky factor.
 constexpr int TR = 256;          // rows per tile = threads per CTA
-constexpr int TCU = 4;           // int4 column-index loads per thread per round (sampled)
-
-template <int KP>
-struct GramTile {   // per-thread upper 4x4 block (ai <= bi) of the tile Gram; row groups g
-  int ai, bi, g, RG;
-  bool active;
-  __device__ void init(int t) {
-    constexpr int nb = KP / 4, pairs = nb * (nb + 1) / 2;
-    RG = TR / pairs;
-    g = t / pairs;
-    const int p = t - g * pairs;
-    active = g < RG;
-    int a = 0, rem = p;
-    while (rem >= nb - a) { rem -= nb - a; ++a; }
-    ai = a; bi = a + rem;
-  }
-  __device__ void tile(const float* s, int rows, double* gacc) const {
-    constexpr int ST = KP + 4;
-    if (!active) return;
-    float acc[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) acc[e] = 0.f;
-    for (int r = g; r < rows; r += RG) {
-      const float4 a4 = *reinterpret_cast<const float4*>(s + r * ST + 4 * ai);
-      const float4 b4 = *reinterpret_cast<const float4*>(s + r * ST + 4 * bi);
-      const float a[4] = {a4.x, a4.y, a4.z, a4.w}, b[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i * 4 + j] = fmaf(a[i], b[j], acc[i * 4 + j]);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (acc[i * 4 + j] != 0.f) atomicAdd(gacc + (4 * ai + i) * KP + 4 * bi + j, (double)acc[i * 4 + j]);
-  }
-};
+constexpr int TCU = 4;           // int4 column-index loads per lane per batch (sampled): 512 nonzeros
+constexpr int TLIST = 32 * 4 * TCU;
+constexpr int TUE = 8;           // gathers in flight per lane group (exact)
 
 __device__ __forceinline__ int tile_row_of(const int* sOff, int rows, int e) {   // sOff[r] <= e < sOff[r+1]
   int lo = 0, hi = rows - 1;
@@ -739,10 +709,17 @@ __device__ __forceinline__ int tile_row_of(const int* sOff, int rows, int e) {  
   return lo;
 }
 
-template <int KP>
-__device__ __forceinline__ void sadd4(float* p, float s, float4 f) {
-  atomicAdd(p, s * f.x); atomicAdd(p + 1, s * f.y); atomicAdd(p + 2, s * f.z); atomicAdd(p + 3, s * f.w);
-}
+template <int KP, bool SAMPLED>
+struct TileSmem {
+  static constexpr int ST = KP + 4;
+  static constexpr int NSLICE = SAMPLED ? TR / 32 : (TR / 32) * (32 / (KP / 4));   // warps or lane groups
+  static constexpr int NCARRY = 2 * NSLICE;
+  static constexpr size_t y = 0;                                               // float [TR][ST]
+  static constexpr size_t carry = y + sizeof(float) * TR * ST;                 // float [NCARRY][KP]
+  static constexpr size_t crow = carry + sizeof(float) * NCARRY * KP;          // int [NCARRY]
+  static constexpr size_t list = crow + sizeof(int) * NCARRY;                  // per warp: int e/row, int u, float a
+  static constexpr size_t bytes = list + (SAMPLED ? sizeof(int) * 3 * TLIST * (TR / 32) : 0);
+};
 
 template <int KP, bool SAMPLED>
 __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
@@ -750,33 +727,31 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
     const float* __restrict__ F, const float* __restrict__ Fs, const uint2* __restrict__ tab,
     const double* __restrict__ G, double alpha, float* __restrict__ X, double* Gacc, double* Gout, float* Rf32,
     unsigned int* counter, int32_t* status) {
-  constexpr int ST = KP + 4, LPR = KP / 4, NG = 32 / LPR;
+  using L = TileSmem<KP, SAMPLED>;
+  constexpr int ST = L::ST, LPR = KP / 4, NG = 32 / LPR;
   __shared__ __align__(16) float sG[KP * KP];     // sG[i*KP + j] = G[j][i], 0 on the diagonal
   __shared__ float sInv[KP];
   __shared__ int sOk[KP];
   __shared__ int sOff[TR + 1];
   extern __shared__ __align__(16) unsigned char smt[];
-  float* sY = reinterpret_cast<float*>(smt);                          // [TR][ST]
-  double* gacc = reinterpret_cast<double*>(smt + sizeof(float) * TR * ST);   // [KP][KP]
-  int* hl = reinterpret_cast<int*>(gacc + KP * KP);                  // per warp: 32 x {row, u, a}
+  float* sY = reinterpret_cast<float*>(smt + L::y);
+  float* sC = reinterpret_cast<float*>(smt + L::carry);
+  int* sCr = reinterpret_cast<int*>(smt + L::crow);
   if (dev_failed(status)) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, grp = lane / LPR, li = lane % LPR;
-  int* wl = hl + wid * 96;
   for (int e = tid; e < KP * KP; e += TR) {
     const int i = e / KP, j = e - i * KP;
     sG[e] = (i != j) ? (float)G[j * KP + i] : 0.f;
-    gacc[e] = 0.0;
   }
   for (int i = tid; i < KP; i += TR) {
     const double den = G[i * KP + i] + alpha;
     sOk[i] = den > 0.0;
     sInv[i] = den > 0.0 ? (float)(1.0 / den) : 0.f;
   }
-  GramTile<KP> gt;
-  gt.init(tid);
+  GramThread gt;
+  gt.init(tid, TR, KP / 4);
   const float a32 = (float)alpha;
   const float4* F4 = reinterpret_cast<const float4*>(F);
-  const float4* Fs4 = reinterpret_cast<const float4*>(Fs);
   const int64_t tiles = (n + TR - 1) / TR;
   for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
     const int64_t r0 = t * TR;
@@ -789,98 +764,201 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
       if (tid == 0) sOff[TR] = (int)(rowptr[r0 + rows] - eb);
 #pragma unroll
       for (int c = 0; c < KP; c += 4) *reinterpret_cast<float4*>(sY + tid * ST + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int e = tid; e < L::NCARRY * KP; e += TR) sC[e] = 0.f;
+      if (tid < L::NCARRY) sCr[tid] = -1;
     }
     __syncthreads();
     const int total = sOff[TR];
-    if (!SAMPLED) {
-      // ---- exact: nnz-balanced slices, one per lane group
-      constexpr int NSL = (TR / 32) * NG;
-      const int L = (total + NSL - 1) / NSL;
-      const int s0 = min(total, (wid * NG + grp) * L), s1 = min(total, s0 + L);
+    if constexpr (!SAMPLED) {
+      // ---- exact: nnz-balanced slices, one per lane group; rows owned or carried
+      const int sl = wid * NG + grp;
+      const int Ls = (total + L::NSLICE - 1) / L::NSLICE;
+      const int s0 = min(total, sl * Ls), s1 = min(total, s0 + Ls);
       if (s0 < s1) {
-        int row = tile_row_of(sOff, rows, s0);
+        const int rfirst = tile_row_of(sOff, rows, s0), rlast = tile_row_of(sOff, rows, s1 - 1);
+        int row = rfirst;
         int rend = sOff[row + 1];
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        bool dirty = false;
-        for (int e = s0; e < s1; e += 4) {
-          int cc[4];
-          float aa[4];
-          float4 ff[4];
+        auto put = [&](int r, float4 v) {   // one write per (slice, row)
+          float* dst = (r == rfirst) ? sC + (2 * sl) * KP : (r == rlast) ? sC + (2 * sl + 1) * KP : sY + r * ST;
+          *reinterpret_cast<float4*>(dst + 4 * li) = v;
+        };
+        if (li == 0) { sCr[2 * sl] = rfirst; sCr[2 * sl + 1] = rlast != rfirst ? rlast : -1; }
+        for (int e = s0; e < s1; e += TUE) {
+          int cc[TUE];
+          float aa[TUE];
+          float4 ff[TUE];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < TUE; ++u) {
             const bool ok = e + u < s1;
             cc[u] = ok ? __ldg(col + eb + e + u) : 0;
             aa[u] = ok ? __ldg(val + eb + e + u) : 0.f;
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) ff[u] = (e + u < s1) ? __ldg(F4 + (int64_t)cc[u] * LPR + li) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int u = 0; u < TUE; ++u)
+            ff[u] = (e + u < s1) ? __ldg(F4 + (int64_t)cc[u] * LPR + li) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < TUE; ++u) {
             if (e + u < s1) {
-              while (e + u >= rend) {
-                if (dirty) { float* p = sY + row * ST + 4 * li; atomicAdd(p, acc.x); atomicAdd(p + 1, acc.y); atomicAdd(p + 2, acc.z); atomicAdd(p + 3, acc.w); }
+              if (e + u >= rend) {
+                put(row, acc);
                 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-                dirty = false;
-                ++row;
+                row = tile_row_of(sOff, rows, e + u);
                 rend = sOff[row + 1];
               }
               acc.x = fmaf(aa[u], ff[u].x, acc.x); acc.y = fmaf(aa[u], ff[u].y, acc.y);
               acc.z = fmaf(aa[u], ff[u].z, acc.z); acc.w = fmaf(aa[u], ff[u].w, acc.w);
-              dirty = true;
             }
           }
         }
-        if (dirty) { float* p = sY + row * ST + 4 * li; atomicAdd(p, acc.x); atomicAdd(p + 1, acc.y); atomicAdd(p + 2, acc.z); atomicAdd(p + 3, acc.w); }
+        put(row, acc);
       }
     } else {
-      // ---- sampled (pull): stream the tile's column indices, test membership in U
+      // ---- sampled (pull): per-warp slice of the aligned column-index span
+      int* lE = reinterpret_cast<int*>(smt + L::list) + wid * 3 * TLIST;   // e, then row
+      int* lU = lE + TLIST;
+      float* lA = reinterpret_cast<float*>(lU + TLIST);
+      const float4* Fs4 = reinterpret_cast<const float4*>(Fs);
       const int ea = (int)(eb & 3);                 // eb - ea is 16-byte aligned
       const int32_t* cbase = col + (eb - ea);
       const int span = total + ea;
-      for (int base = 0; base < span; base += TR * 4 * TCU) {
+      const int Lw = ((span + 8 * 4 - 1) / (8 * 4)) * 4;   // multiple of 4
+      const int w0 = min(span, wid * Lw), w1 = min(span, w0 + Lw);
+      // first / last tile rows this warp can touch
+      const int lo = max(w0, ea), hi = w1 - 1;
+      const int rfirst = lo <= hi ? tile_row_of(sOff, rows, lo - ea) : -1;
+      const int rlast = lo <= hi ? tile_row_of(sOff, rows, hi - ea) : -1;
+      if (lane == 0) { sCr[2 * wid] = rfirst; sCr[2 * wid + 1] = rlast != rfirst ? rlast : -1; }
+      for (int base = w0; base < w1; base += TLIST) {
         int cv[4 * TCU];
 #pragma unroll
         for (int j = 0; j < TCU; ++j) {
-          const int q = base + 4 * (tid + TR * j);
-          if (q + 3 < span) {
+          const int q = base + 4 * (lane + 32 * j);
+          if (q + 3 < w1) {
             const int4 v = __ldg(reinterpret_cast<const int4*>(cbase + q));
             cv[4 * j] = v.x; cv[4 * j + 1] = v.y; cv[4 * j + 2] = v.z; cv[4 * j + 3] = v.w;
           } else {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) cv[4 * j + c] = (q + c < span) ? __ldg(cbase + q + c) : -1;
+            for (int c = 0; c < 4; ++c) cv[4 * j + c] = (q + c < w1) ? __ldg(cbase + q + c) : -1;
           }
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (q + c < ea) cv[4 * j + c] = -1;
         }
         uint2 tv[4 * TCU];
 #pragma unroll
-        for (int j = 0; j < 4 * TCU; ++j) {
-          const int q = base + 4 * (tid + TR * (j >> 2)) + (j & 3);
-          if (q < ea) cv[j] = -1;
-          tv[j] = cv[j] >= 0 ? __ldg(tab + (cv[j] >> 5)) : make_uint2(0u, 0u);
-        }
+        for (int j = 0; j < 4 * TCU; ++j) tv[j] = cv[j] >= 0 ? __ldg(tab + (cv[j] >> 5)) : make_uint2(0u, 0u);
+        // ordered compaction of the hits (nonzero order = row order)
+        int nh = 0;
 #pragma unroll
-        for (int j = 0; j < 4 * TCU; ++j) {
-          const int q = base + 4 * (tid + TR * (j >> 2)) + (j & 3);
-          const int c = cv[j];
-          const uint32_t bit = c >= 0 ? (tv[j].x >> (c & 31)) & 1u : 0u;
-          const uint32_t m = __ballot_sync(0xffffffffu, bit);
-          if (m == 0u) continue;
-          if (bit) {
-            const int rk = __popc(m & ((1u << lane) - 1u));
-            const int e = q - ea;                    // offset in the tile's nonzeros
-            wl[3 * rk] = tile_row_of(sOff, rows, e);
-            wl[3 * rk + 1] = (int)(tv[j].y + __popc(tv[j].x & ((1u << (c & 31)) - 1u)));
-            wl[3 * rk + 2] = __float_as_int(__ldg(val + eb + e));
+        for (int j = 0; j < TCU; ++j) {
+          uint32_t nib = 0u;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int cc = cv[4 * j + c];
+            nib |= (cc >= 0 ? (tv[4 * j + c].x >> (cc & 31)) & 1u : 0u) << c;
           }
-          __syncwarp();
-          const int nh = __popc(m);
-          for (int h = grp; h < nh; h += NG) {
-            const int row = wl[3 * h], u = wl[3 * h + 1];
-            const float a = __int_as_float(wl[3 * h + 2]);
-            sadd4<KP>(sY + row * ST + 4 * li, a, __ldg(Fs4 + (int64_t)u * LPR + li));
+          const int cnt = __popc(nib);
+          int incl = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int t2 = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t2;
+          }
+          int pos = nh + incl - cnt;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            if ((nib >> c) & 1u) {
+              const int cc = cv[4 * j + c];
+              lE[pos] = base + 4 * (lane + 32 * j) + c - ea;   // offset in the tile's nonzeros
+              lU[pos] = (int)(tv[4 * j + c].y + __popc(tv[4 * j + c].x & ((1u << (cc & 31)) - 1u)));
+              ++pos;
+            }
+          }
+          nh += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        __syncwarp();
+        for (int h = lane; h < nh; h += 32) {   // values and rows of the hits (independent loads)
+          const int e = lE[h];
+          lA[h] = __ldg(val + eb + e);
+          lE[h] = tile_row_of(sOff, rows, e);
+        }
+        __syncwarp();
+        // lane group g takes the g-th contiguous chunk of the (row-sorted) hit list: rows are
+        // accumulated in registers (4 gathers of Fs in flight) and written at row changes; a row
+        // straddling two chunks is added by the later group after the others (group order)
+        const int ch = (nh + NG - 1) / NG;
+        const int h0 = min(nh, grp * ch), h1 = min(nh, h0 + ch);
+        int row = h0 < h1 ? lE[h0] : -1;
+        const int row0 = row;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), acc0 = acc;
+        bool first = true;
+        auto flush = [&](int r, float4 v) {
+          float* dst = (r == rfirst) ? sC + (2 * wid) * KP : (r == rlast) ? sC + (2 * wid + 1) * KP : sY + r * ST;
+          float4* d4 = reinterpret_cast<float4*>(dst + 4 * li);
+          float4 cur = *d4;
+          cur.x += v.x; cur.y += v.y; cur.z += v.z; cur.w += v.w;
+          *d4 = cur;
+        };
+        for (int h = h0; h < h1; h += 4) {
+          float4 ff[4];
+          float aa[4];
+          int rr[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const bool ok = h + u < h1;
+            rr[u] = ok ? lE[h + u] : -1;
+            aa[u] = ok ? lA[h + u] : 0.f;
+            ff[u] = ok ? __ldg(Fs4 + (int64_t)lU[h + u] * LPR + li) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (rr[u] < 0) continue;
+            if (rr[u] != row) {            // row change: the finished row is this group's alone,
+              if (first) { acc0 = acc; first = false; }   // except the chunk's first row (deferred)
+              else flush(row, acc);
+              acc = make_float4(0.f, 0.f, 0.f, 0.f);
+              row = rr[u];
+            }
+            acc.x = fmaf(aa[u], ff[u].x, acc.x); acc.y = fmaf(aa[u], ff[u].y, acc.y);
+            acc.z = fmaf(aa[u], ff[u].z, acc.z); acc.w = fmaf(aa[u], ff[u].w, acc.w);
+          }
+        }
+        // the chunk's last row may continue in the next chunk: it is deferred as well
+        const float4 accl = acc;
+        const int rowl = row;
+        if (h0 < h1 && first) { acc0 = accl; }   // single-row chunk: one deferred partial
+        __syncwarp();
+        for (int g = 0; g < NG; ++g) {   // deferred partials in group order (no two writers at once)
+          if (grp == g && h0 < h1) {
+            flush(row0, acc0);
+            if (!first) flush(rowl, accl);
           }
           __syncwarp();
         }
       }
+    }
+    __syncthreads();
+    // ---- carries: runs of equal rows (consecutive slices) summed in slice order, added once
+    for (int e = tid; e < L::NCARRY * LPR; e += TR) {
+      const int c = e / LPR, q = e - c * LPR;
+      const int r = sCr[c];
+      if (r < 0) continue;
+      int prev = c - 1;
+      while (prev >= 0 && sCr[prev] < 0) --prev;
+      if (prev >= 0 && sCr[prev] == r) continue;   // not the head of its run
+      float4 s = *reinterpret_cast<const float4*>(sC + c * KP + 4 * q);
+      for (int c2 = c + 1; c2 < L::NCARRY; ++c2) {
+        const int r2 = sCr[c2];
+        if (r2 < 0) continue;
+        if (r2 != r) break;
+        const float4 v = *reinterpret_cast<const float4*>(sC + c2 * KP + 4 * q);
+        s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+      }
+      float4* d4 = reinterpret_cast<float4*>(sY + r * ST + 4 * q);
+      float4 cur = *d4;
+      cur.x += s.x; cur.y += s.y; cur.z += s.z; cur.w += s.w;
+      *d4 = cur;
     }
     __syncthreads();
     // ---- HALS sweep of row tid: b = y + alpha f, Gauss-Seidel over the KP columns
@@ -920,15 +998,10 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
       }
     }
     __syncthreads();
-    gt.tile(sY, rows, gacc);
+    gt.accumulate(sY, ST, rows, nullptr);
   }
   // ---- commit the CTA's X^T X into a replica of the global accumulator; last CTA finalizes
-  __syncthreads();
-  double* rep = Gacc + (size_t)(blockIdx.x % kGramReplicas) * KP * KP;
-  for (int e = tid; e < KP * KP; e += TR) {
-    const int a = e / KP, b = e - a * KP;
-    if (a <= b && gacc[e] != 0.0) atomicAdd(rep + e, gacc[e]);
-  }
+  gt.commit(Gacc, KP, reinterpret_cast<double*>(smt));
   if (arrive_last(counter)) {
     double* sa = reinterpret_cast<double*>(smt);
     finalize_gram<KP>(Gacc, Gout, KP, Rf32, sa, sa + KP * (KP + 1), status);
@@ -939,8 +1012,8 @@ template <int KP>
 static void csr_tile_sweep_t(const symnmf_matrix& A, const float* F, const float* Fs, const uint2* tab,
                              const double* G, double alpha, float* X, int64_t n, double* Gacc, double* Gout,
                              float* Rf32, unsigned int* counter, int32_t* status, cudaStream_t st) {
-  const size_t smem = std::max(sizeof(float) * TR * (KP + 4) + sizeof(double) * KP * KP + sizeof(int) * 8 * 96,
-                               sizeof(double) * 2 * KP * (KP + 1));
+  const size_t smem = std::max({Fs ? TileSmem<KP, true>::bytes : TileSmem<KP, false>::bytes,
+                                sizeof(double) * 2 * KP * (KP + 1), kRedBytes});
   const int64_t tiles = (n + TR - 1) / TR;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 2));
   if (Fs) {

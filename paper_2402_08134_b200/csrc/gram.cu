@@ -165,9 +165,16 @@ __global__ void cross_gram_finalize(const double* __restrict__ partial, int grid
   const int nba = (ka + 3) >> 2, nbb = (kb + 3) >> 2;
   const int pairs = sym ? nba * (nba + 1) / 2 : nba * nbb;
   const int P16 = pairs * 16;
-  for (int e = threadIdx.x; e < P16; e += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < grid; ++b) s += partial[(int64_t)b * P16 + e];
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < P16; e += gridDim.x * blockDim.x) {
+    // eight independent partial chains (fixed order: deterministic) keep 8 loads in flight
+    double s8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    int pb = 0;
+    for (; pb + 8 <= grid; pb += 8) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s8[q] += __ldcg(partial + (int64_t)(pb + q) * P16 + e);
+    }
+    for (; pb < grid; ++pb) s8[0] += __ldcg(partial + (int64_t)pb * P16 + e);
+    const double s = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
     const int p = e >> 4, i = (e >> 2) & 3, j = e & 3;
     int ai, bi;
     pair_to_blocks(p, nba, nbb, sym, ai, bi);
@@ -218,7 +225,7 @@ void launch_cross_gram(const float* A, int64_t lda, int ka, const float* B, int6
     if (fp64_products) SYMNMF_GRAM_LAUNCH(2, true); else SYMNMF_GRAM_LAUNCH(2, false);
   }
 #undef SYMNMF_GRAM_LAUNCH
-  cross_gram_finalize<<<1, 256, 0, st>>>(partial, grid, ka, kb, sym, out, ldo, status);
+  cross_gram_finalize<<<(pairs * 16 + 127) / 128, 128, 0, st>>>(partial, grid, ka, kb, sym, out, ldo, status);
 }
 
 // ---------------------------------------------------------------- (a2) Cholesky + inverse
