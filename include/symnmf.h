@@ -97,6 +97,16 @@ typedef struct {
   double theta;
 } symnmf_half_stats;
 
+/* Tuning knobs read from the environment when a call is enqueued (host only; results are
+ * the same up to fp32 summation order):
+ *   SYMNMF_CSR_TILE=always|never   EXACT solver on CSR: force / forbid the tile kernel (product
+ *                                  fused with the sweep); default: used from 16M nonzeros.
+ *   SYMNMF_SCATTER_SLICE_MB=<mb>   sampled CSR product: rows of Y per destination-range pass
+ *                                  (default 48 MB, so each pass's slice of Y stays in L2).
+ *   SYMNMF_SMALL=never             LvS solver: do not use the persistent one-launch-per-iteration
+ *                                  kernel for small problems (CSR n <= 2^20 or dense n <= 4096,
+ *                                  k in {8, 16, 32}, no per-iteration residual). */
+
 /* Library version (major*10000 + minor*100 + patch).  Host only. */
 int32_t symnmf_version(void);
 

@@ -3,7 +3,10 @@
 #include <cstdio>
 #include <new>
 #include <vector>
+#include <cstdlib>
+#include <cstring>
 #include "kernels.cuh"
+#include "small_args.cuh"
 
 using namespace symnmf;
 
@@ -421,9 +424,10 @@ struct symnmf_solver {
   SamplerWs sw;
   symnmf_plan plan;
   float* Y;
-  bool tile;               // CSR with kpad(k) == k: product fused into the sweep (csr_tile_sweep)
-  float* Fs;               // LvS tile path: compact omega-scaled sampled rows (cap x k)
-  uint2* tab;              // LvS tile path: U membership table, ceil(n/32) words
+  bool tile;               // EXACT on a large CSR A (kpad(k) == k): product fused into the sweep
+  bool small;              // LvS on a small problem: one persistent launch per iteration (small.cu)
+  double* Gacc2;           // second zeroed Gram accumulator (small path: G_s and X^T X)
+  unsigned int* bar;       // grid barrier words (small path)
   symnmf_half_stats* stats;
   double *resid, *rpart, *rout, *GH;
   double *Zpart, *Z;
@@ -443,6 +447,20 @@ struct symnmf_solver {
 };
 
 namespace {
+
+// LvS on small problems: the persistent iteration kernel; SYMNMF_SMALL=never disables it (symnmf.h)
+bool small_enabled() {
+  const char* e = getenv("SYMNMF_SMALL");
+  return !(e && !strcmp(e, "never"));
+}
+
+// EXACT CSR: the tile kernel from 16M nonzeros; SYMNMF_CSR_TILE=always|never overrides (symnmf.h)
+int64_t tile_min_nnz() {
+  const char* e = getenv("SYMNMF_CSR_TILE");
+  if (e && !strcmp(e, "always")) return 0;
+  if (e && !strcmp(e, "never")) return INT64_MAX;
+  return 16ll << 20;
+}
 
 // Profiling hook: records an event after the launch site just enqueued (no-op unless profiling).
 void mark(symnmf_solver& S, cudaStream_t st, const char* name) {
@@ -471,8 +489,12 @@ void solver_layout(symnmf_solver& S, Carver& c) {
   S.Gs = c.take<double>((size_t)k * k);
   S.GH = c.take<double>((size_t)k * k);
   S.gpart = c.take<double>(gram_partial_doubles(k, k, true, S.ggrid));
-  S.tile = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode != SYMNMF_LAI;
+  // the tile kernel balances hub rows; on small graphs the row-per-group SpMM + sweep is faster
+  S.tile = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode == SYMNMF_EXACT && S.A.nnz >= tile_min_nnz();
   S.Y = c.take<float>(S.tile ? 0 : (size_t)n * k);
+  S.small = S.mode == SYMNMF_LVS && !S.with_resid && S.hasA && small_lvs_supported(S.A, n, k) && small_enabled();
+  S.Gacc2 = c.take<double>(S.small ? (size_t)kGramReplicas * k * k : 0);
+  S.bar = c.take<unsigned int>(S.small ? 4 : 0);
   S.stats = c.take<symnmf_half_stats>((size_t)2 * S.max_iters);
   S.resid = c.take<double>((size_t)S.max_iters);
   S.rgrid = residual_grid(n);
@@ -489,8 +511,6 @@ void solver_layout(symnmf_solver& S, Carver& c) {
     S.plan.uniq_w = c.take<double>(n);
     S.plan.counts = c.take<int64_t>(4);
     S.plan.mass = c.take<double>(2);
-    S.Fs = c.take<float>(S.tile ? (size_t)S.plan.cap * k : 0);
-    S.tab = c.take<uint2>(S.tile ? (size_t)(n + 31) / 32 : 0);
   }
   if (S.mode == SYMNMF_LAI) {
     S.Zpart = c.take<double>(gram_partial_doubles(S.l, k, false, S.ggrid));
@@ -513,8 +533,7 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
   double* Gnext = S.Gbuf[side ^ 1];
   const bool lvs = S.mode == SYMNMF_LVS;
   if (S.mode == SYMNMF_EXACT && S.tile) {
-    launch_csr_tile_sweep(S.A, F, nullptr, nullptr, Gf, S.alpha, X, n, k, S.Gacc, Gnext, nullptr, S.counter, status,
-                          st);
+    launch_csr_tile_sweep(S.A, F, Gf, S.alpha, X, n, k, S.Gacc, Gnext, nullptr, S.counter, status, st);
     mark(S, st, "csr_tile_exact");
   } else if (S.mode == SYMNMF_EXACT) {
     if (!enqueue_product(S.A, F, k, S.Y, S.precision, S.tcs, S.tcs_bytes, status, st)) return false;
@@ -532,17 +551,10 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     launch_uniq_count_fused(S.lev, n, S.T, S.sw, S.plan, S.iter_dev, S.first_iter, S.max_iters, side, S.stats,
                             S.counter, status, st);
     mark(S, st, "samp_uniq_count");
-    launch_samp_uniq_write(S.lev, n, S.T, S.sw, S.plan, status, st, S.tab);
+    launch_samp_uniq_write(S.lev, n, S.T, S.sw, S.plan, status, st);
     mark(S, st, "samp_uniq_write");
-    launch_sampled_gram_fused(F, k, S.plan, S.Gacc, S.Gs, S.counter, status, st, S.Fs);
+    launch_sampled_gram_fused(F, k, S.plan, S.Gacc, S.Gs, S.counter, status, st);
     mark(S, st, "sampled_gram");
-    if (S.tile) {
-      // pull-form Y_s fused with Update(G_s + alpha I, Y_s + alpha F^T), X^T X and its R
-      launch_csr_tile_sweep(S.A, F, S.Fs, S.tab, S.Gs, S.alpha, X, n, k, S.Gacc, Gnext, S.Rinv32, S.counter, status,
-                            st);
-      mark(S, st, "csr_tile_lvs");
-      return true;
-    }
     if (S.A.kind == SYMNMF_CSR)
       launch_sampled_csr_nozero(S.A, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap, S.Y,
                                 status, st);
@@ -566,7 +578,21 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
   return true;
 }
 
+bool enqueue_small(symnmf_solver& S, cudaStream_t st) {
+  SmallArgs a{};
+  a.kind = S.A.kind; a.n = S.n; a.lda = S.A.lda; a.val = S.A.val; a.rowptr = S.A.rowptr; a.colidx = S.A.colidx;
+  a.W = S.W; a.H = S.H; a.k = S.k; a.alpha = S.alpha; a.T = S.T; a.s = S.s; a.seed = S.seed;
+  a.iter_dev = S.iter_dev; a.first_iter = S.first_iter; a.max_iters = S.max_iters; a.stats = S.stats;
+  a.lev = S.lev; a.bw = S.sw.bw; a.bd = S.sw.bd; a.bt = S.sw.bt; a.bu = S.sw.bu; a.P = S.sw.P; a.cnt = S.sw.cnt;
+  a.plan = S.plan; a.Y = S.Y; a.GsAcc = S.Gacc; a.GAcc = S.Gacc2; a.Gout = S.Gbuf[0]; a.R32 = S.Rinv32;
+  a.bar = S.bar; a.status = S.status;
+  if (!launch_small_lvs(a, st)) return false;
+  mark(S, st, "lvs_small");
+  return true;
+}
+
 bool enqueue_iteration(symnmf_solver& S, cudaStream_t st) {
+  if (S.small) return enqueue_small(S, st);
   if (!enqueue_half(S, 0, st) || !enqueue_half(S, 1, st)) return false;
   if (S.with_resid) {
     if (S.A.kind == SYMNMF_CSR) launch_spmm_csr(S.A, S.H, S.k, S.AHres, S.status, st);
@@ -619,7 +645,11 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
   SYMNMF_CUDA_TRY(cudaMemsetAsync(S.resid, 0, sizeof(double) * max_iters, st));
   SYMNMF_CUDA_TRY(cudaMemsetAsync(S.counter, 0, sizeof(unsigned int) * 4, st));
   SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Gacc, 0, sizeof(double) * kGramReplicas * k * k, st));
-  if (mode == SYMNMF_LVS && !S.tile) SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Y, 0, sizeof(float) * n * k, st));
+  if (S.small) {
+    SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Gacc2, 0, sizeof(double) * kGramReplicas * k * k, st));
+    SYMNMF_CUDA_TRY(cudaMemsetAsync(S.bar, 0, sizeof(unsigned int) * 4, st));
+  }
+  if (mode == SYMNMF_LVS) SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Y, 0, sizeof(float) * n * k, st));
   set_i32<<<1, 1, 0, st>>>(S.iter_dev, first_iter);
   // H^T H (and its CholeskyQR factor for LvS) for the first W-half; later halves get
   // theirs from the fused Gram of the preceding sweep.

@@ -16,256 +16,11 @@
 //  sampled_gram_fused  G_s = sum_{i in U} omega_i f_i^T f_i over the compact plan.
 // The "last CTA" pattern uses a per-call-site counter in the workspace that the last CTA
 // resets, so the kernels are CUDA-graph replay safe.
-#include "kernels.cuh"
+#include <cstdlib>
+#include "fused_common.cuh"
 
 
 namespace symnmf {
-
-// ---------------------------------------------------------------- helpers
-__device__ __forceinline__ bool arrive_last(unsigned int* counter) {
-  __shared__ bool last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x * gridDim.y - 1;
-  __syncthreads();
-  if (last) {
-    __threadfence();
-    if (threadIdx.x == 0) *counter = 0;
-  }
-  return last;
-}
-
-// One warp: fp64 Cholesky a = R^T R (upper, in place, ld = k + 1) of G + jitter I with one
-// retry, then x = R^{-1}.  Returns nonzero on failure.
-__device__ int warp_chol_inv(double* a, double* x, const double* G, int k, double shift_rel, bool inverse = true) {
-  const int lane = threadIdx.x & 31, ld = k + 1;
-  // G -> shared memory once (independent loads), trace from shared memory
-  for (int e = lane; e < k * k; e += 32) {
-    const int i = e / k, c = e - i * k;
-    x[i * ld + c] = G[e];
-  }
-  __syncwarp();
-  double tr = 0.0;
-  for (int i = 0; i < k; ++i) tr += x[i * ld + i];
-  int fail = 1;
-  for (int attempt = 0; attempt < 2 && fail; ++attempt) {
-    double jitter = shift_rel * tr + (attempt ? 1e-12 * tr / k : 0.0);
-    if (attempt && !(jitter > 0.0)) break;
-    for (int e = lane; e < k * ld; e += 32) {
-      const int i = e / ld, c = e - i * ld;
-      if (c < k) a[e] = x[e] + (i == c ? jitter : 0.0);
-    }
-    __syncwarp();
-    fail = 0;
-    for (int j = 0; j < k; ++j) {
-      const double d = a[j * ld + j];
-      if (!(d > 0.0) || !isfinite(d)) { fail = 1; break; }
-      const double r = sqrt(d), rinv = 1.0 / r;
-      __syncwarp();
-      for (int c = j + 1 + lane; c < k; c += 32) a[j * ld + c] *= rinv;
-      if (lane == 0) a[j * ld + j] = r;
-      __syncwarp();
-      for (int i = j + 1 + lane; i < k; i += 32) {      // lane-parallel rows of the trailing update
-        const double aji = a[j * ld + i];
-        for (int c = i; c < k; ++c) a[i * ld + c] = fma(-aji, a[j * ld + c], a[i * ld + c]);
-      }
-      __syncwarp();
-    }
-    __syncwarp();
-  }
-  if (fail) return 1;
-  if (!inverse) return 0;
-  for (int c = lane; c < k; c += 32) {
-    x[c * ld + c] = 1.0 / a[c * ld + c];
-    for (int i = c - 1; i >= 0; --i) {
-      double s = 0.0;
-      for (int j = i + 1; j <= c; ++j) s = fma(a[i * ld + j], x[j * ld + c], s);
-      x[i * ld + c] = -s / a[i * ld + i];
-    }
-    for (int i = c + 1; i < k; ++i) x[i * ld + c] = 0.0;
-  }
-  __syncwarp();
-  return 0;
-}
-
-// 1/sqrt(d) in fp64 without the long-latency fp64 sqrt and divide sequences: fp32 MUFU
-// estimate refined by two Newton steps (relative error ~1e-16 for normal d).
-__device__ __forceinline__ double rsqrt_fp64(double d) {
-  if (!(d > 1e-30 && d < 1e30)) return 1.0 / sqrt(d);   // outside the fp32 estimate's safe range
-  double y = (double)rsqrtf((float)d);
-  const double h = 0.5 * d;
-  y = y * fma(-h * y, y, 1.5);
-  y = y * fma(-h * y, y, 1.5);
-  return y;
-}
-
-// One warp, k <= KP <= 32: fp64 Cholesky G + jitter I = R^T R held in registers, lane c owning
-// column c (R[i][c], i <= c).  Step j broadcasts R[j][i] from lane i with compile-time shuffle
-// sources, so there is no shared memory traffic and no barrier.  Padding columns c >= k carry
-// the identity.  Writes R (fp32, KP x KP upper, zero padded) and rd = 1 / diag(R).
-// One factorisation pass over b (fully unrolled: every register index is a compile-time
-// constant, no break, so b stays in registers).  Returns nonzero if a pivot was not positive.
-template <int KP>
-__device__ __forceinline__ int chol_col_pass(double (&b)[KP], int lane, double& myr) {
-  int fail = 0;
-#pragma unroll
-  for (int j = 0; j < KP; ++j) {
-    const double d = __shfl_sync(0xffffffffu, b[j], j);
-    fail |= (!(d > 0.0) || !isfinite(d)) ? 1 : 0;
-    const double dd = fail ? 1.0 : d;
-    const double rinv = rsqrt_fp64(dd), r = dd * rinv;
-    if (lane == j) { b[j] = r; myr = r; }
-    else if (lane > j) b[j] *= rinv;                          // R[j][lane]
-#pragma unroll
-    for (int i = j + 1; i < KP; ++i) {
-      const double rji = __shfl_sync(0xffffffffu, b[j], i);   // R[j][i] from lane i
-      if (lane >= i) b[i] = fma(-rji, b[j], b[i]);            // A[i][lane] -= R[j][i] R[j][lane]
-    }
-  }
-  return fail;
-}
-
-template <int KP>
-__device__ int warp_chol_col(const double* G, int k, double shift_rel, float* R32, float* rd32) {
-  static_assert(KP <= 32, "one column per lane");
-  const int lane = threadIdx.x & 31;
-  double b[KP];   // column `lane` of G (re-read from G for the retry: keeps register use at KP doubles)
-  const double dl = lane < k ? G[lane * k + lane] : 0.0;
-  const double tr = warp_sum(dl);
-  double myr = 1.0;
-  double jitter = shift_rel * tr;
-#pragma unroll
-  for (int i = 0; i < KP; ++i)
-    b[i] = ((lane < k && i < k) ? G[i * k + lane] : (i == lane ? 1.0 : 0.0)) + ((i == lane && lane < k) ? jitter : 0.0);
-  int fail = chol_col_pass<KP>(b, lane, myr);
-  if (fail) {                                   // one retry with 1e-12 tr(G)/k on the diagonal
-    jitter += 1e-12 * tr / k;
-    if (!(jitter > 0.0)) return 1;
-#pragma unroll
-    for (int i = 0; i < KP; ++i)
-      b[i] = ((lane < k && i < k) ? G[i * k + lane] : (i == lane ? 1.0 : 0.0)) + ((i == lane && lane < k) ? jitter : 0.0);
-    fail = chol_col_pass<KP>(b, lane, myr);
-  }
-  if (fail) return 1;
-  if (lane < KP) {
-#pragma unroll
-    for (int i = 0; i < KP; ++i) R32[i * KP + lane] = (i <= lane && lane < k) ? (float)b[i] : 0.f;
-    rd32[lane] = lane < k ? (float)(1.0 / myr) : 0.f;
-  }
-  return 0;
-}
-
-// Per-thread share of a k x k Gram accumulated from row tiles in shared memory:
-// one upper 4x4 block (ai <= bi) per thread, row groups g = t / pairs.
-struct GramThread {
-  int ai, bi, g, RG, p;
-  bool active;
-  float acc[16];
-  double acc64[16];
-  int since;
-  __device__ void init(int t, int nthreads, int nb) {
-    const int pairs = nb * (nb + 1) / 2;
-    RG = nthreads / pairs;
-    g = t / pairs;
-    p = t - g * pairs;
-    active = g < RG;
-    int a = 0, rem = p;
-    while (rem >= nb - a) { rem -= nb - a; ++a; }
-    ai = a; bi = a + rem;
-#pragma unroll
-    for (int e = 0; e < 16; ++e) { acc[e] = 0.f; acc64[e] = 0.0; }
-    since = 0;
-  }
-  // rows r of s (row stride `stride` floats, 16B aligned), optional fp32 row weights w
-  __device__ void accumulate(const float* s, int stride, int rows, const float* w) {
-    if (!active) return;
-    for (int r = g; r < rows; r += RG) {
-      const float4 a4 = *reinterpret_cast<const float4*>(s + r * stride + 4 * ai);
-      const float4 b4 = *reinterpret_cast<const float4*>(s + r * stride + 4 * bi);
-      const float wr = w ? w[r] : 1.f;
-      const float a[4] = {a4.x * wr, a4.y * wr, a4.z * wr, a4.w * wr};
-      const float b[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i * 4 + j] = fmaf(a[i], b[j], acc[i * 4 + j]);
-    }
-    since += (rows + RG - 1) / RG;
-    if (since >= 64) flush();
-  }
-  __device__ void flush() {
-#pragma unroll
-    for (int e = 0; e < 16; ++e) { acc64[e] += (double)acc[e]; acc[e] = 0.f; }
-    since = 0;
-  }
-  // CTA-cooperative commit: reduce the row groups in shared memory (fixed order), then one
-  // fp64 red.add per Gram entry and CTA into replica blockIdx % kGramReplicas of the global
-  // accumulator (k x k upper triangle per replica): bounded same-address contention.
-  // `red` needs RG * pairs * 16 doubles (<= 32 KB); all threads of the CTA must call.
-  __device__ void commit(double* Gacc, int k, double* red) {
-    flush();
-    const int nb = (k + 3) >> 2, pairs = nb * (nb + 1) / 2, P16 = pairs * 16;
-    __syncthreads();
-    if (active) {
-#pragma unroll
-      for (int e = 0; e < 16; ++e) red[g * P16 + p * 16 + e] = acc64[e];
-    }
-    __syncthreads();
-    double* rep = Gacc + (size_t)(blockIdx.x % kGramReplicas) * k * k;
-    for (int idx = threadIdx.x; idx < P16; idx += blockDim.x) {
-      double s = 0.0;
-      for (int gg = 0; gg < RG; ++gg) s += red[gg * P16 + idx];
-      const int pp = idx >> 4, i = (idx >> 2) & 3, j = idx & 3;
-      int a0 = 0, rem = pp;
-      while (rem >= nb - a0) { rem -= nb - a0; ++a0; }
-      const int a = 4 * a0 + i, b = 4 * (a0 + rem) + j;
-      if (a < k && b < k && a <= b && s != 0.0) atomicAdd(rep + a * k + b, s);
-    }
-  }
-};
-
-// Last CTA: G_out (mirrored, fp64) <- sum of the accumulator replicas, replicas <- 0;
-// optional Cholesky -> R^{-1} fp32 (KP x KP).
-// Rf32 (nullable): CholeskyQR factor of G, R upper (KP x KP fp32) followed by 1 / diag(R) (KP).
-template <int KP>
-__device__ void finalize_gram(double* Gacc, double* Gout, int k, float* Rf32, double* sm_a, double* sm_x,
-                              int32_t* status) {
-  const int kk = k * k;
-  for (int e = threadIdx.x; e < kk; e += blockDim.x) {
-    const int a = e / k, b = e - a * k;
-    if (a > b) continue;
-    double v[kGramReplicas];
-#pragma unroll
-    for (int r = 0; r < kGramReplicas; ++r) v[r] = __ldcg(Gacc + (size_t)r * kk + e);
-    double s = 0.0;
-#pragma unroll
-    for (int r = 0; r < kGramReplicas; ++r) s += v[r];
-    Gout[a * k + b] = s;
-    Gout[b * k + a] = s;
-#pragma unroll
-    for (int r = 0; r < kGramReplicas; ++r) Gacc[(size_t)r * kk + e] = 0.0;
-  }
-  __syncthreads();
-  if (!Rf32) return;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    int fail;
-    if constexpr (KP <= 32) {
-      fail = warp_chol_col<KP>(Gout, k, 0.0, Rf32, Rf32 + KP * KP);
-    } else {
-      fail = warp_chol_inv(sm_a, sm_x, Gout, k, 0.0, /*inverse=*/false);
-      if (!fail) {
-        for (int e = threadIdx.x; e < KP * KP; e += 32) {
-          const int i = e / KP, c = e - i * KP;
-          Rf32[e] = (i <= c && c < k) ? (float)sm_a[i * (k + 1) + c] : 0.f;
-        }
-        for (int c = threadIdx.x; c < KP; c += 32) Rf32[KP * KP + c] = c < k ? (float)(1.0 / sm_a[c * (k + 1) + c]) : 0.f;
-      }
-    }
-    if (fail && threadIdx.x == 0) dev_fail(status, SYMNMF_ERR_NOT_PD);
-  }
-}
 
 // ---------------------------------------------------------------- gram_fused
 constexpr int FT = 256;         // threads per CTA
@@ -319,7 +74,7 @@ __global__ void __launch_bounds__(FT) gram_fused(const float* __restrict__ F, in
 
 // ---------------------------------------------------------------- sweep_fused
 template <int KP>
-__global__ void __launch_bounds__(FT) sweep_fused(const double* __restrict__ G, double alpha, float* __restrict__ Y,
+__global__ void __launch_bounds__(FT, KP <= 32 ? 2 : 1) sweep_fused(const double* __restrict__ G, double alpha, float* __restrict__ Y,
                                                   const float* __restrict__ F, float* __restrict__ X, int64_t n, int k,
                                                   int zeroY, double* Gacc, double* Gout, float* Rinv32,
                                                   unsigned int* counter, int32_t* status) {
@@ -385,19 +140,18 @@ __global__ void __launch_bounds__(FT) sweep_fused(const double* __restrict__ G, 
     }
     __syncwarp();
     if (lane < cnt) {
-      float x[KP], b[KP];
+      float x[KP];   // b = Y + alpha F stays in shared memory (read once per column)
+      const float* brow = wB + lane * ST;
 #pragma unroll
       for (int j = 0; j < KP; j += 4) {
         const float4 xv = *reinterpret_cast<const float4*>(wX + lane * ST + j);
-        const float4 bv = *reinterpret_cast<const float4*>(wB + lane * ST + j);
         x[j] = xv.x; x[j + 1] = xv.y; x[j + 2] = xv.z; x[j + 3] = xv.w;
-        b[j] = bv.x; b[j + 1] = bv.y; b[j + 2] = bv.z; b[j + 3] = bv.w;
       }
 #pragma unroll
       for (int i = 0; i < KP; ++i) {
         if (i < k) {
           // four independent partial sums: the column update is a short dependency chain
-          float s0 = b[i], s1 = 0.f, s2 = 0.f, s3 = 0.f;
+          float s0 = brow[i], s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
           for (int j = 0; j < KP; j += 4) {
             const float4 g = *reinterpret_cast<const float4*>(sG + i * KP + j);
@@ -622,8 +376,7 @@ __global__ void __launch_bounds__(FT) sampled_gram_fused(const float* __restrict
                                                          const int32_t* __restrict__ uniq,
                                                          const double* __restrict__ w,
                                                          const int64_t* __restrict__ n_uniq_dev, double* Gacc,
-                                                         double* Gout, float* __restrict__ Fs, unsigned int* counter,
-                                                         int32_t* status) {
+                                                         double* Gout, unsigned int* counter, int32_t* status) {
   constexpr int ST = KP + 4;
   constexpr int ROWS = 64;
   __shared__ __align__(16) float s[ROWS * ST];
@@ -664,15 +417,6 @@ __global__ void __launch_bounds__(FT) sampled_gram_fused(const float* __restrict
       }
     }
     __syncthreads();
-    if (Fs) {   // compact omega-scaled rows (|U| x KP) for the pull-form sampled product
-      for (int e = threadIdx.x; e < rows * (KP / 4); e += FT) {
-        const int r = e / (KP / 4), c = e - r * (KP / 4);
-        float4 v = *reinterpret_cast<const float4*>(s + r * ST + 4 * c);
-        const float om = sw[r];
-        v.x *= om; v.y *= om; v.z *= om; v.w *= om;
-        reinterpret_cast<float4*>(Fs)[(r0 + r) * (KP / 4) + c] = v;
-      }
-    }
     gt.accumulate(s, ST, rows, sw);
   }
   gt.commit(Gacc, k, red);
@@ -680,24 +424,16 @@ __global__ void __launch_bounds__(FT) sampled_gram_fused(const float* __restrict
 }
 
 // ---------------------------------------------------------------- csr_tile_sweep
-// One 256-row tile of the fixed-factor product, computed in shared memory, then swept.
-//   SAMPLED = false: y_c = sum_e A[c, col_e] F[col_e, :]  (Y = A F).  The tile's nonzeros
-//                    are split into 32 equal slices, one per lane group; a group accumulates a row
-//                    in registers and stores it once (rows interior to its slice are its own), the
-//                    first / last row of a slice go to carry slots that are combined in slice order
-//                    afterwards -- no atomics, deterministic, and hub rows are spread over groups.
-//   SAMPLED = true:  y_c = sum_{i in U} omega_i A[i, c] f_i = sum_{i in row c, i in U} A[c, i] Fs[u(i)]
-//                    (Y_s = (SA)^T(SF); row c of A = column c).  Each warp
-//                    streams an equal slice of the tile's column indices (coalesced 128-bit loads),
-//                    tests them against the U membership table, compacts the hits in nonzero order,
-//                    loads their values, and reduces runs of equal rows across its lane groups with a
-//                    segmented shuffle scan (boundary rows again through carries).
-// Then thread r sweeps row r (Eq. 2.6) with G (+alpha I) and b = y + alpha f_r, writes
-// X, and the updated rows of the tile are accumulated into X^T X (fp32 per tile, fp64 registers
-// across tiles), committed once per CTA; the last CTA forms X^T X and its Cholesky factor.
+// Exact CSR product fused with the sweep, for graphs with hub rows: one 256-row tile of
+// Y = A F is computed in shared memory, then swept.  The tile's nonzeros are split into
+// 32 equal slices, one per lane group; a group accumulates a row in registers and stores it once
+// (rows interior to its slice are its own); the first / last row of a slice go to carry slots
+// that are combined in slice order afterwards -- no atomics, deterministic, and a hub row is
+// spread over many groups instead of serialising one.  Then thread r sweeps row r (Eq. 2.6,
+// P:170-175) with G (+alpha I) and b = y + alpha f_r (formed in shared memory), writes X, and the
+// updated rows of the tile are accumulated into X^T X (fp32 per tile, fp64 per-thread slots in
+// shared memory), committed once per CTA; the last CTA forms X^T X and its Cholesky factor.
 constexpr int TR = 256;          // rows per tile = threads per CTA
-constexpr int TCU = 4;           // int4 column-index loads per lane per batch (sampled): 512 nonzeros
-constexpr int TLIST = 32 * 4 * TCU;
 constexpr int TUE = 8;           // gathers in flight per lane group (exact)
 
 __device__ __forceinline__ int tile_row_of(const int* sOff, int rows, int e) {   // sOff[r] <= e < sOff[r+1]
@@ -709,25 +445,75 @@ __device__ __forceinline__ int tile_row_of(const int* sOff, int rows, int e) {  
   return lo;
 }
 
-template <int KP, bool SAMPLED>
+// Per-thread upper 4x4 block (ai <= bi) of the tile Gram over row groups g: fp32 over one tile,
+// added into this thread's own fp64 slot in shared memory (no atomics, no fp64 registers).
+template <int KP>
+struct GramTile {
+  static constexpr int NB = KP / 4, PAIRS = NB * (NB + 1) / 2;
+  int ai, bi, g, RG, p;
+  bool active;
+  __device__ void init(int t) {
+    RG = TR / PAIRS;
+    g = t / PAIRS;
+    p = t - g * PAIRS;
+    active = g < RG;
+    int a = 0, rem = p;
+    while (rem >= NB - a) { rem -= NB - a; ++a; }
+    ai = a; bi = a + rem;
+  }
+  __device__ void tile(const float* s, int stride, int rows, double* slot) const {
+    if (!active) return;
+    float acc[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+    for (int r = g; r < rows; r += RG) {
+      const float4 a4 = *reinterpret_cast<const float4*>(s + r * stride + 4 * ai);
+      const float4 b4 = *reinterpret_cast<const float4*>(s + r * stride + 4 * bi);
+      const float a[4] = {a4.x, a4.y, a4.z, a4.w}, b[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i * 4 + j] = fmaf(a[i], b[j], acc[i * 4 + j]);
+    }
+    double* my = slot + (size_t)threadIdx.x * 16;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) my[e] += (double)acc[e];
+  }
+  // CTA commit: the row groups' slots summed in fixed order, one fp64 red.add per entry into a
+  // replica of the global accumulator.  All threads must call.
+  __device__ void commit(const double* slot, double* Gacc) const {
+    __syncthreads();
+    double* rep = Gacc + (size_t)(blockIdx.x % kGramReplicas) * KP * KP;
+    for (int idx = threadIdx.x; idx < PAIRS * 16; idx += TR) {
+      const int pp = idx >> 4, e = idx & 15;
+      double sum = 0.0;
+      for (int gg = 0; gg < TR / PAIRS; ++gg) sum += slot[(size_t)(gg * PAIRS + pp) * 16 + e];
+      int a0 = 0, rem = pp;
+      while (rem >= NB - a0) { rem -= NB - a0; ++a0; }
+      const int a = 4 * a0 + (e >> 2), b = 4 * (a0 + rem) + (e & 3);
+      if (a <= b && sum != 0.0) atomicAdd(rep + a * KP + b, sum);
+    }
+  }
+};
+
+template <int KP>
 struct TileSmem {
   static constexpr int ST = KP + 4;
-  static constexpr int NSLICE = SAMPLED ? TR / 32 : (TR / 32) * (32 / (KP / 4));   // warps or lane groups
+  static constexpr int NSLICE = (TR / 32) * (32 / (KP / 4));   // lane groups
   static constexpr int NCARRY = 2 * NSLICE;
   static constexpr size_t y = 0;                                               // float [TR][ST]
   static constexpr size_t carry = y + sizeof(float) * TR * ST;                 // float [NCARRY][KP]
   static constexpr size_t crow = carry + sizeof(float) * NCARRY * KP;          // int [NCARRY]
-  static constexpr size_t list = crow + sizeof(int) * NCARRY;                  // per warp: int e/row, int u, float a
-  static constexpr size_t bytes = list + (SAMPLED ? sizeof(int) * 3 * TLIST * (TR / 32) : 0);
+  static constexpr size_t gram = crow + sizeof(int) * NCARRY;                  // double [TR][16]
+  static constexpr size_t bytes = gram + sizeof(double) * TR * 16;
 };
 
-template <int KP, bool SAMPLED>
+template <int KP>
 __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
     const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, const float* __restrict__ val, int64_t n,
-    const float* __restrict__ F, const float* __restrict__ Fs, const uint2* __restrict__ tab,
-    const double* __restrict__ G, double alpha, float* __restrict__ X, double* Gacc, double* Gout, float* Rf32,
-    unsigned int* counter, int32_t* status) {
-  using L = TileSmem<KP, SAMPLED>;
+    const float* __restrict__ F, const double* __restrict__ G, double alpha, float* __restrict__ X, double* Gacc,
+    double* Gout, float* Rf32, unsigned int* counter, int32_t* status) {
+  using L = TileSmem<KP>;
   constexpr int ST = L::ST, LPR = KP / 4, NG = 32 / LPR;
   __shared__ __align__(16) float sG[KP * KP];     // sG[i*KP + j] = G[j][i], 0 on the diagonal
   __shared__ float sInv[KP];
@@ -748,8 +534,11 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
     sOk[i] = den > 0.0;
     sInv[i] = den > 0.0 ? (float)(1.0 / den) : 0.f;
   }
-  GramThread gt;
-  gt.init(tid, TR, KP / 4);
+  double* gslot = reinterpret_cast<double*>(smt + L::gram);
+#pragma unroll
+  for (int e = 0; e < 16; ++e) gslot[tid * 16 + e] = 0.0;
+  GramTile<KP> gt;
+  gt.init(tid);
   const float a32 = (float)alpha;
   const float4* F4 = reinterpret_cast<const float4*>(F);
   const int64_t tiles = (n + TR - 1) / TR;
@@ -757,6 +546,14 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
     const int64_t r0 = t * TR;
     const int rows = (int)min64(TR, n - r0);
     const int64_t eb = rowptr[r0];
+    if (tid < rows) {   // the sweep's X and F rows: fetched into L2 while the product runs
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(X + (r0 + tid) * KP));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(F + (r0 + tid) * KP));
+      if (KP == 64) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(X + (r0 + tid) * KP + 32));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(F + (r0 + tid) * KP + 32));
+      }
+    }
     __syncthreads();   // previous tile's Gram reads of sY are done
     {
       const int64_t ep = rowptr[r0 + min(tid, rows)];
@@ -769,8 +566,8 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
     }
     __syncthreads();
     const int total = sOff[TR];
-    if constexpr (!SAMPLED) {
-      // ---- exact: nnz-balanced slices, one per lane group; rows owned or carried
+    {
+      // ---- nnz-balanced slices, one per lane group; rows owned or carried
       const int sl = wid * NG + grp;
       const int Ls = (total + L::NSLICE - 1) / L::NSLICE;
       const int s0 = min(total, sl * Ls), s1 = min(total, s0 + Ls);
@@ -813,130 +610,6 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
         }
         put(row, acc);
       }
-    } else {
-      // ---- sampled (pull): per-warp slice of the aligned column-index span
-      int* lE = reinterpret_cast<int*>(smt + L::list) + wid * 3 * TLIST;   // e, then row
-      int* lU = lE + TLIST;
-      float* lA = reinterpret_cast<float*>(lU + TLIST);
-      const float4* Fs4 = reinterpret_cast<const float4*>(Fs);
-      const int ea = (int)(eb & 3);                 // eb - ea is 16-byte aligned
-      const int32_t* cbase = col + (eb - ea);
-      const int span = total + ea;
-      const int Lw = ((span + 8 * 4 - 1) / (8 * 4)) * 4;   // multiple of 4
-      const int w0 = min(span, wid * Lw), w1 = min(span, w0 + Lw);
-      // first / last tile rows this warp can touch
-      const int lo = max(w0, ea), hi = w1 - 1;
-      const int rfirst = lo <= hi ? tile_row_of(sOff, rows, lo - ea) : -1;
-      const int rlast = lo <= hi ? tile_row_of(sOff, rows, hi - ea) : -1;
-      if (lane == 0) { sCr[2 * wid] = rfirst; sCr[2 * wid + 1] = rlast != rfirst ? rlast : -1; }
-      for (int base = w0; base < w1; base += TLIST) {
-        int cv[4 * TCU];
-#pragma unroll
-        for (int j = 0; j < TCU; ++j) {
-          const int q = base + 4 * (lane + 32 * j);
-          if (q + 3 < w1) {
-            const int4 v = __ldg(reinterpret_cast<const int4*>(cbase + q));
-            cv[4 * j] = v.x; cv[4 * j + 1] = v.y; cv[4 * j + 2] = v.z; cv[4 * j + 3] = v.w;
-          } else {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) cv[4 * j + c] = (q + c < w1) ? __ldg(cbase + q + c) : -1;
-          }
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (q + c < ea) cv[4 * j + c] = -1;
-        }
-        uint2 tv[4 * TCU];
-#pragma unroll
-        for (int j = 0; j < 4 * TCU; ++j) tv[j] = cv[j] >= 0 ? __ldg(tab + (cv[j] >> 5)) : make_uint2(0u, 0u);
-        // ordered compaction of the hits (nonzero order = row order)
-        int nh = 0;
-#pragma unroll
-        for (int j = 0; j < TCU; ++j) {
-          uint32_t nib = 0u;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const int cc = cv[4 * j + c];
-            nib |= (cc >= 0 ? (tv[4 * j + c].x >> (cc & 31)) & 1u : 0u) << c;
-          }
-          const int cnt = __popc(nib);
-          int incl = cnt;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int t2 = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t2;
-          }
-          int pos = nh + incl - cnt;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            if ((nib >> c) & 1u) {
-              const int cc = cv[4 * j + c];
-              lE[pos] = base + 4 * (lane + 32 * j) + c - ea;   // offset in the tile's nonzeros
-              lU[pos] = (int)(tv[4 * j + c].y + __popc(tv[4 * j + c].x & ((1u << (cc & 31)) - 1u)));
-              ++pos;
-            }
-          }
-          nh += __shfl_sync(0xffffffffu, incl, 31);
-        }
-        __syncwarp();
-        for (int h = lane; h < nh; h += 32) {   // values and rows of the hits (independent loads)
-          const int e = lE[h];
-          lA[h] = __ldg(val + eb + e);
-          lE[h] = tile_row_of(sOff, rows, e);
-        }
-        __syncwarp();
-        // lane group g takes the g-th contiguous chunk of the (row-sorted) hit list: rows are
-        // accumulated in registers (4 gathers of Fs in flight) and written at row changes; a row
-        // straddling two chunks is added by the later group after the others (group order)
-        const int ch = (nh + NG - 1) / NG;
-        const int h0 = min(nh, grp * ch), h1 = min(nh, h0 + ch);
-        int row = h0 < h1 ? lE[h0] : -1;
-        const int row0 = row;
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), acc0 = acc;
-        bool first = true;
-        auto flush = [&](int r, float4 v) {
-          float* dst = (r == rfirst) ? sC + (2 * wid) * KP : (r == rlast) ? sC + (2 * wid + 1) * KP : sY + r * ST;
-          float4* d4 = reinterpret_cast<float4*>(dst + 4 * li);
-          float4 cur = *d4;
-          cur.x += v.x; cur.y += v.y; cur.z += v.z; cur.w += v.w;
-          *d4 = cur;
-        };
-        for (int h = h0; h < h1; h += 4) {
-          float4 ff[4];
-          float aa[4];
-          int rr[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const bool ok = h + u < h1;
-            rr[u] = ok ? lE[h + u] : -1;
-            aa[u] = ok ? lA[h + u] : 0.f;
-            ff[u] = ok ? __ldg(Fs4 + (int64_t)lU[h + u] * LPR + li) : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (rr[u] < 0) continue;
-            if (rr[u] != row) {            // row change: the finished row is this group's alone,
-              if (first) { acc0 = acc; first = false; }   // except the chunk's first row (deferred)
-              else flush(row, acc);
-              acc = make_float4(0.f, 0.f, 0.f, 0.f);
-              row = rr[u];
-            }
-            acc.x = fmaf(aa[u], ff[u].x, acc.x); acc.y = fmaf(aa[u], ff[u].y, acc.y);
-            acc.z = fmaf(aa[u], ff[u].z, acc.z); acc.w = fmaf(aa[u], ff[u].w, acc.w);
-          }
-        }
-        // the chunk's last row may continue in the next chunk: it is deferred as well
-        const float4 accl = acc;
-        const int rowl = row;
-        if (h0 < h1 && first) { acc0 = accl; }   // single-row chunk: one deferred partial
-        __syncwarp();
-        for (int g = 0; g < NG; ++g) {   // deferred partials in group order (no two writers at once)
-          if (grp == g && h0 < h1) {
-            flush(row0, acc0);
-            if (!first) flush(rowl, accl);
-          }
-          __syncwarp();
-        }
-      }
     }
     __syncthreads();
     // ---- carries: runs of equal rows (consecutive slices) summed in slice order, added once
@@ -961,23 +634,33 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
       *d4 = cur;
     }
     __syncthreads();
-    // ---- HALS sweep of row tid: b = y + alpha f, Gauss-Seidel over the KP columns
+    // ---- b = y + alpha f for the tile (coalesced: the tile's F rows are contiguous)
+    {
+      const float4* Ft = F4 + r0 * LPR;
+      for (int q = tid; q < rows * LPR; q += TR) {
+        const int r = q / LPR, c = q - r * LPR;
+        const float4 fv = __ldg(Ft + q);
+        float4* d4 = reinterpret_cast<float4*>(sY + r * ST + 4 * c);
+        float4 y = *d4;
+        y.x = fmaf(a32, fv.x, y.x); y.y = fmaf(a32, fv.y, y.y); y.z = fmaf(a32, fv.z, y.z); y.w = fmaf(a32, fv.w, y.w);
+        *d4 = y;
+      }
+    }
+    __syncthreads();
+    // ---- HALS sweep of row tid, Gauss-Seidel over the KP columns (x in registers, b in smem)
     if (tid < rows) {
       const int64_t r = r0 + tid;
-      float x[KP], b[KP];
+      float x[KP];
       const float4* X4 = reinterpret_cast<const float4*>(X + r * KP);
 #pragma unroll
       for (int j = 0; j < KP; j += 4) {
         const float4 xv = X4[j / 4];
-        const float4 fv = __ldg(F4 + r * LPR + j / 4);
-        const float4 yv = *reinterpret_cast<const float4*>(sY + tid * ST + j);
         x[j] = xv.x; x[j + 1] = xv.y; x[j + 2] = xv.z; x[j + 3] = xv.w;
-        b[j] = fmaf(a32, fv.x, yv.x); b[j + 1] = fmaf(a32, fv.y, yv.y);
-        b[j + 2] = fmaf(a32, fv.z, yv.z); b[j + 3] = fmaf(a32, fv.w, yv.w);
       }
+      const float* brow = sY + tid * ST;
 #pragma unroll
       for (int i = 0; i < KP; ++i) {
-        float s0 = b[i], s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        float s0 = brow[i], s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
         for (int j = 0; j < KP; j += 4) {
           const float4 g = *reinterpret_cast<const float4*>(sG + i * KP + j);
@@ -986,8 +669,8 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
           s2 = fmaf(-x[j + 2], g.z, s2);
           s3 = fmaf(-x[j + 3], g.w, s3);
         }
-        const float s = (s0 + s1) + (s2 + s3);
-        if (sOk[i]) x[i] = fmaxf(0.f, s * sInv[i]);
+        const float sv = (s0 + s1) + (s2 + s3);
+        if (sOk[i]) x[i] = fmaxf(0.f, sv * sInv[i]);
       }
       float4* Xw = reinterpret_cast<float4*>(X + r * KP);
 #pragma unroll
@@ -998,10 +681,10 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
       }
     }
     __syncthreads();
-    gt.accumulate(sY, ST, rows, nullptr);
+    gt.tile(sY, ST, rows, gslot);
   }
   // ---- commit the CTA's X^T X into a replica of the global accumulator; last CTA finalizes
-  gt.commit(Gacc, KP, reinterpret_cast<double*>(smt));
+  gt.commit(gslot, Gacc);
   if (arrive_last(counter)) {
     double* sa = reinterpret_cast<double*>(smt);
     finalize_gram<KP>(Gacc, Gout, KP, Rf32, sa, sa + KP * (KP + 1), status);
@@ -1009,32 +692,25 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
 }
 
 template <int KP>
-static void csr_tile_sweep_t(const symnmf_matrix& A, const float* F, const float* Fs, const uint2* tab,
-                             const double* G, double alpha, float* X, int64_t n, double* Gacc, double* Gout,
-                             float* Rf32, unsigned int* counter, int32_t* status, cudaStream_t st) {
-  const size_t smem = std::max({Fs ? TileSmem<KP, true>::bytes : TileSmem<KP, false>::bytes,
-                                sizeof(double) * 2 * KP * (KP + 1), kRedBytes});
+static void csr_tile_sweep_t(const symnmf_matrix& A, const float* F, const double* G, double alpha, float* X, int64_t n,
+                             double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
+                             cudaStream_t st) {
+  const size_t smem = std::max({TileSmem<KP>::bytes, sizeof(double) * 2 * KP * (KP + 1), kRedBytes});
   const int64_t tiles = (n + TR - 1) / TR;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 2));
-  if (Fs) {
-    cudaFuncSetAttribute(csr_tile_sweep<KP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    launch_pdl(csr_tile_sweep<KP, true>, grid, TR, smem, st, A.rowptr, A.colidx, A.val, n, F, Fs, tab, G, alpha, X,
-               Gacc, Gout, Rf32, counter, status);
-  } else {
-    cudaFuncSetAttribute(csr_tile_sweep<KP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    launch_pdl(csr_tile_sweep<KP, false>, grid, TR, smem, st, A.rowptr, A.colidx, A.val, n, F, Fs, tab, G, alpha, X,
-               Gacc, Gout, Rf32, counter, status);
-  }
+  cudaFuncSetAttribute(csr_tile_sweep<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  launch_pdl(csr_tile_sweep<KP>, grid, TR, smem, st, A.rowptr, A.colidx, A.val, n, F, G, alpha, X, Gacc, Gout, Rf32,
+             counter, status);
 }
 
-void launch_csr_tile_sweep(const symnmf_matrix& A, const float* F, const float* Fs, const uint2* tab,
-                           const double* G, double alpha, float* X, int64_t n, int k, double* Gacc, double* Gout,
-                           float* Rf32, unsigned int* counter, int32_t* status, cudaStream_t st) {
+void launch_csr_tile_sweep(const symnmf_matrix& A, const float* F, const double* G, double alpha, float* X, int64_t n,
+                           int k, double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
+                           cudaStream_t st) {
   switch (k) {
-    case 8: csr_tile_sweep_t<8>(A, F, Fs, tab, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
-    case 16: csr_tile_sweep_t<16>(A, F, Fs, tab, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
-    case 32: csr_tile_sweep_t<32>(A, F, Fs, tab, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
-    default: csr_tile_sweep_t<64>(A, F, Fs, tab, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
+    case 8: csr_tile_sweep_t<8>(A, F, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
+    case 16: csr_tile_sweep_t<16>(A, F, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
+    case 32: csr_tile_sweep_t<32>(A, F, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
+    default: csr_tile_sweep_t<64>(A, F, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
   }
 }
 
@@ -1113,14 +789,13 @@ void launch_uniq_count_fused(const float* lev, int64_t n, double T, const Sample
 }
 
 void launch_sampled_gram_fused(const float* F, int k, const symnmf_plan& plan, double* Gacc, double* Gout,
-                               unsigned int* counter, int32_t* status, cudaStream_t st, float* Fs) {
+                               unsigned int* counter, int32_t* status, cudaStream_t st) {
   const int grid = fused_grid((plan.cap + 63) / 64, 1);
-  if (Fs && kpad(k) != k) Fs = nullptr;   // the compact table needs float4 rows
   switch (kpad(k)) {
-    case 8: launch_pdl(sampled_gram_fused<8>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, Fs, counter, status); break;
-    case 16: launch_pdl(sampled_gram_fused<16>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, Fs, counter, status); break;
-    case 32: launch_pdl(sampled_gram_fused<32>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, Fs, counter, status); break;
-    default: launch_pdl(sampled_gram_fused<64>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, Fs, counter, status); break;
+    case 8: launch_pdl(sampled_gram_fused<8>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
+    case 16: launch_pdl(sampled_gram_fused<16>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
+    case 32: launch_pdl(sampled_gram_fused<32>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
+    default: launch_pdl(sampled_gram_fused<64>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
   }
 }
 

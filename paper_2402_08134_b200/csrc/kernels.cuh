@@ -86,28 +86,30 @@ void launch_leverage_fused(const float* F, int64_t n, int k, const float* Rinv, 
 void launch_uniq_count_fused(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
                              const int32_t* iter_dev, int32_t first_iter, int32_t max_iters, int side,
                              symnmf_half_stats* stats, unsigned int* counter, int32_t* status, cudaStream_t st);
-// Fs (nullable, k in {8,16,32,64}): compact omega-scaled sampled rows, |U| x k, for the pull-form Y_s
 void launch_sampled_gram_fused(const float* F, int k, const symnmf_plan& plan, double* Gacc, double* Gout,
-                               unsigned int* counter, int32_t* status, cudaStream_t st, float* Fs = nullptr);
-// CSR tile kernel: Y of 256-row tiles computed in shared memory (exact: A F with nnz-balanced
-// slices; sampled: pull form of Y_s through the symmetric structure, U membership table `tab`,
-// compact scaled rows Fs), then the HALS sweep of the tile, the Gram of the updated rows and
-// (last CTA) its Cholesky factor.  Requires kpad(k) == k.
-void launch_csr_tile_sweep(const symnmf_matrix& A, const float* F, const float* Fs, const uint2* tab,
-                           const double* G, double alpha, float* X, int64_t n, int k, double* Gacc, double* Gout,
-                           float* Rf32, unsigned int* counter, int32_t* status, cudaStream_t st);
+                               unsigned int* counter, int32_t* status, cudaStream_t st);
+// Exact CSR product fused with the sweep (csr_tile_sweep): 256-row tiles of Y = A F in shared
+// memory with nnz-balanced slices (hub rows spread over lane groups), the HALS sweep of the tile,
+// the Gram of the updated rows and (last CTA) its Cholesky factor.  Requires kpad(k) == k.
+void launch_csr_tile_sweep(const symnmf_matrix& A, const float* F, const double* G, double alpha, float* X, int64_t n,
+                           int k, double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
+                           cudaStream_t st);
 // sampler.cu passes used by the fused path
 void launch_samp_prefix(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
                         int32_t* status, cudaStream_t st);
 void launch_samp_draws(const SamplerWs& w, int64_t n, int64_t s, uint64_t seed, const int32_t* iter_dev,
                        uint32_t iteration, uint32_t side, const symnmf_plan& plan, int32_t* status, cudaStream_t st);
-// tab (nullable): [ceil(n/32)] {bits of U rows in word, U rows before the word} (pull-form Y_s)
 void launch_samp_uniq_write(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
-                            int32_t* status, cudaStream_t st, uint2* tab = nullptr);
+                            int32_t* status, cudaStream_t st);
 // sampled CSR scatter into a Y the caller has zeroed
 void launch_sampled_csr_nozero(const symnmf_matrix& A, const float* F, int k, const int32_t* uniq, const double* w,
                                const int64_t* n_uniq_dev, int64_t cap, float* Y, const int32_t* status,
                                cudaStream_t st);
+
+// ---------------------------------------------------------------- small.cu
+struct SmallArgs;
+bool small_lvs_supported(const symnmf_matrix& A, int64_t n, int k);
+bool launch_small_lvs(const SmallArgs& a, cudaStream_t st);
 
 // ---------------------------------------------------------------- residual.cu
 void launch_residual(const symnmf_matrix& A, const float* H, int k, const float* AH, const double* G,

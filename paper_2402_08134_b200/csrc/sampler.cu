@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(ST) samp_uniq_write(const float* __restrict__ 
                                                       int32_t* __restrict__ cnt, const uint32_t* __restrict__ bu,
                                                       const int64_t* __restrict__ counts, int32_t* __restrict__ uniq,
                                                       double* __restrict__ uw, int64_t cap,
-                                                      uint2* __restrict__ tab, const int32_t* __restrict__ status) {
+                                                      const int32_t* __restrict__ status) {
   __shared__ uint32_t sh[33];
   if (dev_failed(status)) return;
   const int64_t i0 = (int64_t)blockIdx.x * kSampBlock + threadIdx.x * 4;
@@ -234,16 +234,6 @@ __global__ void __launch_bounds__(ST) samp_uniq_write(const float* __restrict__ 
     tf += f[e];
   }
   uint32_t r = block_excl_scan(tf, sh, (uint32_t*)nullptr) + bu[blockIdx.x];
-  if (tab) {
-    // membership table of U for the pull-form sampled product: word w = rows [32w, 32w + 32),
-    // {bit mask of rows in U, number of U rows before 32w}; 8 lanes x 4 rows per word
-    const int lane = threadIdx.x & 31;
-    uint32_t word = (f[0] | (f[1] << 1) | (f[2] << 2) | (f[3] << 3)) << (4 * (lane & 7));
-    word |= __shfl_xor_sync(0xffffffffu, word, 1);
-    word |= __shfl_xor_sync(0xffffffffu, word, 2);
-    word |= __shfl_xor_sync(0xffffffffu, word, 4);
-    if ((lane & 7) == 0 && i0 < n) tab[i0 >> 5] = make_uint2(word, r);
-  }
   const double W = (double)(uint64_t)counts[3];
   const double sR = (double)counts[1];
 #pragma unroll
@@ -284,9 +274,9 @@ void launch_samp_draws(const SamplerWs& w, int64_t n, int64_t s, uint64_t seed, 
 }
 
 void launch_samp_uniq_write(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
-                            int32_t* status, cudaStream_t st, uint2* tab) {
+                            int32_t* status, cudaStream_t st) {
   launch_pdl(samp_uniq_write, (unsigned)samp_blocks(n), ST, 0, st, lev, n, T, w.cnt, w.bu, plan.counts, plan.uniq_idx,
-                                                           plan.uniq_w, plan.cap, tab, status);
+                                                           plan.uniq_w, plan.cap, status);
 }
 
 void launch_hybrid_sample(const float* lev, int64_t n, int k, int64_t s, double T, uint64_t seed,
@@ -300,7 +290,7 @@ void launch_hybrid_sample(const float* lev, int64_t n, int k, int64_t s, double 
   samp_uniq_counts<<<(unsigned)nb, ST, 0, st>>>(lev, n, T, w.cnt, w.bu, status);
   samp_scan_uniq<<<1, 1024, 0, st>>>(nb, w.bu, plan.cap, plan.counts, status);
   samp_uniq_write<<<(unsigned)nb, ST, 0, st>>>(lev, n, T, w.cnt, w.bu, plan.counts, plan.uniq_idx, plan.uniq_w,
-                                               plan.cap, (uint2*)nullptr, status);
+                                               plan.cap, status);
 }
 
 }  // namespace symnmf

@@ -7,6 +7,7 @@
 // independent gathers of F rows (128-bit loads).  Sampled: one warp per
 // sampled row; groups of k/4 lanes scatter-add omega_i a_ic f_i into row c of
 // Y_s with 128-bit vector atomics (red.global.add.v4.f32).
+#include <cstdlib>
 #include "kernels.cuh"
 
 namespace symnmf {
@@ -70,6 +71,13 @@ __global__ void __launch_bounds__(256) spmm_csr_scalar(const int64_t* __restrict
   }
 }
 
+// Y slice per scatter pass (L2 is 126 MB); SYMNMF_SCATTER_SLICE_MB overrides (symnmf.h)
+static int64_t scatter_slice_bytes() {
+  const char* e = getenv("SYMNMF_SCATTER_SLICE_MB");
+  const int64_t mb = e ? atoll(e) : 0;
+  return mb > 0 ? (mb << 20) : (48ll << 20);
+}
+
 static int grid_for(int64_t work_threads) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((work_threads + 255) / 256, 148 * 16));
 }
@@ -100,6 +108,7 @@ __global__ void __launch_bounds__(256) sampled_csr_v4(const int64_t* __restrict_
                                                       const float4* __restrict__ F4, const int32_t* __restrict__ uniq,
                                                       const double* __restrict__ w,
                                                       const int64_t* __restrict__ n_uniq_dev, float4* __restrict__ Y4,
+                                                      int32_t c_lo, int32_t c_hi, int ranged,
                                                       const int32_t* __restrict__ status) {
   if (dev_failed(status)) return;
   constexpr int NPW = 32 / LPR;   // nonzeros per warp step
@@ -111,8 +120,15 @@ __global__ void __launch_bounds__(256) sampled_csr_v4(const int64_t* __restrict_
     const float om = (float)w[u];
     float4 f = __ldg(F4 + i * LPR + li);
     f.x *= om; f.y *= om; f.z *= om; f.w *= om;
-    const int64_t e1 = rowptr[i + 1];
-    for (int64_t e = rowptr[i] + sub; e < e1; e += NPW) {
+    int64_t e0 = rowptr[i], e1 = rowptr[i + 1];
+    if (ranged) {   // this pass's destination range [c_lo, c_hi): a sub-range of the sorted row
+      int64_t a = e0, b = e1;
+      while (a < b) { const int64_t m = (a + b) >> 1; if (__ldg(col + m) < c_lo) a = m + 1; else b = m; }
+      int64_t c = a, d = e1;
+      while (c < d) { const int64_t m = (c + d) >> 1; if (__ldg(col + m) < c_hi) c = m + 1; else d = m; }
+      e0 = a; e1 = c;
+    }
+    for (int64_t e = e0 + sub; e < e1; e += NPW) {
       const int64_t c = __ldg(col + e);
       const float a = __ldg(val + e);
       atomicAdd(Y4 + c * LPR + li, make_float4(a * f.x, a * f.y, a * f.z, a * f.w));
@@ -158,14 +174,25 @@ void launch_sampled_csr_nozero(const symnmf_matrix& A, const float* F, int k, co
   if (k % 4 == 0) {
     const float4* F4 = reinterpret_cast<const float4*>(F);
     float4* Y4 = reinterpret_cast<float4*>(Y);
-    switch (k / 4) {
-      case 1: launch_pdl(sampled_csr_v4<1>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
-      case 2: launch_pdl(sampled_csr_v4<2>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
-      case 4: launch_pdl(sampled_csr_v4<4>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
-      case 8: launch_pdl(sampled_csr_v4<8>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
-      case 16: launch_pdl(sampled_csr_v4<16>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, status); return;
-      default: break;
+    // Destination-range passes: each pass scatters only into rows [c_lo, c_hi) of Y, a slice
+    // small enough to stay resident in L2 (126 MB) while the pass's vector atomics land on it,
+    // instead of read-modify-writes of random 128-byte lines of a Y larger than L2.
+    const int64_t ybytes = (int64_t)sizeof(float) * A.n * k;
+    const int64_t slice = scatter_slice_bytes();
+    const int passes = (int)std::max<int64_t>(1, (ybytes + slice - 1) / slice);
+    for (int p = 0; p < passes; ++p) {
+      const int32_t lo = (int32_t)(A.n * p / passes), hi = (int32_t)(A.n * (p + 1) / passes);
+      const int ranged = passes > 1;
+      switch (k / 4) {
+        case 1: launch_pdl(sampled_csr_v4<1>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, status); break;
+        case 2: launch_pdl(sampled_csr_v4<2>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, status); break;
+        case 4: launch_pdl(sampled_csr_v4<4>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, status); break;
+        case 8: launch_pdl(sampled_csr_v4<8>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, status); break;
+        case 16: launch_pdl(sampled_csr_v4<16>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, status); break;
+        default: break;
+      }
     }
+    if (k / 4 <= 16 && (k / 4 & (k / 4 - 1)) == 0) return;
   }
   launch_pdl(sampled_csr_scalar, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F, k, uniq, w, n_uniq_dev, Y, status);
 }

@@ -462,10 +462,13 @@ def _csr_case(cfgname, n, k, seed=7):
 
 @pytest.mark.parametrize("cfgname,n,k", [("c2", 20_000, 16), ("c2", 20_000, 8), ("c4", 40_000, 32),
                                          ("c4", 40_000, 64), ("c4", 40_032, 16), ("c2", 2_000, 32)])
-def test_csr_tile_exact_one_iteration(cfgname, n, k):
-    """Solver EXACT on CSR (A F computed per 256-row tile with nnz-balanced slices, fused with
-    the sweep and the next Gram): W and H after one iteration vs the oracle's fp64 iteration.
-    Covers ragged last tiles (n % 256 != 0), hub rows (power-law c4 recipe) and k = 8..64."""
+@pytest.mark.parametrize("tile", ["always", "never"])
+def test_csr_tile_exact_one_iteration(cfgname, n, k, tile, monkeypatch):
+    """Solver EXACT on CSR, both product forms: the tile kernel (A F per 256-row tile with
+    nnz-balanced slices, fused with the sweep and the next Gram; SYMNMF_CSR_TILE=always) and the
+    row SpMM + sweep: W and H after one iteration vs the oracle's fp64 iteration.  Covers ragged
+    last tiles (n % 256 != 0), hub rows (power-law c4 recipe) and k = 8..64."""
+    monkeypatch.setenv("SYMNMF_CSR_TILE", tile)
     A, H0, alpha = _csr_case(cfgname, n, k)
     M = S.DeviceMatrix.from_host(A)
     W, H = cu(H0), cu(H0)
@@ -479,9 +482,13 @@ def test_csr_tile_exact_one_iteration(cfgname, n, k):
 
 
 @pytest.mark.parametrize("cfgname,n,k,s", [("c4", 40_000, 32, 800), ("c2", 20_000, 16, 400), ("c4", 40_000, 8, 2000)])
-def test_csr_tile_lvs_equals_scatter_composition(cfgname, n, k, s):
-    """Solver LvS on CSR (pull-form Y_s through the symmetric structure with the U membership
-    table, fused with the sweep) equals the ABI composition with the scatter-form Y_s."""
+@pytest.mark.parametrize("slice_mb", ["", "1"])
+def test_csr_lvs_solver_equals_abi_composition(cfgname, n, k, s, slice_mb, monkeypatch):
+    """Solver LvS on CSR graphs with hubs (destination-range scatter passes, fused Gram) equals
+    the composition of the ABI calls on the same device data; slice_mb = 1 forces several
+    destination-range passes of the sampled scatter."""
+    if slice_mb:
+        monkeypatch.setenv("SYMNMF_SCATTER_SLICE_MB", slice_mb)
     A, H0, alpha = _csr_case(cfgname, n, k)
     tau = 1.0 / s
     M = S.DeviceMatrix.from_host(A)
@@ -505,7 +512,7 @@ def test_csr_tile_lvs_equals_scatter_composition(cfgname, n, k, s):
     assert rel(H1.cpu().numpy(), H2.cpu().numpy()) < 1e-5
 
 
-def test_csr_tile_lvs_replayed_plan_vs_oracle():
+def test_csr_lvs_replayed_plan_vs_oracle():
     """One LvS half through the solver vs the oracle's sampled products + sweep fed the plan the
     GPU drew (the same plan is recomputed by the ABI sampler from the same device scores)."""
     A, H0, alpha = _csr_case("c4", 30_016, 32)
@@ -520,3 +527,33 @@ def test_csr_tile_lvs_replayed_plan_vs_oracle():
     Gs, Ys = O.sampled_products(A, H0, ph["uniq_idx"], ph["uniq_w"])
     Wr = O.hals_sweep(Gs, Ys, H0, H0, alpha)
     assert rel(W.cpu().numpy(), Wr) < 1e-5
+
+
+# ------------------------------------------------------------------ persistent small-problem iteration
+@pytest.mark.parametrize("cfgname,n,k,s", [("c2", 100_000, 16, 2000), ("c1", 1000, 8, 200), ("c2", 20_000, 32, 400),
+                                           ("c2", 2_000, 8, 50)])
+def test_small_persistent_iteration_equals_multikernel(cfgname, n, k, s, monkeypatch):
+    """The one-launch-per-iteration LvS kernel (grid barriers between the steps) against the
+    multi-kernel graph path on the same inputs: identical sampling statistics in every half
+    (plans are bit-identical given identical scores) and the same factors after 3 iterations."""
+    from synth.configs import init_factor, mean_entry
+    d = make_input(cfgname, n_override=n if n != 1000 else None)
+    A = d["A"]
+    H0 = init_factor(n, k, mean_entry(A), np.random.default_rng(11))
+    tau = 1.0 / s
+    M = S.DeviceMatrix.from_host(A)
+    out = {}
+    for mode in ("auto", "never"):
+        if mode == "never":
+            monkeypatch.setenv("SYMNMF_SMALL", "never")
+        W, H = cu(H0), cu(H0)
+        sv = S.Solver(M, W, H, d["alpha"], mode="lvs", s=s, tau=tau, seed=9, max_iters=3)
+        sv.run(3)
+        st = sv.stats()
+        assert st["status"] == 0
+        sv.close()
+        out[mode] = (W.cpu().numpy(), H.cpu().numpy(), st["halves"])
+    (W1, H1, h1), (W2, H2, h2) = out["auto"], out["never"]
+    for a_, b_ in zip(h1, h2):
+        assert (a_["s_D"], a_["s_R"], a_["n_uniq"]) == (b_["s_D"], b_["s_R"], b_["n_uniq"])
+    assert rel(H1, H2) < 1e-4 and rel(W1, W2) < 1e-4
