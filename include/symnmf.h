@@ -103,9 +103,10 @@ typedef struct {
  *                                  fused with the sweep); default: used from 16M nonzeros.
  *   SYMNMF_SCATTER_SLICE_MB=<mb>   sampled CSR product: rows of Y per destination-range pass
  *                                  (default 48 MB, so each pass's slice of Y stays in L2).
- *   SYMNMF_SMALL=never             LvS solver: do not use the persistent one-launch-per-iteration
- *                                  kernel for small problems (CSR n <= 2^20 or dense n <= 4096,
- *                                  k in {8, 16, 32}, no per-iteration residual). */
+ *   SYMNMF_SMALL=always            LvS solver: use the persistent one-launch-per-iteration kernel
+ *                                  (grid barriers between steps) on small problems (CSR n <= 2^20
+ *                                  or dense n <= 4096, k in {8, 16, 32}, no per-iteration
+ *                                  residual); default: the multi-kernel CUDA graph (faster). */
 
 /* Library version (major*10000 + minor*100 + patch).  Host only. */
 int32_t symnmf_version(void);

@@ -448,10 +448,11 @@ struct symnmf_solver {
 
 namespace {
 
-// LvS on small problems: the persistent iteration kernel; SYMNMF_SMALL=never disables it (symnmf.h)
+// LvS on small problems: the persistent iteration kernel only on request (SYMNMF_SMALL=always,
+// symnmf.h): measured slower than the multi-kernel graph on B200 (small.cu)
 bool small_enabled() {
   const char* e = getenv("SYMNMF_SMALL");
-  return !(e && !strcmp(e, "never"));
+  return e && !strcmp(e, "always");
 }
 
 // EXACT CSR: the tile kernel from 16M nonzeros; SYMNMF_CSR_TILE=always|never overrides (symnmf.h)

@@ -302,23 +302,25 @@ static int64_t ldk_for(int64_t n) { return (n + 31) / 32 * 32; }
 
 size_t dense_ah_tc_scratch(int64_t n, int k) { return sizeof(float) * 2 * (size_t)np_for(k) * ldk_for(n) + 1024; }
 
-// Grid: m-groups of MT tiles x K splits, chosen to minimise (waves x per-CTA work), with the B
-// re-reads (one B tile pair per K block per CTA, from L2) charged at half an A tile each.
+// Grid: m-groups of MT tiles x K splits, at most one CTA per SM (one wave: every CTA runs a long
+// pipeline, no tail wave, few split-K atomics).  Minimises the largest per-CTA work MT x kps,
+// ties broken towards larger MT (fewer B re-reads).
 static void tc_plan(int64_t mt, int64_t nkb, int np, int max_mt, int* MT, int* splits, int* kps) {
   const int sms = 148;
-  double best = 1e300;
+  int64_t best = INT64_MAX;
   for (int m = 1; m <= max_mt; ++m) {
     const int64_t groups = (mt + m - 1) / m;
-    for (int64_t sp = 1; sp <= std::min<int64_t>(nkb, 64); ++sp) {
-      const int64_t kp = (nkb + sp - 1) / sp;
-      const int64_t spr = (nkb + kp - 1) / kp;
-      const int64_t ctas = groups * spr;
-      const int64_t waves = (ctas + sms - 1) / sms;
-      const double bcost = 0.5 * (2.0 * np * 128.0) / (16384.0 * m);
-      const double cost = (double)waves * (double)(m * kp) * (1.0 + bcost) + 0.02 * (double)(spr - 1) * m;
-      if (cost < best * 0.999) { best = cost; *MT = m; *splits = (int)spr; *kps = (int)kp; }
-    }
+    if (groups > sms) continue;
+    const int64_t sp0 = std::max<int64_t>(1, std::min<int64_t>(nkb, sms / groups));
+    const int64_t kp = (nkb + sp0 - 1) / sp0;
+    const int64_t spr = (nkb + kp - 1) / kp;
+    const int64_t work = (int64_t)m * kp;
+    if (work < best || (work == best && m > *MT)) { best = work; *MT = m; *splits = (int)spr; *kps = (int)kp; }
   }
+  if (best == INT64_MAX) {   // more m-tiles than SMs x max_mt: several waves of full m-groups
+    *MT = max_mt; *splits = 1; *kps = (int)nkb;
+  }
+  (void)np;
 }
 
 template <int NP>

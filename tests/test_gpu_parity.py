@@ -543,9 +543,8 @@ def test_small_persistent_iteration_equals_multikernel(cfgname, n, k, s, monkeyp
     tau = 1.0 / s
     M = S.DeviceMatrix.from_host(A)
     out = {}
-    for mode in ("auto", "never"):
-        if mode == "never":
-            monkeypatch.setenv("SYMNMF_SMALL", "never")
+    for mode in ("always", "never"):
+        monkeypatch.setenv("SYMNMF_SMALL", mode)
         W, H = cu(H0), cu(H0)
         sv = S.Solver(M, W, H, d["alpha"], mode="lvs", s=s, tau=tau, seed=9, max_iters=3)
         sv.run(3)
@@ -553,7 +552,7 @@ def test_small_persistent_iteration_equals_multikernel(cfgname, n, k, s, monkeyp
         assert st["status"] == 0
         sv.close()
         out[mode] = (W.cpu().numpy(), H.cpu().numpy(), st["halves"])
-    (W1, H1, h1), (W2, H2, h2) = out["auto"], out["never"]
+    (W1, H1, h1), (W2, H2, h2) = out["always"], out["never"]
     for a_, b_ in zip(h1, h2):
         assert (a_["s_D"], a_["s_R"], a_["n_uniq"]) == (b_["s_D"], b_["s_R"], b_["n_uniq"])
     assert rel(H1, H2) < 1e-4 and rel(W1, W2) < 1e-4
