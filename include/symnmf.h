@@ -103,6 +103,8 @@ typedef struct {
  *                                  fused with the sweep); default: used from 16M nonzeros.
  *   SYMNMF_SCATTER_SLICE_MB=<mb>   sampled CSR product: rows of Y per destination-range pass
  *                                  (default 48 MB, so each pass's slice of Y stays in L2).
+ *   SYMNMF_LAI_FUSED=never         LAI solver (k = 64, l <= 80): use the four-kernel half (U^T F,
+ *                                  Lambda scaling, U M, sweep) instead of the fused launch.
  *   SYMNMF_SMALL=always            LvS solver: use the persistent one-launch-per-iteration kernel
  *                                  (grid barriers between steps) on small problems (CSR n <= 2^20
  *                                  or dense n <= 4096, k in {8, 16, 32}, no per-iteration

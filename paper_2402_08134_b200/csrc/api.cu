@@ -432,6 +432,9 @@ struct symnmf_solver {
   double *resid, *rpart, *rout, *GH;
   double *Zpart, *Z;
   float* M32;
+  bool lai_fused;          // LAI: one fused launch per half (lai_fused.cu)
+  float* Mside[2];         // Mside[side] = Lambda U^T F of half `side` (LP x k fp32)
+  double* UXacc;           // zeroed kGramReplicas x LP x k accumulator of U^T X
   void* tcs;
   size_t tcs_bytes;
   cudaGraph_t graph;
@@ -447,6 +450,12 @@ struct symnmf_solver {
 };
 
 namespace {
+
+// LAI: the fused one-launch half (k = 64, l <= 80); SYMNMF_LAI_FUSED=never disables it (symnmf.h)
+bool lai_enabled() {
+  const char* e = getenv("SYMNMF_LAI_FUSED");
+  return !(e && !strcmp(e, "never"));
+}
 
 // LvS on small problems: the persistent iteration kernel only on request (SYMNMF_SMALL=always,
 // symnmf.h): measured slower than the multi-kernel graph on B200 (small.cu)
@@ -517,6 +526,11 @@ void solver_layout(symnmf_solver& S, Carver& c) {
     S.Zpart = c.take<double>(gram_partial_doubles(S.l, k, false, S.ggrid));
     S.Z = c.take<double>((size_t)S.l * k);
     S.M32 = c.take<float>((size_t)S.l * k);
+    S.lai_fused = lai_fused_supported(k, S.l) && lai_enabled();
+    const size_t lp = S.lai_fused ? (size_t)lai_lp(S.l) : 0;
+    S.Mside[0] = c.take<float>(lp * k);
+    S.Mside[1] = c.take<float>(lp * k);
+    S.UXacc = c.take<double>(lp * k * kGramReplicas);
   }
   S.tcs_bytes = (S.hasA && S.A.kind == SYMNMF_DENSE && S.precision == SYMNMF_3XTF32) ? dense_ah_tc_scratch(n, k) : 0;
   S.tcs = c.take<char>(S.tcs_bytes);
@@ -566,6 +580,11 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     // Update(G_s + alpha I, Y_s + alpha F^T); Y re-zeroed for the next scatter; X^T X and its R^{-1}
     launch_sweep_fused(S.Gs, S.alpha, S.Y, F, X, n, k, true, S.Gacc, Gnext, S.Rinv32, S.counter, status, st);
     mark(S, st, "hals_sweep");
+  } else if (S.lai_fused) {
+    // Y = U (Lambda U^T F), sweep, X^T X and Lambda U^T X for the next half, in one launch
+    launch_lai_sweep_fused(S.U, S.l, n, k, S.Mside[side], Gf, S.alpha, F, X, S.lam, S.Gacc, S.UXacc, Gnext,
+                           S.Mside[side ^ 1], S.counter, status, st);
+    mark(S, st, "lai_fused");
   } else {
     launch_cross_gram(S.U, S.l, S.l, F, k, k, false, n, nullptr, nullptr, nullptr, S.Zpart, S.ggrid, S.Z, k, status,
                       st);
@@ -646,6 +665,16 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
   SYMNMF_CUDA_TRY(cudaMemsetAsync(S.resid, 0, sizeof(double) * max_iters, st));
   SYMNMF_CUDA_TRY(cudaMemsetAsync(S.counter, 0, sizeof(unsigned int) * 4, st));
   SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Gacc, 0, sizeof(double) * kGramReplicas * k * k, st));
+  if (S.mode == SYMNMF_LAI && S.lai_fused) {
+    const size_t lp = (size_t)lai_lp(S.l);
+    SYMNMF_CUDA_TRY(cudaMemsetAsync(S.UXacc, 0, sizeof(double) * lp * k * kGramReplicas, st));
+    SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Mside[0], 0, sizeof(float) * lp * k, st));
+    SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Mside[1], 0, sizeof(float) * lp * k, st));
+    // Lambda U^T H for the first W-half; later halves get theirs from the preceding launch
+    launch_cross_gram(S.U, S.l, S.l, H, k, k, false, n, nullptr, nullptr, nullptr, S.Zpart, S.ggrid, S.Z, k, S.status,
+                      st);
+    launch_scale_rows(S.Z, S.l, k, S.lam, S.Mside[0], S.status, st);
+  }
   if (S.small) {
     SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Gacc2, 0, sizeof(double) * kGramReplicas * k * k, st));
     SYMNMF_CUDA_TRY(cudaMemsetAsync(S.bar, 0, sizeof(unsigned int) * 4, st));

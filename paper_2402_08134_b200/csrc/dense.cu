@@ -109,11 +109,14 @@ void launch_dense_ah_simt(const float* A, int64_t lda, int64_t n, const float* F
 // ---------------------------------------------------------------- sampled dense
 // Y_s[c, :] = sum_u A[U_u, c] (omega_u F[U_u, :])  (A[U,:]^T = A[:,U] by symmetry, Z28).
 // CTA tile: 128 output rows c x KP columns; thread = 4 rows c (one float4 of each gathered row of
-// A) x JB columns.  The gathered 32 x 128 slab of A is staged through shared memory with cp.async
-// (double buffered: the next slab is in flight while the current one is consumed); omega F[U]
-// rows are scaled once while staged.  fp32 FMAs, flushed into fp64 registers every stage (16-32 sampled
-// rows).  gridDim.y splits U (fp32 atomics into a zeroed Y) so that ~4 CTAs run per SM.
-constexpr int SDC = 128;   // output rows per CTA
+// A) x JB columns.  The CTA's range of U (indices and weights) is loaded into shared memory
+// once; the gathered SDU x 128 slabs of A and the SDU raw rows F[U_u, :] then stream through an
+// SDS-stage cp.async ring, so no load on the critical path depends on another; omega_u scales
+// the A value at use.  fp32 FMAs, flushed into fp64 registers every stage.  gridDim.y splits U
+// (fp32 atomics into a zeroed Y) so that the grid fills the SMs.
+constexpr int SDC = 128;    // output rows per CTA
+constexpr int SDS = 4;      // pipeline stages
+constexpr int SDUMAX = 2048;   // U entries per CTA (indices + weights in shared memory)
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool ok) {
   const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
@@ -125,17 +128,29 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int KP, int JB, int SDU>   // SDU sampled rows per stage
-__global__ void __launch_bounds__(32 * (KP / JB)) sampled_dense_v2(const float* __restrict__ A, int64_t lda, int64_t n,
+struct SdSmem {
+  static constexpr size_t a = 0;                                              // float [SDS][SDU][SDC]
+  static constexpr size_t f = a + sizeof(float) * SDS * SDU * SDC;            // float [SDS][SDU][KP]
+  static constexpr size_t row = f + sizeof(float) * SDS * SDU * KP;           // int64 [SDUMAX]
+  static constexpr size_t w = row + sizeof(int64_t) * SDUMAX;                 // float [SDUMAX]
+  static constexpr size_t bytes = w + sizeof(float) * SDUMAX;
+};
+
+template <int KP, int JB, int SDU>
+__global__ void __launch_bounds__(32 * (KP / JB)) sampled_dense_v3(const float* __restrict__ A, int64_t lda, int64_t n,
                                                                   const float* __restrict__ F, int k,
                                                                   const int32_t* __restrict__ uniq,
                                                                   const double* __restrict__ w,
                                                                   const int64_t* __restrict__ n_uniq_dev,
                                                                   float* __restrict__ Y, int vec,
                                                                   const int32_t* __restrict__ status) {
+  using L = SdSmem<KP, JB, SDU>;
   constexpr int NT = 32 * (KP / JB);
-  __shared__ __align__(16) float sA[2][SDU][SDC];
-  __shared__ __align__(16) float sF[2][SDU][KP];
-  __shared__ int64_t sRow[2][SDU];
+  extern __shared__ __align__(16) unsigned char sds[];
+  float* sA = reinterpret_cast<float*>(sds + L::a);
+  float* sF = reinterpret_cast<float*>(sds + L::f);
+  int64_t* sRow = reinterpret_cast<int64_t*>(sds + L::row);
+  float* sW = reinterpret_cast<float*>(sds + L::w);
   if (dev_failed(status)) return;
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
   const int64_t c0 = (int64_t)blockIdx.x * SDC;
@@ -143,33 +158,47 @@ __global__ void __launch_bounds__(32 * (KP / JB)) sampled_dense_v2(const float* 
   const int64_t per = ((nu + gridDim.y - 1) / gridDim.y + SDU - 1) / SDU * SDU;
   const int64_t u0 = (int64_t)blockIdx.y * per, u1 = min64(nu, u0 + per);
   if (u0 >= u1) return;
-  const int nst = (int)((u1 - u0 + SDU - 1) / SDU);
-  // stage s: row indices + scaled F rows (plain loads) and the A slab (cp.async)
-  auto stage_rows = [&](int s, int buf) {
-    const int64_t ub = u0 + (int64_t)s * SDU;
-    if (tid < SDU) sRow[buf][tid] = (ub + tid < u1) ? (int64_t)uniq[ub + tid] : -1;
-  };
-  auto stage_data = [&](int s, int buf) {
-    const int64_t ub = u0 + (int64_t)s * SDU;
-    for (int e = tid; e < SDU * (SDC / 4); e += NT) {
-      const int r = e / (SDC / 4), q = e - r * (SDC / 4);
-      const int64_t row = sRow[buf][r];
-      const int64_t c = c0 + 4 * q;
-      float* dst = &sA[buf][r][4 * q];
-      if (vec) {
-        const bool ok = row >= 0 && c < n;   // n % 4 == 0 and 16B-aligned rows: whole float4 in range
-        cp_async16(dst, ok ? (const void*)(A + row * lda + c) : (const void*)A, ok);
-      } else {
+  const int cnt = (int)(u1 - u0);
+  for (int e = tid; e < ((cnt + SDU - 1) / SDU) * SDU; e += NT) {
+    const bool ok = e < cnt;
+    sRow[e] = ok ? (int64_t)__ldg(uniq + u0 + e) : -1;
+    sW[e] = ok ? (float)__ldg(w + u0 + e) : 0.f;
+  }
+  __syncthreads();
+  const int nst = (cnt + SDU - 1) / SDU;
+  auto issue = [&](int s) {
+    if (s < nst) {
+      const int buf = s % SDS;
+      float* a = sA + (size_t)buf * SDU * SDC;
+      for (int e = tid; e < SDU * (SDC / 4); e += NT) {
+        const int r = e / (SDC / 4), q = e - r * (SDC / 4);
+        const int64_t row = sRow[s * SDU + r];
+        const int64_t c = c0 + 4 * q;
+        float* dst = a + r * SDC + 4 * q;
+        if (vec) {
+          const bool ok = row >= 0 && c < n;
+          cp_async16(dst, ok ? (const void*)(A + row * lda + c) : (const void*)A, ok);
+        } else {
 #pragma unroll
-        for (int t = 0; t < 4; ++t) dst[t] = (row >= 0 && c + t < n) ? __ldg(A + row * lda + c + t) : 0.f;
+          for (int t = 0; t < 4; ++t) dst[t] = (row >= 0 && c + t < n) ? __ldg(A + row * lda + c + t) : 0.f;
+        }
+      }
+      float* f = sF + (size_t)buf * SDU * KP;
+      if (k == KP) {
+        for (int e = tid; e < SDU * (KP / 4); e += NT) {
+          const int r = e / (KP / 4), q = e - r * (KP / 4);
+          const int64_t row = sRow[s * SDU + r];
+          cp_async16(f + r * KP + 4 * q, row >= 0 ? (const void*)(F + row * KP + 4 * q) : (const void*)F, row >= 0);
+        }
+      } else {
+        for (int e = tid; e < SDU * KP; e += NT) {
+          const int r = e / KP, j = e - r * KP;
+          const int64_t row = sRow[s * SDU + r];
+          f[r * KP + j] = (row >= 0 && j < k) ? __ldg(F + row * k + j) : 0.f;
+        }
       }
     }
-    for (int e = tid; e < SDU * KP; e += NT) {
-      const int r = e / KP, j = e - r * KP;
-      const int64_t row = sRow[buf][r];
-      sF[buf][r][j] = (row >= 0 && j < k) ? (float)w[ub + r] * __ldg(F + row * k + j) : 0.f;
-    }
-    cp_async_commit();
+    cp_async_commit();   // (possibly empty) group per stage keeps the wait count uniform
   };
   float acc[4][JB];
   double acc64[4][JB];
@@ -177,40 +206,36 @@ __global__ void __launch_bounds__(32 * (KP / JB)) sampled_dense_v2(const float* 
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < JB; ++j) { acc[i][j] = 0.f; acc64[i][j] = 0.0; }
-  stage_rows(0, 0);
-  __syncthreads();
-  stage_data(0, 0);
+#pragma unroll
+  for (int s = 0; s < SDS - 1; ++s) issue(s);
   for (int s = 0; s < nst; ++s) {
-    const int buf = s & 1;
-    if (s + 1 < nst) {
-      stage_rows(s + 1, buf ^ 1);
-      __syncthreads();
-      stage_data(s + 1, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    issue(s + SDS - 1);
+    cp_async_wait<SDS - 1>();
     __syncthreads();
+    const int buf = s % SDS;
+    const float* a = sA + (size_t)buf * SDU * SDC;
+    const float* f = sF + (size_t)buf * SDU * KP;
 #pragma unroll 8
     for (int r = 0; r < SDU; ++r) {
-      const float4 a = *reinterpret_cast<const float4*>(&sA[buf][r][4 * tx]);
-      float f[JB];
+      const float om = sW[s * SDU + r];
+      const float4 a4 = *reinterpret_cast<const float4*>(a + r * SDC + 4 * tx);
+      float fv[JB];
 #pragma unroll
       for (int j = 0; j < JB; j += 4) {
-        const float4 v = *reinterpret_cast<const float4*>(&sF[buf][r][ty * JB + j]);
-        f[j] = v.x; f[j + 1] = v.y; f[j + 2] = v.z; f[j + 3] = v.w;
+        const float4 v = *reinterpret_cast<const float4*>(f + r * KP + ty * JB + j);
+        fv[j] = v.x; fv[j + 1] = v.y; fv[j + 2] = v.z; fv[j + 3] = v.w;
       }
-      const float av[4] = {a.x, a.y, a.z, a.w};
+      const float av[4] = {a4.x * om, a4.y * om, a4.z * om, a4.w * om};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < JB; ++j) acc[i][j] = fmaf(av[i], f[j], acc[i][j]);
+        for (int j = 0; j < JB; ++j) acc[i][j] = fmaf(av[i], fv[j], acc[i][j]);
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < JB; ++j) { acc64[i][j] += (double)acc[i][j]; acc[i][j] = 0.f; }
-    __syncthreads();   // buffer `buf` is refilled by the next iteration's stage_data
+    __syncthreads();   // buffer `buf` is refilled by a later issue()
   }
   const bool atomic = gridDim.y > 1;
 #pragma unroll
@@ -232,12 +257,15 @@ template <int KP, int JB, int SDU = (KP == 64 ? 16 : 32)>
 static void launch_sd_t(const float* A, int64_t lda, int64_t n, const float* F, int k, const int32_t* uniq,
                         const double* w, const int64_t* nu, int64_t cap, float* Y, const int32_t* status,
                         cudaStream_t st) {
+  using L = SdSmem<KP, JB, SDU>;
   const int64_t cb = (n + SDC - 1) / SDC;
   int64_t splits = std::max<int64_t>(1, std::min<int64_t>((148 * 4 + cb - 1) / cb, (cap + 4 * SDU - 1) / (4 * SDU)));
+  splits = std::max<int64_t>(splits, (cap + SDUMAX - 1) / SDUMAX);   // U range of a CTA fits shared memory
   if (splits > 1) cudaMemsetAsync(Y, 0, sizeof(float) * n * k, st);
   const int vec = (lda % 4 == 0 && n % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) ? 1 : 0;
-  sampled_dense_v2<KP, JB, SDU><<<dim3((unsigned)cb, (unsigned)splits), 32 * (KP / JB), 0, st>>>(A, lda, n, F, k, uniq, w,
-                                                                                          nu, Y, vec, status);
+  cudaFuncSetAttribute(sampled_dense_v3<KP, JB, SDU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
+  sampled_dense_v3<KP, JB, SDU><<<dim3((unsigned)cb, (unsigned)splits), 32 * (KP / JB), L::bytes, st>>>(
+      A, lda, n, F, k, uniq, w, nu, Y, vec, status);
 }
 
 void launch_sampled_dense(const float* A, int64_t lda, int64_t n, const float* F, int k, const int32_t* uniq,

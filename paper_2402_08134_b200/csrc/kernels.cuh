@@ -106,6 +106,13 @@ void launch_sampled_csr_nozero(const symnmf_matrix& A, const float* F, int k, co
                                const int64_t* n_uniq_dev, int64_t cap, float* Y, const int32_t* status,
                                cudaStream_t st);
 
+// ---------------------------------------------------------------- lai_fused.cu
+int lai_lp(int l);
+bool lai_fused_supported(int k, int l);
+void launch_lai_sweep_fused(const float* U, int l, int64_t n, int k, const float* Mcur, const double* G, double alpha,
+                            const float* F, float* X, const double* lam, double* GXacc, double* UXacc, double* Gout,
+                            float* Mnext, unsigned int* counter, int32_t* status, cudaStream_t st);
+
 // ---------------------------------------------------------------- small.cu
 struct SmallArgs;
 bool small_lvs_supported(const symnmf_matrix& A, int64_t n, int k);

@@ -23,6 +23,7 @@ namespace symnmf {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 32;          // fp32 elements per 128-byte row
+template <int NP> constexpr int tc_stages() { return NP <= 80 ? 4 : 3; }
 constexpr int TC_THREADS = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -89,60 +90,39 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-// M-grouped kernel: one CTA owns MT consecutive 128-row tiles of A (an "m-group") and a range of
-// K blocks; the MT accumulators live side by side in TMEM (MT * NP <= 512 columns).  Per K block the
-// B tiles (X_hi^T, X_lo^T, NP x 32) are loaded ONCE into a 2-slot ring and reused by the MT A tiles
-// that stream through the S-stage A ring, so L2 -> SM traffic for B drops by MT.
-template <int NP> constexpr int tc_max_mt() { return 512 / NP >= 16 ? 16 : 512 / NP; }
-template <int NP> constexpr uint32_t tc_tmem_cols(int mt) {
-  return mt * NP <= 32 ? 32 : mt * NP <= 64 ? 64 : mt * NP <= 128 ? 128 : mt * NP <= 256 ? 256 : 512;
-}
-constexpr int TC_SMEM_MAX = 227 * 1024;
-template <int NP> constexpr int tc_b_bytes() { return NP * TC_BK * 4; }
-template <int NP> constexpr int tc_stages_mg() {
-  return (TC_SMEM_MAX - 1024 - 4 * tc_b_bytes<NP>() - 256) / (2 * TC_BM * TC_BK * 4) > 6
-             ? 6 : (TC_SMEM_MAX - 1024 - 4 * tc_b_bytes<NP>() - 256) / (2 * TC_BM * TC_BK * 4);
-}
-
 template <int NP>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_3xtf32(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBhi,
-                   const __grid_constant__ CUtensorMap mapBlo, int64_t n, int64_t mt_total, int MT, int kb_per_split,
-                   int64_t nkb_total, float* __restrict__ Y, int64_t ldy, int k, int atomic,
-                   const int32_t* __restrict__ status) {
-  constexpr int S = tc_stages_mg<NP>();
+                   const __grid_constant__ CUtensorMap mapBlo, int64_t n, int kb_per_split, int64_t nkb_total,
+                   float* __restrict__ Y, int64_t ldy, int k, const int32_t* __restrict__ status) {
   constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;   // 16 KB
-  constexpr uint32_t B_BYTES = tc_b_bytes<NP>();    // NP x 128 B
+  constexpr uint32_t B_BYTES = NP * TC_BK * 4;      // NP x 128 B
+  constexpr uint32_t STAGE = 2 * A_BYTES + 2 * B_BYTES;
+  constexpr uint32_t TMEM_COLS = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : 256;
   constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-  unsigned char* sB = sm + S * 2 * A_BYTES;                 // 2 slots x (hi, lo)
-  uint64_t* fullA = reinterpret_cast<uint64_t*>(sB + 4 * B_BYTES);
-  uint64_t* convA = fullA + S;
-  uint64_t* emptyA = convA + S;
-  uint64_t* fullB = emptyA + S;
-  uint64_t* emptyB = fullB + 2;
-  uint64_t* tmem_full = emptyB + 2;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + tc_stages<NP>() * STAGE);
+  uint64_t* conv = full + tc_stages<NP>();
+  uint64_t* empty = conv + tc_stages<NP>();
+  uint64_t* tmem_full = empty + tc_stages<NP>();
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
   if (dev_failed(status)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t t0 = (int64_t)blockIdx.x * MT;
-  const int mtiles = (int)min64(MT, mt_total - t0);
+  const int64_t m0 = (int64_t)blockIdx.x * TC_BM;
   const int64_t kb0 = (int64_t)blockIdx.y * kb_per_split;
   const int nkb = (int)min64(kb_per_split, nkb_total - kb0);
-  if (nkb <= 0 || mtiles <= 0) return;
-  const uint32_t tcols = tc_tmem_cols<NP>(MT);
+  if (nkb <= 0) return;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) { mbar_init(fullA + s, 1); mbar_init(convA + s, 128); mbar_init(emptyA + s, 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(fullB + s, 1); mbar_init(emptyB + s, 1); }
+    for (int s = 0; s < tc_stages<NP>(); ++s) { mbar_init(full + s, 1); mbar_init(conv + s, 128); mbar_init(empty + s, 1); }
     mbar_init(tmem_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(tcols)
+                 "r"(TMEM_COLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -153,58 +133,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      int i = 0;
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int bs = kb & 1;
-        if (kb >= 2) mbar_wait(emptyB + bs, ((kb >> 1) - 1) & 1);
-        const int kx = (int)((kb0 + kb) * TC_BK);
-        unsigned char* b = sB + bs * 2 * B_BYTES;
-        mbar_expect_tx(fullB + bs, 2 * B_BYTES);
-        tma_load_2d(&mapBhi, fullB + bs, b, kx, 0);
-        tma_load_2d(&mapBlo, fullB + bs, b + B_BYTES, kx, 0);
-        for (int t = 0; t < mtiles; ++t, ++i) {
-          const int s = i % S;
-          if (i >= S) mbar_wait(emptyA + s, ((i / S) - 1) & 1);
-          mbar_expect_tx(fullA + s, A_BYTES);
-          tma_load_2d(&mapA, fullA + s, sm + s * 2 * A_BYTES, kx, (int)((t0 + t) * TC_BM));
-        }
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % tc_stages<NP>();
+        if (i >= tc_stages<NP>()) mbar_wait(empty + s, ((i / tc_stages<NP>()) - 1) & 1);
+        unsigned char* st = sm + s * STAGE;
+        const int kx = (int)((kb0 + i) * TC_BK);
+        mbar_expect_tx(full + s, A_BYTES + 2 * B_BYTES);
+        tma_load_2d(&mapA, full + s, st, kx, (int)m0);
+        tma_load_2d(&mapBhi, full + s, st + 2 * A_BYTES, kx, 0);
+        tma_load_2d(&mapBlo, full + s, st + 2 * A_BYTES + B_BYTES, kx, 0);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      int i = 0;
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int bs = kb & 1;
-        mbar_wait(fullB + bs, (kb >> 1) & 1);
-        const uint32_t b_hi = smem_u32(sB + bs * 2 * B_BYTES), b_lo = b_hi + B_BYTES;
-        for (int t = 0; t < mtiles; ++t, ++i) {
-          const int s = i % S;
-          mbar_wait(convA + s, (i / S) & 1);
-          tc_fence_after();
-          const uint32_t a_hi = smem_u32(sm + s * 2 * A_BYTES), a_lo = a_hi + A_BYTES;
-          const uint32_t d = tmem + (uint32_t)(t * NP);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % tc_stages<NP>();
+        mbar_wait(conv + s, (i / tc_stages<NP>()) & 1);
+        tc_fence_after();
+        const uint32_t a_hi = smem_u32(sm + s * STAGE), a_lo = a_hi + A_BYTES;
+        const uint32_t b_hi = a_hi + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < TC_BK / 8; ++kk) {
-            const uint32_t off = kk * 32;   // 8 tf32 = 32 bytes along the swizzled row
-            const uint32_t acc0 = (kb | kk) ? 1u : 0u;
-            mma_tf32(d, smem_desc_k128(a_hi + off), smem_desc_k128(b_hi + off), IDESC, acc0);
-            mma_tf32(d, smem_desc_k128(a_hi + off), smem_desc_k128(b_lo + off), IDESC, 1u);
-            mma_tf32(d, smem_desc_k128(a_lo + off), smem_desc_k128(b_hi + off), IDESC, 1u);
-          }
-          mma_commit(emptyA + s);
+        for (int kk = 0; kk < TC_BK / 8; ++kk) {
+          const uint32_t off = kk * 32;   // 8 tf32 = 32 bytes along the swizzled row
+          const uint32_t acc0 = (i | kk) ? 1u : 0u;
+          mma_tf32(tmem, smem_desc_k128(a_hi + off), smem_desc_k128(b_hi + off), IDESC, acc0);
+          mma_tf32(tmem, smem_desc_k128(a_hi + off), smem_desc_k128(b_lo + off), IDESC, 1u);
+          mma_tf32(tmem, smem_desc_k128(a_lo + off), smem_desc_k128(b_hi + off), IDESC, 1u);
         }
-        mma_commit(emptyB + bs);
+        mma_commit(empty + s);
       }
       mma_commit(tmem_full);
     }
   } else if (warp >= 4) {
     const int t = threadIdx.x - 128;   // 0..127
-    const int total = nkb * mtiles;
-    for (int i = 0; i < total; ++i) {
-      const int s = i % S;
-      mbar_wait(fullA + s, (i / S) & 1);
-      uint4* a = reinterpret_cast<uint4*>(sm + s * 2 * A_BYTES);
-      uint4* lo = reinterpret_cast<uint4*>(sm + s * 2 * A_BYTES + A_BYTES);
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % tc_stages<NP>();
+      mbar_wait(full + s, (i / tc_stages<NP>()) & 1);
+      uint4* a = reinterpret_cast<uint4*>(sm + s * STAGE);
+      uint4* lo = reinterpret_cast<uint4*>(sm + s * STAGE + A_BYTES);
 #pragma unroll 4
       for (int e = t; e < (int)(A_BYTES / 16); e += 128) {
         const uint4 v = a[e];
@@ -218,35 +184,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         lo[e] = l;
       }
       fence_proxy_async();
-      mbar_arrive(convA + s);
+      mbar_arrive(conv + s);
     }
-    // epilogue: TMEM lane = tile row, column t * NP + c = output column c of m-tile t
+    // epilogue: TMEM lane = tile row, column = output column
     mbar_wait(tmem_full, 0);
     tc_fence_after();
     const int wq = warp & 3;
-    for (int tt = 0; tt < mtiles; ++tt) {
-      const int64_t row = (t0 + tt) * TC_BM + wq * 32 + lane;
+    const int64_t row = m0 + wq * 32 + lane;
 #pragma unroll
-      for (int c0 = 0; c0 < NP; c0 += 16) {
-        uint32_t r[16];
-        const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(tt * NP + c0);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (row < n) {
-          if (atomic) {
+    for (int c0 = 0; c0 < NP; c0 += 16) {
+      uint32_t r[16];
+      const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)c0;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < n) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (c0 + j < k) atomicAdd(Y + row * ldy + c0 + j, __uint_as_float(r[j]));
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (c0 + j < k) Y[row * ldy + c0 + j] = __uint_as_float(r[j]);
-          }
-        }
+        for (int j = 0; j < 16; ++j)
+          if (c0 + j < k) atomicAdd(Y + row * ldy + c0 + j, __uint_as_float(r[j]));
       }
     }
     tc_fence_before();
@@ -254,7 +212,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
   }
 }
 
@@ -302,27 +260,6 @@ static int64_t ldk_for(int64_t n) { return (n + 31) / 32 * 32; }
 
 size_t dense_ah_tc_scratch(int64_t n, int k) { return sizeof(float) * 2 * (size_t)np_for(k) * ldk_for(n) + 1024; }
 
-// Grid: m-groups of MT tiles x K splits, at most one CTA per SM (one wave: every CTA runs a long
-// pipeline, no tail wave, few split-K atomics).  Minimises the largest per-CTA work MT x kps,
-// ties broken towards larger MT (fewer B re-reads).
-static void tc_plan(int64_t mt, int64_t nkb, int np, int max_mt, int* MT, int* splits, int* kps) {
-  const int sms = 148;
-  int64_t best = INT64_MAX;
-  for (int m = 1; m <= max_mt; ++m) {
-    const int64_t groups = (mt + m - 1) / m;
-    if (groups > sms) continue;
-    const int64_t sp0 = std::max<int64_t>(1, std::min<int64_t>(nkb, sms / groups));
-    const int64_t kp = (nkb + sp0 - 1) / sp0;
-    const int64_t spr = (nkb + kp - 1) / kp;
-    const int64_t work = (int64_t)m * kp;
-    if (work < best || (work == best && m > *MT)) { best = work; *MT = m; *splits = (int)spr; *kps = (int)kp; }
-  }
-  if (best == INT64_MAX) {   // more m-tiles than SMs x max_mt: several waves of full m-groups
-    *MT = max_mt; *splits = 1; *kps = (int)nkb;
-  }
-  (void)np;
-}
-
 template <int NP>
 static bool launch_tc_t(const float* A, int64_t lda, int64_t n, const float* X, int64_t ldx, int k, float* Y,
                         int64_t ldy, void* scratch, const int32_t* status, cudaStream_t st) {
@@ -334,18 +271,18 @@ static bool launch_tc_t(const float* A, int64_t lda, int64_t n, const float* X, 
   if (!make_map(&mH, hiT, (uint64_t)ldk, (uint64_t)NP, (uint64_t)ldk * 4, TC_BK, NP)) return false;
   if (!make_map(&mL, loT, (uint64_t)ldk, (uint64_t)NP, (uint64_t)ldk * 4, TC_BK, NP)) return false;
   split_transpose<<<(unsigned)((ldk + 255) / 256), 256, 0, st>>>(X, ldx, n, k, NP, ldk, hiT, loT);
+  cudaMemset2DAsync(Y, sizeof(float) * ldy, 0, sizeof(float) * k, n, st);
   const int64_t mt = (n + TC_BM - 1) / TC_BM;
   const int64_t nkb = (n + TC_BK - 1) / TC_BK;
-  int MT = 1, splits = 1, kps = (int)nkb;
-  tc_plan(mt, nkb, NP, tc_max_mt<NP>(), &MT, &splits, &kps);
-  if (splits > 1) cudaMemset2DAsync(Y, sizeof(float) * ldy, 0, sizeof(float) * k, n, st);
-  constexpr size_t smem = 1024 + (size_t)tc_stages_mg<NP>() * 2 * TC_BM * TC_BK * 4 + 4 * (size_t)tc_b_bytes<NP>() +
-                          (3 * tc_stages_mg<NP>() + 5) * 8 + 16;
-  static_assert(smem <= (size_t)TC_SMEM_MAX, "tc_gemm shared memory");
+  int64_t splits = std::max<int64_t>(1, (148 * 4 + mt - 1) / mt);
+  splits = std::min<int64_t>(splits, nkb);
+  const int kps = (int)((nkb + splits - 1) / splits);
+  splits = (nkb + kps - 1) / kps;
+  constexpr size_t STAGE = 2 * TC_BM * TC_BK * 4 + 2 * NP * TC_BK * 4;
+  const size_t smem = 1024 + tc_stages<NP>() * STAGE + (3 * tc_stages<NP>() + 1) * 8 + 16;
   cudaFuncSetAttribute(tc_gemm_3xtf32<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int64_t groups = (mt + MT - 1) / MT;
-  tc_gemm_3xtf32<NP><<<dim3((unsigned)groups, (unsigned)splits), TC_THREADS, smem, st>>>(
-      mA, mH, mL, n, mt, MT, kps, nkb, Y, ldy, k, splits > 1 ? 1 : 0, status);
+  tc_gemm_3xtf32<NP><<<dim3((unsigned)mt, (unsigned)splits), TC_THREADS, smem, st>>>(mA, mH, mL, n, kps, nkb, Y, ldy,
+                                                                                     k, status);
   return true;
 }
 

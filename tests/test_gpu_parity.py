@@ -556,3 +556,31 @@ def test_small_persistent_iteration_equals_multikernel(cfgname, n, k, s, monkeyp
     for a_, b_ in zip(h1, h2):
         assert (a_["s_D"], a_["s_R"], a_["n_uniq"]) == (b_["s_D"], b_["s_R"], b_["n_uniq"])
     assert rel(H1, H2) < 1e-4 and rel(W1, W2) < 1e-4
+
+
+# ------------------------------------------------------------------ LAI fused half (k = 64)
+@pytest.mark.parametrize("n,l", [(3000, 74), (2_049, 40)])
+def test_lai_fused_half_matches_oracle_and_four_kernel_path(n, l, monkeypatch):
+    """LAI-SymNMF with k = 64: the fused launch per half (Y = U (Lambda U^T F) per tile, sweep,
+    X^T X and Lambda U^T X for the next half) against the four-kernel half and the fp64 oracle
+    iterating on the same U, Lambda.  n = 2049 leaves a 1-row last tile."""
+    from synth.configs import init_factor
+    X = np.random.default_rng(3).random((n, 16))
+    A = (X @ X.T / 16).astype(np.float32)
+    k = 64
+    H0 = init_factor(n, k, float(A.mean()), np.random.default_rng(4))
+    alpha = float(A.max())
+    M = S.DeviceMatrix.from_host(A)
+    U, lam = S.rangefinder(M, l, 1, seed=0)
+    res = {}
+    for mode in ("auto", "never"):
+        if mode == "never":
+            monkeypatch.setenv("SYMNMF_LAI_FUSED", "never")
+        W, H = cu(H0), cu(H0)
+        S.iterate(M, W, H, alpha, 3, mode="lai", U=U, lam=lam)
+        res[mode] = (W.cpu().numpy(), H.cpu().numpy())
+    _, Hr, _ = O.iterate(A, H0, H0, alpha, 3, "lai", U=U.cpu().numpy(), lam=lam.cpu().numpy())
+    assert rel(res["auto"][1], Hr) < 1e-4 and rel(res["never"][1], Hr) < 1e-4
+    # the two fp32 paths differ in summation order only (U^T X per tile vs one cross Gram)
+    assert rel(res["auto"][1], res["never"][1]) < 5e-5
+    assert rel(res["auto"][0], res["never"][0]) < 5e-5
