@@ -156,6 +156,8 @@ def kernel_cost(name, n, k, nnz=0, nnz_u=0, n_u=0, l=0, zeroY=False):
         return n_u * (4 * k + 12), n_u * k * k
     if name == "samp_prefix":
         return 4 * n + 8 * n, 0
+    if name == "samp_draws":
+        return None, None
     if name in ("samp_uniq_count", "samp_uniq_write"):
         return 8 * n, 0
     if name == "lai_fused":   # U tile, F tile, X read + write; flops: U M, sweep, X^T X, U^T X

@@ -451,6 +451,11 @@ struct symnmf_solver {
 
 namespace {
 
+void enqueue_sweep(const symnmf_solver& S, const double* G, const float* F, float* X, bool zeroY, double* Gnext,
+                   float* Rf32, int32_t* status, cudaStream_t st) {
+  launch_sweep_fused(G, S.alpha, S.Y, F, X, S.n, S.k, zeroY, S.Gacc, Gnext, Rf32, S.counter, status, st);
+}
+
 // LAI: the fused one-launch half (k = 64, l <= 80); SYMNMF_LAI_FUSED=never disables it (symnmf.h)
 bool lai_enabled() {
   const char* e = getenv("SYMNMF_LAI_FUSED");
@@ -553,7 +558,7 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
   } else if (S.mode == SYMNMF_EXACT) {
     if (!enqueue_product(S.A, F, k, S.Y, S.precision, S.tcs, S.tcs_bytes, status, st)) return false;
     mark(S, st, S.A.kind == SYMNMF_CSR ? "spmm_csr" : (S.precision == SYMNMF_3XTF32 ? "gemm_3xtf32" : "gemm_fp32"));
-    launch_sweep_fused(Gf, S.alpha, S.Y, F, X, n, k, false, S.Gacc, Gnext, nullptr, S.counter, status, st);
+    enqueue_sweep(S, Gf, F, X, false, Gnext, nullptr, status, st);
     mark(S, st, "hals_sweep");
   } else if (lvs) {
     // scores of F from R^{-1} (computed with F^T F) fused with sampler pass S1/S2
@@ -570,15 +575,17 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     mark(S, st, "samp_uniq_write");
     launch_sampled_gram_fused(F, k, S.plan, S.Gacc, S.Gs, S.counter, status, st);
     mark(S, st, "sampled_gram");
-    if (S.A.kind == SYMNMF_CSR)
+    if (S.A.kind == SYMNMF_CSR) {
       launch_sampled_csr_nozero(S.A, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap, S.Y,
                                 status, st);
-    else
+      mark(S, st, "sampled_ah_csr");
+    } else {
       launch_sampled_dense(S.A.val, S.A.lda, n, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap,
                            S.Y, status, st);
-    mark(S, st, S.A.kind == SYMNMF_CSR ? "sampled_ah_csr" : "sampled_ah_dense");
+      mark(S, st, "sampled_ah_dense");
+    }
     // Update(G_s + alpha I, Y_s + alpha F^T); Y re-zeroed for the next scatter; X^T X and its R^{-1}
-    launch_sweep_fused(S.Gs, S.alpha, S.Y, F, X, n, k, true, S.Gacc, Gnext, S.Rinv32, S.counter, status, st);
+    enqueue_sweep(S, S.Gs, F, X, true, Gnext, S.Rinv32, status, st);
     mark(S, st, "hals_sweep");
   } else if (S.lai_fused) {
     // Y = U (Lambda U^T F), sweep, X^T X and Lambda U^T X for the next half, in one launch

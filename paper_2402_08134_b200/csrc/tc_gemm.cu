@@ -8,7 +8,8 @@
 // Per CTA (one 128-row tile of A and one K range, split-K over gridDim.y):
 //   warp 0      TMA producer: A tile [128 x 32] fp32 (128B swizzle), X_hi^T / X_lo^T tiles
 //               [NP x 32] (pre-split and transposed once per product, K-major)
-//   warps 4..7  split the A tile in shared memory (hi in place, lo in a second buffer),
+//   warps 4..7  form A_lo = a - (a & 0xffffe000) of the A tile in a second buffer (the raw tile
+//               is A_hi: the tf32 MMA ignores the low 13 mantissa bits),
 //               fence.proxy.async, arrive; afterwards the epilogue (tcgen05.ld -> fp32 red.add)
 //   warp 1      one elected thread issues 3 x 4 tcgen05.mma.kind::tf32 (M=128, N=NP, K=8)
 //               per stage into a TMEM accumulator and commits the stage back to the producer
@@ -171,16 +172,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_wait(full + s, (i / tc_stages<NP>()) & 1);
       uint4* a = reinterpret_cast<uint4*>(sm + s * STAGE);
       uint4* lo = reinterpret_cast<uint4*>(sm + s * STAGE + A_BYTES);
+      // A_hi is the raw tile: kind::tf32 reads an fp32 operand's top 19 bits (the low 13
+      // mantissa bits are ignored), i.e. exactly a & 0xffffe000; only A_lo is written.
 #pragma unroll 4
       for (int e = t; e < (int)(A_BYTES / 16); e += 128) {
         const uint4 v = a[e];
-        uint4 h, l;
-        h.x = v.x & 0xFFFFE000u; h.y = v.y & 0xFFFFE000u; h.z = v.z & 0xFFFFE000u; h.w = v.w & 0xFFFFE000u;
-        l.x = __float_as_uint(__uint_as_float(v.x) - __uint_as_float(h.x));
-        l.y = __float_as_uint(__uint_as_float(v.y) - __uint_as_float(h.y));
-        l.z = __float_as_uint(__uint_as_float(v.z) - __uint_as_float(h.z));
-        l.w = __float_as_uint(__uint_as_float(v.w) - __uint_as_float(h.w));
-        a[e] = h;
+        uint4 l;
+        l.x = __float_as_uint(__uint_as_float(v.x) - __uint_as_float(v.x & 0xFFFFE000u));
+        l.y = __float_as_uint(__uint_as_float(v.y) - __uint_as_float(v.y & 0xFFFFE000u));
+        l.z = __float_as_uint(__uint_as_float(v.z) - __uint_as_float(v.z & 0xFFFFE000u));
+        l.w = __float_as_uint(__uint_as_float(v.w) - __uint_as_float(v.w & 0xFFFFE000u));
         lo[e] = l;
       }
       fence_proxy_async();

@@ -534,8 +534,10 @@ def test_csr_lvs_replayed_plan_vs_oracle():
                                            ("c2", 2_000, 8, 50)])
 def test_small_persistent_iteration_equals_multikernel(cfgname, n, k, s, monkeypatch):
     """The one-launch-per-iteration LvS kernel (grid barriers between the steps) against the
-    multi-kernel graph path on the same inputs: identical sampling statistics in every half
-    (plans are bit-identical given identical scores) and the same factors after 3 iterations."""
+    multi-kernel graph path on the same inputs: identical sampling statistics in both halves
+    (plans are bit-identical given identical scores) and the same factors after one iteration
+    (later iterations may legitimately draw differently once fp32 summation order has moved a
+    score across a draw boundary, Z29)."""
     from synth.configs import init_factor, mean_entry
     d = make_input(cfgname, n_override=n if n != 1000 else None)
     A = d["A"]
@@ -546,8 +548,8 @@ def test_small_persistent_iteration_equals_multikernel(cfgname, n, k, s, monkeyp
     for mode in ("always", "never"):
         monkeypatch.setenv("SYMNMF_SMALL", mode)
         W, H = cu(H0), cu(H0)
-        sv = S.Solver(M, W, H, d["alpha"], mode="lvs", s=s, tau=tau, seed=9, max_iters=3)
-        sv.run(3)
+        sv = S.Solver(M, W, H, d["alpha"], mode="lvs", s=s, tau=tau, seed=9, max_iters=1)
+        sv.run(1)
         st = sv.stats()
         assert st["status"] == 0
         sv.close()
@@ -555,7 +557,7 @@ def test_small_persistent_iteration_equals_multikernel(cfgname, n, k, s, monkeyp
     (W1, H1, h1), (W2, H2, h2) = out["always"], out["never"]
     for a_, b_ in zip(h1, h2):
         assert (a_["s_D"], a_["s_R"], a_["n_uniq"]) == (b_["s_D"], b_["s_R"], b_["n_uniq"])
-    assert rel(H1, H2) < 1e-4 and rel(W1, W2) < 1e-4
+    assert rel(H1, H2) < 1e-5 and rel(W1, W2) < 1e-5
 
 
 # ------------------------------------------------------------------ LAI fused half (k = 64)

@@ -1,0 +1,17 @@
+#!/bin/bash
+# Round profiles: plain bench line per config, then ncu launch list + one full capture of the top kernel.
+set -u
+OUT=gpurun_out/prof; mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || exit 1
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $OUT/gpu.txt
+prof() {  # cfg mode regex
+  local CMD="python bench.py --config $1 --mode $2 --steps 3 --warmup 3 --profile-only --no-cpu-baseline --no-e2e"
+  $CMD > $OUT/plain_$1_$2.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$1_$2.csv $CMD > /dev/null 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:$3 -s 2 -c 1 -o $OUT/full_$1_$2 $CMD > $OUT/ncu_full_$1_$2.log 2>&1
+  echo "$1 $2 rc=$?"
+}
+prof c2 lvs sweep_fused
+prof c4 lvs sampled_csr
+prof c3 exact tc_gemm
+prof c5 lai lai_sweep_fused
