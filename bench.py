@@ -246,13 +246,16 @@ def run_ours(args, ws, rank, local, pg):
     if args.mode == "lvs":
         kw = dict(s=cfg.s, tau=cfg.tau, seed=cfg.seed)
     elif args.mode == "lai":
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        U, lam = S.rangefinder(M, cfg.l, cfg.q, cfg.seed, precision=precision)
-        e1.record()
-        torch.cuda.synchronize()
-        extra["rangefinder_ms"] = e0.elapsed_time(e1)
+        # the range finder (Alg. RRF + Apx-EVD) runs once per solve: first call (module load,
+        # descriptor setup) and a warm call are both reported
+        for key in ("rangefinder_first_ms", "rangefinder_ms"):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            U, lam = S.rangefinder(M, cfg.l, cfg.q, cfg.seed, precision=precision)
+            e1.record()
+            torch.cuda.synchronize()
+            extra[key] = e0.elapsed_time(e1)
         kw = dict(U=U, lam=lam)
     total = args.warmup + args.steps
     solver = S.Solver(M, W, H, alpha, mode=args.mode, precision=precision, max_iters=total, **kw)
