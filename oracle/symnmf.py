@@ -19,7 +19,7 @@ __all__ = [
     "as_f64", "gram", "ah", "leverage_scores", "hybrid_threshold", "fixed_point_mass",
     "draw_indices", "build_plan", "sampled_products", "hals_sweep", "hals_sweep_explicit",
     "surrogate_objective", "iterate", "gaussian_omega", "orth", "rangefinder", "lai_apply",
-    "residual", "residual_fast", "nls_bruteforce", "frob_sq",
+    "residual", "residual_fast", "nls_bruteforce", "frob_sq", "projected_gradient", "stop_index", "solve",
 ]
 
 TWO40 = float(2 ** 40)
@@ -362,6 +362,54 @@ def residual_fast(A, W, H, AH=None) -> float:
     a2 = frob_sq(A64)
     r2 = a2 + float(np.trace((W.T @ W) @ (H.T @ H))) - 2.0 * float((W * AH).sum())
     return math.sqrt(max(r2, 0.0)) / math.sqrt(a2)
+
+
+# ----------------------------------------------------------------------- NEXT-3 convergence protocol
+def projected_gradient(A, H):
+    """Projected-gradient norm of the SymNMF objective f(H) = ||A - H H^T||_F^2 (App. D).
+
+    grad f = 4 (H H^T - A) H  (P:1588-1589), written as 4 (H (H^T H) - A H);
+    (P grad)_ij = grad_ij if grad_ij < 0 or H_ij > 0, else 0 (the KKT mask).
+    Returns (||P grad||_F, ||grad||_F) in fp64.
+    """
+    A64 = as_f64(A)
+    H = np.asarray(H, dtype=np.float64)
+    grad = 4.0 * (H @ (H.T @ H) - A64 @ H)
+    pg = np.where((grad < 0.0) | (H > 0.0), grad, 0.0)
+    return float(np.sqrt((pg * pg).sum())), float(np.sqrt((grad * grad).sum()))
+
+
+def stop_index(resids, tol: float = 1e-4, patience: int = 4):
+    """The experiments' stopping rule: stop once the normalised residual has failed to
+    decrease by more than `tol` for `patience` consecutive iterations.  `resids[t]` is the
+    residual after iteration t (t = 0, 1, ...); the decrease of iteration t is
+    resids[t-1] - resids[t] (iteration 0 is compared with nothing and never counts).
+    Reading Z30: "by more than 1e-4" is an absolute decrease of the normalised residual.
+    Returns the number of iterations run (the stop happens after iteration t -> t + 1), or
+    None if the rule never fires within the sequence.
+    """
+    run = 0
+    for t in range(1, len(resids)):
+        run = run + 1 if resids[t - 1] - resids[t] <= tol else 0
+        if run >= patience:
+            return t + 1
+    return None
+
+
+def solve(A, H0, alpha: float, max_iters: int, mode: str = "exact", tol: float = 1e-4, patience: int = 4, **kw):
+    """NEXT-3 driver: iterations of `iterate` one at a time with the residual after each (O-14) and the
+    stopping rule of P:1086.  Returns (W, H, resids, iterations run)."""
+    W = np.array(H0, dtype=np.float64, copy=True)
+    H = np.array(H0, dtype=np.float64, copy=True)
+    resids = []
+    first = kw.pop("first_iter", 0)
+    for t in range(max_iters):
+        W, H, _ = iterate(A, W, H, alpha, 1, mode, first_iter=first + t, **kw)
+        resids.append(residual(A, H))
+        done = stop_index(resids, tol, patience)
+        if done is not None:
+            return W, H, resids, done
+    return W, H, resids, max_iters
 
 
 # ----------------------------------------------------------------------- pins helper

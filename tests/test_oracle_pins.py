@@ -355,3 +355,59 @@ def test_lai_iterate_on_low_rank_matches_exact():
     _, H1, _ = O.iterate(A, H0, H0, alpha, 5, "exact")
     _, H2, _ = O.iterate(A, H0, H0, alpha, 5, "lai", U=U, lam=lam)
     assert np.allclose(H1, H2, rtol=1e-6, atol=1e-9)
+
+
+# ------------------------------------------------------------------ NEXT-3: projected gradient, stopping rule
+def test_projected_gradient_vanishes_at_exact_factorization():
+    """A = H0 H0^T: grad f(H0) = 4 (H0 H0^T - A) H0 = 0 exactly."""
+    H0 = np.random.default_rng(0).random((40, 3))
+    pg, g = O.projected_gradient(H0 @ H0.T, H0)
+    assert pg < 1e-12 and g < 1e-12
+
+
+def test_projected_gradient_matches_finite_differences():
+    """The unprojected gradient equals central differences of f(H) = ||A - H H^T||_F^2 (an
+    independent route to the formula of P:1588), and the KKT mask of P:1577-1583 drops
+    exactly the entries with H = 0 and a positive gradient."""
+    for seed in range(1, 60):   # the first draw whose mask drops at least one entry
+        r = np.random.default_rng(seed)
+        X = r.random((9, 9))
+        A = (X + X.T) / 2
+        H = r.random((9, 3)) * 0.3
+        H[[0, 2, 5, 7], [1, 0, 2, 1]] = 0.0
+        G = 4 * (H @ H.T - A) @ H
+        if ((G > 0) & (H == 0)).any():
+            break
+    f = lambda Hm: float(((A - Hm @ Hm.T) ** 2).sum())
+    fd = np.zeros_like(H)
+    eps = 1e-6
+    for i in range(9):
+        for j in range(3):
+            Hp, Hm = H.copy(), H.copy()
+            Hp[i, j] += eps
+            Hm[i, j] -= eps
+            fd[i, j] = (f(Hp) - f(Hm)) / (2 * eps)
+    pg, g = O.projected_gradient(A, H)
+    assert abs(g - np.linalg.norm(fd)) <= 1e-6 * np.linalg.norm(fd)
+    keep = (fd < 0) | (H > 0)
+    assert abs(pg - np.linalg.norm(np.where(keep, fd, 0.0))) <= 1e-6 * np.linalg.norm(fd)
+    assert (~keep).sum() >= 1 and pg < g
+
+
+def test_stop_index_rule():
+    """four consecutive iterations that fail to reduce the residual by more than 1e-4."""
+    r = [0.5, 0.3, 0.2, 0.19995, 0.19991, 0.1999, 0.19985, 0.1998]
+    # decreases: .2 .1 5e-5 4e-5 1e-5 5e-5 5e-5 -> the 4th small one in a row is iteration 6
+    assert O.stop_index(r) == 7
+    assert O.stop_index([0.5, 0.4, 0.3]) is None
+    # a large decrease resets the count
+    assert O.stop_index([1, .99995, .9999, .9998, 0.5, .49999, .49998, .49997, .49996]) == 9
+
+
+def test_solve_planted_stops_and_converges():
+    """The NEXT-3 driver on a noise-free planted problem: stops by the rule with a small residual."""
+    from synth import make_input
+    d = make_input("c1", noise=False)
+    W, H, res, done = O.solve(d["A"], d["H0"], d["alpha"], 400)
+    assert done < 400 and res[-1] < 1e-2
+    assert O.stop_index(res) == done
