@@ -373,7 +373,7 @@ def test_projected_gradient_matches_finite_differences():
         r = np.random.default_rng(seed)
         X = r.random((9, 9))
         A = (X + X.T) / 2
-        H = r.random((9, 3)) * 0.3
+        H = r.random((9, 3)) * 1.5   # H H^T > A on most entries: positive gradients exist
         H[[0, 2, 5, 7], [1, 0, 2, 1]] = 0.0
         G = 4 * (H @ H.T - A) @ H
         if ((G > 0) & (H == 0)).any():
