@@ -18,9 +18,9 @@
  *    256-byte aligned.  Its first 256 bytes hold a device status word (see
  *    symnmf_status_read) that kernels set on device-side failure; kernels
  *    downstream of a failure become no-ops.
- *  - Asynchrony: every function except symnmf_iterate, symnmf_solver_stats
- *    and symnmf_status_read only enqueues work on `st` (no host sync) and is
- *    CUDA-graph capturable.
+ *  - Asynchrony: every function except symnmf_iterate, symnmf_solver_stats,
+ *    symnmf_solver_run_until, symnmf_solver_pgrad and symnmf_status_read only
+ *    enqueues work on `st` (no host sync) and is CUDA-graph capturable.
  *  - Errors never cross the ABI as exceptions; every entry point returns a
  *    symnmf_status.  SYMNMF_ERR_ARG is returned synchronously, before any work
  *    is enqueued, for null pointers, n < 1, k < 1 or k > 64, s < 1,
@@ -193,6 +193,13 @@ symnmf_status symnmf_hals_sweep(const double* G, const float* Y, const float* F,
 symnmf_status symnmf_residual(const symnmf_matrix* A, const float* H, int32_t k, double* out,
                               void* ws, size_t* ws_bytes, cudaStream_t st);
 
+/* NEXT-3 projected gradient of the SymNMF objective f(H) = ||A - H H^T||_F^2 (App. D,
+ * P:1560-1590): grad = 4 (H (H^T H) - A H), entries kept where grad < 0 or
+ * H > 0 (the KKT mask).  A H uses `precision` as in symnmf_ah (CSR: FP32);
+ * H^T H and the norms are fp64.  out fp64 device [2] = {||P grad||_F, ||grad||_F}. */
+symnmf_status symnmf_projected_gradient(const symnmf_matrix* A, const float* H, int32_t k, int32_t precision,
+                                        double* out, void* ws, size_t* ws_bytes, cudaStream_t st);
+
 /* (a14) Iteration driver of Alg. LvS-SymNMF, LAI-SymNMF
  * or exact HALS: per iteration t the W-half (side 0, F = H) then
  * the H-half (side 1, F = W) (Z11-Z13); iteration index first_iter + t keys
@@ -231,6 +238,17 @@ symnmf_status symnmf_solver_run(symnmf_solver* solver, int32_t iters, cudaStream
 symnmf_status symnmf_solver_stats(symnmf_solver* solver, int32_t* iters_done_host,
                                   symnmf_half_stats* stats_host, double* resid_host, cudaStream_t st);
 symnmf_status symnmf_solver_destroy(symnmf_solver* solver);
+/* NEXT-3 convergence protocol (solver created with with_residual = 1, else SYMNMF_ERR_ARG):
+ * runs iterations one at a time, reading back the normalised residual after each (8 bytes,
+ * one stream synchronisation), and stops once it has failed to decrease by more than `tol`
+ * for `patience` consecutive iterations (tol = 1e-4, patience = 4; reading Z30), or
+ * after max_iters iterations, or when max_iters recorded slots are used up.
+ * *iters_run_host receives the number of iterations run. */
+symnmf_status symnmf_solver_run_until(symnmf_solver* solver, int32_t max_iters, double tol, int32_t patience,
+                                      int32_t* iters_run_host, cudaStream_t st);
+/* Per-iteration projected-gradient norms ||P grad f(H)||_F of the recorded iterations (solver
+ * created with with_residual = 1); syncs `st`. */
+symnmf_status symnmf_solver_pgrad(symnmf_solver* solver, double* pgrad_host, cudaStream_t st);
 /* Per-kernel device timing (host only, synchronising): runs `iters` iterations EAGERLY (not
  * from the graph; W and H advance exactly as with symnmf_solver_run) with a CUDA event after
  * every launch site, and returns for each site of one iteration (in launch order) its name

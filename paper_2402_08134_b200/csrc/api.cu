@@ -393,6 +393,42 @@ extern "C" symnmf_status symnmf_residual(const symnmf_matrix* A, const float* H,
   return finish();
 }
 
+// ---------------------------------------------------------------- NEXT-3 projected gradient
+extern "C" symnmf_status symnmf_projected_gradient(const symnmf_matrix* A, const float* H, int32_t k,
+                                                   int32_t precision, double* out, void* ws, size_t* ws_bytes,
+                                                   cudaStream_t st) {
+  if (bad_matrix(A) || !H || !out || bad_k(k)) return SYMNMF_ERR_ARG;
+  if (precision != SYMNMF_FP32 && precision != SYMNMF_3XTF32) return SYMNMF_ERR_ARG;
+  if (A->kind == SYMNMF_CSR && precision != SYMNMF_FP32) return SYMNMF_ERR_ARG;
+  const int64_t n = A->n;
+  const int pg = pgrad_grid(n), ggrid = gram_grid(n);
+  const size_t tcs_bytes = (A->kind == SYMNMF_DENSE && precision == SYMNMF_3XTF32) ? dense_ah_tc_scratch(n, k) : 0;
+  auto layout = [&](Carver& c, double** pp, float** AH, double** G, double** gp, char** tcs) {
+    *pp = c.take<double>((size_t)2 * pg);
+    *AH = c.take<float>((size_t)n * k);
+    *G = c.take<double>((size_t)k * k);
+    *gp = c.take<double>(gram_partial_doubles(k, k, true, ggrid));
+    *tcs = c.take<char>(tcs_bytes);
+  };
+  double *pp, *G, *gp;
+  float* AH;
+  char* tcs;
+  Carver c(nullptr);
+  layout(c, &pp, &AH, &G, &gp, &tcs);
+  bool q;
+  symnmf_status r = ws_protocol(ws, ws_bytes, c.bytes(), &q);
+  if (r != SYMNMF_OK || q) return r;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  layout(w, &pp, &AH, &G, &gp, &tcs);
+  int32_t* status = ws_status(ws);
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
+  if (!enqueue_product(*A, H, k, AH, precision, tcs, tcs_bytes, status, st)) return SYMNMF_ERR_UNSUPPORTED;
+  enqueue_gram(H, n, k, gp, ggrid, G, status, st);
+  launch_pgrad(H, AH, G, n, k, pp, pg, out, status, st);
+  return finish();
+}
+
 // ---------------------------------------------------------------- (a14) solver
 struct symnmf_solver {
   symnmf_matrix A;
@@ -430,6 +466,9 @@ struct symnmf_solver {
   unsigned int* bar;       // grid barrier words (small path)
   symnmf_half_stats* stats;
   double *resid, *rpart, *rout, *GH;
+  double *pgrad, *ppart, *pout;   // NEXT-3: per-iteration projected-gradient norm (with_resid)
+  float* AHpg;                      // A H of the updated H for the projected gradient
+  int pgrid;
   double *Zpart, *Z;
   float* M32;
   bool lai_fused;          // LAI: one fused launch per half (lai_fused.cu)
@@ -515,6 +554,12 @@ void solver_layout(symnmf_solver& S, Carver& c) {
   S.rgrid = residual_grid(n);
   S.rpart = c.take<double>((size_t)2 * S.rgrid);
   S.rout = c.take<double>(4);
+  S.pgrid = pgrad_grid(n);
+  S.pgrad = c.take<double>(S.with_resid ? (size_t)S.max_iters : 0);
+  S.ppart = c.take<double>(S.with_resid ? (size_t)2 * S.pgrid : 0);
+  S.pout = c.take<double>(S.with_resid ? 2 : 0);
+  // CSR reuses AHres for the projected gradient; dense needs its own A H
+  S.AHpg = c.take<float>((S.with_resid && S.hasA && S.A.kind == SYMNMF_DENSE) ? (size_t)n * k : 0);
   if (S.mode == SYMNMF_LVS) {
     S.Rinv32 = c.take<float>((size_t)kp * kp + kp);   // R (upper) | 1 / diag(R)
     S.lev = c.take<float>(n);
@@ -626,6 +671,13 @@ bool enqueue_iteration(symnmf_solver& S, cudaStream_t st) {
     // Gbuf[0] now holds H^T H of the updated H (fused Gram of the H-half sweep)
     launch_residual(S.A, S.H, S.k, S.AHres, S.Gbuf[0], S.rpart, S.rgrid, S.rout, S.status, st);
     launch_pdl(record_resid, 1, 1, 0, st, S.iter_dev, S.first_iter, S.max_iters, S.rout, S.resid);
+    // projected gradient of the SymNMF objective at the new H (App. D)
+    float* AH = S.A.kind == SYMNMF_CSR ? S.AHres : S.AHpg;
+    if (S.A.kind == SYMNMF_DENSE &&
+        !enqueue_product(S.A, S.H, S.k, AH, S.precision, S.tcs, S.tcs_bytes, S.status, st))
+      return false;
+    launch_pgrad(S.H, AH, S.Gbuf[0], S.n, S.k, S.ppart, S.pgrid, S.pout, S.status, st);
+    launch_pdl(record_resid, 1, 1, 0, st, S.iter_dev, S.first_iter, S.max_iters, S.pout, S.pgrad);
     mark(S, st, "residual");
   }
   launch_pdl(bump_iter, 1, 1, 0, st, S.iter_dev);
@@ -724,6 +776,42 @@ extern "C" symnmf_status symnmf_solver_run(symnmf_solver* S, int32_t iters, cuda
   if (!S || iters < 0) return SYMNMF_ERR_ARG;
   for (int t = 0; t < iters; ++t) SYMNMF_CUDA_TRY(cudaGraphLaunch(S->exec, st));
   S->iters_done += iters;
+  return SYMNMF_OK;
+}
+
+extern "C" symnmf_status symnmf_solver_run_until(symnmf_solver* S, int32_t max_iters, double tol, int32_t patience,
+                                                 int32_t* iters_run_host, cudaStream_t st) {
+  // NEXT-3 stopping rule (reading Z30): stop once the normalised residual has failed to
+  // decrease by more than tol for `patience` consecutive iterations.  One residual read-back
+  // (8 bytes, a stream synchronisation) per iteration.
+  if (!S || max_iters < 0 || !(tol >= 0.0) || patience < 1 || !S->with_resid) return SYMNMF_ERR_ARG;
+  int32_t run = 0, done = 0;
+  double prev = 0.0;
+  for (int32_t t = 0; t < max_iters; ++t) {
+    const int32_t slot = S->iters_done;
+    if (slot >= S->max_iters) break;
+    SYMNMF_CUDA_TRY(cudaGraphLaunch(S->exec, st));
+    S->iters_done += 1;
+    ++done;
+    double r = 0.0;
+    SYMNMF_CUDA_TRY(cudaMemcpyAsync(&r, S->resid + slot, sizeof(double), cudaMemcpyDeviceToHost, st));
+    SYMNMF_CUDA_TRY(cudaStreamSynchronize(st));
+    if (t > 0) {
+      run = (prev - r <= tol) ? run + 1 : 0;
+      if (run >= patience) break;
+    }
+    prev = r;
+  }
+  if (iters_run_host) *iters_run_host = done;
+  return SYMNMF_OK;
+}
+
+extern "C" symnmf_status symnmf_solver_pgrad(symnmf_solver* S, double* pgrad_host, cudaStream_t st) {
+  if (!S || !pgrad_host || !S->with_resid) return SYMNMF_ERR_ARG;
+  const int32_t m = std::min(S->iters_done, S->max_iters);
+  if (m > 0)
+    SYMNMF_CUDA_TRY(cudaMemcpyAsync(pgrad_host, S->pgrad, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
+  SYMNMF_CUDA_TRY(cudaStreamSynchronize(st));
   return SYMNMF_OK;
 }
 

@@ -122,5 +122,9 @@ bool launch_small_lvs(const SmallArgs& a, cudaStream_t st);
 void launch_residual(const symnmf_matrix& A, const float* H, int k, const float* AH, const double* G,
                      double* partial, int grid, double* out, const int32_t* status, cudaStream_t st);
 int residual_grid(int64_t n);
+// NEXT-3 projected gradient: out[0] = ||P grad||_F, out[1] = ||grad||_F, grad = 4 (H G - AH), G = H^T H.
+void launch_pgrad(const float* H, const float* AH, const double* G, int64_t n, int k, double* partial, int grid,
+                  double* out, const int32_t* status, cudaStream_t st);
+int pgrad_grid(int64_t n);
 
 }  // namespace symnmf

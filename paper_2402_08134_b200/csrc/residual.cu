@@ -99,6 +99,65 @@ __global__ void resid_csr_final(const double* __restrict__ partial, int grid, co
   out[3] = g2;
 }
 
+// NEXT-3: projected-gradient norm of the SymNMF objective (App. D):
+// grad = 4 (H (H^T H) - A H), computed per entry in fp64 from the fp32 H, AH and
+// the fp64 Gram; the KKT mask keeps grad_ij if grad_ij < 0 or H_ij > 0.
+// partial[2b] = sum of masked grad^2, partial[2b+1] = sum of grad^2 over block b's rows.
+template <int KP>
+__global__ void __launch_bounds__(256) pgrad_partial(const float* __restrict__ H, const float* __restrict__ AH,
+                                                     const double* __restrict__ G, int64_t n, int k,
+                                                     double* __restrict__ partial, const int32_t* __restrict__ status) {
+  __shared__ double sG[KP * KP];
+  __shared__ double red[32];
+  if (dev_failed(status)) return;
+  for (int e = threadIdx.x; e < KP * KP; e += blockDim.x) {
+    const int a = e / KP, b = e - a * KP;
+    sG[e] = (a < k && b < k) ? G[a * k + b] : 0.0;
+  }
+  __syncthreads();
+  double p2 = 0.0, g2 = 0.0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    double h[KP];
+#pragma unroll
+    for (int a = 0; a < KP; ++a) h[a] = a < k ? (double)H[r * k + a] : 0.0;
+#pragma unroll 1
+    for (int j = 0; j < k; ++j) {
+      double hg = 0.0;
+#pragma unroll
+      for (int a = 0; a < KP; ++a) hg = fma(h[a], sG[a * KP + j], hg);
+      const double g = 4.0 * (hg - (double)AH[r * k + j]);
+      g2 += g * g;
+      if (g < 0.0 || H[r * k + j] > 0.f) p2 += g * g;   // KKT mask
+    }
+  }
+  p2 = block_sum(p2, red);
+  g2 = block_sum(g2, red);
+  if (threadIdx.x == 0) { partial[2 * blockIdx.x] = p2; partial[2 * blockIdx.x + 1] = g2; }
+}
+
+__global__ void pgrad_final(const double* __restrict__ partial, int grid, double* __restrict__ out,
+                            const int32_t* __restrict__ status) {
+  if (dev_failed(status)) return;
+  if (threadIdx.x != 0) return;
+  double p2 = 0.0, g2 = 0.0;
+  for (int b = 0; b < grid; ++b) { p2 += partial[2 * b]; g2 += partial[2 * b + 1]; }
+  out[0] = sqrt(p2);
+  out[1] = sqrt(g2);
+}
+
+int pgrad_grid(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 4)); }
+
+void launch_pgrad(const float* H, const float* AH, const double* G, int64_t n, int k, double* partial, int grid,
+                  double* out, const int32_t* status, cudaStream_t st) {
+  switch (kpad(k)) {
+    case 8: pgrad_partial<8><<<grid, 256, 0, st>>>(H, AH, G, n, k, partial, status); break;
+    case 16: pgrad_partial<16><<<grid, 256, 0, st>>>(H, AH, G, n, k, partial, status); break;
+    case 32: pgrad_partial<32><<<grid, 256, 0, st>>>(H, AH, G, n, k, partial, status); break;
+    default: pgrad_partial<64><<<grid, 256, 0, st>>>(H, AH, G, n, k, partial, status); break;
+  }
+  pgrad_final<<<1, 32, 0, st>>>(partial, grid, out, status);
+}
+
 int residual_grid(int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((n + RB_ROWS - 1) / RB_ROWS, 148 * 4));
 }

@@ -260,6 +260,14 @@ def residual(M: DeviceMatrix, H: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def projected_gradient(M: DeviceMatrix, H: torch.Tensor, precision: str = "fp32") -> torch.Tensor:
+    """[||P grad f||_F, ||grad f||_F] of f(H) = ||A - H H^T||^2 (fp64, device), symnmf_projected_gradient."""
+    _cuda(H, torch.float32)
+    out = torch.empty(2, dtype=torch.float64, device=H.device)
+    _call("symnmf_projected_gradient", (M.ref(), _p(H), H.shape[1], _PREC[precision], _p(out)), (_stream(),))
+    return out
+
+
 # ------------------------------------------------------------------ (a14)
 class Solver:
     """Captured-graph iteration driver (symnmf_solver_*)."""
@@ -284,6 +292,22 @@ class Solver:
 
     def run(self, iters: int):
         A.check("symnmf_solver_run", lib().symnmf_solver_run(self.h, int(iters), _stream()))
+
+    def run_until(self, max_iters: int, tol: float = 1e-4, patience: int = 4) -> int:
+        """NEXT-3 stopping rule: iterate until the residual fails to decrease by more than
+        `tol` for `patience` consecutive iterations (needs with_residual=True).  Returns iterations run."""
+        done = C.c_int32(0)
+        A.check("symnmf_solver_run_until", lib().symnmf_solver_run_until(self.h, int(max_iters), float(tol),
+                                                                         int(patience), C.byref(done), _stream()))
+        return done.value
+
+    def pgrad(self):
+        """Projected-gradient norms ||P grad f(H)||_F after each recorded iteration (with_residual=True)."""
+        m = self.max_iters
+        buf = (C.c_double * m)()
+        A.check("symnmf_solver_pgrad", lib().symnmf_solver_pgrad(self.h, buf, _stream()))
+        done = self.stats()["iters"]
+        return [buf[i] for i in range(min(done, m))]
 
     def stats(self):
         m = self.max_iters

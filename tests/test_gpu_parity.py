@@ -586,3 +586,62 @@ def test_lai_fused_half_matches_oracle_and_four_kernel_path(n, l, monkeypatch):
     # the two fp32 paths differ in summation order only (U^T X per tile vs one cross Gram)
     assert rel(res["auto"][1], res["never"][1]) < 5e-5
     assert rel(res["auto"][0], res["never"][0]) < 5e-5
+
+
+# ------------------------------------------------------------------ NEXT-3 convergence protocol
+@pytest.mark.parametrize("which,precision", [("c1", "fp32"), ("c1", "3xtf32"), ("c2small", "fp32")])
+def test_projected_gradient_vs_oracle(which, precision, c1, c2small):
+    """||P grad f(H)|| and ||grad f(H)|| (App. D) at the initial factor and after two
+    HALS iterations (where part of H has hit the bound and the KKT mask matters)."""
+    d = c1 if which == "c1" else c2small
+    A, H0, alpha = d["A"], d["H0"], d["alpha"]
+    M = S.DeviceMatrix.from_host(A)
+    tol = 1e-5 if precision == "fp32" else 2e-4
+    W, H = cu(H0), cu(H0)
+    for it in range(2):
+        pg = S.projected_gradient(M, H, precision).cpu().numpy()
+        opg, og = O.projected_gradient(A, H.cpu().numpy())
+        assert abs(pg[0] - opg) <= tol * opg and abs(pg[1] - og) <= tol * og
+        S.iterate(M, W, H, alpha, 2, mode="exact")
+    Hn = H.cpu().numpy()
+    assert (Hn == 0).any()   # the mask is exercised
+
+
+@pytest.mark.parametrize("mode", ["exact", "lvs"])
+def test_solver_records_projected_gradient(mode, c1):
+    """The solver's per-iteration projected-gradient norm (with_residual) equals the oracle's
+    formula evaluated on the GPU's own H after each of 4 iterations."""
+    A, H0, alpha, cfg = c1["A"], c1["H0"], c1["alpha"], c1["cfg"]
+    M = S.DeviceMatrix.from_host(A)
+    W, H = cu(H0), cu(H0)
+    kw = dict(s=cfg.s, tau=cfg.tau, seed=0) if mode == "lvs" else {}
+    sv = S.Solver(M, W, H, alpha, mode=mode, max_iters=4, with_residual=True, **kw)
+    pgs = []
+    for t in range(4):
+        sv.run(1)
+        pgs.append(O.projected_gradient(A, H.cpu().numpy())[0])
+    got = sv.pgrad()
+    assert sv.stats()["status"] == 0
+    for g, o in zip(got, pgs):
+        assert abs(g - o) <= 1e-5 * o
+    sv.close()
+
+
+def test_run_until_stops_where_the_oracle_stops(c1):
+    """P:1086 stopping rule on c1 EXACT: the GPU solver stops after the same number of iterations
+    as the oracle's driver (unless a residual decrease lies within 1e-6 of the 1e-4 threshold,
+    where fp32 rounding may decide either way)."""
+    A, H0, alpha = c1["A"], c1["H0"], c1["alpha"]
+    _, _, res, done = O.solve(A, H0, alpha, 300)
+    M = S.DeviceMatrix.from_host(A)
+    W, H = cu(H0), cu(H0)
+    sv = S.Solver(M, W, H, alpha, mode="exact", max_iters=300, with_residual=True)
+    ran = sv.run_until(300)
+    r_gpu = sv.stats()["residual"]
+    sv.close()
+    assert len(r_gpu) == ran
+    margins = [abs((res[t - 1] - res[t]) - 1e-4) for t in range(1, len(res))]
+    if min(margins) > 1e-6:
+        assert ran == done
+    assert abs(r_gpu[-1] - res[min(ran, len(res)) - 1]) <= 1e-4 * res[-1]
+    assert O.stop_index(r_gpu) == ran
