@@ -20,6 +20,7 @@ __all__ = [
     "draw_indices", "build_plan", "sampled_products", "hals_sweep", "hals_sweep_explicit",
     "surrogate_objective", "iterate", "gaussian_omega", "orth", "rangefinder", "lai_apply",
     "residual", "residual_fast", "nls_bruteforce", "frob_sq", "projected_gradient", "stop_index", "solve",
+    "rangefinder_adaptive", "solve_lai_ir",
 ]
 
 TWO40 = float(2 ** 40)
@@ -321,6 +322,60 @@ def rangefinder(A, l: int, q: int, seed: int, Omega=None):
     order = np.argsort(-np.abs(lam), kind="stable")
     lam, V = lam[order], V[:, order]
     return Q @ V, lam, Q
+
+
+def rangefinder_adaptive(A, l: int, q_max: int, seed: int, tol: float = 1e-3, Omega=None):
+    """NEXT-2: Alg. Ada-RRF (App. E) for symmetric A, then Apx-EVD.
+
+    Omega Gaussian (O-12); Q = qr(A Omega); then, while j <= q_max (reading Z31: j counts the
+    passes of the loop, which the pseudocode never increments):
+        B^T = A^T Q = A Q;  r = sqrt(||A||^2 - ||B||^2) / ||A||  (the QB residual trick)
+        Q = qr(B^T)
+        stop if r has decreased by no more than tol since the previous pass ("iterates
+        until the normalized residual ceases to decrease by 1e-3 per power iteration") or j = q_max
+        Y = A Q;  Q = qr(Y)
+    Apx-EVD of the returned Q: T = Q^T A Q (symmetrised), T = V Lambda V^T, U = Q V by |lambda|.
+    Returns (U, lam, Q, passes, residuals per pass).
+    """
+    A64 = as_f64(A)
+    n = A64.shape[0]
+    a2 = frob_sq(A64)
+    Om = gaussian_omega(n, l, seed) if Omega is None else np.asarray(Omega)
+    Q = orth(A64 @ Om.astype(np.float64))
+    res = []
+    j = 0
+    while True:
+        j += 1
+        Bt = A64 @ Q
+        b2 = float((Bt * Bt).sum())
+        res.append(math.sqrt(max(a2 - b2, 0.0)) / math.sqrt(a2))
+        Q = orth(Bt)
+        if j >= q_max or (len(res) > 1 and res[-2] - res[-1] <= tol):
+            break
+        Q = orth(A64 @ Q)
+    Z = A64 @ Q
+    T = Q.T @ Z
+    T = 0.5 * (T + T.T)
+    lam, V = np.linalg.eigh(T)
+    order = np.argsort(-np.abs(lam), kind="stable")
+    lam, V = lam[order], V[:, order]
+    return Q @ V, lam, Q, j, res
+
+
+def solve_lai_ir(A, H0, alpha: float, U, lam, max_iters: int, tol: float = 1e-4, patience: int = 4):
+    """NEXT-2 Iterative Refinement: LAI-SymNMF iterations until the stopping
+    rule of P:1086 fires on the residual against the full A, then exact iterations on the full A
+    from that point with the same rule.  Returns (W, H, resids LAI, resids exact)."""
+    W, H, r1, d1 = solve(A, H0, alpha, max_iters, "lai", tol, patience, U=U, lam=lam)
+    W2 = np.array(W, copy=True)
+    H2 = np.array(H, copy=True)
+    r2 = []
+    for t in range(max_iters):
+        W2, H2, _ = iterate(A, W2, H2, alpha, 1, "exact")
+        r2.append(residual(A, H2))
+        if stop_index(r2, tol, patience) is not None:
+            break
+    return W2, H2, r1, r2
 
 
 def lai_apply(U, lam, F):

@@ -411,3 +411,52 @@ def test_solve_planted_stops_and_converges():
     W, H, res, done = O.solve(d["A"], d["H0"], d["alpha"], 400)
     assert done < 400 and res[-1] < 1e-2
     assert O.stop_index(res) == done
+
+
+# ------------------------------------------------------------------ NEXT-2: Ada-RRF, Iterative Refinement
+def test_adaptive_rangefinder_residual_trick_and_stop():
+    """Ada-RRF: every recorded residual equals the direct ||A - Q Q^T A||_F / ||A||_F
+    for the basis of that pass (P:1594-1597 trick, checked by recomputation); an exact-rank A
+    stops after the second pass (no further decrease) with residual ~0; the residuals never increase
+    by much and the loop stops as soon as the decrease falls to 1e-3 or less."""
+    r = np.random.default_rng(5)
+    Hp = r.random((300, 4))
+    A = Hp @ Hp.T
+    U, lam, Q, passes, res = O.rangefinder_adaptive(A, 10, 8, seed=1)
+    assert passes == 2 and res[-1] < 1e-6 and res[0] < 1e-6
+    X = r.random((200, 200))
+    A2 = (X + X.T) / 2 + 200 * np.diag(np.linspace(1, 0, 200) ** 6)
+    U2, lam2, Q2, p2, res2 = O.rangefinder_adaptive(A2, 12, 10, seed=2)
+    # the last Q of the loop is the one whose B produced res2[-1]'s successor basis; check the
+    # trick on the returned Q directly: ||A - Q Q^T A||^2 = ||A||^2 - ||A Q||^2
+    direct = np.linalg.norm(A2 - Q2 @ (Q2.T @ A2)) ** 2
+    trick = (A2 * A2).sum() - ((A2 @ Q2) ** 2).sum()
+    assert abs(direct - trick) <= 1e-8 * (A2 * A2).sum()
+    assert all(res2[i] - res2[i + 1] > 1e-3 for i in range(len(res2) - 2))
+    assert p2 == 10 or res2[-2] - res2[-1] <= 1e-3
+    assert 1 <= p2 <= 10
+
+
+def test_adaptive_rangefinder_fixed_point_equals_rrf_basis_span():
+    """With q_max = 1 Ada-RRF returns qr(A qr(A Omega)) -- the same span as Alg. RRF with one
+    extra application; its LAI operator matches RRF(q=0) composed with one power step."""
+    r = np.random.default_rng(6)
+    X = r.random((120, 120))
+    A = (X + X.T) / 2
+    U, lam, Q, p, res = O.rangefinder_adaptive(A, 8, 1, seed=3)
+    Om = O.gaussian_omega(120, 8, 3).astype(np.float64)
+    Qr = O.orth(A @ O.orth(A @ Om))
+    assert p == 1
+    assert np.linalg.norm(Q @ Q.T - Qr @ Qr.T) < 1e-10
+
+
+def test_iterative_refinement_improves_on_lai():
+    """Iterative Refinement: continuing with exact iterations on the full A never ends
+    at a larger residual than where LAI stopped, on a problem the LAI cannot fit exactly."""
+    from synth import make_input
+    d = make_input("c1")
+    A, H0, alpha = d["A"], d["H0"], d["alpha"]
+    U, lam, Q = O.rangefinder(A, 4, 1, seed=0)        # rank 4 < k = 8: LAI loses information
+    W, H, r_lai, r_ex = O.solve_lai_ir(A, H0, alpha, U, lam, 200)
+    assert r_ex[-1] <= r_lai[-1] + 1e-12
+    assert r_ex[-1] < r_lai[-1] - 1e-3
