@@ -193,6 +193,17 @@ symnmf_status symnmf_hals_sweep(const double* G, const float* Y, const float* F,
 symnmf_status symnmf_residual(const symnmf_matrix* A, const float* H, int32_t k, double* out,
                               void* ws, size_t* ws_bytes, cudaStream_t st);
 
+/* NEXT-2 Alg. Ada-RRF (App. E) + Apx-EVD on dense symmetric A: Q = qr(A Omega);
+ * then per pass j = 1, 2, ...: B^T = A Q, residual ||A - Q B||_F / ||A||_F from the trick
+ * ||A||^2 - ||B||^2 (fp64), Q = qr(B^T); stop when j = q_max or the residual
+ * decreased by no more than `tol` since the previous pass (tol = 1e-3; reading Z31),
+ * else Y = A Q, Q = qr(Y).  Then T = sym(Q^T A Q) = V Lambda V^T, U = Q V (as
+ * symnmf_rangefinder).  Host-synchronising (one 8-byte read-back per pass).  passes_host
+ * receives the number of passes, resid_host (nullable, q_max entries) the residual per pass. */
+symnmf_status symnmf_rangefinder_adaptive(const symnmf_matrix* A, int32_t l, int32_t q_max, double tol, uint64_t seed,
+                                          int32_t precision, float* U, double* lambda, int32_t* passes_host,
+                                          double* resid_host, void* ws, size_t* ws_bytes, cudaStream_t st);
+
 /* NEXT-3 projected gradient of the SymNMF objective f(H) = ||A - H H^T||_F^2 (App. D,
  * P:1560-1590): grad = 4 (H (H^T H) - A H), entries kept where grad < 0 or
  * H > 0 (the KKT mask).  A H uses `precision` as in symnmf_ah (CSR: FP32);
@@ -246,6 +257,17 @@ symnmf_status symnmf_solver_destroy(symnmf_solver* solver);
  * *iters_run_host receives the number of iterations run. */
 symnmf_status symnmf_solver_run_until(symnmf_solver* solver, int32_t max_iters, double tol, int32_t patience,
                                       int32_t* iters_run_host, cudaStream_t st);
+/* NEXT-2/3 driver (host-synchronising): iterations of `mode` (arguments as symnmf_iterate) until
+ * the stopping rule of P:1086 (tol, patience; see symnmf_solver_run_until) or max_iters; with
+ * refine = 1 (Iterative Refinement, P:557-563, P:1088 -- meant for mode = LAI) it then continues
+ * with EXACT iterations on the full A from the factors reached, under the same rule.
+ * iters_host (nullable) [2] = iterations of each phase; resid_host (nullable, 2 * max_iters) =
+ * the residual after every iteration of phase 0 then phase 1.  One workspace serves both phases. */
+symnmf_status symnmf_solve(const symnmf_matrix* A, int64_t n, float* W, float* H, int32_t k, double alpha,
+                           int32_t mode, int32_t precision, int64_t s, double tau, uint64_t seed,
+                           const float* U, const double* lambda, int32_t l, int32_t max_iters, double tol,
+                           int32_t patience, int32_t refine, int32_t* iters_host, double* resid_host,
+                           void* ws, size_t* ws_bytes, cudaStream_t st);
 /* Per-iteration projected-gradient norms ||P grad f(H)||_F of the recorded iterations (solver
  * created with with_residual = 1); syncs `st`. */
 symnmf_status symnmf_solver_pgrad(symnmf_solver* solver, double* pgrad_host, cudaStream_t st);

@@ -49,6 +49,8 @@ SIGNATURES = {
     "symnmf_sampled_ah": (I32, [PM, P, I32, PP, P, P, P, PSZ, P]),
     "symnmf_rangefinder": (I32, [PM, I32, I32, U64, I32, P, P, P, PSZ, P]),
     "symnmf_gaussian": (I32, [I64, I32, U64, P, P]),
+    "symnmf_rangefinder_adaptive": (I32, [PM, I32, I32, F64, U64, I32, P, P, C.POINTER(I32), C.POINTER(F64), P,
+                                          PSZ, P]),
     "symnmf_lai_ah": (I32, [P, P, I64, I32, P, I32, P, P, PSZ, P]),
     "symnmf_hals_sweep": (I32, [P, P, P, P, I64, I32, F64, P, P, PSZ, P]),
     "symnmf_residual": (I32, [PM, P, I32, P, P, PSZ, P]),
@@ -62,6 +64,8 @@ SIGNATURES = {
     "symnmf_solver_destroy": (I32, [P]),
     "symnmf_solver_run_until": (I32, [P, I32, F64, I32, C.POINTER(I32), P]),
     "symnmf_solver_pgrad": (I32, [P, C.POINTER(F64), P]),
+    "symnmf_solve": (I32, [PM, I64, P, P, I32, F64, I32, I32, I64, F64, U64, P, P, I32, I32, F64, I32, I32,
+                           C.POINTER(I32), C.POINTER(F64), P, PSZ, P]),
     "symnmf_solver_graph_nodes": (I32, [P, C.POINTER(I32), C.POINTER(I32)]),
     "symnmf_solver_profile": (I32, [P, I32, I32, C.c_void_p, C.POINTER(C.c_float), C.POINTER(I32), P]),
 }

@@ -3,6 +3,7 @@
 #include <cstdio>
 #include <new>
 #include <vector>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include "kernels.cuh"
@@ -302,6 +303,67 @@ extern "C" symnmf_status symnmf_rangefinder(const symnmf_matrix* A, int32_t l, i
       enqueue_orth(L, n, l, L.Yb, L.Q, status, st);
     }
   }
+  enqueue_dense_apply(*A, L.Q, l, L.Yb, precision, L, status, st);        // Z = A Q
+  launch_cross_gram(L.Q, l, l, L.Yb, l, l, false, n, nullptr, nullptr, nullptr, L.part, L.grid, L.T, l, status, st,
+                    true);
+  launch_symmetrize(L.T, l, st);                                            // T = Q^T A Q
+  launch_jacobi_evd(L.T, l, L.V, lambda, status, st);                       // T = V Lambda V^T
+  launch_rowapply64(L.Q, l, n, l, L.V, l, U, l, status, st);                // U = Q V
+  return finish();
+}
+
+// ---------------------------------------------------------------- NEXT-2 Ada-RRF
+extern "C" symnmf_status symnmf_rangefinder_adaptive(const symnmf_matrix* A, int32_t l, int32_t q_max, double tol,
+                                                     uint64_t seed, int32_t precision, float* U, double* lambda,
+                                                     int32_t* passes_host, double* resid_host, void* ws,
+                                                     size_t* ws_bytes, cudaStream_t st) {
+  // Alg. Ada-RRF (App. E) + Apx-EVD; reading Z31 (symnmf.h)
+  if (bad_matrix(A) || A->kind != SYMNMF_DENSE || l < 1 || l > kMaxL || l > A->n || q_max < 1 || !U || !lambda ||
+      !(tol >= 0.0))
+    return SYMNMF_ERR_ARG;
+  if (precision != SYMNMF_FP32 && precision != SYMNMF_3XTF32) return SYMNMF_ERR_ARG;
+  const int64_t n = A->n;
+  RfLayout L;
+  double *sq_part = nullptr, *sq = nullptr;
+  auto layout = [&](Carver& c) {
+    rf_layout(c, n, l, precision, &L);
+    sq_part = c.take<double>(sumsq_grid());
+    sq = c.take<double>(2);
+  };
+  Carver c(nullptr);
+  layout(c);
+  bool qq;
+  symnmf_status r = ws_protocol(ws, ws_bytes, c.bytes(), &qq);
+  if (r != SYMNMF_OK || qq) return r;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  layout(w);
+  int32_t* status = ws_status(ws);
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
+  double a2 = 0.0, b2 = 0.0;
+  launch_sumsq(A->val, n, n, A->lda, sq_part, sq, status, st);              // ||A||_F^2
+  SYMNMF_CUDA_TRY(cudaMemcpyAsync(&a2, sq, sizeof(double), cudaMemcpyDeviceToHost, st));
+  launch_gaussian(n, l, seed, L.Om, st);                                   // Draw Omega
+  if (!enqueue_dense_apply(*A, L.Om, l, L.Yb, precision, L, status, st)) return SYMNMF_ERR_UNSUPPORTED;
+  enqueue_orth(L, n, l, L.Yb, L.Q, status, st);                             // Q = qr(A Omega)
+  SYMNMF_CUDA_TRY(cudaStreamSynchronize(st));
+  double prev = 0.0;
+  int32_t j = 0;
+  for (;;) {
+    ++j;
+    enqueue_dense_apply(*A, L.Q, l, L.Yb, precision, L, status, st);      // B^T = A^T Q = A Q
+    launch_sumsq(L.Yb, n, l, l, sq_part, sq, status, st);                   // ||B||_F^2
+    SYMNMF_CUDA_TRY(cudaMemcpyAsync(&b2, sq, sizeof(double), cudaMemcpyDeviceToHost, st));
+    enqueue_orth(L, n, l, L.Yb, L.Q, status, st);                           // Q = qr(B^T)
+    SYMNMF_CUDA_TRY(cudaStreamSynchronize(st));
+    const double res = std::sqrt(std::max(a2 - b2, 0.0)) / std::sqrt(a2);  // QB residual trick
+    if (resid_host) resid_host[j - 1] = res;
+    if (j >= q_max || (j > 1 && prev - res <= tol)) break;                 // stopping criterion
+    prev = res;
+    enqueue_dense_apply(*A, L.Q, l, L.Yb, precision, L, status, st);      // Y = A Q
+    enqueue_orth(L, n, l, L.Yb, L.Q, status, st);                           // Q = qr(Y)
+  }
+  if (passes_host) *passes_host = j;
   enqueue_dense_apply(*A, L.Q, l, L.Yb, precision, L, status, st);        // Z = A Q
   launch_cross_gram(L.Q, l, l, L.Yb, l, l, false, n, nullptr, nullptr, nullptr, L.part, L.grid, L.T, l, status, st,
                     true);
@@ -803,6 +865,48 @@ extern "C" symnmf_status symnmf_solver_run_until(symnmf_solver* S, int32_t max_i
     prev = r;
   }
   if (iters_run_host) *iters_run_host = done;
+  return SYMNMF_OK;
+}
+
+extern "C" symnmf_status symnmf_solve(const symnmf_matrix* A, int64_t n, float* W, float* H, int32_t k,
+                                      double alpha, int32_t mode, int32_t precision, int64_t s, double tau,
+                                      uint64_t seed, const float* U, const double* lambda, int32_t l,
+                                      int32_t max_iters, double tol, int32_t patience, int32_t refine,
+                                      int32_t* iters_host, double* resid_host, void* ws, size_t* ws_bytes,
+                                      cudaStream_t st) {
+  // NEXT-2/3 driver: `mode` iterations until the P:1086 stopping rule, then (refine = 1, the
+  // Iterative Refinement of P:557-563 / P:1088) EXACT iterations on the full A until the same
+  // rule.  Both phases reuse one workspace (the first solver is destroyed before the second).
+  if (!A || max_iters < 1 || patience < 1 || !(tol >= 0.0) || (refine && bad_matrix(A))) return SYMNMF_ERR_ARG;
+  const int32_t prec2 = (A && !bad_matrix(A) && A->kind == SYMNMF_CSR) ? SYMNMF_FP32 : precision;
+  size_t b1 = 0, b2 = 0;
+  symnmf_status r = symnmf_solver_create(nullptr, A, n, W, H, k, alpha, mode, precision, s, tau, seed, 0, max_iters,
+                                         U, lambda, l, 1, nullptr, &b1, st);
+  if (r != SYMNMF_OK) return r;
+  if (refine) {
+    r = symnmf_solver_create(nullptr, A, n, W, H, k, alpha, SYMNMF_EXACT, prec2, 0, 1.0, seed, 0, max_iters, nullptr,
+                             nullptr, 0, 1, nullptr, &b2, st);
+    if (r != SYMNMF_OK) return r;
+  }
+  bool q;
+  r = ws_protocol(ws, ws_bytes, std::max(b1, b2), &q);
+  if (r != SYMNMF_OK || q) return r;
+  int32_t ran[2] = {0, 0};
+  for (int phase = 0; phase < (refine ? 2 : 1); ++phase) {
+    symnmf_solver* S = nullptr;
+    size_t bytes = *ws_bytes;
+    r = phase == 0 ? symnmf_solver_create(&S, A, n, W, H, k, alpha, mode, precision, s, tau, seed, 0, max_iters, U,
+                                          lambda, l, 1, ws, &bytes, st)
+                   : symnmf_solver_create(&S, A, n, W, H, k, alpha, SYMNMF_EXACT, prec2, 0, 1.0, seed, 0, max_iters,
+                                          nullptr, nullptr, 0, 1, ws, &bytes, st);
+    if (r != SYMNMF_OK) return r;
+    r = symnmf_solver_run_until(S, max_iters, tol, patience, &ran[phase], st);
+    if (r == SYMNMF_OK)
+      r = symnmf_solver_stats(S, nullptr, nullptr, resid_host ? resid_host + (size_t)phase * max_iters : nullptr, st);
+    symnmf_solver_destroy(S);
+    if (r != SYMNMF_OK) return r;
+  }
+  if (iters_host) { iters_host[0] = ran[0]; iters_host[1] = ran[1]; }
   return SYMNMF_OK;
 }
 

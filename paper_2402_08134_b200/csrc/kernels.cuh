@@ -126,5 +126,9 @@ int residual_grid(int64_t n);
 void launch_pgrad(const float* H, const float* AH, const double* G, int64_t n, int k, double* partial, int grid,
                   double* out, const int32_t* status, cudaStream_t st);
 int pgrad_grid(int64_t n);
+// out[0] = sum of squares (fp64) of a rows x cols block (leading dimension ld); partial: sumsq_grid() doubles.
+void launch_sumsq(const float* X, int64_t rows, int64_t cols, int64_t ld, double* partial, double* out,
+                  const int32_t* status, cudaStream_t st);
+int sumsq_grid();
 
 }  // namespace symnmf

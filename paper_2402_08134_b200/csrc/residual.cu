@@ -158,6 +158,42 @@ void launch_pgrad(const float* H, const float* AH, const double* G, int64_t n, i
   pgrad_final<<<1, 32, 0, st>>>(partial, grid, out, status);
 }
 
+// Sum of squares of a rows x cols fp32 block with leading dimension ld, fp64 accumulation
+// (||A||_F^2 and ||B||_F^2 of Ada-RRF's residual trick).  partial[b] per block,
+// out[0] = fixed-order sum of the partials.
+__global__ void __launch_bounds__(256) sumsq_partial(const float* __restrict__ X, int64_t rows, int64_t cols,
+                                                     int64_t ld, double* __restrict__ partial,
+                                                     const int32_t* __restrict__ status) {
+  __shared__ double red[32];
+  if (dev_failed(status)) return;
+  double s = 0.0;
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / cols, c = e - r * cols;
+    const double v = (double)X[r * ld + c];
+    s = fma(v, v, s);
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+__global__ void sumsq_final(const double* __restrict__ partial, int grid, double* __restrict__ out,
+                            const int32_t* __restrict__ status) {
+  if (dev_failed(status)) return;
+  if (threadIdx.x != 0) return;
+  double s = 0.0;
+  for (int b = 0; b < grid; ++b) s += partial[b];
+  out[0] = s;
+}
+
+int sumsq_grid() { return 148 * 8; }
+
+void launch_sumsq(const float* X, int64_t rows, int64_t cols, int64_t ld, double* partial, double* out,
+                  const int32_t* status, cudaStream_t st) {
+  sumsq_partial<<<sumsq_grid(), 256, 0, st>>>(X, rows, cols, ld, partial, status);
+  sumsq_final<<<1, 32, 0, st>>>(partial, sumsq_grid(), out, status);
+}
+
 int residual_grid(int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((n + RB_ROWS - 1) / RB_ROWS, 148 * 4));
 }

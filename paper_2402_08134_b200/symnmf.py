@@ -230,6 +230,17 @@ def rangefinder(M: DeviceMatrix, l: int, q: int, seed: int, precision="fp32", ch
     return U, lam
 
 
+def rangefinder_adaptive(M: DeviceMatrix, l: int, q_max: int, seed: int, tol: float = 1e-3, precision="fp32"):
+    """(U, lambda, passes, residual per pass) of Alg. Ada-RRF + Apx-EVD, symnmf_rangefinder_adaptive."""
+    U = torch.empty((M.n, l), dtype=torch.float32, device="cuda")
+    lam = torch.empty(l, dtype=torch.float64, device="cuda")
+    passes = C.c_int32(0)
+    res = (C.c_double * q_max)()
+    _call("symnmf_rangefinder_adaptive", (M.ref(), l, q_max, float(tol), int(seed), _PREC[precision], _p(U), _p(lam),
+                                          C.byref(passes), res), (_stream(),))
+    return U, lam, passes.value, [res[i] for i in range(passes.value)]
+
+
 def lai_ah(U: torch.Tensor, lam: torch.Tensor, F: torch.Tensor) -> torch.Tensor:
     """Y = U (Lambda (U^T F)), symnmf_lai_ah."""
     _cuda(U, torch.float32); _cuda(lam, torch.float64); _cuda(F, torch.float32)
@@ -368,3 +379,21 @@ def iterate(M, W, H, alpha, iters, mode="exact", precision="fp32", s=0, tau=1.0,
     halves = [{"s_D": st[i].s_d, "s_R": st[i].s_r, "n_uniq": st[i].n_uniq, "theta": st[i].theta}
               for i in range(2 * iters)]
     return {"halves": halves, "residual": list(rs) if with_residual else None}
+
+
+def solve(M, W, H, alpha, max_iters, mode="exact", precision="fp32", s=0, tau=1.0, seed=0, U=None, lam=None,
+          tol=1e-4, patience=4, refine=False):
+    """symnmf_solve: iterate until the P:1086 stopping rule; refine=True adds Iterative Refinement
+    (EXACT on the full A after LAI).  Returns {"iters": [phase0, phase1], "residual": [list, list]}."""
+    _cuda(W, torch.float32); _cuda(H, torch.float32)
+    n, k = H.shape
+    l = U.shape[1] if U is not None else 0
+    its = (C.c_int32 * 2)()
+    rs = (C.c_double * (2 * max_iters))()
+    pre = (M.ref() if M is not None else None, n, _p(W), _p(H), k, float(alpha), _MODE[mode], _PREC[precision],
+           int(s), float(tau), int(seed), _p(U), _p(lam), l, int(max_iters), float(tol), int(patience),
+           1 if refine else 0, its, rs)
+    ws = _call("symnmf_solve", pre, (_stream(),))
+    del ws
+    return {"iters": [its[0], its[1]],
+            "residual": [[rs[i] for i in range(its[0])], [rs[max_iters + i] for i in range(its[1])]]}

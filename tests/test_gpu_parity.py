@@ -645,3 +645,51 @@ def test_run_until_stops_where_the_oracle_stops(c1):
         assert ran == done
     assert abs(r_gpu[-1] - res[min(ran, len(res)) - 1]) <= 1e-4 * res[-1]
     assert O.stop_index(r_gpu) == ran
+
+
+# ------------------------------------------------------------------ NEXT-2 Ada-RRF + Iterative Refinement
+@pytest.mark.parametrize("precision", ["fp32", "3xtf32"])
+def test_adaptive_rangefinder_vs_oracle(precision):
+    """Ada-RRF: same number of passes as the oracle (unless a residual decrease lies
+    within 1e-5 of the 1e-3 threshold), residual trick values within 1e-5, and the same LAI
+    operator U Lambda U^T on a probe block."""
+    r = np.random.default_rng(8)
+    n = 2048
+    X = r.standard_normal((n, 32))
+    A = (X @ X.T / 32 + 0.02 * np.eye(n)).astype(np.float32)
+    M = S.DeviceMatrix.from_host(A)
+    U, lam, passes, res = S.rangefinder_adaptive(M, 40, 8, seed=4, tol=1e-3, precision=precision)
+    Uo, lamo, Qo, po, reso = O.rangefinder_adaptive(A, 40, 8, seed=4, tol=1e-3)
+    # the trick r^2 = 1 - ||B||^2 / ||A||^2 cancels: a relative product error eps (<= 1e-5, the
+    # bound the 3xTF32 / fp32 product tests assert) moves r by about eps / r
+    dr = [max(1e-5, 1e-5 / b_) for b_ in reso]
+    margins = [abs((reso[i] - reso[i + 1]) - 1e-3) - dr[i] - dr[i + 1] for i in range(len(reso) - 1)]
+    if not margins or min(margins) > 0:
+        assert passes == po
+    for a_, b_, d_ in zip(res, reso, dr):
+        assert abs(a_ - b_) <= d_
+    P = r.standard_normal((n, 6))
+    Ug, lg = U.cpu().numpy().astype(np.float64), lam.cpu().numpy()
+    got = Ug @ (lg[:, None] * (Ug.T @ P))
+    ref = Uo @ (lamo[:, None] * (Uo.T @ P))
+    assert rel(got, ref) < (1e-4 if precision == "fp32" else 5e-4)
+
+
+def test_solve_lai_with_iterative_refinement_vs_oracle(c1):
+    """LAI-SymNMF until the P:1086 rule, then Iterative Refinement on the full A: the
+    GPU driver ends where the oracle's does (residual within 1e-4 relative; iteration counts
+    equal unless a decrease sits within 1e-6 of the rule's 1e-4) and below the LAI phase."""
+    A, H0, alpha = c1["A"], c1["H0"], c1["alpha"]
+    M = S.DeviceMatrix.from_host(A)
+    U, lam = S.rangefinder(M, 4, 1, seed=0)
+    W, H = cu(H0), cu(H0)
+    out = S.solve(M, W, H, alpha, 200, mode="lai", U=U, lam=lam, refine=True)
+    _, _, r1, r2 = O.solve_lai_ir(A, H0, alpha, U.cpu().numpy(), lam.cpu().numpy(), 200)
+    g1, g2 = out["residual"]
+    assert len(g1) == out["iters"][0] and len(g2) == out["iters"][1]
+    near = lambda r: min([abs((r[t - 1] - r[t]) - 1e-4) for t in range(1, len(r))] or [1.0]) <= 1e-6
+    if not near(r1) and not near(r2):
+        assert out["iters"] == [len(r1), len(r2)]
+    assert abs(g2[-1] - r2[-1]) <= 1e-4 * r2[-1]
+    assert g2[-1] < g1[-1]
+    assert abs(O.residual(A, H.cpu().numpy()) - g2[-1]) <= 1e-5
