@@ -20,7 +20,7 @@ __all__ = [
     "draw_indices", "build_plan", "sampled_products", "hals_sweep", "hals_sweep_explicit",
     "surrogate_objective", "iterate", "gaussian_omega", "orth", "rangefinder", "lai_apply",
     "residual", "residual_fast", "nls_bruteforce", "frob_sq", "projected_gradient", "stop_index", "solve",
-    "rangefinder_adaptive", "solve_lai_ir",
+    "rangefinder_adaptive", "solve_lai_ir", "bpp_nnls", "bpp_update",
 ]
 
 TWO40 = float(2 ** 40)
@@ -220,9 +220,61 @@ def surrogate_objective(A, W, H, alpha: float) -> float:
     return float(((A - W @ H.T) ** 2).sum() + alpha * ((W - H) ** 2).sum())
 
 
+# ----------------------------------------------------------------------- NEXT-1 BPP
+def bpp_nnls(G, b, max_iter: int = 500):
+    """argmin_{x >= 0} x^T G x - 2 b^T x (G SPD) by block principal pivoting, the ANLS solver the
+    paper uses (App. G; Kim & Park's full exchange with the backup rule,
+    which the paper cites without restating -- SPEC S:254 accepts any exact active-set method).
+
+    Passive set F (free variables), x_F = G_FF^{-1} b_F, dual y = G x - b on the rest;
+    infeasible V = {i in F: x_i < 0} u {i not in F: y_i < 0}; exchange all of V while |V|
+    shrinks (or up to 3 times without progress), else only max(V).
+    """
+    G = np.asarray(G, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    k = b.shape[0]
+    inF = np.zeros(k, dtype=bool)
+    x = np.zeros(k)
+    y = -b.copy()
+    ninf, p = k + 1, 3
+    for _ in range(max_iter):
+        V = (inF & (x < 0)) | (~inF & (y < 0))
+        nv = int(V.sum())
+        if nv == 0:
+            break
+        if nv < ninf:
+            ninf, p = nv, 3
+        elif p >= 1:
+            p -= 1
+        else:
+            j = int(np.nonzero(V)[0].max())
+            V = np.zeros(k, dtype=bool)
+            V[j] = True
+        inF = inF ^ V
+        x = np.zeros(k)
+        if inF.any():
+            idx = np.nonzero(inF)[0]
+            x[idx] = np.linalg.solve(G[np.ix_(idx, idx)], b[idx])
+        y = G @ x - b
+        y[inF] = 0.0
+    return x
+
+
+def bpp_update(G, Y, F, alpha: float):
+    """Update(G + alpha I, Y + alpha F^T) by exact per-row NLS (ANLS, App. G): row r of
+    the new factor solves min_{x >= 0} x^T (G + alpha I) x - 2 (Y_r + alpha F_r)^T x (bpp_nnls)."""
+    G = np.asarray(G, dtype=np.float64)
+    Y = np.asarray(Y, dtype=np.float64)
+    F = np.asarray(F, dtype=np.float64)
+    k = G.shape[0]
+    Gh = G + alpha * np.eye(k)
+    B = Y + alpha * F
+    return np.stack([bpp_nnls(Gh, B[r]) for r in range(B.shape[0])]) if B.shape[0] else np.zeros((0, k))
+
+
 # ----------------------------------------------------------------------- O-11 / O-13
 def iterate(A, W0, H0, alpha: float, iters: int, mode: str = "exact", s: int = 0, tau: float = 1.0,
-            seed: int = 0, first_iter: int = 0, U=None, lam=None, plans=None, record=False):
+            seed: int = 0, first_iter: int = 0, U=None, lam=None, plans=None, record=False, rule: str = "hals"):
     """O-11 / O-13: the driver of Alg. LvS-SymNMF / LAI-SymNMF / plain HALS.
 
     One iteration = W-half (side 0, H fixed) then H-half (side 1, W fixed)
@@ -232,7 +284,8 @@ def iterate(A, W0, H0, alpha: float, iters: int, mode: str = "exact", s: int = 0
                plan (O-4..O-7) keyed by (seed, first_iter + t, side), G_s, Y_s (O-8);
                `plans[(it, side)]` replays a given plan instead (replay mode).
       "lai"  : G = F^T F, Y = U (Lambda (U^T F))
-    then W or H <- hals_sweep(G, Y, F, X, alpha) (Update with G + alpha I, Y + alpha F^T).
+    then W or H <- Update(G + alpha I, Y + alpha F^T): one HALS sweep (rule "hals", Eq. 2.6)
+    or the exact per-row NLS solution (rule "bpp", NEXT-1).
     Returns (W, H, trace); trace lists per-half plan statistics.
     """
     A64 = as_f64(A)
@@ -262,7 +315,7 @@ def iterate(A, W0, H0, alpha: float, iters: int, mode: str = "exact", s: int = 0
                     st["plan"] = pl
             else:
                 raise ValueError(mode)
-            Xn = hals_sweep(G, Y, F, X, alpha)
+            Xn = hals_sweep(G, Y, F, X, alpha) if rule == "hals" else bpp_update(G, Y, F, alpha)
             if side == 0:
                 W = Xn
             else:

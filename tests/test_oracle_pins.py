@@ -460,3 +460,51 @@ def test_iterative_refinement_improves_on_lai():
     W, H, r_lai, r_ex = O.solve_lai_ir(A, H0, alpha, U, lam, 200)
     assert r_ex[-1] <= r_lai[-1] + 1e-12
     assert r_ex[-1] < r_lai[-1] - 1e-3
+
+
+# ------------------------------------------------------------------ NEXT-1 BPP
+def test_bpp_equals_bruteforce_nls():
+    """BPP (App. G) solves the per-row NLS exactly: equal to 2^k active-set enumeration
+     on random SPD problems, k = 2..6, including sign-mixed right-hand sides."""
+    r = np.random.default_rng(21)
+    for k in range(2, 7):
+        for _ in range(25):
+            M = r.standard_normal((k + 3, k))
+            G = M.T @ M + 0.1 * np.eye(k)
+            b = r.standard_normal(k)
+            x = O.bpp_nnls(G, b)
+            xb = O.nls_bruteforce(G, b)
+            assert np.allclose(x, xb, atol=1e-10, rtol=1e-10)
+
+
+def test_bpp_kkt_larger_k():
+    """KKT conditions for k = 16, 32: x >= 0, y = G x - b >= 0 where x = 0, y = 0 where
+    x > 0, complementarity x^T y = 0."""
+    r = np.random.default_rng(22)
+    for k in (16, 32):
+        for _ in range(10):
+            M = r.standard_normal((2 * k, k))
+            G = M.T @ M
+            b = r.standard_normal(k)
+            x = O.bpp_nnls(G, b)
+            y = G @ x - b
+            scale = np.linalg.norm(G) * max(np.linalg.norm(x), 1) + np.linalg.norm(b)
+            assert (x >= 0).all()
+            assert (y[x == 0] >= -1e-10 * scale).all()
+            assert np.abs(y[x > 0]).max(initial=0) <= 1e-10 * scale
+
+
+def test_bpp_update_is_the_fixed_point_of_hals_sweeps():
+    """Update by BPP equals the limit of repeated HALS sweeps on the same (G, Y) (both solve the
+    same strictly convex NLS, P:162-175 vs App. G)."""
+    r = np.random.default_rng(23)
+    n, k = 30, 5
+    F = r.random((n, k))
+    G = F.T @ F
+    Y = r.random((n, k)) * 3
+    alpha = 0.7
+    Xb = O.bpp_update(G, Y, F, alpha)
+    X = r.random((n, k))
+    for _ in range(3000):
+        X = O.hals_sweep(G, Y, F, X, alpha)
+    assert np.allclose(X, Xb, atol=1e-9)
