@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--mode", default=None, choices=[None, "lvs", "exact", "lai"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rule", default="hals", choices=["hals", "bpp"], help="Update(): HALS sweep or BPP (NEXT-1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
@@ -148,6 +149,8 @@ def kernel_cost(name, n, k, nnz=0, nnz_u=0, n_u=0, l=0, zeroY=False):
         return 8 * nnz + 8 * (n + 1) + 12 * n * k, 2 * nnz * k + 2 * n * k * k
     if name == "csr_tile_lvs":     # sampled product (SURVEY §8(d) N8 bytes) + sweep, fused
         return 8 * nnz_u + 16 * n_u + 4 * n_u * k + 12 * n * k, 2 * nnz_u * k + 2 * n * k * k
+    if name == "bpp_update":   # read Y, F, write X (+ Y re-zero in LvS); pivoting solves are fp64 ALU work
+        return (20 if zeroY else 16) * n * k, None
     if name == "hals_sweep":
         return (20 if zeroY else 16) * n * k, 2 * n * k * k
     if name == "leverage":
@@ -184,12 +187,12 @@ def oracle_steps(args, d, steps, warmup, budget_s=None):
     W = H = d["H0"].astype(np.float64)
     it = 0
     for _ in range(warmup):
-        W, H, _ = O.iterate(A, W, H, alpha, 1, args.mode, first_iter=it, **kw)
+        W, H, _ = O.iterate(A, W, H, alpha, 1, args.mode, first_iter=it, rule=args.rule, **kw)
         it += 1
     t0 = time.perf_counter()
     done = 0
     while done < steps:
-        W, H, _ = O.iterate(A, W, H, alpha, 1, args.mode, first_iter=it, **kw)
+        W, H, _ = O.iterate(A, W, H, alpha, 1, args.mode, first_iter=it, rule=args.rule, **kw)
         it += 1
         done += 1
         if budget_s is not None and time.perf_counter() - t0 > budget_s:
@@ -258,7 +261,7 @@ def run_ours(args, ws, rank, local, pg):
             extra[key] = e0.elapsed_time(e1)
         kw = dict(U=U, lam=lam)
     total = args.warmup + args.steps
-    solver = S.Solver(M, W, H, alpha, mode=args.mode, precision=precision, max_iters=total, **kw)
+    solver = S.Solver(M, W, H, alpha, mode=args.mode, precision=precision, max_iters=total, rule=args.rule, **kw)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MiB > 126 MB L2
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -294,7 +297,8 @@ def run_ours(args, ws, rank, local, pg):
     if args.mode == "lvs":
         ex_steps = max(3, min(args.steps, 30))
         W2, H2 = torch.from_numpy(H0).to(dev), torch.from_numpy(H0).to(dev)
-        sx = S.Solver(M, W2, H2, alpha, mode="exact", precision=precision, max_iters=args.warmup + ex_steps)
+        sx = S.Solver(M, W2, H2, alpha, mode="exact", precision=precision, max_iters=args.warmup + ex_steps,
+                      rule=args.rule)
         sx.run(args.warmup)
         torch.cuda.synchronize()
         acc = 0.0
@@ -374,7 +378,8 @@ def run_ours(args, ws, rank, local, pg):
         oW, oH = torch.empty_like(hW).pin_memory(), torch.empty_like(hH).pin_memory()
         W3, H3 = torch.empty_like(W), torch.empty_like(H)
         e2e_steps = max(3, min(args.steps, 30))
-        s3 = S.Solver(M, W3, H3, alpha, mode=args.mode, precision=precision, max_iters=args.warmup + e2e_steps, **kw)
+        s3 = S.Solver(M, W3, H3, alpha, mode=args.mode, precision=precision, max_iters=args.warmup + e2e_steps,
+                      rule=args.rule, **kw)
 
         def e2e_step():
             for h, dd in zip(host_in, dev_in):
@@ -404,7 +409,7 @@ def run_ours(args, ws, rank, local, pg):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": args.config, "n": n, "nnz": int(nnz), "k": k, "mode": args.mode,
+            "config": {"workload": args.config, "n": n, "nnz": int(nnz), "k": k, "mode": args.mode, "rule": args.rule,
                        "precision": precision, "s": cfg.s if args.mode == "lvs" else None,
                        "tau": cfg.tau if args.mode == "lvs" else None, "l": cfg.l or None, "q": cfg.q or None,
                        "l2": "flushed (256 MiB write) before every timed step", "parallelism": f"replicas{ws}",

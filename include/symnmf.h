@@ -52,6 +52,9 @@ typedef enum {
 enum { SYMNMF_DENSE = 0, SYMNMF_CSR = 1 };        /* symnmf_matrix.kind              */
 enum { SYMNMF_FP32 = 0, SYMNMF_3XTF32 = 1 };      /* precision of a dense product     */
 enum { SYMNMF_EXACT = 0, SYMNMF_LVS = 1, SYMNMF_LAI = 2 };  /* symnmf_iterate mode     */
+/* OR-ed into a mode: Update() by exact per-row NLS with block principal pivoting (ANLS-BPP,
+ * P:155, App. G) instead of one HALS sweep (NEXT-1; k <= 32, else SYMNMF_ERR_UNSUPPORTED). */
+enum { SYMNMF_RULE_BPP = 16 };
 
 /* Symmetric n x n input A (Eq. 2.2).  The caller guarantees
  * A = A^T.  DENSE: val is n x lda fp32 (lda >= n, lda % 4 == 0 for 3XTF32).
@@ -185,6 +188,15 @@ symnmf_status symnmf_lai_ah(const float* U, const double* lambda, int64_t n, int
 symnmf_status symnmf_hals_sweep(const double* G, const float* Y, const float* F, float* X,
                                 int64_t n, int32_t k, double alpha, double* G_new,
                                 void* ws, size_t* ws_bytes, cudaStream_t st);
+
+/* NEXT-1 Update by block principal pivoting (App. G; Kim & Park full exchange
+ * with the backup rule): X[r,:] = argmin_{x >= 0} x^T (G + alpha I) x - 2 (Y[r,:] + alpha F[r,:])^T x
+ * for every row r, fp64 solves (G fp64 k x k, Y F X n x k fp32, k <= 32).  G_new (nullable)
+ * receives X^T X.  nonconv_host (nullable; host-synchronising) receives the number of rows that
+ * hit the 256-step pivoting cap (their last iterate, clipped at 0, is written). */
+symnmf_status symnmf_bpp_update(const double* G, const float* Y, const float* F, float* X, int64_t n, int32_t k,
+                                double alpha, double* G_new, int32_t* nonconv_host, void* ws, size_t* ws_bytes,
+                                cudaStream_t st);
 
 /* (a15) Normalised residual ||A - H H^T||_F / ||A||_F in fp64 (P:101-103,
  * P:1530-1532).  DENSE: direct sum of (A_ij - h_i.h_j)^2; CSR: the trace

@@ -15,6 +15,7 @@ STATUS_NAMES = {0: "OK", 1: "ERR_ARG", 2: "ERR_NOT_PD", 3: "ERR_WORKSPACE", 4: "
 DENSE, CSR = 0, 1
 FP32, TF32X3 = 0, 1
 EXACT, LVS, LAI = 0, 1, 2
+RULE_BPP = 16
 
 # name -> (restype, argtypes); the authoritative list of exported entry points.
 P = C.c_void_p
@@ -54,6 +55,7 @@ SIGNATURES = {
     "symnmf_lai_ah": (I32, [P, P, I64, I32, P, I32, P, P, PSZ, P]),
     "symnmf_hals_sweep": (I32, [P, P, P, P, I64, I32, F64, P, P, PSZ, P]),
     "symnmf_residual": (I32, [PM, P, I32, P, P, PSZ, P]),
+    "symnmf_bpp_update": (I32, [P, P, P, P, I64, I32, F64, P, C.POINTER(I32), P, PSZ, P]),
     "symnmf_projected_gradient": (I32, [PM, P, I32, I32, P, P, PSZ, P]),
     "symnmf_iterate": (I32, [PM, I64, P, P, I32, F64, I32, I32, I64, F64, U64, I32, I32, P, P, I32,
                              C.POINTER(HalfStats), C.POINTER(F64), P, PSZ, P]),

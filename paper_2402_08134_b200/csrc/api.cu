@@ -422,6 +422,39 @@ extern "C" symnmf_status symnmf_hals_sweep(const double* G, const float* Y, cons
   return finish();
 }
 
+// ---------------------------------------------------------------- NEXT-1 BPP update
+extern "C" symnmf_status symnmf_bpp_update(const double* G, const float* Y, const float* F, float* X, int64_t n,
+                                           int32_t k, double alpha, double* G_new, int32_t* nonconv_host, void* ws,
+                                           size_t* ws_bytes, cudaStream_t st) {
+  if (!G || !Y || !F || !X || n < 1 || bad_k(k) || !(alpha >= 0.0)) return SYMNMF_ERR_ARG;
+  if (!bpp_supported(k)) return SYMNMF_ERR_UNSUPPORTED;
+  const int grid = gram_grid(n);
+  auto layout = [&](Carver& c, double** part, int32_t** nc) {
+    *part = c.take<double>(gram_partial_doubles(k, k, true, grid));
+    *nc = c.take<int32_t>(1);
+  };
+  double* part;
+  int32_t* nc;
+  Carver c(nullptr);
+  layout(c, &part, &nc);
+  bool q;
+  symnmf_status r = ws_protocol(ws, ws_bytes, c.bytes(), &q);
+  if (r != SYMNMF_OK || q) return r;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  layout(w, &part, &nc);
+  int32_t* status = ws_status(ws);
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(nc, 0, sizeof(int32_t), st));
+  launch_bpp(G, const_cast<float*>(Y), F, X, n, k, alpha, false, nc, status, st);
+  if (G_new) enqueue_gram(X, n, k, part, grid, G_new, status, st);
+  if (nonconv_host) {
+    SYMNMF_CUDA_TRY(cudaMemcpyAsync(nonconv_host, nc, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    SYMNMF_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  return finish();
+}
+
 // ---------------------------------------------------------------- (a15)
 extern "C" symnmf_status symnmf_residual(const symnmf_matrix* A, const float* H, int32_t k, double* out, void* ws,
                                          size_t* ws_bytes, cudaStream_t st) {
@@ -522,6 +555,8 @@ struct symnmf_solver {
   SamplerWs sw;
   symnmf_plan plan;
   float* Y;
+  bool bpp;                // Update rule: exact per-row NLS by block principal pivoting (NEXT-1)
+  int32_t* nonconv;        // BPP rows that hit the pivoting cap (device counter)
   bool tile;               // EXACT on a large CSR A (kpad(k) == k): product fused into the sweep
   bool small;              // LvS on a small problem: one persistent launch per iteration (small.cu)
   double* Gacc2;           // second zeroed Gram accumulator (small path: G_s and X^T X)
@@ -552,8 +587,15 @@ struct symnmf_solver {
 
 namespace {
 
+// Update(G + alpha I, Y + alpha F^T): one HALS sweep with the next half's Gram (and R) fused, or
+// (rule BPP) the exact per-row NLS followed by the Gram of the new factor.
 void enqueue_sweep(const symnmf_solver& S, const double* G, const float* F, float* X, bool zeroY, double* Gnext,
                    float* Rf32, int32_t* status, cudaStream_t st) {
+  if (S.bpp) {
+    launch_bpp(G, S.Y, F, X, S.n, S.k, S.alpha, zeroY, S.nonconv, status, st);
+    launch_gram_fused(X, S.n, S.k, S.Gacc, Gnext, Rf32, S.counter, status, st);
+    return;
+  }
   launch_sweep_fused(G, S.alpha, S.Y, F, X, S.n, S.k, zeroY, S.Gacc, Gnext, Rf32, S.counter, status, st);
 }
 
@@ -606,7 +648,9 @@ void solver_layout(symnmf_solver& S, Carver& c) {
   S.GH = c.take<double>((size_t)k * k);
   S.gpart = c.take<double>(gram_partial_doubles(k, k, true, S.ggrid));
   // the tile kernel balances hub rows; on small graphs the row-per-group SpMM + sweep is faster
-  S.tile = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode == SYMNMF_EXACT && S.A.nnz >= tile_min_nnz();
+  S.tile = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode == SYMNMF_EXACT && !S.bpp &&
+           S.A.nnz >= tile_min_nnz();
+  S.nonconv = c.take<int32_t>(1);
   S.Y = c.take<float>(S.tile ? 0 : (size_t)n * k);
   S.small = S.mode == SYMNMF_LVS && !S.with_resid && S.hasA && small_lvs_supported(S.A, n, k) && small_enabled();
   S.Gacc2 = c.take<double>(S.small ? (size_t)kGramReplicas * k * k : 0);
@@ -638,7 +682,7 @@ void solver_layout(symnmf_solver& S, Carver& c) {
     S.Zpart = c.take<double>(gram_partial_doubles(S.l, k, false, S.ggrid));
     S.Z = c.take<double>((size_t)S.l * k);
     S.M32 = c.take<float>((size_t)S.l * k);
-    S.lai_fused = lai_fused_supported(k, S.l) && lai_enabled();
+    S.lai_fused = lai_fused_supported(k, S.l) && lai_enabled() && !S.bpp;
     const size_t lp = S.lai_fused ? (size_t)lai_lp(S.l) : 0;
     S.Mside[0] = c.take<float>(lp * k);
     S.Mside[1] = c.take<float>(lp * k);
@@ -666,7 +710,7 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     if (!enqueue_product(S.A, F, k, S.Y, S.precision, S.tcs, S.tcs_bytes, status, st)) return false;
     mark(S, st, S.A.kind == SYMNMF_CSR ? "spmm_csr" : (S.precision == SYMNMF_3XTF32 ? "gemm_3xtf32" : "gemm_fp32"));
     enqueue_sweep(S, Gf, F, X, false, Gnext, nullptr, status, st);
-    mark(S, st, "hals_sweep");
+    mark(S, st, S.bpp ? "bpp_update" : "hals_sweep");
   } else if (lvs) {
     // scores of F from R^{-1} (computed with F^T F) fused with sampler pass S1/S2
     launch_leverage_fused(F, n, k, S.Rinv32, S.lev, S.T, S.sw, S.s, S.plan, S.counter, status, st);
@@ -693,7 +737,7 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     }
     // Update(G_s + alpha I, Y_s + alpha F^T); Y re-zeroed for the next scatter; X^T X and its R^{-1}
     enqueue_sweep(S, S.Gs, F, X, true, Gnext, S.Rinv32, status, st);
-    mark(S, st, "hals_sweep");
+    mark(S, st, S.bpp ? "bpp_update" : "hals_sweep");
   } else if (S.lai_fused) {
     // Y = U (Lambda U^T F), sweep, X^T X and Lambda U^T X for the next half, in one launch
     launch_lai_sweep_fused(S.U, S.l, n, k, S.Mside[side], Gf, S.alpha, F, X, S.lam, S.Gacc, S.UXacc, Gnext,
@@ -706,8 +750,8 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     launch_scale_rows(S.Z, S.l, k, S.lam, S.M32, status, st);
     launch_rowapply32(S.U, S.l, n, S.l, S.M32, k, S.Y, k, status, st);
     mark(S, st, "lai_uz");
-    launch_sweep_fused(Gf, S.alpha, S.Y, F, X, n, k, false, S.Gacc, Gnext, nullptr, S.counter, status, st);
-    mark(S, st, "hals_sweep");
+    enqueue_sweep(S, Gf, F, X, false, Gnext, nullptr, status, st);
+    mark(S, st, S.bpp ? "bpp_update" : "hals_sweep");
   }
   return true;
 }
@@ -755,7 +799,10 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
                                               int32_t max_iters, const float* U, const double* lambda, int32_t l,
                                               int32_t with_residual, void* ws, size_t* ws_bytes, cudaStream_t st) {
   if (n < 1 || !W || !H || bad_k(k) || !(alpha >= 0.0) || max_iters < 1 || first_iter < 0) return SYMNMF_ERR_ARG;
+  const bool bpp = (mode & SYMNMF_RULE_BPP) != 0;
+  mode &= ~SYMNMF_RULE_BPP;
   if (mode != SYMNMF_EXACT && mode != SYMNMF_LVS && mode != SYMNMF_LAI) return SYMNMF_ERR_ARG;
+  if (bpp && !bpp_supported(k)) return SYMNMF_ERR_UNSUPPORTED;
   if (precision != SYMNMF_FP32 && precision != SYMNMF_3XTF32) return SYMNMF_ERR_ARG;
   const bool needA = mode != SYMNMF_LAI || with_residual;
   if (needA && (bad_matrix(A) || A->n != n)) return SYMNMF_ERR_ARG;
@@ -765,7 +812,7 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
   symnmf_solver S{};
   S.hasA = A && !bad_matrix(A);
   if (S.hasA) S.A = *A;
-  S.n = n; S.W = W; S.H = H; S.k = k; S.alpha = alpha; S.mode = mode; S.precision = precision;
+  S.n = n; S.W = W; S.H = H; S.k = k; S.alpha = alpha; S.mode = mode; S.precision = precision; S.bpp = bpp;
   S.s = mode == SYMNMF_LVS ? s : 0;
   S.T = tau * (double)k;   // reading Z1
   S.seed = seed; S.first_iter = first_iter; S.max_iters = max_iters;
@@ -785,6 +832,7 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
   SYMNMF_CUDA_TRY(cudaMemsetAsync(S.stats, 0, sizeof(symnmf_half_stats) * 2 * max_iters, st));
   SYMNMF_CUDA_TRY(cudaMemsetAsync(S.resid, 0, sizeof(double) * max_iters, st));
   SYMNMF_CUDA_TRY(cudaMemsetAsync(S.counter, 0, sizeof(unsigned int) * 4, st));
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(S.nonconv, 0, sizeof(int32_t), st));
   SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Gacc, 0, sizeof(double) * kGramReplicas * k * k, st));
   if (S.mode == SYMNMF_LAI && S.lai_fused) {
     const size_t lp = (size_t)lai_lp(S.l);
@@ -884,8 +932,8 @@ extern "C" symnmf_status symnmf_solve(const symnmf_matrix* A, int64_t n, float* 
                                          U, lambda, l, 1, nullptr, &b1, st);
   if (r != SYMNMF_OK) return r;
   if (refine) {
-    r = symnmf_solver_create(nullptr, A, n, W, H, k, alpha, SYMNMF_EXACT, prec2, 0, 1.0, seed, 0, max_iters, nullptr,
-                             nullptr, 0, 1, nullptr, &b2, st);
+    r = symnmf_solver_create(nullptr, A, n, W, H, k, alpha, SYMNMF_EXACT | (mode & SYMNMF_RULE_BPP), prec2, 0, 1.0,
+                             seed, 0, max_iters, nullptr, nullptr, 0, 1, nullptr, &b2, st);
     if (r != SYMNMF_OK) return r;
   }
   bool q;
@@ -897,8 +945,8 @@ extern "C" symnmf_status symnmf_solve(const symnmf_matrix* A, int64_t n, float* 
     size_t bytes = *ws_bytes;
     r = phase == 0 ? symnmf_solver_create(&S, A, n, W, H, k, alpha, mode, precision, s, tau, seed, 0, max_iters, U,
                                           lambda, l, 1, ws, &bytes, st)
-                   : symnmf_solver_create(&S, A, n, W, H, k, alpha, SYMNMF_EXACT, prec2, 0, 1.0, seed, 0, max_iters,
-                                          nullptr, nullptr, 0, 1, ws, &bytes, st);
+                   : symnmf_solver_create(&S, A, n, W, H, k, alpha, SYMNMF_EXACT | (mode & SYMNMF_RULE_BPP), prec2, 0,
+                                          1.0, seed, 0, max_iters, nullptr, nullptr, 0, 1, ws, &bytes, st);
     if (r != SYMNMF_OK) return r;
     r = symnmf_solver_run_until(S, max_iters, tol, patience, &ran[phase], st);
     if (r == SYMNMF_OK)

@@ -106,6 +106,13 @@ void launch_sampled_csr_nozero(const symnmf_matrix& A, const float* F, int k, co
                                const int64_t* n_uniq_dev, int64_t cap, float* Y, const int32_t* status,
                                cudaStream_t st);
 
+// ---------------------------------------------------------------- bpp.cu (NEXT-1)
+// X <- exact per-row NLS with (G + alpha I, Y + alpha F) (block principal pivoting, k <= 32);
+// zeroY re-zeroes Y after reading; *nonconv counts rows that hit the pivoting-step cap.
+bool bpp_supported(int k);
+void launch_bpp(const double* G, float* Y, const float* F, float* X, int64_t n, int k, double alpha, bool zeroY,
+                int32_t* nonconv, int32_t* status, cudaStream_t st);
+
 // ---------------------------------------------------------------- lai_fused.cu
 int lai_lp(int l);
 bool lai_fused_supported(int k, int l);

@@ -16,6 +16,7 @@ from . import _abi as A
 
 _PREC = {"fp32": A.FP32, "3xtf32": A.TF32X3, A.FP32: A.FP32, A.TF32X3: A.TF32X3}
 _MODE = {"exact": A.EXACT, "lvs": A.LVS, "lai": A.LAI}
+_RULE = {"hals": 0, "bpp": A.RULE_BPP}
 
 
 def lib():
@@ -262,6 +263,18 @@ def hals_sweep(G: torch.Tensor, Y: torch.Tensor, F: torch.Tensor, X: torch.Tenso
     return (X, Gn) if return_gram else X
 
 
+def bpp_update(G: torch.Tensor, Y: torch.Tensor, F: torch.Tensor, X: torch.Tensor, alpha: float,
+               return_gram=False):
+    """X <- exact per-row NLS with (G + alpha I, Y + alpha F^T) by block principal pivoting,
+    symnmf_bpp_update.  Returns X (and X^T X if return_gram) and the non-converged row count."""
+    _cuda(G, torch.float64); _cuda(Y, torch.float32); _cuda(F, torch.float32); _cuda(X, torch.float32)
+    n, k = X.shape
+    Gn = torch.empty((k, k), dtype=torch.float64, device=X.device) if return_gram else None
+    nc = C.c_int32(0)
+    _call("symnmf_bpp_update", (_p(G), _p(Y), _p(F), _p(X), n, k, float(alpha), _p(Gn), C.byref(nc)), (_stream(),))
+    return (X, Gn, nc.value) if return_gram else (X, nc.value)
+
+
 # ------------------------------------------------------------------ (a15)
 def residual(M: DeviceMatrix, H: torch.Tensor) -> torch.Tensor:
     """[||A - H H^T|| / ||A||, ||A||^2, tr(H^T A H), ||H^T H||^2] (fp64, device), symnmf_residual."""
@@ -284,14 +297,14 @@ class Solver:
     """Captured-graph iteration driver (symnmf_solver_*)."""
 
     def __init__(self, M, W, H, alpha, mode="exact", precision="fp32", s=0, tau=1.0, seed=0, first_iter=0,
-                 max_iters=1, U=None, lam=None, with_residual=False):
+                 max_iters=1, U=None, lam=None, with_residual=False, rule="hals"):
         _cuda(W, torch.float32); _cuda(H, torch.float32)
         n, k = H.shape
         self.M, self.W, self.H, self.U, self.lam = M, W, H, U, lam
         self.max_iters = max_iters
         l = U.shape[1] if U is not None else 0
         mref = M.ref() if M is not None else None
-        pre = (mref, n, _p(W), _p(H), k, float(alpha), _MODE[mode], _PREC[precision], int(s), float(tau),
+        pre = (mref, n, _p(W), _p(H), k, float(alpha), _MODE[mode] | _RULE[rule], _PREC[precision], int(s), float(tau),
                int(seed), int(first_iter), int(max_iters), _p(U), _p(lam), l, 1 if with_residual else 0)
         fn = lib().symnmf_solver_create
         size = C.c_size_t(0)
@@ -364,15 +377,15 @@ class Solver:
 
 
 def iterate(M, W, H, alpha, iters, mode="exact", precision="fp32", s=0, tau=1.0, seed=0, first_iter=0, U=None,
-            lam=None, with_residual=False):
+            lam=None, with_residual=False, rule="hals"):
     """symnmf_iterate: `iters` iterations in place on (W, H); returns stats and residual trace."""
     _cuda(W, torch.float32); _cuda(H, torch.float32)
     n, k = H.shape
     l = U.shape[1] if U is not None else 0
     st = (A.HalfStats * (2 * iters))()
     rs = (C.c_double * iters)()
-    pre = (M.ref() if M is not None else None, n, _p(W), _p(H), k, float(alpha), _MODE[mode], _PREC[precision],
-           int(s), float(tau), int(seed), int(first_iter), int(iters), _p(U), _p(lam), l, st,
+    pre = (M.ref() if M is not None else None, n, _p(W), _p(H), k, float(alpha), _MODE[mode] | _RULE[rule],
+           _PREC[precision], int(s), float(tau), int(seed), int(first_iter), int(iters), _p(U), _p(lam), l, st,
            rs if with_residual else None)
     ws = _call("symnmf_iterate", pre, (_stream(),))
     del ws
@@ -382,7 +395,7 @@ def iterate(M, W, H, alpha, iters, mode="exact", precision="fp32", s=0, tau=1.0,
 
 
 def solve(M, W, H, alpha, max_iters, mode="exact", precision="fp32", s=0, tau=1.0, seed=0, U=None, lam=None,
-          tol=1e-4, patience=4, refine=False):
+          tol=1e-4, patience=4, refine=False, rule="hals"):
     """symnmf_solve: iterate until the P:1086 stopping rule; refine=True adds Iterative Refinement
     (EXACT on the full A after LAI).  Returns {"iters": [phase0, phase1], "residual": [list, list]}."""
     _cuda(W, torch.float32); _cuda(H, torch.float32)
@@ -390,8 +403,8 @@ def solve(M, W, H, alpha, max_iters, mode="exact", precision="fp32", s=0, tau=1.
     l = U.shape[1] if U is not None else 0
     its = (C.c_int32 * 2)()
     rs = (C.c_double * (2 * max_iters))()
-    pre = (M.ref() if M is not None else None, n, _p(W), _p(H), k, float(alpha), _MODE[mode], _PREC[precision],
-           int(s), float(tau), int(seed), _p(U), _p(lam), l, int(max_iters), float(tol), int(patience),
+    pre = (M.ref() if M is not None else None, n, _p(W), _p(H), k, float(alpha), _MODE[mode] | _RULE[rule],
+           _PREC[precision], int(s), float(tau), int(seed), _p(U), _p(lam), l, int(max_iters), float(tol), int(patience),
            1 if refine else 0, its, rs)
     ws = _call("symnmf_solve", pre, (_stream(),))
     del ws

@@ -693,3 +693,41 @@ def test_solve_lai_with_iterative_refinement_vs_oracle(c1):
     assert abs(g2[-1] - r2[-1]) <= 1e-4 * r2[-1]
     assert g2[-1] < g1[-1]
     assert abs(O.residual(A, H.cpu().numpy()) - g2[-1]) <= 1e-5
+
+
+# ------------------------------------------------------------------ NEXT-1 BPP update
+@pytest.mark.parametrize("n,k", [(3000, 8), (2049, 16), (1500, 32), (777, 5), (40, 3)])
+def test_bpp_update_vs_oracle(n, k):
+    """Exact per-row NLS by block principal pivoting (App. G) vs the fp64 oracle BPP on the
+    same (G, Y, F): regularised problems from a random factor, right-hand sides with mixed signs
+    so that active sets are non-trivial."""
+    r = np.random.default_rng(n + k)
+    F = r.random((n, k)).astype(np.float32)
+    G = F.astype(np.float64).T @ F.astype(np.float64)
+    Y = (r.standard_normal((n, k)) * 3 + 1).astype(np.float32)
+    alpha = 0.5
+    X = cu(np.zeros((n, k), np.float32))
+    Xg, Gn, nc = S.bpp_update(cu(G), cu(Y), cu(F), X, alpha, return_gram=True)
+    Xo = O.bpp_update(G, Y, F, alpha)
+    assert nc == 0
+    assert rel(Xg.cpu().numpy(), Xo) < 1e-6
+    assert (Xg.cpu().numpy() == 0).any() and (Xg.cpu().numpy() > 0).any()
+    assert rel(Gn.cpu().numpy(), O.gram(Xg.cpu().numpy())) < 1e-6
+
+
+@pytest.mark.parametrize("mode", ["exact", "lvs"])
+def test_solver_bpp_rule_vs_oracle(mode, c1):
+    """ANLS-BPP / LvS-BPP iterations through the solver vs the oracle's
+    iterate(rule="bpp"): normalised residual after 5 iterations within 1e-4 (LvS: same plans, the
+    scores of an exactly solved factor being reproducible to fp32 rounding)."""
+    A, H0, alpha, cfg = c1["A"], c1["H0"], c1["alpha"], c1["cfg"]
+    kw = dict(s=cfg.s, tau=cfg.tau, seed=0) if mode == "lvs" else {}
+    M = S.DeviceMatrix.from_host(A)
+    W, H = cu(H0), cu(H0)
+    out = S.iterate(M, W, H, alpha, 5, mode=mode, rule="bpp", **kw)
+    _, Hr, tr = O.iterate(A, H0, H0, alpha, 5, mode, rule="bpp", **kw)
+    if mode == "lvs":
+        for g, o in zip(out["halves"], tr):
+            assert (g["s_D"], g["s_R"], g["n_uniq"]) == (o["s_D"], o["s_R"], o["n_uniq"])
+    rg, ro = O.residual(A, H.cpu().numpy()), O.residual(A, Hr)
+    assert abs(rg - ro) <= 1e-4 * ro
