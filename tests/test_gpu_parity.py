@@ -711,6 +711,10 @@ def test_bpp_update_vs_oracle(n, k):
     Xo = O.bpp_update(G, Y, F, alpha)
     assert nc == 0
     assert rel(Xg.cpu().numpy(), Xo) < 1e-6
+    # warm start from an arbitrary support reaches the same (unique) minimiser
+    Xw = cu((r.random((n, k)) > 0.5).astype(np.float32))
+    Xw, nc2 = S.bpp_update(cu(G), cu(Y), cu(F), Xw, alpha)
+    assert nc2 == 0 and rel(Xw.cpu().numpy(), Xo) < 1e-6
     assert (Xg.cpu().numpy() == 0).any() and (Xg.cpu().numpy() > 0).any()
     assert rel(Gn.cpu().numpy(), O.gram(Xg.cpu().numpy())) < 1e-6
 
