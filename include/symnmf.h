@@ -191,9 +191,8 @@ symnmf_status symnmf_hals_sweep(const double* G, const float* Y, const float* F,
 
 /* NEXT-1 Update by block principal pivoting (App. G; Kim & Park full exchange
  * with the backup rule): X[r,:] = argmin_{x >= 0} x^T (G + alpha I) x - 2 (Y[r,:] + alpha F[r,:])^T x
- * for every row r, fp64 solves (G fp64 k x k, Y F X n x k fp32, k <= 32).  X on entry is the
- * warm start (its support seeds the passive sets; the minimiser is unique), on exit the
- * solution.  G_new (nullable)
+ * for every row r, fp64 solves (G fp64 k x k, Y F X n x k fp32, k <= 32); X is overwritten
+ * (its entry value is not used).  G_new (nullable)
  * receives X^T X.  nonconv_host (nullable; host-synchronising) receives the number of rows that
  * hit the 256-step pivoting cap (their last iterate, clipped at 0, is written). */
 symnmf_status symnmf_bpp_update(const double* G, const float* Y, const float* F, float* X, int64_t n, int32_t k,

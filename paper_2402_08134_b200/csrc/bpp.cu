@@ -2,8 +2,7 @@
 // uses with block principal pivoting (App. G; Kim & Park's full exchange with
 // the backup rule, cited but not restated by the paper):
 //   row r:  min_{x >= 0} x^T Gh x - 2 b^T x,   Gh = G + alpha I,  b = Y_r + alpha F_r.
-// One warp per row, lane c <-> variable c (k <= 32), warm-started from the support of the
-// factor being replaced.  Each pivoting step factors the passive-set
+// One warp per row, lane c <-> variable c (k <= 32).  Each pivoting step factors the passive-set
 // system in fp64 registers: the lane-per-column Cholesky (chol_col_pass) of Gh with the active
 // rows / columns replaced by the identity and a zero right-hand side there, so x_active = 0 falls
 // out of the same solve; forward substitution broadcasts z_j lane by lane, back substitution
@@ -33,24 +32,20 @@ __global__ void __launch_bounds__(BT, 1) bpp_rows(const double* __restrict__ G, 
   const int64_t nw = (int64_t)gridDim.x * (BT / 32);
   for (int64_t r = (int64_t)blockIdx.x * (BT / 32) + (threadIdx.x >> 5); r < n; r += nw) {
     const double bh = act ? (double)Y[r * k + lane] + alpha * (double)F[r * k + lane] : 0.0;
-    // warm start: the passive set of the factor being replaced (ANLS changes it little from one
-    // iteration to the next); the NLS minimiser is unique, so the start only changes the path
-    bool inF = act && X[r * k + lane] > 0.f;
+    // cold start (F empty, x = 0, y = -b): measured faster than starting from the support of the
+    // replaced factor, which the sampled LvS problems move from one half to the next
+    bool inF = false;
     double x = 0.0, y = -bh;
     int ninf = k + 1, p = 3, it = 0;
-    bool first = __any_sync(0xffffffffu, inF);   // solve for the warm passive set before testing
     for (; it < kBppMaxIt; ++it) {
-      if (!first) {
-        const bool inf = act && (inF ? x < 0.0 : y < 0.0);
-        unsigned V = __ballot_sync(0xffffffffu, inf);
-        if (!V) break;
-        const int nv = __popc(V);
-        if (nv < ninf) { ninf = nv; p = 3; }      // full exchange while the infeasible set shrinks
-        else if (p >= 1) { --p; }                 // ... or up to 3 times without progress
-        else V = 1u << (31 - __clz(V));           // backup rule: exchange only max(V)
-        if ((V >> lane) & 1u) inF = !inF;
-      }
-      first = false;
+      const bool inf = act && (inF ? x < 0.0 : y < 0.0);
+      unsigned V = __ballot_sync(0xffffffffu, inf);
+      if (!V) break;
+      const int nv = __popc(V);
+      if (nv < ninf) { ninf = nv; p = 3; }        // full exchange while the infeasible set shrinks
+      else if (p >= 1) { --p; }                   // ... or up to 3 times without progress
+      else V = 1u << (31 - __clz(V));             // backup rule: exchange only max(V)
+      if ((V >> lane) & 1u) inF = !inF;
       const unsigned Fm = __ballot_sync(0xffffffffu, inF);
       // passive-set system: column `lane` of Gh_FF, identity elsewhere
       double b[KP];

@@ -24,7 +24,7 @@ namespace symnmf {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 32;          // fp32 elements per 128-byte row
-template <int NP> constexpr int tc_stages() { return NP <= 80 ? 4 : 3; }
+template <int NP> constexpr int tc_stages() { return NP <= 32 ? 5 : NP <= 80 ? 4 : 3; }
 constexpr int TC_THREADS = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }

@@ -711,7 +711,7 @@ def test_bpp_update_vs_oracle(n, k):
     Xo = O.bpp_update(G, Y, F, alpha)
     assert nc == 0
     assert rel(Xg.cpu().numpy(), Xo) < 1e-6
-    # warm start from an arbitrary support reaches the same (unique) minimiser
+    # the entry value of X is not used
     Xw = cu((r.random((n, k)) > 0.5).astype(np.float32))
     Xw, nc2 = S.bpp_update(cu(G), cu(Y), cu(F), Xw, alpha)
     assert nc2 == 0 and rel(Xw.cpu().numpy(), Xo) < 1e-6
