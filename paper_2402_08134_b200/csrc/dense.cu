@@ -112,7 +112,7 @@ void launch_dense_ah_simt(const float* A, int64_t lda, int64_t n, const float* F
 // A) x JB columns.  The CTA's range of U (indices and weights) is loaded into shared memory
 // once; the gathered SDU x 128 slabs of A and the SDU raw rows F[U_u, :] then stream through an
 // SDS-stage cp.async ring, so no load on the critical path depends on another; omega_u scales
-// the A value at use.  fp32 FMAs, flushed into fp64 registers every stage.  gridDim.y splits U
+// the staged F rows once per stage.  fp32 FMAs, flushed into fp64 registers every stage.  gridDim.y splits U
 // (fp32 atomics into a zeroed Y) so that the grid fills the SMs.
 constexpr int SDC = 128;    // output rows per CTA
 constexpr int SDS = 4;      // pipeline stages
@@ -214,10 +214,12 @@ __global__ void __launch_bounds__(32 * (KP / JB)) sampled_dense_v3(const float* 
     __syncthreads();
     const int buf = s % SDS;
     const float* a = sA + (size_t)buf * SDU * SDC;
-    const float* f = sF + (size_t)buf * SDU * KP;
+    float* fs = sF + (size_t)buf * SDU * KP;
+    for (int e = tid; e < SDU * KP; e += NT) fs[e] *= sW[s * SDU + e / KP];   // omega_u F[U_u, :], once
+    __syncthreads();
+    const float* f = fs;
 #pragma unroll 8
     for (int r = 0; r < SDU; ++r) {
-      const float om = sW[s * SDU + r];
       const float4 a4 = *reinterpret_cast<const float4*>(a + r * SDC + 4 * tx);
       float fv[JB];
 #pragma unroll
@@ -225,7 +227,7 @@ __global__ void __launch_bounds__(32 * (KP / JB)) sampled_dense_v3(const float* 
         const float4 v = *reinterpret_cast<const float4*>(f + r * KP + ty * JB + j);
         fv[j] = v.x; fv[j + 1] = v.y; fv[j + 2] = v.z; fv[j + 3] = v.w;
       }
-      const float av[4] = {a4.x * om, a4.y * om, a4.z * om, a4.w * om};
+      const float av[4] = {a4.x, a4.y, a4.z, a4.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
