@@ -158,86 +158,91 @@ __global__ void __launch_bounds__(32 * (KP / JB)) sampled_dense_v3(const float* 
   const int64_t per = ((nu + gridDim.y - 1) / gridDim.y + SDU - 1) / SDU * SDU;
   const int64_t u0 = (int64_t)blockIdx.y * per, u1 = min64(nu, u0 + per);
   if (u0 >= u1) return;
-  const int cnt = (int)(u1 - u0);
-  for (int e = tid; e < ((cnt + SDU - 1) / SDU) * SDU; e += NT) {
-    const bool ok = e < cnt;
-    sRow[e] = ok ? (int64_t)__ldg(uniq + u0 + e) : -1;
-    sW[e] = ok ? (float)__ldg(w + u0 + e) : 0.f;
-  }
-  __syncthreads();
-  const int nst = (cnt + SDU - 1) / SDU;
-  auto issue = [&](int s) {
-    if (s < nst) {
-      const int buf = s % SDS;
-      float* a = sA + (size_t)buf * SDU * SDC;
-      for (int e = tid; e < SDU * (SDC / 4); e += NT) {
-        const int r = e / (SDC / 4), q = e - r * (SDC / 4);
-        const int64_t row = sRow[s * SDU + r];
-        const int64_t c = c0 + 4 * q;
-        float* dst = a + r * SDC + 4 * q;
-        if (vec) {
-          const bool ok = row >= 0 && c < n;
-          cp_async16(dst, ok ? (const void*)(A + row * lda + c) : (const void*)A, ok);
-        } else {
-#pragma unroll
-          for (int t = 0; t < 4; ++t) dst[t] = (row >= 0 && c + t < n) ? __ldg(A + row * lda + c + t) : 0.f;
-        }
-      }
-      float* f = sF + (size_t)buf * SDU * KP;
-      if (k == KP) {
-        for (int e = tid; e < SDU * (KP / 4); e += NT) {
-          const int r = e / (KP / 4), q = e - r * (KP / 4);
-          const int64_t row = sRow[s * SDU + r];
-          cp_async16(f + r * KP + 4 * q, row >= 0 ? (const void*)(F + row * KP + 4 * q) : (const void*)F, row >= 0);
-        }
-      } else {
-        for (int e = tid; e < SDU * KP; e += NT) {
-          const int r = e / KP, j = e - r * KP;
-          const int64_t row = sRow[s * SDU + r];
-          f[r * KP + j] = (row >= 0 && j < k) ? __ldg(F + row * k + j) : 0.f;
-        }
-      }
-    }
-    cp_async_commit();   // (possibly empty) group per stage keeps the wait count uniform
-  };
   float acc[4][JB];
   double acc64[4][JB];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < JB; ++j) { acc[i][j] = 0.f; acc64[i][j] = 0.0; }
-#pragma unroll
-  for (int s = 0; s < SDS - 1; ++s) issue(s);
-  for (int s = 0; s < nst; ++s) {
-    issue(s + SDS - 1);
-    cp_async_wait<SDS - 1>();
+  // the CTA's U range in chunks of SDUMAX entries (indices + weights staged once per chunk)
+  for (int64_t cu0 = u0; cu0 < u1; cu0 += SDUMAX) {
+    const int cnt = (int)min64(SDUMAX, u1 - cu0);
     __syncthreads();
-    const int buf = s % SDS;
-    const float* a = sA + (size_t)buf * SDU * SDC;
-    float* fs = sF + (size_t)buf * SDU * KP;
-    for (int e = tid; e < SDU * KP; e += NT) fs[e] *= sW[s * SDU + e / KP];   // omega_u F[U_u, :], once
+    for (int e = tid; e < ((cnt + SDU - 1) / SDU) * SDU; e += NT) {
+      const bool ok = e < cnt;
+      sRow[e] = ok ? (int64_t)__ldg(uniq + cu0 + e) : -1;
+      sW[e] = ok ? (float)__ldg(w + cu0 + e) : 0.f;
+    }
     __syncthreads();
-    const float* f = fs;
-#pragma unroll 8
-    for (int r = 0; r < SDU; ++r) {
-      const float4 a4 = *reinterpret_cast<const float4*>(a + r * SDC + 4 * tx);
-      float fv[JB];
+    const int nst = (cnt + SDU - 1) / SDU;
+    auto issue = [&](int s) {
+      if (s < nst) {
+        const int buf = s % SDS;
+        float* a = sA + (size_t)buf * SDU * SDC;
+        for (int e = tid; e < SDU * (SDC / 4); e += NT) {
+          const int r = e / (SDC / 4), q = e - r * (SDC / 4);
+          const int64_t row = sRow[s * SDU + r];
+          const int64_t c = c0 + 4 * q;
+          float* dst = a + r * SDC + 4 * q;
+          if (vec) {
+            const bool ok = row >= 0 && c < n;
+            cp_async16(dst, ok ? (const void*)(A + row * lda + c) : (const void*)A, ok);
+          } else {
 #pragma unroll
-      for (int j = 0; j < JB; j += 4) {
-        const float4 v = *reinterpret_cast<const float4*>(f + r * KP + ty * JB + j);
-        fv[j] = v.x; fv[j + 1] = v.y; fv[j + 2] = v.z; fv[j + 3] = v.w;
+            for (int t = 0; t < 4; ++t) dst[t] = (row >= 0 && c + t < n) ? __ldg(A + row * lda + c + t) : 0.f;
+          }
+        }
+        float* f = sF + (size_t)buf * SDU * KP;
+        if (k == KP) {
+          for (int e = tid; e < SDU * (KP / 4); e += NT) {
+            const int r = e / (KP / 4), q = e - r * (KP / 4);
+            const int64_t row = sRow[s * SDU + r];
+            cp_async16(f + r * KP + 4 * q, row >= 0 ? (const void*)(F + row * KP + 4 * q) : (const void*)F, row >= 0);
+          }
+        } else {
+          for (int e = tid; e < SDU * KP; e += NT) {
+            const int r = e / KP, j = e - r * KP;
+            const int64_t row = sRow[s * SDU + r];
+            f[r * KP + j] = (row >= 0 && j < k) ? __ldg(F + row * k + j) : 0.f;
+          }
+        }
       }
-      const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+      cp_async_commit();   // (possibly empty) group per stage keeps the wait count uniform
+    };
+#pragma unroll
+    for (int s = 0; s < SDS - 1; ++s) issue(s);
+    for (int s = 0; s < nst; ++s) {
+      issue(s + SDS - 1);
+      cp_async_wait<SDS - 1>();
+      __syncthreads();
+      const int buf = s % SDS;
+      const float* a = sA + (size_t)buf * SDU * SDC;
+      float* fs = sF + (size_t)buf * SDU * KP;
+      for (int e = tid; e < SDU * KP; e += NT) fs[e] *= sW[s * SDU + e / KP];   // omega_u F[U_u, :], once
+      __syncthreads();
+      const float* f = fs;
+#pragma unroll 8
+      for (int r = 0; r < SDU; ++r) {
+        const float4 a4 = *reinterpret_cast<const float4*>(a + r * SDC + 4 * tx);
+        float fv[JB];
+#pragma unroll
+        for (int j = 0; j < JB; j += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(f + r * KP + ty * JB + j);
+          fv[j] = v.x; fv[j + 1] = v.y; fv[j + 2] = v.z; fv[j + 3] = v.w;
+        }
+        const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < JB; ++j) acc[i][j] = fmaf(av[i], fv[j], acc[i][j]);
+      }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < JB; ++j) acc[i][j] = fmaf(av[i], fv[j], acc[i][j]);
+        for (int j = 0; j < JB; ++j) { acc64[i][j] += (double)acc[i][j]; acc[i][j] = 0.f; }
+      __syncthreads();   // buffer `buf` is refilled by a later issue()
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < JB; ++j) { acc64[i][j] += (double)acc[i][j]; acc[i][j] = 0.f; }
-    __syncthreads();   // buffer `buf` is refilled by a later issue()
+    cp_async_wait<0>();
   }
   const bool atomic = gridDim.y > 1;
 #pragma unroll
@@ -261,11 +266,22 @@ static void launch_sd_t(const float* A, int64_t lda, int64_t n, const float* F, 
                         cudaStream_t st) {
   using L = SdSmem<KP, JB, SDU>;
   const int64_t cb = (n + SDC - 1) / SDC;
-  int64_t splits = std::max<int64_t>(1, std::min<int64_t>((148 * 4 + cb - 1) / cb, (cap + 4 * SDU - 1) / (4 * SDU)));
-  splits = std::max<int64_t>(splits, (cap + SDUMAX - 1) / SDUMAX);   // U range of a CTA fits shared memory
+  cudaFuncSetAttribute(sampled_dense_v3<KP, JB, SDU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sampled_dense_v3<KP, JB, SDU>, 32 * (KP / JB), L::bytes);
+  const int64_t slots = 148 * (int64_t)std::max(1, occ);
+  // U splits: whole waves of CTAs (the sampled rows are the long K dimension), at most what the
+  // expected |U| <= min(cap, n) keeps busy with >= 4 stages per CTA
+  int64_t splits = 1;
+  double best = 0.0;
+  const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(16, (cap + 4 * SDU - 1) / (4 * SDU)));
+  for (int64_t sp = 1; sp <= smax; ++sp) {
+    const int64_t ctas = cb * sp, waves = (ctas + slots - 1) / slots;
+    const double eff = (double)ctas / (double)(waves * slots) * (1.0 - 0.01 * (double)sp);
+    if (eff > best + 1e-9) { best = eff; splits = sp; }
+  }
   if (splits > 1) cudaMemsetAsync(Y, 0, sizeof(float) * n * k, st);
   const int vec = (lda % 4 == 0 && n % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) ? 1 : 0;
-  cudaFuncSetAttribute(sampled_dense_v3<KP, JB, SDU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
   sampled_dense_v3<KP, JB, SDU><<<dim3((unsigned)cb, (unsigned)splits), 32 * (KP / JB), L::bytes, st>>>(
       A, lda, n, F, k, uniq, w, nu, Y, vec, status);
 }
