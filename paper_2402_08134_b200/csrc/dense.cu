@@ -137,7 +137,7 @@ struct SdSmem {
 };
 
 template <int KP, int JB, int SDU>
-__global__ void __launch_bounds__(32 * (KP / JB)) sampled_dense_v3(const float* __restrict__ A, int64_t lda, int64_t n,
+__global__ void __launch_bounds__(32 * (KP / JB), 2) sampled_dense_v3(const float* __restrict__ A, int64_t lda, int64_t n,
                                                                   const float* __restrict__ F, int k,
                                                                   const int32_t* __restrict__ uniq,
                                                                   const double* __restrict__ w,
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(32 * (KP / JB)) sampled_dense_v3(const float* 
       for (int e = tid; e < SDU * KP; e += NT) fs[e] *= sW[s * SDU + e / KP];   // omega_u F[U_u, :], once
       __syncthreads();
       const float* f = fs;
-#pragma unroll 8
+#pragma unroll 4
       for (int r = 0; r < SDU; ++r) {
         const float4 a4 = *reinterpret_cast<const float4*>(a + r * SDC + 4 * tx);
         float fv[JB];
