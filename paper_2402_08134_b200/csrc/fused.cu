@@ -270,14 +270,21 @@ __global__ void __launch_bounds__(FT) leverage_fused(const float* __restrict__ F
         const float4 v = *reinterpret_cast<const float4*>(sF + tid * ST + a);
         f[a] = v.x; f[a + 1] = v.y; f[a + 2] = v.z; f[a + 3] = v.w;
       }
-      // q = f R^{-1} by forward substitution q R = f (R upper, rd = 1 / diag R), l = ||q||^2
+      // q = f R^{-1} by forward substitution q R = f (R upper, rd = 1 / diag R), l = ||q||^2.
+      // Row a of R is read as float4 groups from the aligned group holding column a: entries
+      // c <= a of f are dead once q_a is formed, so updating them too is harmless (R is stored
+      // with zeros below the diagonal), and the shared-memory loads drop fourfold.
       float l = 0.f;
 #pragma unroll
       for (int a = 0; a < KP; ++a) {
         const float q = f[a] * sRd[a];
         l = fmaf(q, q, l);
 #pragma unroll
-        for (int c = a + 1; c < KP; ++c) f[c] = fmaf(-q, sR[a * KP + c], f[c]);
+        for (int c = (a + 1) & ~3; c < KP; c += 4) {
+          const float4 r4 = *reinterpret_cast<const float4*>(sR + a * KP + c);
+          f[c] = fmaf(-q, r4.x, f[c]); f[c + 1] = fmaf(-q, r4.y, f[c + 1]);
+          f[c + 2] = fmaf(-q, r4.z, f[c + 2]); f[c + 3] = fmaf(-q, r4.w, f[c + 3]);
+        }
       }
       lev[r0 + tid] = l;
       const double ld = (double)l;
