@@ -575,6 +575,8 @@ struct symnmf_solver {
   size_t tcs_bytes;
   cudaGraph_t graph;
   cudaGraphExec_t exec;
+  cudaStream_t side;                   // second branch of the iteration graph (G_s || Y_s)
+  cudaEvent_t ev_fork[2], ev_join[2];  // per half
   int32_t iters_done;
   // profiling (symnmf_solver_profile): an event after every launch site of an eager iteration
   struct Prof {
@@ -724,8 +726,11 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     mark(S, st, "samp_uniq_count");
     launch_samp_uniq_write(S.lev, n, S.T, S.sw, S.plan, status, st);
     mark(S, st, "samp_uniq_write");
-    launch_sampled_gram_fused(F, k, S.plan, S.Gacc, S.Gs, S.counter, status, st);
-    mark(S, st, "sampled_gram");
+    // G_s and Y_s only read the plan: G_s runs on a second branch of the graph, concurrently
+    cudaEventRecord(S.ev_fork[side], st);
+    cudaStreamWaitEvent(S.side, S.ev_fork[side], 0);
+    launch_sampled_gram_fused(F, k, S.plan, S.Gacc, S.Gs, S.counter, status, S.side);
+    cudaEventRecord(S.ev_join[side], S.side);
     if (S.A.kind == SYMNMF_CSR) {
       launch_sampled_csr_nozero(S.A, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap, S.Y,
                                 status, st);
@@ -735,6 +740,7 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
                            S.Y, status, st);
       mark(S, st, "sampled_ah_dense");
     }
+    cudaStreamWaitEvent(st, S.ev_join[side], 0);
     // Update(G_s + alpha I, Y_s + alpha F^T); Y re-zeroed for the next scatter; X^T X and its R^{-1}
     enqueue_sweep(S, S.Gs, F, X, true, Gnext, S.Rinv32, status, st);
     mark(S, st, S.bpp ? "bpp_update" : "hals_sweep");
@@ -855,6 +861,11 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
   launch_gram_fused(H, n, k, S.Gacc, S.Gbuf[0], mode == SYMNMF_LVS ? S.Rinv32 : nullptr, S.counter, S.status, st);
   if (finish() != SYMNMF_OK) return SYMNMF_ERR_CUDA;
   // Capture one iteration on a private stream (the caller's may be the legacy default stream).
+  SYMNMF_CUDA_TRY(cudaStreamCreateWithFlags(&S.side, cudaStreamNonBlocking));
+  for (int h = 0; h < 2; ++h) {
+    SYMNMF_CUDA_TRY(cudaEventCreateWithFlags(&S.ev_fork[h], cudaEventDisableTiming));
+    SYMNMF_CUDA_TRY(cudaEventCreateWithFlags(&S.ev_join[h], cudaEventDisableTiming));
+  }
   cudaStream_t cs;
   SYMNMF_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
@@ -985,6 +996,8 @@ extern "C" symnmf_status symnmf_solver_stats(symnmf_solver* S, int32_t* iters_do
 extern "C" symnmf_status symnmf_solver_destroy(symnmf_solver* S) {
   if (!S) return SYMNMF_ERR_ARG;
   cudaGraphExecDestroy(S->exec);
+  cudaStreamDestroy(S->side);
+  for (int h = 0; h < 2; ++h) { cudaEventDestroy(S->ev_fork[h]); cudaEventDestroy(S->ev_join[h]); }
   cudaGraphDestroy(S->graph);
   delete S;
   return SYMNMF_OK;
