@@ -115,3 +115,43 @@ def test_solver_create_query_without_gpu(lib):
     rc = lib.symnmf_solver_create(None, C.byref(dense), 1000, W, H, 8, 1.0, 2, 0, 0, 1.0, 0, 0, 20,
                                   None, None, 0, 0, None, C.byref(sz), None)
     assert rc == 1                                                      # LAI without U / lambda
+
+
+def test_next_items_argument_validation_without_gpu(lib):
+    """NEXT-1/2/3 entry points reject bad arguments synchronously and answer workspace queries."""
+    from paper_2402_08134_b200._abi import Matrix, RULE_BPP
+    sz = C.c_size_t(0)
+    G, Y, F, X = (C.c_void_p(256),) * 4
+    # BPP: alpha < 0, k > 32 unsupported, query ok
+    assert lib.symnmf_bpp_update(G, Y, F, X, 100, 8, -1.0, None, None, None, C.byref(sz), None) == 1
+    assert lib.symnmf_bpp_update(G, Y, F, X, 100, 40, 1.0, None, None, None, C.byref(sz), None) == 5
+    assert lib.symnmf_bpp_update(G, Y, F, X, 100, 16, 1.0, None, None, None, C.byref(sz), None) == 0
+    dense = Matrix(0, 0, 1000, 256, 1000, None, None, 0)
+    csr = Matrix(1, 0, 1000, 256, 0, 256, 256, 5000)
+    U, lam = C.c_void_p(256), C.c_void_p(256)
+    passes = C.c_int32(0)
+    # Ada-RRF: q_max < 1, tol < 0, CSR input
+    assert lib.symnmf_rangefinder_adaptive(C.byref(dense), 10, 0, 1e-3, 0, 0, U, lam, C.byref(passes), None, None,
+                                           C.byref(sz), None) == 1
+    assert lib.symnmf_rangefinder_adaptive(C.byref(dense), 10, 4, -1.0, 0, 0, U, lam, C.byref(passes), None, None,
+                                           C.byref(sz), None) == 1
+    assert lib.symnmf_rangefinder_adaptive(C.byref(csr), 10, 4, 1e-3, 0, 0, U, lam, C.byref(passes), None, None,
+                                           C.byref(sz), None) == 1
+    assert lib.symnmf_rangefinder_adaptive(C.byref(dense), 10, 4, 1e-3, 0, 1, U, lam, C.byref(passes), None, None,
+                                           C.byref(sz), None) == 0 and sz.value > 4 * 1000 * 10
+    # projected gradient: CSR with 3XTF32, bad precision, query ok
+    out = C.c_void_p(256)
+    assert lib.symnmf_projected_gradient(C.byref(csr), F, 8, 1, out, None, C.byref(sz), None) == 1
+    assert lib.symnmf_projected_gradient(C.byref(dense), F, 8, 7, out, None, C.byref(sz), None) == 1
+    assert lib.symnmf_projected_gradient(C.byref(dense), F, 8, 0, out, None, C.byref(sz), None) == 0
+    # solve: patience < 1, tol < 0; the BPP rule bit is accepted by the solver query
+    its = (C.c_int32 * 2)()
+    W = H = C.c_void_p(256)
+    assert lib.symnmf_solve(C.byref(dense), 1000, W, H, 8, 1.0, 0, 0, 0, 1.0, 0, None, None, 0, 50, 1e-4, 0, 0,
+                            its, None, None, C.byref(sz), None) == 1
+    assert lib.symnmf_solve(C.byref(dense), 1000, W, H, 8, 1.0, 0, 0, 0, 1.0, 0, None, None, 0, 50, -1.0, 4, 0,
+                            its, None, None, C.byref(sz), None) == 1
+    assert lib.symnmf_solve(C.byref(dense), 1000, W, H, 8, 1.0, 0 | RULE_BPP, 0, 0, 1.0, 0, None, None, 0, 50, 1e-4,
+                            4, 1, its, None, None, C.byref(sz), None) == 0
+    assert lib.symnmf_solver_create(None, C.byref(dense), 1000, W, H, 40, 1.0, RULE_BPP, 0, 0, 1.0, 0, 0, 5,
+                                    None, None, 0, 0, None, C.byref(sz), None) == 5     # BPP needs k <= 32

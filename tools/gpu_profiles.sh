@@ -1,5 +1,6 @@
 #!/bin/bash
-# Round profiles: plain bench line per config, then ncu launch list + one full capture of the top kernel.
+# Round profiles: per config, the plain bench command, then an ncu launch list and one --set full
+# capture of the dominant kernel (same command line, exited 0 just before).
 set -u
 OUT=gpurun_out/prof; mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || exit 1
@@ -12,6 +13,7 @@ prof() {  # cfg mode regex
   echo "$1 $2 rc=$?"
 }
 prof c2 lvs sweep_fused
-prof c4 lvs sampled_csr
+prof c3 lvs sampled_dense
 prof c3 exact tc_gemm
+prof c4 lvs sampled_csr
 prof c5 lai lai_sweep_fused
