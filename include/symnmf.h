@@ -104,8 +104,6 @@ typedef struct {
  * the same up to fp32 summation order):
  *   SYMNMF_CSR_TILE=always|never   EXACT solver on CSR: force / forbid the tile kernel (product
  *                                  fused with the sweep); default: used from 16M nonzeros.
- *   SYMNMF_TILE_BLOCKS=<b>         tile kernel: column-block passes (default: factor slices of
- *                                  <= 64 MB so each pass's gathers stay in L2).
  *   SYMNMF_SCATTER_SLICE_MB=<mb>   sampled CSR product: rows of Y per destination-range pass
  *                                  (default 48 MB, so each pass's slice of Y stays in L2).
  *   SYMNMF_LAI_FUSED=never         LAI solver (k = 64, l <= 80): use the four-kernel half (U^T F,

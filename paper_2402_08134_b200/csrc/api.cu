@@ -558,9 +558,6 @@ struct symnmf_solver {
   bool bpp;                // Update rule: exact per-row NLS by block principal pivoting (NEXT-1)
   int32_t* nonconv;        // BPP rows that hit the pivoting cap (device counter)
   bool tile;               // EXACT on a large CSR A (kpad(k) == k): product fused into the sweep
-  int nblk;                // tile path: column-block passes (F slice per pass <= 64 MB, L2-resident)
-  int32_t* boff;           // tile path: (nblk - 1) x n per-row block boundaries
-  float* Yp;               // tile path: partial product of the earlier passes
   bool small;              // LvS on a small problem: one persistent launch per iteration (small.cu)
   double* Gacc2;           // second zeroed Gram accumulator (small path: G_s and X^T X)
   unsigned int* bar;       // grid barrier words (small path)
@@ -610,15 +607,6 @@ bool lai_enabled() {
   return !(e && !strcmp(e, "never"));
 }
 
-// Column blocks of the tile path: the factor slice a pass gathers from must stay in L2 (126 MB):
-// 64 MB per slice.  SYMNMF_TILE_BLOCKS=<b> overrides (symnmf.h).
-int tile_blocks(int64_t n, int k) {
-  const char* e = getenv("SYMNMF_TILE_BLOCKS");
-  if (e && atoi(e) > 0) return std::min<int64_t>(atoi(e), n);
-  const int64_t fbytes = (int64_t)sizeof(float) * n * k;
-  return (int)std::max<int64_t>(1, (fbytes + (64ll << 20) - 1) / (64ll << 20));
-}
-
 // LvS on small problems: the persistent iteration kernel only on request (SYMNMF_SMALL=always,
 // symnmf.h): measured slower than the multi-kernel graph on B200 (small.cu)
 bool small_enabled() {
@@ -666,9 +654,6 @@ void solver_layout(symnmf_solver& S, Carver& c) {
            S.A.nnz >= tile_min_nnz();
   S.nonconv = c.take<int32_t>(1);
   S.Y = c.take<float>(S.tile ? 0 : (size_t)n * k);
-  S.nblk = S.tile ? tile_blocks(n, k) : 1;
-  S.boff = c.take<int32_t>(S.nblk > 1 ? (size_t)(S.nblk - 1) * n : 0);
-  S.Yp = c.take<float>(S.nblk > 1 ? (size_t)n * k : 0);
   S.small = S.mode == SYMNMF_LVS && !S.with_resid && S.hasA && small_lvs_supported(S.A, n, k) && small_enabled();
   S.Gacc2 = c.take<double>(S.small ? (size_t)kGramReplicas * k * k : 0);
   S.bar = c.take<unsigned int>(S.small ? 4 : 0);
@@ -721,8 +706,7 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
   double* Gnext = S.Gbuf[side ^ 1];
   const bool lvs = S.mode == SYMNMF_LVS;
   if (S.mode == SYMNMF_EXACT && S.tile) {
-    launch_csr_tile_sweep(S.A, F, Gf, S.alpha, X, n, k, S.Gacc, Gnext, nullptr, S.counter, status, st, S.boff, S.nblk,
-                          S.Yp);
+    launch_csr_tile_sweep(S.A, F, Gf, S.alpha, X, n, k, S.Gacc, Gnext, nullptr, S.counter, status, st);
     mark(S, st, "csr_tile_exact");
   } else if (S.mode == SYMNMF_EXACT) {
     if (!enqueue_product(S.A, F, k, S.Y, S.precision, S.tcs, S.tcs_bytes, status, st)) return false;
@@ -866,7 +850,6 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
                       st);
     launch_scale_rows(S.Z, S.l, k, S.lam, S.Mside[0], S.status, st);
   }
-  if (S.tile) launch_csr_block_offsets(S.A, S.nblk, S.boff, st);   // once per matrix
   if (S.small) {
     SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Gacc2, 0, sizeof(double) * kGramReplicas * k * k, st));
     SYMNMF_CUDA_TRY(cudaMemsetAsync(S.bar, 0, sizeof(unsigned int) * 4, st));

@@ -511,8 +511,7 @@ struct TileSmem {
   static constexpr size_t y = 0;                                               // float [TR][ST]
   static constexpr size_t carry = y + sizeof(float) * TR * ST;                 // float [NCARRY][KP]
   static constexpr size_t crow = carry + sizeof(float) * NCARRY * KP;          // int [NCARRY]
-  static constexpr size_t start = crow + sizeof(int) * NCARRY;                 // int [TR]: row start - eb
-  static constexpr size_t gram = (start + sizeof(int) * TR + 15) / 16 * 16;     // double [TR][16]
+  static constexpr size_t gram = crow + sizeof(int) * NCARRY;                  // double [TR][16]
   static constexpr size_t bytes = gram + sizeof(double) * TR * 16;
 };
 
@@ -520,8 +519,7 @@ template <int KP>
 __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
     const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, const float* __restrict__ val, int64_t n,
     const float* __restrict__ F, const double* __restrict__ G, double alpha, float* __restrict__ X, double* Gacc,
-    double* Gout, float* Rf32, unsigned int* counter, int32_t* status, const int32_t* __restrict__ boff, int nblk,
-    int blk, float* __restrict__ Yp) {
+    double* Gout, float* Rf32, unsigned int* counter, int32_t* status) {
   using L = TileSmem<KP>;
   constexpr int ST = L::ST, LPR = KP / 4, NG = 32 / LPR;
   __shared__ __align__(16) float sG[KP * KP];     // sG[i*KP + j] = G[j][i], 0 on the diagonal
@@ -532,9 +530,6 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
   float* sY = reinterpret_cast<float*>(smt + L::y);
   float* sC = reinterpret_cast<float*>(smt + L::carry);
   int* sCr = reinterpret_cast<int*>(smt + L::crow);
-  int* sStart = reinterpret_cast<int*>(smt + L::start);
-  __shared__ int sScan[33];
-  const bool last = blk == nblk - 1;   // the pass that adds the partial Y and sweeps
   if (dev_failed(status)) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, grp = lane / LPR, li = lane % LPR;
   for (int e = tid; e < KP * KP; e += TR) {
@@ -558,7 +553,7 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
     const int64_t r0 = t * TR;
     const int rows = (int)min64(TR, n - r0);
     const int64_t eb = rowptr[r0];
-    if (last && tid < rows) {   // the sweep's X and F rows: fetched into L2 while the product runs
+    if (tid < rows) {   // the sweep's X and F rows: fetched into L2 while the product runs
       asm volatile("prefetch.global.L2 [%0];" ::"l"(X + (r0 + tid) * KP));
       asm volatile("prefetch.global.L2 [%0];" ::"l"(F + (r0 + tid) * KP));
       if (KP == 64) {
@@ -568,21 +563,9 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
     }
     __syncthreads();   // previous tile's Gram reads of sY are done
     {
-      // this pass's nonzeros of row r0 + tid: column block `blk` of the row (its offsets within
-      // the sorted row come from boff); sOff = exclusive scan of their counts over the tile
-      int st = 0, cnt = 0;
-      if (tid < rows) {
-        const int64_t rs = rowptr[r0 + tid], re = rowptr[r0 + tid + 1];
-        const int a = blk == 0 ? 0 : boff[(int64_t)(blk - 1) * n + r0 + tid];
-        const int b = last ? (int)(re - rs) : boff[(int64_t)blk * n + r0 + tid];
-        st = (int)(rs - eb) + a;
-        cnt = b - a;
-      }
-      int tot;
-      const int ex = block_excl_scan(cnt, sScan, &tot);
-      sOff[tid] = ex;
-      sStart[tid] = st;
-      if (tid == 0) sOff[TR] = tot;
+      const int64_t ep = rowptr[r0 + min(tid, rows)];
+      sOff[tid] = (int)(ep - eb);
+      if (tid == 0) sOff[TR] = (int)(rowptr[r0 + rows] - eb);
 #pragma unroll
       for (int c = 0; c < KP; c += 4) *reinterpret_cast<float4*>(sY + tid * ST + c) = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int e = tid; e < L::NCARRY * KP; e += TR) sC[e] = 0.f;
@@ -605,9 +588,6 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
           *reinterpret_cast<float4*>(dst + 4 * li) = v;
         };
         if (li == 0) { sCr[2 * sl] = rfirst; sCr[2 * sl + 1] = rlast != rfirst ? rlast : -1; }
-        // position p of the pass maps to nonzero eb + sStart[row] + (p - sOff[row])
-        int lr = row, lre = rend;
-        int64_t lb = eb + sStart[row] - sOff[row];
         for (int e = s0; e < s1; e += TUE) {
           int cc[TUE];
           float aa[TUE];
@@ -615,11 +595,8 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
 #pragma unroll
           for (int u = 0; u < TUE; ++u) {
             const bool ok = e + u < s1;
-            if (ok) {
-              while (e + u >= lre) { ++lr; lre = sOff[lr + 1]; lb = eb + sStart[lr] - sOff[lr]; }
-            }
-            cc[u] = ok ? __ldg(col + lb + e + u) : 0;
-            aa[u] = ok ? __ldg(val + lb + e + u) : 0.f;
+            cc[u] = ok ? __ldg(col + eb + e + u) : 0;
+            aa[u] = ok ? __ldg(val + eb + e + u) : 0.f;
           }
 #pragma unroll
           for (int u = 0; u < TUE; ++u)
@@ -664,17 +641,7 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
       *d4 = cur;
     }
     __syncthreads();
-    if (!last) {   // a partial column-block pass: y of the tile's rows into (or onto) Yp
-      for (int q = tid; q < rows * LPR; q += TR) {
-        const int r = q / LPR, c = q - r * LPR;
-        float4 y = *reinterpret_cast<const float4*>(sY + r * ST + 4 * c);
-        float4* d = reinterpret_cast<float4*>(Yp) + (r0 + r) * LPR + c;
-        if (blk > 0) { const float4 o = *d; y.x += o.x; y.y += o.y; y.z += o.z; y.w += o.w; }
-        *d = y;
-      }
-      continue;
-    }
-    // ---- b = y (+ the earlier column-block passes' partial y) + alpha f for the tile
+    // ---- b = y + alpha f for the tile (coalesced: the tile's F rows are contiguous)
     {
       const float4* Ft = F4 + r0 * LPR;
       for (int q = tid; q < rows * LPR; q += TR) {
@@ -682,10 +649,6 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
         const float4 fv = __ldg(Ft + q);
         float4* d4 = reinterpret_cast<float4*>(sY + r * ST + 4 * c);
         float4 y = *d4;
-        if (nblk > 1) {
-          const float4 o = reinterpret_cast<const float4*>(Yp)[r0 * LPR + q];
-          y.x += o.x; y.y += o.y; y.z += o.z; y.w += o.w;
-        }
         y.x = fmaf(a32, fv.x, y.x); y.y = fmaf(a32, fv.y, y.y); y.z = fmaf(a32, fv.z, y.z); y.w = fmaf(a32, fv.w, y.w);
         *d4 = y;
       }
@@ -727,7 +690,6 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
     __syncthreads();
     gt.tile(sY, ST, rows, gslot);
   }
-  if (!last) return;
   // ---- commit the CTA's X^T X into a replica of the global accumulator; last CTA finalizes
   gt.commit(gslot, Gacc);
   if (arrive_last(counter)) {
@@ -736,46 +698,26 @@ __global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
   }
 }
 
-// Per-row offsets of the column-block boundaries c_b = b n / nblk (b = 1..nblk-1) inside each
-// sorted CSR row: boff[(b-1) n + r] = #nonzeros of row r with col < c_b.  Once per matrix.
-__global__ void csr_block_offsets(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, int64_t n,
-                                  int nblk, int32_t* __restrict__ boff) {
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t rs = rowptr[r], re = rowptr[r + 1];
-    for (int b = 1; b < nblk; ++b) {
-      const int32_t cb = (int32_t)(n * b / nblk);
-      int64_t lo = rs, hi = re;
-      while (lo < hi) { const int64_t m = (lo + hi) >> 1; if (col[m] < cb) lo = m + 1; else hi = m; }
-      boff[(int64_t)(b - 1) * n + r] = (int32_t)(lo - rs);
-    }
-  }
-}
-
-void launch_csr_block_offsets(const symnmf_matrix& A, int nblk, int32_t* boff, cudaStream_t st) {
-  if (nblk > 1) csr_block_offsets<<<148 * 8, 256, 0, st>>>(A.rowptr, A.colidx, A.n, nblk, boff);
-}
-
 template <int KP>
 static void csr_tile_sweep_t(const symnmf_matrix& A, const float* F, const double* G, double alpha, float* X, int64_t n,
                              double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
-                             cudaStream_t st, const int32_t* boff, int nblk, float* Yp) {
+                             cudaStream_t st) {
   const size_t smem = std::max({TileSmem<KP>::bytes, sizeof(double) * 2 * KP * (KP + 1), kRedBytes});
   const int64_t tiles = (n + TR - 1) / TR;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 2));
   cudaFuncSetAttribute(csr_tile_sweep<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  for (int b = 0; b < nblk; ++b)   // column-block passes: each pass's slice of F stays in L2
-    launch_pdl(csr_tile_sweep<KP>, grid, TR, smem, st, A.rowptr, A.colidx, A.val, n, F, G, alpha, X, Gacc, Gout,
-               Rf32, counter, status, boff, nblk, b, Yp);
+  launch_pdl(csr_tile_sweep<KP>, grid, TR, smem, st, A.rowptr, A.colidx, A.val, n, F, G, alpha, X, Gacc, Gout, Rf32,
+             counter, status);
 }
 
 void launch_csr_tile_sweep(const symnmf_matrix& A, const float* F, const double* G, double alpha, float* X, int64_t n,
                            int k, double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
-                           cudaStream_t st, const int32_t* boff, int nblk, float* Yp) {
+                           cudaStream_t st) {
   switch (k) {
-    case 8: csr_tile_sweep_t<8>(A, F, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st, boff, nblk, Yp); break;
-    case 16: csr_tile_sweep_t<16>(A, F, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st, boff, nblk, Yp); break;
-    case 32: csr_tile_sweep_t<32>(A, F, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st, boff, nblk, Yp); break;
-    default: csr_tile_sweep_t<64>(A, F, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st, boff, nblk, Yp); break;
+    case 8: csr_tile_sweep_t<8>(A, F, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
+    case 16: csr_tile_sweep_t<16>(A, F, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
+    case 32: csr_tile_sweep_t<32>(A, F, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
+    default: csr_tile_sweep_t<64>(A, F, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
   }
 }
 

@@ -91,12 +91,9 @@ void launch_sampled_gram_fused(const float* F, int k, const symnmf_plan& plan, d
 // Exact CSR product fused with the sweep (csr_tile_sweep): 256-row tiles of Y = A F in shared
 // memory with nnz-balanced slices (hub rows spread over lane groups), the HALS sweep of the tile,
 // the Gram of the updated rows and (last CTA) its Cholesky factor.  Requires kpad(k) == k.
-// nblk column-block passes (nblk = 1: one pass); boff: (nblk - 1) x n row offsets of the block
-// boundaries (launch_csr_block_offsets, once per matrix); Yp: n x k partial product (nblk > 1).
 void launch_csr_tile_sweep(const symnmf_matrix& A, const float* F, const double* G, double alpha, float* X, int64_t n,
                            int k, double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
-                           cudaStream_t st, const int32_t* boff = nullptr, int nblk = 1, float* Yp = nullptr);
-void launch_csr_block_offsets(const symnmf_matrix& A, int nblk, int32_t* boff, cudaStream_t st);
+                           cudaStream_t st);
 // sampler.cu passes used by the fused path
 void launch_samp_prefix(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
                         int32_t* status, cudaStream_t st);

@@ -462,15 +462,13 @@ def _csr_case(cfgname, n, k, seed=7):
 
 @pytest.mark.parametrize("cfgname,n,k", [("c2", 20_000, 16), ("c2", 20_000, 8), ("c4", 40_000, 32),
                                          ("c4", 40_000, 64), ("c4", 40_032, 16), ("c2", 2_000, 32)])
-@pytest.mark.parametrize("tile", ["always", "never", "blocks3"])
+@pytest.mark.parametrize("tile", ["always", "never"])
 def test_csr_tile_exact_one_iteration(cfgname, n, k, tile, monkeypatch):
     """Solver EXACT on CSR, both product forms: the tile kernel (A F per 256-row tile with
     nnz-balanced slices, fused with the sweep and the next Gram; SYMNMF_CSR_TILE=always) and the
     row SpMM + sweep: W and H after one iteration vs the oracle's fp64 iteration.  Covers ragged
     last tiles (n % 256 != 0), hub rows (power-law c4 recipe) and k = 8..64."""
-    monkeypatch.setenv("SYMNMF_CSR_TILE", "always" if tile == "blocks3" else tile)
-    if tile == "blocks3":   # three column-block passes (partial products through HBM)
-        monkeypatch.setenv("SYMNMF_TILE_BLOCKS", "3")
+    monkeypatch.setenv("SYMNMF_CSR_TILE", tile)
     A, H0, alpha = _csr_case(cfgname, n, k)
     M = S.DeviceMatrix.from_host(A)
     W, H = cu(H0), cu(H0)
