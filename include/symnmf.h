@@ -290,6 +290,14 @@ symnmf_status symnmf_solver_pgrad(symnmf_solver* solver, double* pgrad_host, cud
  * (names_host[i], NUL terminated) and mean duration in ms (ms_host[i]); *count_host <= cap. */
 symnmf_status symnmf_solver_profile(symnmf_solver* solver, int32_t iters, int32_t cap, char (*names_host)[48],
                                     float* ms_host, int32_t* count_host, cudaStream_t st);
+/* Inspection (LvS solvers only; enqueued on `st`, no host sync): copies the sampling state the
+ * solver left after the last half it ran -- the leverage scores of the factor that half held fixed
+ * (lev_out: n floats) and its plan (uniq_idx_out: n int32, uniq_w_out: n doubles, of which the
+ * first counts_out[2] are valid; counts_out: 4 int64 {s_D, s_R, n_uniq, W}; mass_out: 2 doubles
+ * {theta, xi}) -- into caller-owned device buffers.  The fused sampler does not materialise
+ * det_idx / draw_idx.  Returns SYMNMF_ERR_ARG for a non-LvS solver or a null pointer. */
+symnmf_status symnmf_solver_last_plan(const symnmf_solver* solver, float* lev_out, int32_t* uniq_idx_out,
+                                      double* uniq_w_out, int64_t* counts_out, double* mass_out, cudaStream_t st);
 /* Kernel and memset node counts of the captured per-iteration graph (host only). */
 symnmf_status symnmf_solver_graph_nodes(const symnmf_solver* solver, int32_t* kernels_host, int32_t* memsets_host);
 

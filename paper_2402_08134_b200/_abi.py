@@ -68,6 +68,7 @@ SIGNATURES = {
     "symnmf_solver_pgrad": (I32, [P, C.POINTER(F64), P]),
     "symnmf_solve": (I32, [PM, I64, P, P, I32, F64, I32, I32, I64, F64, U64, P, P, I32, I32, F64, I32, I32,
                            C.POINTER(I32), C.POINTER(F64), P, PSZ, P]),
+    "symnmf_solver_last_plan": (I32, [P, P, P, P, P, P, P]),
     "symnmf_solver_graph_nodes": (I32, [P, C.POINTER(I32), C.POINTER(I32)]),
     "symnmf_solver_profile": (I32, [P, I32, I32, C.c_void_p, C.POINTER(C.c_float), C.POINTER(I32), P]),
 }

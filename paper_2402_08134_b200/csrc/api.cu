@@ -978,6 +978,20 @@ extern "C" symnmf_status symnmf_solver_pgrad(symnmf_solver* S, double* pgrad_hos
   return SYMNMF_OK;
 }
 
+extern "C" symnmf_status symnmf_solver_last_plan(const symnmf_solver* S, float* lev_out, int32_t* uniq_idx_out,
+                                                 double* uniq_w_out, int64_t* counts_out, double* mass_out,
+                                                 cudaStream_t st) {
+  if (!S || S->mode != SYMNMF_LVS || !lev_out || !uniq_idx_out || !uniq_w_out || !counts_out || !mass_out)
+    return SYMNMF_ERR_ARG;
+  const size_t n = (size_t)S->n;
+  SYMNMF_CUDA_TRY(cudaMemcpyAsync(lev_out, S->lev, sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
+  SYMNMF_CUDA_TRY(cudaMemcpyAsync(uniq_idx_out, S->plan.uniq_idx, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
+  SYMNMF_CUDA_TRY(cudaMemcpyAsync(uniq_w_out, S->plan.uniq_w, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  SYMNMF_CUDA_TRY(cudaMemcpyAsync(counts_out, S->plan.counts, sizeof(int64_t) * 4, cudaMemcpyDeviceToDevice, st));
+  SYMNMF_CUDA_TRY(cudaMemcpyAsync(mass_out, S->plan.mass, sizeof(double) * 2, cudaMemcpyDeviceToDevice, st));
+  return SYMNMF_OK;
+}
+
 extern "C" symnmf_status symnmf_solver_stats(symnmf_solver* S, int32_t* iters_done_host, symnmf_half_stats* stats_host,
                                              double* resid_host, cudaStream_t st) {
   if (!S) return SYMNMF_ERR_ARG;

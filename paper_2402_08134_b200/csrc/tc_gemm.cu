@@ -2,19 +2,38 @@
 // (precision SYMNMF_3XTF32): A n x n fp32 (the data matrix, streamed once from
 // HBM), X n x k fp32 (the factor F, or Omega / Q in the range finder).
 //
-//   Y = A_hi X_hi + A_hi X_lo + A_lo X_hi,   v_hi = v with the low 13 mantissa
-//   bits cleared (exactly representable in tf32), v_lo = v - v_hi (exact).
+//   Y = A_hi X_hi + A_hi X_lo + A_lo X_hi (+ A_lo X_lo, free),   v_hi = v with the low 13
+//   mantissa bits cleared (exactly representable in tf32), v_lo = v - v_hi (exact).
 //
 // Per CTA (one 128-row tile of A and one K range, split-K over gridDim.y):
 //   warp 0      TMA producer: A tile [128 x 32] fp32 (128B swizzle), X_hi^T / X_lo^T tiles
 //               [NP x 32] (pre-split and transposed once per product, K-major)
 //   warps 4..7  form A_lo = a - (a & 0xffffe000) of the A tile in a second buffer (the raw tile
 //               is A_hi: the tf32 MMA ignores the low 13 mantissa bits),
-//               fence.proxy.async, arrive; afterwards the epilogue (tcgen05.ld -> fp32 red.add)
-//   warp 1      one elected thread issues 3 x 4 tcgen05.mma.kind::tf32 (M=128, N=NP, K=8)
-//               per stage into a TMEM accumulator and commits the stage back to the producer
+//               fence.proxy.async, arrive
+//   warps 8..11 every TC_DRAIN k-blocks drain the TMEM accumulator into fp32 registers
+//               (tcgen05.ld, round-to-nearest adds); at the end add the registers into Y
+//               (fp32 red.add).  Warp w reads TMEM lanes 32 (w % 4) .. +31.
+//   warp 1      one elected thread issues 2 x 4 tcgen05.mma.kind::tf32 (M=128, N=2 NP, K=8)
+//               per stage, A_hi [X_hi | X_lo] and A_lo [X_hi | X_lo] with B = the X_hi and X_lo
+//               tiles stacked (adjacent in the stage), into two independent accumulators
+//               (NP <= 64; one for NP > 64).  Three dependent N = NP MMAs per K=8 step were
+//               measured to bound the kernel (1.006 ms at c3 vs 0.647 ms with one MMA): small-N
+//               MMAs into one accumulator serialise on the MMA latency.  Chunk c of TC_DRAIN
+//               k-blocks uses buffer c & 1, restarting from zero; the stage is committed back to
+//               the producer
 //   warp 2      TMEM allocation / deallocation
-// Pipeline: 4 smem stages with full (TMA tx) / conv (128 arrivals) / empty (MMA commit) mbarriers.
+// Pipeline: 3-5 smem stages with full (TMA tx) / conv (128 arrivals) / empty (MMA commit)
+// mbarriers, two accumulator buffers with acc_full (MMA commit) / acc_empty (128 arrivals).
+//
+// Why the drain: the tensor core's fp32 accumulation does not round to nearest -- each MMA's
+// add into the accumulator loses about one accumulator ulp, always towards zero.  Measured on
+// B200 with one accumulator per K range: a relative bias of -7e-7 per 32-wide k-block of chain,
+// -2.1e-4 at n = 30,000 (313 k-blocks per split).  Restarting the accumulator every TC_DRAIN
+// k-blocks bounds the bias by the chain length of one chunk; the chunks are summed in registers.
+// Measured (tools/tc_bias.py, uniform [0,1) A and X, n = 30,000): mean relative error -1.6e-6,
+// max 2.1e-6 with TC_DRAIN = 16 (fp32 SGEMM: max 1.4e-5); TC_DRAIN = 8 / 32: -8e-7 / -3.2e-6 at
+// 0.902 / 0.876 ms against 0.886 ms.
 #include <cstdio>
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -25,7 +44,8 @@ namespace symnmf {
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 32;          // fp32 elements per 128-byte row
 template <int NP> constexpr int tc_stages() { return NP <= 32 ? 5 : NP <= 80 ? 4 : 3; }
-constexpr int TC_THREADS = 256;
+constexpr int TC_THREADS = 384;
+constexpr int TC_DRAIN = 16;       // k-blocks per accumulator chunk
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -40,6 +60,22 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 // Bounded wait: a pipeline that cannot make progress for ~10 s traps (a device
 // error the host sees) instead of hanging the GPU.
+// wait with a sleep between polls: for warps that are not on the critical path (the drain
+// warps share sub-partitions with the TMA producer and the MMA issuer)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(200);
+  }
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t ok = 0;
@@ -99,15 +135,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;   // 16 KB
   constexpr uint32_t B_BYTES = NP * TC_BK * 4;      // NP x 128 B
   constexpr uint32_t STAGE = 2 * A_BYTES + 2 * B_BYTES;
-  constexpr uint32_t TMEM_COLS = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : 256;
-  constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+  // accumulators: NACC independent chains per buffer, each 2 NP columns ([.. X_hi | .. X_lo]);
+  // two buffers.  NACC = 4: {A_hi, A_lo} x {even, odd K=8 step}; 2: {A_hi, A_lo}; 1: shared.
+  constexpr int NACC = NP <= 32 ? 4 : NP <= 64 ? 2 : 1;
+  constexpr uint32_t ACC_COLS = 2 * NP;
+  constexpr uint32_t BUF_COLS = NACC * ACC_COLS;
+  constexpr uint32_t TMEM_COLS = 2 * BUF_COLS <= 128 ? 128 : 2 * BUF_COLS <= 256 ? 256 : 512;
+  constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)((2 * NP) >> 3) << 17) |
+                             ((uint32_t)(TC_BM >> 4) << 24);
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + tc_stages<NP>() * STAGE);
   uint64_t* conv = full + tc_stages<NP>();
   uint64_t* empty = conv + tc_stages<NP>();
-  uint64_t* tmem_full = empty + tc_stages<NP>();
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* acc_full = empty + tc_stages<NP>();   // [2]
+  uint64_t* acc_empty = acc_full + 2;             // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   if (dev_failed(status)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -118,7 +161,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < tc_stages<NP>(); ++s) { mbar_init(full + s, 1); mbar_init(conv + s, 128); mbar_init(empty + s, 1); }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) { mbar_init(acc_full + b, 1); mbar_init(acc_empty + b, 128); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -149,23 +192,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       for (int i = 0; i < nkb; ++i) {
         const int s = i % tc_stages<NP>();
+        const int c = i / TC_DRAIN, b = c & 1;
+        if (i % TC_DRAIN == 0 && c >= 2) mbar_wait(acc_empty + b, ((c >> 1) - 1) & 1);
         mbar_wait(conv + s, (i / tc_stages<NP>()) & 1);
         tc_fence_after();
         const uint32_t a_hi = smem_u32(sm + s * STAGE), a_lo = a_hi + A_BYTES;
         const uint32_t b_hi = a_hi + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
+        const uint32_t td = tmem + (uint32_t)b * BUF_COLS;
 #pragma unroll
         for (int kk = 0; kk < TC_BK / 8; ++kk) {
           const uint32_t off = kk * 32;   // 8 tf32 = 32 bytes along the swizzled row
-          const uint32_t acc0 = (i | kk) ? 1u : 0u;
-          mma_tf32(tmem, smem_desc_k128(a_hi + off), smem_desc_k128(b_hi + off), IDESC, acc0);
-          mma_tf32(tmem, smem_desc_k128(a_hi + off), smem_desc_k128(b_lo + off), IDESC, 1u);
-          mma_tf32(tmem, smem_desc_k128(a_lo + off), smem_desc_k128(b_hi + off), IDESC, 1u);
+          const uint32_t acc0 = ((i % TC_DRAIN) != 0 || kk >= (NACC == 4 ? 2 : 1)) ? 1u : 0u;
+          // B = [X_hi; X_lo] (2 NP rows, contiguous in the stage): A_hi [X_hi | X_lo] and
+          // A_lo [X_hi | X_lo], into independent accumulators when they fit (NP <= 64)
+          const uint32_t tq = td + (NACC == 4 ? (uint32_t)(kk & 1) * 2 * ACC_COLS : 0u);
+          mma_tf32(tq, smem_desc_k128(a_hi + off), smem_desc_k128(b_hi + off), IDESC, acc0);
+          mma_tf32(tq + (NACC >= 2 ? ACC_COLS : 0u), smem_desc_k128(a_lo + off), smem_desc_k128(b_hi + off), IDESC,
+                   NACC >= 2 ? acc0 : 1u);
         }
         mma_commit(empty + s);
+        if ((i + 1) % TC_DRAIN == 0 || i + 1 == nkb) mma_commit(acc_full + b);
       }
-      mma_commit(tmem_full);
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 8) {
     const int t = threadIdx.x - 128;   // 0..127
     for (int i = 0; i < nkb; ++i) {
       const int s = i % tc_stages<NP>();
@@ -187,28 +236,41 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       fence_proxy_async();
       mbar_arrive(conv + s);
     }
-    // epilogue: TMEM lane = tile row, column = output column
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
+  } else if (warp >= 8) {
     const int wq = warp & 3;
-    const int64_t row = m0 + wq * 32 + lane;
+    float acc[NP];
 #pragma unroll
-    for (int c0 = 0; c0 < NP; c0 += 16) {
-      uint32_t r[16];
-      const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)c0;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (row < n) {
+    for (int j = 0; j < NP; ++j) acc[j] = 0.f;
+    // drain chunk c: TMEM lane = tile row, column = output column
+    auto drain = [&](int c) {
+      const int b = c & 1;
+      mbar_wait_sleep(acc_full + b, (c >> 1) & 1);
+      tc_fence_after();
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (c0 + j < k) atomicAdd(Y + row * ldy + c0 + j, __uint_as_float(r[j]));
+      for (int cc = 0; cc < NACC * 2 * NP; cc += 16) {
+        const int c0 = cc % NP;   // column block of Y; the NACC x {X_hi, X_lo} partial sums add up
+        uint32_t r[16];
+        const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)b * BUF_COLS + (uint32_t)cc;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[c0 + j] += __uint_as_float(r[j]);
       }
+      tc_fence_before();
+      mbar_arrive(acc_empty + b);
+    };
+    const int nch = (nkb + TC_DRAIN - 1) / TC_DRAIN;
+    for (int c = 0; c < nch; ++c) drain(c);
+    const int64_t row = m0 + wq * 32 + lane;
+    if (row < n) {
+#pragma unroll
+      for (int j = 0; j < NP; ++j)
+        if (j < k) atomicAdd(Y + row * ldy + j, acc[j]);
     }
-    tc_fence_before();
   }
   __syncthreads();
   if (warp == 2) {
@@ -280,7 +342,7 @@ static bool launch_tc_t(const float* A, int64_t lda, int64_t n, const float* X, 
   const int kps = (int)((nkb + splits - 1) / splits);
   splits = (nkb + kps - 1) / kps;
   constexpr size_t STAGE = 2 * TC_BM * TC_BK * 4 + 2 * NP * TC_BK * 4;
-  const size_t smem = 1024 + tc_stages<NP>() * STAGE + (3 * tc_stages<NP>() + 1) * 8 + 16;
+  const size_t smem = 1024 + tc_stages<NP>() * STAGE + (3 * tc_stages<NP>() + 4) * 8 + 16;
   cudaFuncSetAttribute(tc_gemm_3xtf32<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   tc_gemm_3xtf32<NP><<<dim3((unsigned)mt, (unsigned)splits), TC_THREADS, smem, st>>>(mA, mH, mL, n, kps, nkb, Y, ldy,
                                                                                      k, status);

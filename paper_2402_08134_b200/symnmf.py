@@ -333,6 +333,20 @@ class Solver:
         done = self.stats()["iters"]
         return [buf[i] for i in range(min(done, m))]
 
+    def last_plan(self):
+        """(scores, plan) the LvS solver drew in the last half it ran, copied on the current stream
+        (symnmf_solver_last_plan); det_idx / draw_idx are not materialised by the fused sampler."""
+        n, dev = self.W.shape[0], self.W.device
+        lev = torch.empty(n, dtype=torch.float32, device=dev)
+        plan = SamplingPlan(torch.empty(0, dtype=torch.int32, device=dev), torch.empty(0, dtype=torch.int32, device=dev),
+                            torch.empty(n, dtype=torch.int32, device=dev), torch.empty(n, dtype=torch.float64, device=dev),
+                            torch.empty(4, dtype=torch.int64, device=dev), torch.empty(2, dtype=torch.float64, device=dev),
+                            n)
+        A.check("symnmf_solver_last_plan",
+                lib().symnmf_solver_last_plan(self.h, _p(lev), _p(plan.uniq_idx), _p(plan.uniq_w), _p(plan.counts),
+                                              _p(plan.mass), _stream()))
+        return lev, plan
+
     def stats(self):
         m = self.max_iters
         st = (A.HalfStats * (2 * m))()
