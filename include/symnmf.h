@@ -60,7 +60,8 @@ enum { SYMNMF_RULE_BPP = 16 };
  * A = A^T.  DENSE: val is n x lda fp32 (lda >= n, lda % 4 == 0 for 3XTF32).
  * CSR: both triangles stored ("row/column slicing ... because the
  * matrix is symmetric"), rowptr int64 [n+1], colidx int32 [nnz] sorted and
- * unique within a row, val fp32 [nnz]. */
+ * unique within a row, val fp32 [nnz]; empty rows are allowed, and nnz = 0 (A = 0, colidx
+ * and val may be NULL). */
 typedef struct {
   int32_t kind;
   int32_t reserved;

@@ -23,9 +23,9 @@ bool device_ok() {
 bool bad_k(int k) { return k < 1 || k > kMaxK; }
 
 bool bad_matrix(const symnmf_matrix* A) {
-  if (!A || A->n < 1 || !A->val) return true;
-  if (A->kind == SYMNMF_DENSE) return A->lda < A->n;
-  if (A->kind == SYMNMF_CSR) return !A->rowptr || (!A->colidx && A->nnz > 0) || A->nnz < 0;
+  if (!A || A->n < 1) return true;
+  if (A->kind == SYMNMF_DENSE) return !A->val || A->lda < A->n;
+  if (A->kind == SYMNMF_CSR) return !A->rowptr || A->nnz < 0 || (A->nnz > 0 && (!A->colidx || !A->val));
   return true;
 }
 

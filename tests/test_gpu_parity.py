@@ -735,3 +735,62 @@ def test_solver_bpp_rule_vs_oracle(mode, c1):
             assert (g["s_D"], g["s_R"], g["n_uniq"]) == (o["s_D"], o["s_R"], o["n_uniq"])
     rg, ro = O.residual(A, H.cpu().numpy()), O.residual(A, Hr)
     assert abs(rg - ro) <= 1e-4 * ro
+
+
+def _drop_vertices(A, frac, tail, seed=3):
+    """A with every entry of a random `frac` of the vertices and of the last `tail` vertices
+    removed (rows and columns): isolated vertices, i.e. empty CSR rows, incl. an empty tail."""
+    from synth.configs import CsrMatrix
+    rng = np.random.default_rng(seed)
+    drop = rng.random(A.n) < frac
+    drop[A.n - tail:] = True
+    rows = np.repeat(np.arange(A.n), np.diff(A.rowptr))
+    keep = ~drop[rows] & ~drop[A.colidx]
+    rowptr = np.zeros(A.n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows[keep], minlength=A.n), out=rowptr[1:])
+    return CsrMatrix(A.n, rowptr, A.colidx[keep].copy(), A.val[keep].copy())
+
+
+@pytest.mark.parametrize("tile", ["always", "never"])
+def test_csr_empty_rows(tile, monkeypatch):
+    """Isolated vertices (empty CSR rows, 10% random + an empty 300-row tail): the product, the
+    sampled product over all rows, and one EXACT solver iteration (tile kernel and row SpMM)."""
+    monkeypatch.setenv("SYMNMF_CSR_TILE", tile)
+    A0, H0, alpha = _csr_case("c2", 20_000, 16)
+    A = _drop_vertices(A0, 0.1, 300)
+    assert (np.diff(A.rowptr) == 0).sum() >= 2000
+    M = S.DeviceMatrix.from_host(A)
+    Y = S.ah(M, cu(H0)).cpu().numpy()
+    assert rel(Y, O.ah(A, H0)) < 1e-5
+    assert not Y[-300:].any()
+    W, H = cu(H0), cu(H0)
+    sv = S.Solver(M, W, H, alpha, mode="exact", max_iters=1)
+    sv.run(1)
+    assert sv.stats()["status"] == 0
+    sv.close()
+    Wr, Hr, _ = O.iterate(A, H0, H0, alpha, 1, "exact")
+    assert rel(W.cpu().numpy(), Wr) < 1e-5
+    assert rel(H.cpu().numpy(), Hr) < 1e-5
+
+
+def test_csr_zero_matrix():
+    """A = 0 (nnz = 0, no colidx / val storage): A F = 0 exactly, and one EXACT and one LvS solver
+    iteration reduce to the regularisation pull W <- max(0, (alpha F - X G + ...)) of Eq. 2.6."""
+    from synth.configs import CsrMatrix
+    n, k, alpha = 3_000, 8, 0.5
+    A = CsrMatrix(n, np.zeros(n + 1, dtype=np.int64), np.zeros(0, dtype=np.int32), np.zeros(0, dtype=np.float32))
+    H0 = np.random.default_rng(1).random((n, k)).astype(np.float32)
+    M = S.DeviceMatrix.from_host(A)
+    Y = S.ah(M, cu(H0)).cpu().numpy()
+    assert not Y.any()
+    for mode, kw in (("exact", {}), ("lvs", dict(s=300, tau=1.0 / 300, seed=2))):
+        W, H = cu(H0), cu(H0)
+        sv = S.Solver(M, W, H, alpha, mode=mode, max_iters=1, **kw)
+        sv.run(1)
+        assert sv.stats()["status"] == 0
+        sv.close()
+        Wg = W.cpu().numpy()
+        if mode == "exact":
+            Wr, Hr, _ = O.iterate(A, H0, H0, alpha, 1, "exact")
+            assert rel(Wg, Wr) < 1e-5 and rel(H.cpu().numpy(), Hr) < 1e-5
+        assert np.isfinite(Wg).all() and (Wg >= 0).all()
