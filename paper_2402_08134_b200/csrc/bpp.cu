@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(BT, 1) bpp_rows(const double* __restrict__ G, 
 #pragma unroll
       for (int j = 0; j < KP; ++j) {
         const double xj = __shfl_sync(0xffffffffu, x, j);
-        if (lane < KP) yy = fma(sG[lane * KP + j], xj, yy);
+        if (lane < KP) yy = fma(sG[j * KP + lane], xj, yy);   // Gh symmetric: row j, lane-contiguous
       }
       y = inF ? 0.0 : yy;
     }

@@ -102,8 +102,12 @@ __device__ __forceinline__ int chol_col_pass(double (&b)[KP], int lane, double& 
     const double rinv = rsqrt_fp64(dd), r = dd * rinv;
     if (lane == j) { b[j] = r; myr = r; }
     else if (lane > j) b[j] *= rinv;                          // R[j][lane]
+    // constant trip count (i > j as a predicate): unrolls whatever order the compiler unrolls
+    // the two loops in, so b[] stays in registers (with `i = j + 1` bounds, the BPP kernel's
+    // copy kept b[] in local memory)
 #pragma unroll
-    for (int i = j + 1; i < KP; ++i) {
+    for (int i = 1; i < KP; ++i) {
+      if (i <= j) continue;
       const double rji = __shfl_sync(0xffffffffu, b[j], i);   // R[j][i] from lane i
       if (lane >= i) b[i] = fma(-rji, b[j], b[i]);            // A[i][lane] -= R[j][i] R[j][lane]
     }

@@ -1,14 +1,14 @@
 #!/bin/bash
-# A/B a kernel source: bash tools/gpu_variants.sh <dst.cu> "<bench cfg:mode ...>" <variant.cu>...
+# A/B a kernel source: bash tools/gpu_variants.sh <dst.cu> "<bench cfg:mode[:rule] ...>" <variant.cu>...
 dst=$1; specs=$2; shift 2
 OUT=gpurun_out/var; mkdir -p $OUT
 for v in "$@"; do
   cp $v $dst
   python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { echo "build fail $v"; tail -5 $OUT/build.log; continue; }
   for spec in $specs; do
-    IFS=: read c m <<< "$spec"
+    IFS=: read c m r <<< "$spec"
     for rep in 1 2; do
-      timeout 600 python bench.py --config $c --mode $m --steps 20 --no-cpu-baseline --no-e2e > $OUT/b.json 2> $OUT/b.err
+      timeout 600 python bench.py --config $c --mode $m --rule ${r:-hals} --steps 20 --no-cpu-baseline --no-e2e > $OUT/b.json 2> $OUT/b.err
       python - $v $spec <<'PY'
 import json, sys
 d = json.loads(open("gpurun_out/var/b.json").read().strip().splitlines()[-1])
