@@ -18,9 +18,12 @@
  *    256-byte aligned.  Its first 256 bytes hold a device status word (see
  *    symnmf_status_read) that kernels set on device-side failure; kernels
  *    downstream of a failure become no-ops.
- *  - Asynchrony: every function except symnmf_iterate, symnmf_solver_stats,
- *    symnmf_solver_run_until, symnmf_solver_pgrad and symnmf_status_read only
- *    enqueues work on `st` (no host sync) and is CUDA-graph capturable.
+ *  - Asynchrony: every function except symnmf_iterate, symnmf_solve,
+ *    symnmf_rangefinder_adaptive (its stopping test reads residuals on the host),
+ *    symnmf_bpp_update with nonconv_host != NULL, symnmf_solver_create / _stats /
+ *    _run_until / _pgrad / _profile / _graph_nodes / _destroy and symnmf_status_read
+ *    only enqueues work on `st` (no host sync) and is CUDA-graph capturable
+ *    (tests/test_gpu_api_contract.py captures the per-half ABI sequence).
  *  - Errors never cross the ABI as exceptions; every entry point returns a
  *    symnmf_status.  SYMNMF_ERR_ARG is returned synchronously, before any work
  *    is enqueued, for null pointers, n < 1, k < 1 or k > 64, s < 1,
