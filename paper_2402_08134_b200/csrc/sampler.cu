@@ -310,7 +310,9 @@ void launch_samp_draws(const SamplerWs& w, int64_t n, int64_t s, uint64_t seed, 
                        uint32_t iteration, uint32_t side, const symnmf_plan& plan, int32_t* status, cudaStream_t st) {
   const int64_t dblocks = std::max<int64_t>(1, (s + 255) / 256);
   const int64_t nb = samp_blocks(n);
-  if (nb <= 6144 && s <= 8192) {   // few draws: one warp each (c2: 8.0k -> 8.06k it/s)
+  // few draws over many prefix blocks: one warp per draw (c2: 8.0k -> 8.06k it/s); a one-block
+  // prefix (c1, n = 1,000) is cheaper to binary-search (12.23k vs 12.54k it/s with the warp form)
+  if (nb <= 6144 && nb >= 16 && s <= 8192) {
     launch_pdl(samp_draws_warp, (unsigned)std::max<int64_t>(1, (s + 7) / 8), 256, sizeof(uint64_t) * nb, st,
                w.P, w.bw, nb, n, seed, iter_dev, iteration, side, plan.counts, plan.draw_idx, w.cnt, status);
     return;
