@@ -109,7 +109,7 @@ typedef struct {
  *   SYMNMF_CSR_TILE=always|never   EXACT solver on CSR: force / forbid the tile kernel (product
  *                                  fused with the sweep); default: used from 16M nonzeros.
  *   SYMNMF_SCATTER_SLICE_MB=<mb>   sampled CSR product: rows of Y per destination-range pass
- *                                  (default 48 MB, so each pass's slice of Y stays in L2).
+ *                                  (default 86 MB, so each pass's slice of Y stays in L2).
  *   SYMNMF_LAI_FUSED=never         LAI solver (k = 64, l <= 80): use the four-kernel half (U^T F,
  *                                  Lambda scaling, U M, sweep) instead of the fused launch.
  *   SYMNMF_SMALL=always            LvS solver: use the persistent one-launch-per-iteration kernel

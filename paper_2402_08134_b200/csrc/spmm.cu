@@ -71,11 +71,14 @@ __global__ void __launch_bounds__(256) spmm_csr_scalar(const int64_t* __restrict
   }
 }
 
-// Y slice per scatter pass (L2 is 126 MB); SYMNMF_SCATTER_SLICE_MB overrides (symnmf.h)
+// Y slice per scatter pass (L2 is 126 MB); SYMNMF_SCATTER_SLICE_MB overrides (symnmf.h).
+// Measured on c4 (Y = 256 MB), LvS it/s by slice: 48 MB 425, 64 MB 433, 86 MB 435, 128 MB 427,
+// 256 MB (one pass) 400 -- every pass rescans the sampled nonzeros, so fewer passes win until the
+// slice stops fitting in L2 next to the streamed rows of A.
 static int64_t scatter_slice_bytes() {
   const char* e = getenv("SYMNMF_SCATTER_SLICE_MB");
   const int64_t mb = e ? atoll(e) : 0;
-  return mb > 0 ? (mb << 20) : (48ll << 20);
+  return mb > 0 ? (mb << 20) : (86ll << 20);
 }
 
 static int grid_for(int64_t work_threads) {

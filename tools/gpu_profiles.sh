@@ -12,8 +12,10 @@ prof() {  # cfg mode regex
   ncu --set full --clock-control none --import-source on -k regex:$3 -s 2 -c 1 -o $OUT/full_$1_$2 $CMD > $OUT/ncu_full_$1_$2.log 2>&1
   echo "$1 $2 rc=$?"
 }
-prof c2 lvs sweep_fused
-prof c3 lvs sampled_dense
-prof c3 exact tc_gemm
-prof c4 lvs sampled_csr
-prof c5 lai lai_sweep_fused
+ONLY=${1:-all}   # optional: one of c2_lvs c3_lvs c3_exact c4_lvs c5_lai
+run() { [ "$ONLY" = all ] || [ "$ONLY" = "$1_$2" ] && prof "$@"; }
+run c2 lvs sweep_fused
+run c3 lvs sampled_dense
+run c3 exact tc_gemm
+run c4 lvs sampled_csr
+run c5 lai lai_sweep_fused
