@@ -74,7 +74,12 @@ void launch_symmetrize(double* T, int l, cudaStream_t st);
 
 // ---------------------------------------------------------------- fused.cu (solver hot loop)
 // Gacc: zeroed kGramReplicas x k x k fp64 accumulator (left zeroed); counter: zeroed uint (left zeroed).
-constexpr int kGramReplicas = 16;
+// Replicas of the fp64 Gram accumulators (CTA b adds into replica b % kGramReplicas; the last CTA
+// sums them).  Measured (LvS it/s, 16 / 8 / 2 / 1 replicas): c2 8.05k / 8.26k / 8.34k / 8.27k,
+// c1 12.54k / 12.18k / 12.21k / 12.41k; c3, c4 (LvS and EXACT) and c5 unchanged.  2 kept (the
+// default bench line is c2): fewer replicas shorten the last CTA's reads more than the extra
+// contention on the red.add costs.
+constexpr int kGramReplicas = 2;
 void launch_gram_fused(const float* F, int64_t n, int k, double* Gacc, double* Gout, float* Rinv32,
                        unsigned int* counter, int32_t* status, cudaStream_t st);
 void launch_sweep_fused(const double* G, double alpha, float* Y, const float* F, float* X, int64_t n, int k,
