@@ -508,3 +508,101 @@ def test_bpp_update_is_the_fixed_point_of_hals_sweeps():
     for _ in range(3000):
         X = O.hals_sweep(G, Y, F, X, alpha)
     assert np.allclose(X, Xb, atol=1e-9)
+
+
+# ------------------------------------------------------------------ hybrid regime (s_D > 0), Eq. 4.1-4.2
+def _hybrid_case():
+    """A factor with a few heavy rows, so tau = 1/s puts rows in I_D (s_D > 0, theta ~ k/2)."""
+    r = rng(41)
+    n, k, s = 400, 4, 40
+    F = r.random((n, k)) ** 3
+    F[[7, 50, 123, 260, 301, 377]] *= 25.0
+    A = r.random((n, n))
+    A = (A + A.T) / 2
+    return A, F, n, k, s
+
+
+def _hybrid_samples(A, F, k, s, N, mutate=None):
+    """Y_s and ||S_H F||_F^2 for N independent plans (seed 5, iterations 0..N-1), tau = 1/s.
+
+    `mutate` rewrites the drawn-row weights of each oracle plan -- used only to check that the
+    statistical pins below have the power to reject the two plausible mistakes the advisor named.
+    """
+    lev = O.leverage_scores(F).astype(np.float32)
+    Ys, sq = [], []
+    for t in range(N):
+        pl = O.build_plan(lev, k, s, 1.0 / s, seed=5, iteration=t, side=0)
+        w = pl["uniq_w"].copy()
+        if mutate is not None:
+            w = mutate(pl, lev, w)
+        G_s, Y_s = O.sampled_products(A, F, pl["uniq_idx"], w)
+        Ys.append(Y_s)
+        sq.append(float(np.trace(G_s)))              # ||S_H F||_F^2 = tr(F^T S^T S F)
+    return np.array(Ys), np.array(sq), pl
+
+
+def _hybrid_checks(A, F, Ys, sq):
+    """E[Y_s] = A F and E||S_H F||^2 = ||F||^2, each within 4 standard errors of the mean."""
+    exact = O.ah(A, F)
+    N = Ys.shape[0]
+    dev = Ys - exact
+    se_y = np.sqrt(((dev - dev.mean(0)) ** 2).sum() / (N - 1) / N)
+    ok_y = np.linalg.norm(dev.mean(0)) < 4 * se_y + 1e-12
+    f2 = float((F ** 2).sum())
+    se_s = sq.std(ddof=1) / math.sqrt(N)
+    ok_s = abs(sq.mean() - f2) < 4 * se_s
+    return ok_y, ok_s
+
+
+def test_hybrid_plan_exact_invariants():
+    """Eq. 4.1: S_D is a row selection (weight exactly 1), the random block draws s_R =
+    s - s_D rows (reading Z2), I_D and the drawn rows are disjoint, and p~ renormalises the scores
+    of I_R only (p~_i = l_i / (k - theta))."""
+    A, F, n, k, s = _hybrid_case()
+    lev = O.leverage_scores(F).astype(np.float32)
+    for t in range(20):
+        pl = O.build_plan(lev, k, s, 1.0 / s, seed=5, iteration=t, side=0)
+        assert pl["s_D"] >= 3 and pl["s_D"] + pl["s_R"] == s
+        det = set(pl["det_idx"].tolist())
+        w_of = dict(zip(pl["uniq_idx"].tolist(), pl["uniq_w"].tolist()))
+        assert all(w_of[i] == 1.0 for i in det)
+        assert int(pl["counts"].sum()) == pl["s_R"]
+        assert not det & set(pl["draw_idx"].tolist())
+        # theta + xi = k exactly as defined (P:741), and the realised mass of I_R is W / 2^40 ~ k - theta
+        assert abs(pl["theta"] + pl["xi"] - k) < 1e-12
+        l64 = lev.astype(np.float64)
+        assert abs(pl["W"] / 2.0 ** 40 - l64[~np.isin(np.arange(n), pl["det_idx"])].sum()) < n * 2.0 ** -40
+        # drawn-row weight / per-draw scale: omega_i / c_i = 1 / (s_R p~_i), p~_i = l_i / (k - theta)
+        for i, wi in w_of.items():
+            if i in det:
+                continue
+            p_tilde = float(lev[i]) / (sum(float(lev[j]) for j in range(n) if j not in det))
+            assert abs(wi / pl["counts"][i] * pl["s_R"] * p_tilde - 1.0) < 1e-9
+
+
+def test_hybrid_sampled_product_unbiased_and_norm_preserving():
+    """Hybrid regime (tau = 1/s, s_D > 0): E[Y_s] = A F (Eq. 2.11 scaling on I_R) and
+    E||S_H F||_F^2 = ||F||_F^2, over 600 seeds; both statistical pins must also REJECT
+    the two plausible mistakes -- dividing by s instead of s_R, and renormalising by the mass of all
+    rows instead of I_R -- so a wrong oracle cannot pass them."""
+    A, F, n, k, s = _hybrid_case()
+    N = 600
+    Ys, sq, pl = _hybrid_samples(A, F, k, s, N)
+    assert pl["s_D"] >= 3 and pl["theta"] > 0.5
+    ok_y, ok_s = _hybrid_checks(A, F, Ys, sq)
+    assert ok_y and ok_s
+    det_mask = lambda p: np.isin(p["uniq_idx"], p["det_idx"])
+    lev64 = O.leverage_scores(F).astype(np.float32).astype(np.float64)
+    W_all = int(np.floor(lev64 * 2.0 ** 40).astype(np.uint64).sum(dtype=np.uint64))
+
+    def by_s(p, lev, w):            # omega = c W / (s w) instead of c W / (s_R w)
+        w = w.copy(); m = ~det_mask(p); w[m] *= p["s_R"] / s
+        return w
+
+    def by_all_mass(p, lev, w):     # W = mass of every row instead of I_R
+        w = w.copy(); m = ~det_mask(p); w[m] *= W_all / p["W"]
+        return w
+
+    for mut in (by_s, by_all_mass):
+        Ym, sqm, _ = _hybrid_samples(A, F, k, s, N, mutate=mut)
+        assert _hybrid_checks(A, F, Ym, sqm) != (True, True), mut.__name__
