@@ -120,17 +120,20 @@ def sbm_csr(n: int, n_comm: int, deg_in: float, deg_out: float, rng: np.random.G
     m = n // n_comm
     p_in = deg_in / (m - 1)
     p_out = deg_out / (n - m)
+    # block a holds rows [a m, a m + sz[a]); the last block absorbs the n % n_comm remainder
+    # (identical draws to equal blocks when n_comm divides n)
+    sz = [m] * (n_comm - 1) + [n - (n_comm - 1) * m]
     keys = []
     for a in range(n_comm):
         for b in range(a, n_comm):
             if a == b:
-                cnt = rng.binomial(m * (m - 1) // 2, p_in)
-                i = rng.integers(0, m, cnt) + a * m
-                j = rng.integers(0, m, cnt) + a * m
+                cnt = rng.binomial(sz[a] * (sz[a] - 1) // 2, p_in)
+                i = rng.integers(0, sz[a], cnt) + a * m
+                j = rng.integers(0, sz[a], cnt) + a * m
             else:
-                cnt = rng.binomial(m * m, p_out)
-                i = rng.integers(0, m, cnt) + a * m
-                j = rng.integers(0, m, cnt) + b * m
+                cnt = rng.binomial(sz[a] * sz[b], p_out)
+                i = rng.integers(0, sz[a], cnt) + a * m
+                j = rng.integers(0, sz[b], cnt) + b * m
             keep = i != j
             i, j = i[keep], j[keep]
             keys.append(np.minimum(i, j).astype(np.int64) * n + np.maximum(i, j))
@@ -159,7 +162,11 @@ def powerlaw_csr(n: int, n_comm: int, mean_deg: float, tail: float, mix: float,
     theta = np.minimum(theta, math.sqrt(theta.sum()))
     cum = np.cumsum(theta)
     total = cum[-1]
-    comm_end = cum[m - 1::m]
+    # community c = rows [c m, last[c]]; the last one absorbs the n % n_comm remainder (identical
+    # to equal communities when n_comm divides n)
+    last = np.minimum(np.arange(1, n_comm + 1) * m, n) - 1
+    last[-1] = n - 1
+    comm_end = cum[last]
     comm_start = np.concatenate([[0.0], comm_end[:-1]])
     comm_mass = comm_end - comm_start
     target = int(n * mean_deg) // 2
@@ -169,11 +176,11 @@ def powerlaw_csr(n: int, n_comm: int, mean_deg: float, tail: float, mix: float,
         u = np.searchsorted(cum, rng.random(B) * total, side="right")
         u = np.minimum(u, n - 1)
         inter = rng.random(B) < mix
-        c = u // m
+        c = np.minimum(u // m, n_comm - 1)
         x = np.where(inter, rng.random(B) * total, comm_start[c] + rng.random(B) * comm_mass[c])
         v = np.searchsorted(cum, x, side="right")
         v = np.minimum(v, n - 1)
-        v = np.where(inter, v, np.clip(v, c * m, c * m + m - 1))
+        v = np.where(inter, v, np.clip(v, c * m, last[c]))
         keep = u != v
         u, v = u[keep], v[keep]
         key = np.minimum(u, v).astype(np.int64) * n + np.maximum(u, v)
