@@ -558,6 +558,11 @@ struct symnmf_solver {
   bool bpp;                // Update rule: exact per-row NLS by block principal pivoting (NEXT-1)
   int32_t* nonconv;        // BPP rows that hit the pivoting cap (device counter)
   bool tile;               // EXACT on a large CSR A (kpad(k) == k): product fused into the sweep
+  int nblk;                // tile path: column blocks of A per product (tile.cu); cuts (nblk - 1) x n
+  int64_t* cuts;
+  bool bucket;             // LvS on a large CSR A (kpad(k) == k): destination-bucketed sampled product
+  BucketWs bk;
+  float* Zt;               // bucket gather table Z[t] = omega_t f_{u_t} (cap x k)
   bool small;              // LvS on a small problem: one persistent launch per iteration (small.cu)
   double* Gacc2;           // second zeroed Gram accumulator (small path: G_s and X^T X)
   unsigned int* bar;       // grid barrier words (small path)
@@ -622,6 +627,25 @@ int64_t tile_min_nnz() {
   return 16ll << 20;
 }
 
+// LvS CSR: the destination-bucketed sampled product fused into the sweep from 16M nonzeros;
+// SYMNMF_BUCKET=always|never overrides (symnmf.h)
+int64_t bucket_min_nnz() {
+  const char* e = getenv("SYMNMF_BUCKET");
+  if (e && !strcmp(e, "always")) return 0;
+  if (e && !strcmp(e, "never")) return INT64_MAX;
+  return 16ll << 20;
+}
+
+// EXACT CSR tile path: column blocks so each pass's rows of F (n / nblk x 4k bytes) stay L2
+// resident: 4k n / 64 MB rounded up; SYMNMF_CSR_BLOCKS=<m> overrides (symnmf.h)
+int csr_blocks(int64_t n, int k) {
+  const char* e = getenv("SYMNMF_CSR_BLOCKS");
+  const int64_t v = e ? atoll(e) : 0;
+  if (v > 0) return (int)std::min<int64_t>(v, 64);
+  const int64_t fb = 4ll * k * n;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(64, (fb + (64ll << 20) - 1) / (64ll << 20)));
+}
+
 // Profiling hook: records an event after the launch site just enqueued (no-op unless profiling).
 void mark(symnmf_solver& S, cudaStream_t st, const char* name) {
   if (!S.prof || S.prof->n >= symnmf_solver::Prof::kMax) return;
@@ -652,8 +676,12 @@ void solver_layout(symnmf_solver& S, Carver& c) {
   // the tile kernel balances hub rows; on small graphs the row-per-group SpMM + sweep is faster
   S.tile = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode == SYMNMF_EXACT && !S.bpp &&
            S.A.nnz >= tile_min_nnz();
+  S.nblk = S.tile ? csr_blocks(n, k) : 1;
+  S.cuts = c.take<int64_t>(S.tile ? (size_t)(S.nblk - 1) * n : 0);
+  S.bucket = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode == SYMNMF_LVS && !S.bpp &&
+             S.A.nnz < (int64_t)INT32_MAX && S.A.nnz >= bucket_min_nnz();
   S.nonconv = c.take<int32_t>(1);
-  S.Y = c.take<float>(S.tile ? 0 : (size_t)n * k);
+  S.Y = c.take<float>((S.tile && S.nblk == 1) || S.bucket ? 0 : (size_t)n * k);
   S.small = S.mode == SYMNMF_LVS && !S.with_resid && S.hasA && small_lvs_supported(S.A, n, k) && small_enabled();
   S.Gacc2 = c.take<double>(S.small ? (size_t)kGramReplicas * k * k : 0);
   S.bar = c.take<unsigned int>(S.small ? 4 : 0);
@@ -679,6 +707,10 @@ void solver_layout(symnmf_solver& S, Carver& c) {
     S.plan.uniq_w = c.take<double>(n);
     S.plan.counts = c.take<int64_t>(4);
     S.plan.mass = c.take<double>(2);
+    if (S.bucket) {
+      bucket_layout(c, n, S.A.nnz, S.plan.cap, &S.bk);
+      S.Zt = c.take<float>((size_t)S.plan.cap * k);
+    }
   }
   if (S.mode == SYMNMF_LAI) {
     S.Zpart = c.take<double>(gram_partial_doubles(S.l, k, false, S.ggrid));
@@ -706,7 +738,8 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
   double* Gnext = S.Gbuf[side ^ 1];
   const bool lvs = S.mode == SYMNMF_LVS;
   if (S.mode == SYMNMF_EXACT && S.tile) {
-    launch_csr_tile_sweep(S.A, F, Gf, S.alpha, X, n, k, S.Gacc, Gnext, nullptr, S.counter, status, st);
+    launch_csr_tile_passes(S.A, S.nblk, S.cuts, S.Y, F, Gf, S.alpha, X, n, k, S.Gacc, Gnext, nullptr, S.counter,
+                           status, st);
     mark(S, st, "csr_tile_exact");
   } else if (S.mode == SYMNMF_EXACT) {
     if (!enqueue_product(S.A, F, k, S.Y, S.precision, S.tcs, S.tcs_bytes, status, st)) return false;
@@ -729,8 +762,17 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     // G_s and Y_s only read the plan: G_s runs on a second branch of the graph, concurrently
     cudaEventRecord(S.ev_fork[side], st);
     cudaStreamWaitEvent(S.side, S.ev_fork[side], 0);
-    launch_sampled_gram_fused(F, k, S.plan, S.Gacc, S.Gs, S.counter, status, S.side);
+    launch_sampled_gram_fused(F, k, S.plan, S.Gacc, S.Gs, S.counter, status, S.side, S.bucket ? S.Zt : nullptr);
     cudaEventRecord(S.ev_join[side], S.side);
+    if (S.bucket) {
+      // sampled nonzeros counting-sorted by destination row; the sweep pulls Y_s from the buckets
+      launch_bucket_build(S.A, S.plan.uniq_idx, S.plan.counts + 2, S.bk, S.counter + 1, status, st);
+      mark(S, st, "bucket_build");
+      cudaStreamWaitEvent(st, S.ev_join[side], 0);
+      launch_bucket_tile_sweep(S.bk, S.Zt, F, S.Gs, S.alpha, X, n, k, S.Gacc, Gnext, S.Rinv32, S.counter, status, st);
+      mark(S, st, "bucket_sweep");
+      return true;
+    }
     if (S.A.kind == SYMNMF_CSR) {
       launch_sampled_csr_nozero(S.A, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap, S.Y,
                                 status, st);
@@ -854,7 +896,19 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
     SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Gacc2, 0, sizeof(double) * kGramReplicas * k * k, st));
     SYMNMF_CUDA_TRY(cudaMemsetAsync(S.bar, 0, sizeof(unsigned int) * 4, st));
   }
-  if (mode == SYMNMF_LVS) SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Y, 0, sizeof(float) * n * k, st));
+  if (mode == SYMNMF_LVS && S.Y) SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Y, 0, sizeof(float) * n * k, st));
+  if (S.bucket) SYMNMF_CUDA_TRY(cudaMemsetAsync(S.bk.cnt, 0, sizeof(int32_t) * n, st));
+  if (S.tile || S.bucket) {
+    // column cuts of the EXACT passes; both paths need every row's columns sorted, unique, in range
+    int32_t* bad = S.nonconv;
+    SYMNMF_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int32_t), st));
+    launch_csr_cuts(S.A, S.tile ? S.nblk : 1, S.cuts, bad, st);
+    int32_t hbad = 0;
+    SYMNMF_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    SYMNMF_CUDA_TRY(cudaStreamSynchronize(st));
+    SYMNMF_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int32_t), st));
+    if (hbad) return SYMNMF_ERR_ARG;
+  }
   set_i32<<<1, 1, 0, st>>>(S.iter_dev, first_iter);
   // H^T H (and its CholeskyQR factor for LvS) for the first W-half; later halves get
   // theirs from the fused Gram of the preceding sweep.

@@ -1,0 +1,279 @@
+// (a9) The sampled CSR product Y_s = sum_{i in U} omega_i A[i,:]^T f_i
+// in destination-bucketed form: the sampled rows' nonzeros are counting-sorted by their column
+// (= the destination row of Y_s, since row i of A is column i), so the HALS sweep that
+// consumes Y_s can pull each destination row's terms from one contiguous bucket and Y_s never
+// exists in HBM.  Steps (all on the solver's stream, after the plan):
+//
+//   plan_row_offsets  pre[t] = sum_{t' < t} nnz(u_t') over the plan's unique rows (one CTA), and
+//                     rb[t] = rowptr[u_t] - pre[t], so entry j of the concatenated sampled rows is
+//                     nonzero e = rb[t] + j of A for the t with pre[t] <= j < pre[t+1].
+//   bucket_count      slot[e] = atomicAdd(&cnt[col[e]], 1) for every sampled nonzero e: the count
+//                     of each bucket and the entry's place in it (nnz-balanced warp chunks, so a
+//                     hub row is spread over many warps).
+//   bucket_scan_*     off = exclusive scan of cnt (two passes: tile sums + last-CTA scan of the
+//                     tile sums, then the tiles), cnt re-zeroed for the next plan.
+//   bucket_fill       ent[off[c] + slot[e]] = (t, a_e): the bucket entries.
+//   (tile sweep)      fused.cu: tile_sweep over (off, ent) with the gather table Z[t] = omega_t f_u_t.
+//
+// The order of the entries inside a bucket follows the atomics (run to run it may differ), so the
+// fp32 sum of a bucket is compared by tolerance, like every other GPU product sum (reading Z29).
+#include "kernels.cuh"
+
+namespace symnmf {
+
+constexpr int kBucketChunk = 1024;   // sampled nonzeros per warp chunk (32 per lane)
+constexpr int kBucketUnroll = 4;     // independent entries in flight per lane
+
+// ---------------------------------------------------------------- plan_row_offsets (1 CTA)
+__global__ void __launch_bounds__(1024) plan_row_offsets(const int64_t* __restrict__ rowptr,
+                                                         const int32_t* __restrict__ uniq,
+                                                         const int64_t* __restrict__ n_uniq_dev,
+                                                         int64_t* __restrict__ pre, int64_t* __restrict__ rb,
+                                                         const int32_t* __restrict__ status) {
+  __shared__ int64_t sh[33];
+  if (dev_failed(status)) return;
+  const int64_t nu = *n_uniq_dev;
+  constexpr int PER = 8;
+  int64_t run = 0;
+  for (int64_t base = 0; base < nu; base += 1024 * PER) {
+    int64_t len[PER], start[PER];
+    int64_t tot = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int64_t t = base + (int64_t)threadIdx.x * PER + q;
+      if (t < nu) {
+        const int64_t u = uniq[t];
+        start[q] = rowptr[u];
+        len[q] = rowptr[u + 1] - start[q];
+      } else {
+        start[q] = 0;
+        len[q] = 0;
+      }
+      tot += len[q];
+    }
+    int64_t chunk_tot;
+    int64_t p = run + block_excl_scan(tot, sh, &chunk_tot);
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int64_t t = base + (int64_t)threadIdx.x * PER + q;
+      if (t < nu) {
+        pre[t] = p;
+        rb[t] = start[q] - p;
+      }
+      p += len[q];
+    }
+    run += chunk_tot;
+  }
+  if (threadIdx.x == 0) pre[nu] = run;
+}
+
+// Largest t in [lo, hi] with pre[t] <= j (pre non-decreasing, pre[lo] <= j).
+__device__ __forceinline__ int64_t row_of_entry(const int64_t* __restrict__ pre, int64_t lo, int64_t hi, int64_t j) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (__ldg(pre + mid) <= j) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Visit every sampled nonzero in nnz-balanced warp chunks: fn(t, e) with t the plan slot and e the
+// nonzero of A.  Each lane keeps kBucketUnroll entries in flight.
+template <class Fn>
+__device__ __forceinline__ void for_sampled_nonzeros(const int64_t* __restrict__ pre, const int64_t* __restrict__ rb,
+                                                     int64_t nu, Fn&& fn) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total = pre[nu];
+  const int64_t nchunks = (total + kBucketChunk - 1) / kBucketChunk;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t ch = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; ch < nchunks; ch += nw) {
+    const int64_t j0 = ch * kBucketChunk, j1 = min64(total, j0 + kBucketChunk);
+    const int64_t thi = row_of_entry(pre, 0, nu - 1, j1 - 1);
+    int64_t tcur = row_of_entry(pre, 0, thi, j0);
+    for (int64_t jb = j0; jb < j1; jb += 32 * kBucketUnroll) {
+      int64_t t[kBucketUnroll], e[kBucketUnroll];
+#pragma unroll
+      for (int u = 0; u < kBucketUnroll; ++u) {
+        const int64_t j = jb + 32 * u + lane;
+        t[u] = j < j1 ? row_of_entry(pre, tcur, thi, j) : -1;
+        e[u] = t[u] >= 0 ? __ldg(rb + t[u]) + j : 0;
+      }
+      fn(t, e);
+      // the group's last entry's row starts the next group's search
+      const int64_t jl = min64(j1, jb + 32 * kBucketUnroll) - 1;
+      tcur = row_of_entry(pre, tcur, thi, jl);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) bucket_count(const int32_t* __restrict__ col, const int64_t* __restrict__ pre,
+                                                    const int64_t* __restrict__ rb,
+                                                    const int64_t* __restrict__ n_uniq_dev, int32_t* __restrict__ cnt,
+                                                    int32_t* __restrict__ slot, const int32_t* __restrict__ status) {
+  if (dev_failed(status)) return;
+  const int64_t nu = *n_uniq_dev;
+  if (nu <= 0) return;
+  for_sampled_nonzeros(pre, rb, nu, [&](const int64_t (&t)[kBucketUnroll], const int64_t (&e)[kBucketUnroll]) {
+    int32_t c[kBucketUnroll], s[kBucketUnroll];
+#pragma unroll
+    for (int u = 0; u < kBucketUnroll; ++u) c[u] = t[u] >= 0 ? __ldcs(col + e[u]) : 0;
+#pragma unroll
+    for (int u = 0; u < kBucketUnroll; ++u) s[u] = t[u] >= 0 ? atomicAdd(cnt + c[u], 1) : 0;
+#pragma unroll
+    for (int u = 0; u < kBucketUnroll; ++u)
+      if (t[u] >= 0) slot[e[u]] = s[u];
+  });
+}
+
+// ---------------------------------------------------------------- exclusive scan of cnt
+constexpr int kScanTile = 4096;   // 256 threads x 16
+inline int64_t bucket_scan_tiles(int64_t n) { return (n + kScanTile - 1) / kScanTile; }
+
+__global__ void __launch_bounds__(256) bucket_scan_sums(const int32_t* __restrict__ cnt, int64_t n,
+                                                        int32_t* __restrict__ tsum, int32_t* __restrict__ off,
+                                                        unsigned int* counter, int32_t* __restrict__ status) {
+  __shared__ int32_t sh[33];
+  if (dev_failed(status)) return;
+  const int64_t i0 = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 16;
+  int32_t s = 0;
+  if (i0 + 16 <= n) {
+    const int4* c4 = reinterpret_cast<const int4*>(cnt + i0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int4 v = __ldcg(c4 + q);
+      s += v.x + v.y + v.z + v.w;
+    }
+  } else {
+    for (int64_t i = i0; i < min64(n, i0 + 16); ++i) s += __ldcg(cnt + i);
+  }
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) tsum[blockIdx.x] = s;
+  // last CTA: exclusive scan of the tile sums (in place) and the grand total off[n]
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) *counter = 0;
+  const int64_t nt = gridDim.x;
+  int32_t run = 0;
+  for (int64_t base = 0; base < nt; base += 256) {
+    const int64_t i = base + threadIdx.x;
+    const int32_t v = i < nt ? __ldcg(tsum + i) : 0;
+    int32_t tot;
+    const int32_t e = block_excl_scan(v, sh, &tot);
+    if (i < nt) tsum[i] = run + e;
+    run += tot;
+  }
+  if (threadIdx.x == 0) off[n] = run;
+}
+
+__global__ void __launch_bounds__(256) bucket_scan_write(int32_t* __restrict__ cnt, int64_t n,
+                                                         const int32_t* __restrict__ tsum, int32_t* __restrict__ off,
+                                                         const int32_t* __restrict__ status) {
+  __shared__ int32_t sh[33];
+  if (dev_failed(status)) return;
+  const int64_t i0 = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 16;
+  int32_t v[16];
+  if (i0 + 16 <= n) {
+    const int4* c4 = reinterpret_cast<const int4*>(cnt + i0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int4 x = __ldcg(c4 + q);
+      v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = i0 + q < n ? __ldcg(cnt + i0 + q) : 0;
+  }
+  int32_t tot = 0;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) tot += v[q];
+  int32_t run = block_excl_scan(tot, sh, (int32_t*)nullptr) + tsum[blockIdx.x];
+  if (i0 + 16 <= n) {
+    int4* o4 = reinterpret_cast<int4*>(off + i0);
+    int4* c4 = reinterpret_cast<int4*>(cnt + i0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int4 x;
+      x.x = run; run += v[4 * q];
+      x.y = run; run += v[4 * q + 1];
+      x.z = run; run += v[4 * q + 2];
+      x.w = run; run += v[4 * q + 3];
+      o4[q] = x;
+      c4[q] = make_int4(0, 0, 0, 0);   // buckets empty for the next plan
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      if (i0 + q < n) {
+        off[i0 + q] = run;
+        cnt[i0 + q] = 0;
+      }
+      run += v[q];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- bucket_fill
+__global__ void __launch_bounds__(256) bucket_fill(const int32_t* __restrict__ col, const float* __restrict__ val,
+                                                   const int64_t* __restrict__ pre, const int64_t* __restrict__ rb,
+                                                   const int64_t* __restrict__ n_uniq_dev,
+                                                   const int32_t* __restrict__ off, const int32_t* __restrict__ slot,
+                                                   int2* __restrict__ ent, const int32_t* __restrict__ status) {
+  if (dev_failed(status)) return;
+  const int64_t nu = *n_uniq_dev;
+  if (nu <= 0) return;
+  for_sampled_nonzeros(pre, rb, nu, [&](const int64_t (&t)[kBucketUnroll], const int64_t (&e)[kBucketUnroll]) {
+    int32_t c[kBucketUnroll], s[kBucketUnroll];
+    float a[kBucketUnroll];
+#pragma unroll
+    for (int u = 0; u < kBucketUnroll; ++u) {
+      const bool ok = t[u] >= 0;
+      c[u] = ok ? __ldcs(col + e[u]) : 0;
+      s[u] = ok ? __ldcs(slot + e[u]) : 0;
+      a[u] = ok ? __ldcs(val + e[u]) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < kBucketUnroll; ++u)
+      if (t[u] >= 0) ent[__ldg(off + c[u]) + s[u]] = make_int2((int32_t)t[u], __float_as_int(a[u]));
+  });
+}
+
+// ---------------------------------------------------------------- launchers
+size_t bucket_ws_bytes(int64_t n, int64_t nnz, int64_t cap) {
+  // pre, rb [cap + 1] int64; cnt, off [n + 1] int32; tsum; slot [nnz] int32; ent [nnz] int2
+  return sizeof(int64_t) * 2 * (size_t)(cap + 1) + sizeof(int32_t) * 2 * (size_t)(n + 4) +
+         sizeof(int32_t) * (size_t)(bucket_scan_tiles(n) + 4) + sizeof(int32_t) * (size_t)nnz +
+         sizeof(int2) * (size_t)nnz + 6 * 256;
+}
+
+void bucket_layout(Carver& c, int64_t n, int64_t nnz, int64_t cap, BucketWs* b) {
+  b->pre = c.take<int64_t>((size_t)cap + 1);
+  b->rb = c.take<int64_t>((size_t)cap + 1);
+  b->cnt = c.take<int32_t>((size_t)n + 4);
+  b->off = c.take<int32_t>((size_t)n + 4);
+  b->tsum = c.take<int32_t>((size_t)bucket_scan_tiles(n) + 4);
+  b->slot = c.take<int32_t>((size_t)nnz);
+  b->ent = c.take<int2>((size_t)nnz);
+}
+
+static int bucket_grid(int64_t cap_entries) {
+  const int64_t warps = (cap_entries + kBucketChunk - 1) / kBucketChunk;
+  return (int)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, 148 * 8));
+}
+
+void launch_bucket_build(const symnmf_matrix& A, const int32_t* uniq, const int64_t* n_uniq_dev, const BucketWs& b,
+                         unsigned int* counter, int32_t* status, cudaStream_t st) {
+  const int64_t n = A.n;
+  launch_pdl(plan_row_offsets, 1, 1024, 0, st, A.rowptr, uniq, n_uniq_dev, b.pre, b.rb, status);
+  const int grid = bucket_grid(A.nnz);
+  launch_pdl(bucket_count, grid, 256, 0, st, A.colidx, b.pre, b.rb, n_uniq_dev, b.cnt, b.slot, status);
+  const int tiles = (int)bucket_scan_tiles(n);
+  launch_pdl(bucket_scan_sums, tiles, 256, 0, st, b.cnt, n, b.tsum, b.off, counter, status);
+  launch_pdl(bucket_scan_write, tiles, 256, 0, st, b.cnt, n, b.tsum, b.off, status);
+  launch_pdl(bucket_fill, grid, 256, 0, st, A.colidx, A.val, b.pre, b.rb, n_uniq_dev, b.off, b.slot, b.ent, status);
+}
+
+}  // namespace symnmf

@@ -283,6 +283,47 @@ def random_factor(n: int, k: int, seed: int, scale: float = 1.0) -> np.ndarray:
 
 
 # ---------------------------------------------------------------- top level
+def _cache_dir(name: str, seed: int, noise: bool, n: int):
+    """Directory caching a large generated input (SYMNMF_INPUT_CACHE, default /tmp/symnmf_inputs;
+    "off" disables), keyed by the recipe (config, seed, noise, n) and this file's bytes, so a cached
+    input is the same bits a fresh draw gives.  Generation is outside every timed region; the
+    cache only saves minutes when several runs of one session use c3/c4."""
+    root = os.environ.get("SYMNMF_INPUT_CACHE", "/tmp/symnmf_inputs")
+    if root == "off" or name not in ("c3", "c4") or n < 100_000 and name == "c4":
+        return None
+    import hashlib
+    h = hashlib.sha1(open(__file__, "rb").read()).hexdigest()[:12]
+    return os.path.join(root, f"{name}_s{seed}_n{n}_{int(noise)}_{h}")
+
+
+def _cache_load(d):
+    try:
+        if d is None or not os.path.exists(os.path.join(d, "done")):
+            return None
+        z = {f[:-4]: np.load(os.path.join(d, f)) for f in os.listdir(d) if f.endswith(".npy")}
+        if "rowptr" in z:
+            return CsrMatrix(int(z["n"]), z["rowptr"], z["colidx"], z["val"]), z
+        return z["A"], z
+    except Exception:
+        return None
+
+
+def _cache_save(d, A, extra):
+    try:
+        os.makedirs(d, exist_ok=True)
+        if isinstance(A, CsrMatrix):
+            for k_, v in (("rowptr", A.rowptr), ("colidx", A.colidx), ("val", A.val), ("n", np.array(A.n))):
+                np.save(os.path.join(d, k_ + ".npy"), v)
+        else:
+            np.save(os.path.join(d, "A.npy"), A)
+        for k_ in ("points", "sigma"):
+            if k_ in extra:
+                np.save(os.path.join(d, k_ + ".npy"), np.asarray(extra[k_]))
+        open(os.path.join(d, "done"), "w").close()
+    except Exception:
+        pass
+
+
 def make_input(name: str, seed: int | None = None, noise: bool = True, n_override: int | None = None):
     """Generate config `name`.  Returns dict(cfg, A, H0, alpha, zeta, extra).
 
@@ -293,6 +334,16 @@ def make_input(name: str, seed: int | None = None, noise: bool = True, n_overrid
     n = n_override or cfg.n
     drng, irng = _streams(seed)
     extra = {}
+    cdir = _cache_dir(name, seed, noise, n)
+    hit = _cache_load(cdir)
+    if hit is not None:
+        A, z = hit
+        if "points" in z:
+            extra.update(points=z["points"], sigma=float(z["sigma"]))
+        zeta = mean_entry(A)
+        H0 = init_factor(n, cfg.k, zeta, irng)
+        return {"cfg": cfg, "n": n, "A": A, "H0": H0, "alpha": alpha_of(A), "zeta": zeta,
+                "seed": seed, "extra": extra}
     if name == "c1":
         A, H0p = planted_dense(n, cfg.k, 0.01 if noise else 0.0, drng)
         extra["H0_planted"] = H0p
@@ -307,6 +358,8 @@ def make_input(name: str, seed: int | None = None, noise: bool = True, n_overrid
         extra.update(points=X, sigma=sigma)
     else:
         raise KeyError(name)
+    if cdir is not None:
+        _cache_save(cdir, A, extra)
     zeta = mean_entry(A)
     H0 = init_factor(n, cfg.k, zeta, irng)
     return {"cfg": cfg, "n": n, "A": A, "H0": H0, "alpha": alpha_of(A), "zeta": zeta,

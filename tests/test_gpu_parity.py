@@ -7,6 +7,8 @@ normalised residual after 10 iterations 1e-4 relative.
 """
 import math
 
+import os
+
 import numpy as np
 import pytest
 
@@ -462,13 +464,17 @@ def _csr_case(cfgname, n, k, seed=7):
 
 @pytest.mark.parametrize("cfgname,n,k", [("c2", 20_000, 16), ("c2", 20_000, 8), ("c4", 40_000, 32),
                                          ("c4", 40_000, 64), ("c4", 40_032, 16), ("c2", 2_000, 32)])
-@pytest.mark.parametrize("tile", ["always", "never"])
+@pytest.mark.parametrize("tile", ["always", "never", "blocks3", "blocks7"])
 def test_csr_tile_exact_one_iteration(cfgname, n, k, tile, monkeypatch):
     """Solver EXACT on CSR, both product forms: the tile kernel (A F per 256-row tile with
-    nnz-balanced slices, fused with the sweep and the next Gram; SYMNMF_CSR_TILE=always) and the
-    row SpMM + sweep: W and H after one iteration vs the oracle's fp64 iteration.  Covers ragged
-    last tiles (n % 256 != 0), hub rows (power-law c4 recipe) and k = 8..64."""
-    monkeypatch.setenv("SYMNMF_CSR_TILE", tile)
+    nnz-balanced slices, fused with the sweep and the next Gram; SYMNMF_CSR_TILE=always), also in
+    3 and 7 column-block passes (SYMNMF_CSR_BLOCKS: partial products through HBM, the last pass
+    fused with the sweep), and the row SpMM + sweep: W and H after one iteration vs the oracle's
+    fp64 iteration.  Covers ragged last tiles (n % 256 != 0), hub rows (power-law c4 recipe) and
+    k = 8..64."""
+    monkeypatch.setenv("SYMNMF_CSR_TILE", "never" if tile == "never" else "always")
+    if tile.startswith("blocks"):
+        monkeypatch.setenv("SYMNMF_CSR_BLOCKS", tile[6:])
     A, H0, alpha = _csr_case(cfgname, n, k)
     M = S.DeviceMatrix.from_host(A)
     W, H = cu(H0), cu(H0)
@@ -482,12 +488,14 @@ def test_csr_tile_exact_one_iteration(cfgname, n, k, tile, monkeypatch):
 
 
 @pytest.mark.parametrize("cfgname,n,k,s", [("c4", 40_000, 32, 800), ("c2", 20_000, 16, 400), ("c4", 40_000, 8, 2000)])
-@pytest.mark.parametrize("slice_mb", ["", "1"])
+@pytest.mark.parametrize("slice_mb", ["", "1", "bucket"])
 def test_csr_lvs_solver_equals_abi_composition(cfgname, n, k, s, slice_mb, monkeypatch):
     """Solver LvS on CSR graphs with hubs (destination-range scatter passes, fused Gram) equals
     the composition of the ABI calls on the same device data; slice_mb = 1 forces several
-    destination-range passes of the sampled scatter."""
-    if slice_mb:
+    destination-range passes of the sampled scatter; "bucket" the destination-bucketed sampled
+    product fused into the sweep (bucket.cu + tile.cu)."""
+    monkeypatch.setenv("SYMNMF_BUCKET", "always" if slice_mb == "bucket" else "never")
+    if slice_mb == "1":
         monkeypatch.setenv("SYMNMF_SCATTER_SLICE_MB", slice_mb)
     A, H0, alpha = _csr_case(cfgname, n, k)
     tau = 1.0 / s
@@ -512,9 +520,11 @@ def test_csr_lvs_solver_equals_abi_composition(cfgname, n, k, s, slice_mb, monke
     assert rel(H1.cpu().numpy(), H2.cpu().numpy()) < 1e-5
 
 
-def test_csr_lvs_replayed_plan_vs_oracle():
+@pytest.mark.parametrize("bucket", ["always", "never"])
+def test_csr_lvs_replayed_plan_vs_oracle(bucket, monkeypatch):
     """One LvS half through the solver vs the oracle's sampled products + sweep fed the plan the
     GPU drew (the same plan is recomputed by the ABI sampler from the same device scores)."""
+    monkeypatch.setenv("SYMNMF_BUCKET", bucket)
     A, H0, alpha = _csr_case("c4", 30_016, 32)
     s, tau = 600, 1.0 / 600
     M = S.DeviceMatrix.from_host(A)
@@ -751,11 +761,14 @@ def _drop_vertices(A, frac, tail, seed=3):
     return CsrMatrix(A.n, rowptr, A.colidx[keep].copy(), A.val[keep].copy())
 
 
-@pytest.mark.parametrize("tile", ["always", "never"])
+@pytest.mark.parametrize("tile", ["always", "never", "blocks3"])
 def test_csr_empty_rows(tile, monkeypatch):
     """Isolated vertices (empty CSR rows, 10% random + an empty 300-row tail): the product, the
-    sampled product over all rows, and one EXACT solver iteration (tile kernel and row SpMM)."""
-    monkeypatch.setenv("SYMNMF_CSR_TILE", tile)
+    sampled product over all rows, one EXACT solver iteration (tile kernel in one or three
+    column-block passes, and row SpMM), and one LvS half of the bucketed solver path."""
+    monkeypatch.setenv("SYMNMF_CSR_TILE", "never" if tile == "never" else "always")
+    if tile == "blocks3":
+        monkeypatch.setenv("SYMNMF_CSR_BLOCKS", "3")
     A0, H0, alpha = _csr_case("c2", 20_000, 16)
     A = _drop_vertices(A0, 0.1, 300)
     assert (np.diff(A.rowptr) == 0).sum() >= 2000
@@ -771,6 +784,17 @@ def test_csr_empty_rows(tile, monkeypatch):
     Wr, Hr, _ = O.iterate(A, H0, H0, alpha, 1, "exact")
     assert rel(W.cpu().numpy(), Wr) < 1e-5
     assert rel(H.cpu().numpy(), Hr) < 1e-5
+    # LvS, bucketed sampled product: W-half vs the oracle fed the plan the GPU draws
+    monkeypatch.setenv("SYMNMF_BUCKET", "always")
+    s_, tau = 800, 1.0 / 800
+    W, H = cu(H0), cu(H0)
+    sv = S.Solver(M, W, H, alpha, mode="lvs", s=s_, tau=tau, seed=5, max_iters=1)
+    sv.run(1)
+    assert sv.stats()["status"] == 0
+    sv.close()
+    ph = S.hybrid_sample(S.leverage_scores(cu(H0)), 16, s_, tau, 5, 0, 0).to_host()
+    Gs, Ys = O.sampled_products(A, H0, ph["uniq_idx"], ph["uniq_w"])
+    assert rel(W.cpu().numpy(), O.hals_sweep(Gs, Ys, H0, H0, alpha)) < 1e-5
 
 
 def test_csr_zero_matrix():
@@ -783,7 +807,9 @@ def test_csr_zero_matrix():
     M = S.DeviceMatrix.from_host(A)
     Y = S.ah(M, cu(H0)).cpu().numpy()
     assert not Y.any()
-    for mode, kw in (("exact", {}), ("lvs", dict(s=300, tau=1.0 / 300, seed=2))):
+    for mode, kw, env in (("exact", {}, "never"), ("lvs", dict(s=300, tau=1.0 / 300, seed=2), "never"),
+                          ("exact", {}, "always"), ("lvs", dict(s=300, tau=1.0 / 300, seed=2), "always")):
+        os.environ["SYMNMF_CSR_TILE"] = os.environ["SYMNMF_BUCKET"] = env
         W, H = cu(H0), cu(H0)
         sv = S.Solver(M, W, H, alpha, mode=mode, max_iters=1, **kw)
         sv.run(1)
@@ -794,3 +820,4 @@ def test_csr_zero_matrix():
             Wr, Hr, _ = O.iterate(A, H0, H0, alpha, 1, "exact")
             assert rel(Wg, Wr) < 1e-5 and rel(H.cpu().numpy(), Hr) < 1e-5
         assert np.isfinite(Wg).all() and (Wg >= 0).all()
+    os.environ.pop("SYMNMF_CSR_TILE"); os.environ.pop("SYMNMF_BUCKET")
