@@ -108,14 +108,19 @@ typedef struct {
  * the same up to fp32 summation order):
  *   SYMNMF_CSR_TILE=always|never   EXACT solver on CSR: force / forbid the tile kernel (product
  *                                  fused with the sweep); default: used from 16M nonzeros.
- *   SYMNMF_SCATTER_SLICE_MB=<mb>   sampled CSR product: rows of Y per destination-range pass
- *                                  (default 86 MB, so each pass's slice of Y stays in L2).
+ *   SYMNMF_CSR_BLOCKS=<m>          EXACT tile kernel: column blocks of A per product (m passes, the
+ *                                  partial products through an n x k buffer, the last pass fused
+ *                                  with the sweep); default ceil(4 n k / 64 MB), so the rows of F a
+ *                                  pass gathers stay resident in L2.
+ *   SYMNMF_BUCKET=always|never     LvS solver on CSR (k in {8,16,32,64}): force / forbid the
+ *                                  destination-bucketed sampled product fused with the sweep;
+ *                                  default: used from 16M nonzeros.
+ *   SYMNMF_SCATTER_SLICE_MB=<mb>   sampled CSR scatter product: rows of Y per destination-range
+ *                                  pass (default 86 MB, so each pass's slice of Y stays in L2).
  *   SYMNMF_LAI_FUSED=never         LAI solver (k = 64, l <= 80): use the four-kernel half (U^T F,
  *                                  Lambda scaling, U M, sweep) instead of the fused launch.
- *   SYMNMF_SMALL=always            LvS solver: use the persistent one-launch-per-iteration kernel
- *                                  (grid barriers between steps) on small problems (CSR n <= 2^20
- *                                  or dense n <= 4096, k in {8, 16, 32}, no per-iteration
- *                                  residual); default: the multi-kernel CUDA graph (faster). */
+ * CSR inputs: every row's column indices must be sorted, unique and in [0, n) (both triangles
+ * stored); symnmf_solver_create checks this on the device and returns SYMNMF_ERR_ARG otherwise. */
 
 /* Library version (major*10000 + minor*100 + patch).  Host only. */
 int32_t symnmf_version(void);

@@ -7,7 +7,6 @@
 #include <cstdlib>
 #include <cstring>
 #include "kernels.cuh"
-#include "small_args.cuh"
 
 using namespace symnmf;
 
@@ -563,9 +562,6 @@ struct symnmf_solver {
   bool bucket;             // LvS on a large CSR A (kpad(k) == k): destination-bucketed sampled product
   BucketWs bk;
   float* Zt;               // bucket gather table Z[t] = omega_t f_{u_t} (cap x k)
-  bool small;              // LvS on a small problem: one persistent launch per iteration (small.cu)
-  double* Gacc2;           // second zeroed Gram accumulator (small path: G_s and X^T X)
-  unsigned int* bar;       // grid barrier words (small path)
   symnmf_half_stats* stats;
   double *resid, *rpart, *rout, *GH;
   double *pgrad, *ppart, *pout;   // NEXT-3: per-iteration projected-gradient norm (with_resid)
@@ -610,13 +606,6 @@ void enqueue_sweep(const symnmf_solver& S, const double* G, const float* F, floa
 bool lai_enabled() {
   const char* e = getenv("SYMNMF_LAI_FUSED");
   return !(e && !strcmp(e, "never"));
-}
-
-// LvS on small problems: the persistent iteration kernel only on request (SYMNMF_SMALL=always,
-// symnmf.h): measured slower than the multi-kernel graph on B200 (small.cu)
-bool small_enabled() {
-  const char* e = getenv("SYMNMF_SMALL");
-  return e && !strcmp(e, "always");
 }
 
 // EXACT CSR: the tile kernel from 16M nonzeros; SYMNMF_CSR_TILE=always|never overrides (symnmf.h)
@@ -682,9 +671,6 @@ void solver_layout(symnmf_solver& S, Carver& c) {
              S.A.nnz < (int64_t)INT32_MAX && S.A.nnz >= bucket_min_nnz();
   S.nonconv = c.take<int32_t>(1);
   S.Y = c.take<float>((S.tile && S.nblk == 1) || S.bucket ? 0 : (size_t)n * k);
-  S.small = S.mode == SYMNMF_LVS && !S.with_resid && S.hasA && small_lvs_supported(S.A, n, k) && small_enabled();
-  S.Gacc2 = c.take<double>(S.small ? (size_t)kGramReplicas * k * k : 0);
-  S.bar = c.take<unsigned int>(S.small ? 4 : 0);
   S.stats = c.take<symnmf_half_stats>((size_t)2 * S.max_iters);
   S.resid = c.take<double>((size_t)S.max_iters);
   S.rgrid = residual_grid(n);
@@ -804,21 +790,7 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
   return true;
 }
 
-bool enqueue_small(symnmf_solver& S, cudaStream_t st) {
-  SmallArgs a{};
-  a.kind = S.A.kind; a.n = S.n; a.lda = S.A.lda; a.val = S.A.val; a.rowptr = S.A.rowptr; a.colidx = S.A.colidx;
-  a.W = S.W; a.H = S.H; a.k = S.k; a.alpha = S.alpha; a.T = S.T; a.s = S.s; a.seed = S.seed;
-  a.iter_dev = S.iter_dev; a.first_iter = S.first_iter; a.max_iters = S.max_iters; a.stats = S.stats;
-  a.lev = S.lev; a.bw = S.sw.bw; a.bd = S.sw.bd; a.bt = S.sw.bt; a.bu = S.sw.bu; a.P = S.sw.P; a.cnt = S.sw.cnt;
-  a.plan = S.plan; a.Y = S.Y; a.GsAcc = S.Gacc; a.GAcc = S.Gacc2; a.Gout = S.Gbuf[0]; a.R32 = S.Rinv32;
-  a.bar = S.bar; a.status = S.status;
-  if (!launch_small_lvs(a, st)) return false;
-  mark(S, st, "lvs_small");
-  return true;
-}
-
 bool enqueue_iteration(symnmf_solver& S, cudaStream_t st) {
-  if (S.small) return enqueue_small(S, st);
   if (!enqueue_half(S, 0, st) || !enqueue_half(S, 1, st)) return false;
   if (S.with_resid) {
     if (S.A.kind == SYMNMF_CSR) launch_spmm_csr(S.A, S.H, S.k, S.AHres, S.status, st);
@@ -892,14 +864,11 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
                       st);
     launch_scale_rows(S.Z, S.l, k, S.lam, S.Mside[0], S.status, st);
   }
-  if (S.small) {
-    SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Gacc2, 0, sizeof(double) * kGramReplicas * k * k, st));
-    SYMNMF_CUDA_TRY(cudaMemsetAsync(S.bar, 0, sizeof(unsigned int) * 4, st));
-  }
   if (mode == SYMNMF_LVS && S.Y) SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Y, 0, sizeof(float) * n * k, st));
   if (S.bucket) SYMNMF_CUDA_TRY(cudaMemsetAsync(S.bk.cnt, 0, sizeof(int32_t) * n, st));
-  if (S.tile || S.bucket) {
-    // column cuts of the EXACT passes; both paths need every row's columns sorted, unique, in range
+  if (S.hasA && S.A.kind == SYMNMF_CSR) {
+    // every sparse path assumes each row's columns sorted, unique and in range (the column cuts of
+    // the EXACT tile passes and the destination ranges of the sampled scatter search them)
     int32_t* bad = S.nonconv;
     SYMNMF_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int32_t), st));
     launch_csr_cuts(S.A, S.tile ? S.nblk : 1, S.cuts, bad, st);

@@ -1,5 +1,5 @@
 // Device helpers shared by the fused solver kernels (fused.cu) and the persistent
-// small-problem iteration kernel (small.cu): last-CTA detection, the fp64 warp Cholesky
+// row-tile kernels (tile.cu): last-CTA detection, the fp64 warp Cholesky
 // of CholeskyQR, register-blocked Gram partials and the
 // last-CTA Gram finalize.  Included by .cu files only.
 #pragma once

@@ -155,11 +155,6 @@ void launch_lai_sweep_fused(const float* U, int l, int64_t n, int k, const float
                             const float* F, float* X, const double* lam, double* GXacc, double* UXacc, double* Gout,
                             float* Mnext, unsigned int* counter, int32_t* status, cudaStream_t st);
 
-// ---------------------------------------------------------------- small.cu
-struct SmallArgs;
-bool small_lvs_supported(const symnmf_matrix& A, int64_t n, int k);
-bool launch_small_lvs(const SmallArgs& a, cudaStream_t st);
-
 // ---------------------------------------------------------------- residual.cu
 void launch_residual(const symnmf_matrix& A, const float* H, int k, const float* AH, const double* G,
                      double* partial, int grid, double* out, const int32_t* status, cudaStream_t st);

@@ -114,3 +114,30 @@ def test_two_solvers_on_two_streams(mode):
             sv.close()
     for (Wa, Ha), (Wb, Hb) in zip(alone, both):
         assert rel(Wb, Wa) < 1e-6 and rel(Hb, Ha) < 1e-6
+
+
+@pytest.mark.parametrize("defect", ["unsorted", "duplicate", "out_of_range"])
+def test_solver_rejects_malformed_csr(defect):
+    """symnmf.h "CSR inputs": every sparse path searches sorted rows (the column cuts of the EXACT
+    tile passes, the destination ranges of the sampled scatter), so solver creation checks each
+    row's columns on the device and returns SYMNMF_ERR_ARG instead of silently misrouting."""
+    from synth.configs import CsrMatrix
+    d = make_input("c2", n_override=4_000)
+    A, H0, alpha = d["A"], d["H0"], d["alpha"]
+    col = A.colidx.copy()
+    r = int(np.argmax(np.diff(A.rowptr) >= 3))
+    s0 = int(A.rowptr[r])
+    if defect == "unsorted":
+        col[s0], col[s0 + 1] = col[s0 + 1], col[s0]
+    elif defect == "duplicate":
+        col[s0 + 1] = col[s0]
+    else:
+        col[s0 + 2] = A.n
+    B = CsrMatrix(A.n, A.rowptr, col, A.val)
+    M = S.DeviceMatrix.from_host(B)
+    for mode, kw in (("exact", {}), ("lvs", dict(s=200, tau=1.0 / 200, seed=1))):
+        with pytest.raises(S.A.SymNMFError):
+            S.Solver(M, cu(H0), cu(H0), alpha, mode=mode, max_iters=1, **kw)
+    # the well-formed matrix is accepted
+    sv = S.Solver(S.DeviceMatrix.from_host(A), cu(H0), cu(H0), alpha, mode="exact", max_iters=1)
+    sv.close()

@@ -539,38 +539,6 @@ def test_csr_lvs_replayed_plan_vs_oracle(bucket, monkeypatch):
     assert rel(W.cpu().numpy(), Wr) < 1e-5
 
 
-# ------------------------------------------------------------------ persistent small-problem iteration
-@pytest.mark.parametrize("cfgname,n,k,s", [("c2", 100_000, 16, 2000), ("c1", 1000, 8, 200), ("c2", 20_000, 32, 400),
-                                           ("c2", 2_000, 8, 50)])
-def test_small_persistent_iteration_equals_multikernel(cfgname, n, k, s, monkeypatch):
-    """The one-launch-per-iteration LvS kernel (grid barriers between the steps) against the
-    multi-kernel graph path on the same inputs: identical sampling statistics in both halves
-    (plans are bit-identical given identical scores) and the same factors after one iteration
-    (later iterations may legitimately draw differently once fp32 summation order has moved a
-    score across a draw boundary, Z29)."""
-    from synth.configs import init_factor, mean_entry
-    d = make_input(cfgname, n_override=n if n != 1000 else None)
-    A = d["A"]
-    H0 = init_factor(n, k, mean_entry(A), np.random.default_rng(11))
-    tau = 1.0 / s
-    M = S.DeviceMatrix.from_host(A)
-    out = {}
-    for mode in ("always", "never"):
-        monkeypatch.setenv("SYMNMF_SMALL", mode)
-        W, H = cu(H0), cu(H0)
-        sv = S.Solver(M, W, H, d["alpha"], mode="lvs", s=s, tau=tau, seed=9, max_iters=1)
-        sv.run(1)
-        st = sv.stats()
-        assert st["status"] == 0
-        sv.close()
-        out[mode] = (W.cpu().numpy(), H.cpu().numpy(), st["halves"])
-    (W1, H1, h1), (W2, H2, h2) = out["always"], out["never"]
-    for a_, b_ in zip(h1, h2):
-        assert (a_["s_D"], a_["s_R"], a_["n_uniq"]) == (b_["s_D"], b_["s_R"], b_["n_uniq"])
-    assert rel(H1, H2) < 1e-5 and rel(W1, W2) < 1e-5
-
-
-# ------------------------------------------------------------------ LAI fused half (k = 64)
 @pytest.mark.parametrize("n,l", [(3000, 74), (2_049, 40)])
 def test_lai_fused_half_matches_oracle_and_four_kernel_path(n, l, monkeypatch):
     """LAI-SymNMF with k = 64: the fused launch per half (Y = U (Lambda U^T F) per tile, sweep,
