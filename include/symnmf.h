@@ -58,6 +58,9 @@ enum { SYMNMF_EXACT = 0, SYMNMF_LVS = 1, SYMNMF_LAI = 2 };  /* symnmf_iterate mo
 /* OR-ed into a mode: Update() by exact per-row NLS with block principal pivoting (ANLS-BPP,
  * P:155, App. G) instead of one HALS sweep (NEXT-1; k <= 32, else SYMNMF_ERR_UNSUPPORTED). */
 enum { SYMNMF_RULE_BPP = 16 };
+/* Solver mode flag (LvS): keep the scores and plan of every half in device memory for
+ * symnmf_solver_plan_history (costs ~20 n bytes per half; for parity tests, not for timing). */
+enum { SYMNMF_RECORD_PLANS = 32 };
 
 /* Symmetric n x n input A (Eq. 2.2).  The caller guarantees
  * A = A^T.  DENSE: val is n x lda fp32 (lda >= n, lda % 4 == 0 for 3XTF32).
@@ -307,6 +310,12 @@ symnmf_status symnmf_solver_profile(symnmf_solver* solver, int32_t iters, int32_
  * det_idx / draw_idx.  Returns SYMNMF_ERR_ARG for a non-LvS solver or a null pointer. */
 symnmf_status symnmf_solver_last_plan(const symnmf_solver* solver, float* lev_out, int32_t* uniq_idx_out,
                                       double* uniq_w_out, int64_t* counts_out, double* mass_out, cudaStream_t st);
+/* LvS solver created with SYMNMF_RECORD_PLANS: copy the scores and plan the solver drew in half
+ * `side` of iteration first_iter + t (same outputs as symnmf_solver_last_plan).  Returns
+ * SYMNMF_ERR_ARG if plans were not recorded or (t, side) has not run. */
+symnmf_status symnmf_solver_plan_history(const symnmf_solver* solver, int32_t t, int32_t side, float* lev_out,
+                                         int32_t* uniq_idx_out, double* uniq_w_out, int64_t* counts_out,
+                                         double* mass_out, cudaStream_t st);
 /* Kernel and memset node counts of the captured per-iteration graph (host only). */
 symnmf_status symnmf_solver_graph_nodes(const symnmf_solver* solver, int32_t* kernels_host, int32_t* memsets_host);
 

@@ -16,6 +16,7 @@ DENSE, CSR = 0, 1
 FP32, TF32X3 = 0, 1
 EXACT, LVS, LAI = 0, 1, 2
 RULE_BPP = 16
+RECORD_PLANS = 32
 
 # name -> (restype, argtypes); the authoritative list of exported entry points.
 P = C.c_void_p
@@ -69,6 +70,7 @@ SIGNATURES = {
     "symnmf_solve": (I32, [PM, I64, P, P, I32, F64, I32, I32, I64, F64, U64, P, P, I32, I32, F64, I32, I32,
                            C.POINTER(I32), C.POINTER(F64), P, PSZ, P]),
     "symnmf_solver_last_plan": (I32, [P, P, P, P, P, P, P]),
+    "symnmf_solver_plan_history": (I32, [P, I32, I32, P, P, P, P, P, P]),
     "symnmf_solver_graph_nodes": (I32, [P, C.POINTER(I32), C.POINTER(I32)]),
     "symnmf_solver_profile": (I32, [P, I32, I32, C.c_void_p, C.POINTER(C.c_float), C.POINTER(I32), P]),
 }

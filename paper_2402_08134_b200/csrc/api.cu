@@ -524,6 +524,25 @@ extern "C" symnmf_status symnmf_projected_gradient(const symnmf_matrix* A, const
 }
 
 // ---------------------------------------------------------------- (a14) solver
+// SYMNMF_RECORD_PLANS: copy this half's scores and plan into history slot 2 (it - first) + side.
+__global__ void record_plan(int64_t n, const float* __restrict__ lev, const int32_t* __restrict__ uniq,
+                            const double* __restrict__ w, const int64_t* __restrict__ counts,
+                            const double* __restrict__ mass, const int32_t* __restrict__ iter_dev, int32_t first_iter,
+                            int32_t max_iters, int side, int64_t cap, float* __restrict__ hlev,
+                            int32_t* __restrict__ huniq, double* __restrict__ hw, int64_t* __restrict__ hcounts,
+                            double* __restrict__ hmass, const int32_t* __restrict__ status) {
+  if (dev_failed(status)) return;
+  const int t = *iter_dev - first_iter;
+  if (t < 0 || t >= max_iters) return;
+  const size_t h = (size_t)2 * t + side;
+  const int64_t nu = counts[2];
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = i0; i < n; i += step) hlev[h * n + i] = lev[i];
+  for (int64_t i = i0; i < nu; i += step) { huniq[h * cap + i] = uniq[i]; hw[h * cap + i] = w[i]; }
+  if (i0 < 4) hcounts[h * 4 + i0] = counts[i0];
+  if (i0 < 2) hmass[h * 2 + i0] = mass[i0];
+}
+
 struct symnmf_solver {
   symnmf_matrix A;
   bool hasA;
@@ -559,6 +578,12 @@ struct symnmf_solver {
   bool tile;               // EXACT on a large CSR A (kpad(k) == k): product fused into the sweep
   int nblk;                // tile path: column blocks of A per product (tile.cu); cuts (nblk - 1) x n
   int64_t* cuts;
+  bool record;             // SYMNMF_RECORD_PLANS: per-half copies of the scores and plan
+  float* hlev;
+  int32_t* huniq;
+  double* hw;
+  int64_t* hcounts;
+  double* hmass;
   bool bucket;             // LvS on a large CSR A (kpad(k) == k): destination-bucketed sampled product
   BucketWs bk;
   float* Zt;               // bucket gather table Z[t] = omega_t f_{u_t} (cap x k)
@@ -693,6 +718,12 @@ void solver_layout(symnmf_solver& S, Carver& c) {
     S.plan.uniq_w = c.take<double>(n);
     S.plan.counts = c.take<int64_t>(4);
     S.plan.mass = c.take<double>(2);
+    const size_t halves = S.record ? (size_t)2 * S.max_iters : 0;
+    S.hlev = c.take<float>(halves * n);
+    S.huniq = c.take<int32_t>(halves * S.plan.cap);
+    S.hw = c.take<double>(halves * S.plan.cap);
+    S.hcounts = c.take<int64_t>(halves * 4);
+    S.hmass = c.take<double>(halves * 2);
     if (S.bucket) {
       bucket_layout(c, n, S.A.nnz, S.plan.cap, &S.bk);
       S.Zt = c.take<float>((size_t)S.plan.cap * k);
@@ -745,6 +776,10 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     mark(S, st, "samp_uniq_count");
     launch_samp_uniq_write(S.lev, n, S.T, S.sw, S.plan, status, st);
     mark(S, st, "samp_uniq_write");
+    if (S.record)
+      launch_pdl(record_plan, 148 * 4, 256, 0, st, n, S.lev, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts,
+                 S.plan.mass, S.iter_dev, S.first_iter, S.max_iters, side, S.plan.cap, S.hlev, S.huniq, S.hw,
+                 S.hcounts, S.hmass, status);
     // G_s and Y_s only read the plan: G_s runs on a second branch of the graph, concurrently
     cudaEventRecord(S.ev_fork[side], st);
     cudaStreamWaitEvent(S.side, S.ev_fork[side], 0);
@@ -820,7 +855,8 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
                                               int32_t with_residual, void* ws, size_t* ws_bytes, cudaStream_t st) {
   if (n < 1 || !W || !H || bad_k(k) || !(alpha >= 0.0) || max_iters < 1 || first_iter < 0) return SYMNMF_ERR_ARG;
   const bool bpp = (mode & SYMNMF_RULE_BPP) != 0;
-  mode &= ~SYMNMF_RULE_BPP;
+  const bool record = (mode & SYMNMF_RECORD_PLANS) != 0;
+  mode &= ~(SYMNMF_RULE_BPP | SYMNMF_RECORD_PLANS);
   if (mode != SYMNMF_EXACT && mode != SYMNMF_LVS && mode != SYMNMF_LAI) return SYMNMF_ERR_ARG;
   if (bpp && !bpp_supported(k)) return SYMNMF_ERR_UNSUPPORTED;
   if (precision != SYMNMF_FP32 && precision != SYMNMF_3XTF32) return SYMNMF_ERR_ARG;
@@ -833,6 +869,7 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
   S.hasA = A && !bad_matrix(A);
   if (S.hasA) S.A = *A;
   S.n = n; S.W = W; S.H = H; S.k = k; S.alpha = alpha; S.mode = mode; S.precision = precision; S.bpp = bpp;
+  S.record = record && mode == SYMNMF_LVS;
   S.s = mode == SYMNMF_LVS ? s : 0;
   S.T = tau * (double)k;   // reading Z1
   S.seed = seed; S.first_iter = first_iter; S.max_iters = max_iters;
@@ -1012,6 +1049,20 @@ extern "C" symnmf_status symnmf_solver_last_plan(const symnmf_solver* S, float* 
   SYMNMF_CUDA_TRY(cudaMemcpyAsync(uniq_w_out, S->plan.uniq_w, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   SYMNMF_CUDA_TRY(cudaMemcpyAsync(counts_out, S->plan.counts, sizeof(int64_t) * 4, cudaMemcpyDeviceToDevice, st));
   SYMNMF_CUDA_TRY(cudaMemcpyAsync(mass_out, S->plan.mass, sizeof(double) * 2, cudaMemcpyDeviceToDevice, st));
+  return SYMNMF_OK;
+}
+
+extern "C" symnmf_status symnmf_solver_plan_history(const symnmf_solver* S, int32_t t, int32_t side, float* lev_out,
+                                                    int32_t* uniq_idx_out, double* uniq_w_out, int64_t* counts_out,
+                                                    double* mass_out, cudaStream_t st) {
+  if (!S || !S->record || !lev_out || !uniq_idx_out || !uniq_w_out || !counts_out || !mass_out) return SYMNMF_ERR_ARG;
+  if (t < 0 || t >= std::min(S->iters_done, S->max_iters) || (side != 0 && side != 1)) return SYMNMF_ERR_ARG;
+  const size_t h = (size_t)2 * t + side, n = (size_t)S->n, cap = (size_t)S->plan.cap;
+  SYMNMF_CUDA_TRY(cudaMemcpyAsync(lev_out, S->hlev + h * n, sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
+  SYMNMF_CUDA_TRY(cudaMemcpyAsync(uniq_idx_out, S->huniq + h * cap, sizeof(int32_t) * cap, cudaMemcpyDeviceToDevice, st));
+  SYMNMF_CUDA_TRY(cudaMemcpyAsync(uniq_w_out, S->hw + h * cap, sizeof(double) * cap, cudaMemcpyDeviceToDevice, st));
+  SYMNMF_CUDA_TRY(cudaMemcpyAsync(counts_out, S->hcounts + h * 4, sizeof(int64_t) * 4, cudaMemcpyDeviceToDevice, st));
+  SYMNMF_CUDA_TRY(cudaMemcpyAsync(mass_out, S->hmass + h * 2, sizeof(double) * 2, cudaMemcpyDeviceToDevice, st));
   return SYMNMF_OK;
 }
 

@@ -297,14 +297,15 @@ class Solver:
     """Captured-graph iteration driver (symnmf_solver_*)."""
 
     def __init__(self, M, W, H, alpha, mode="exact", precision="fp32", s=0, tau=1.0, seed=0, first_iter=0,
-                 max_iters=1, U=None, lam=None, with_residual=False, rule="hals"):
+                 max_iters=1, U=None, lam=None, with_residual=False, rule="hals", record_plans=False):
         _cuda(W, torch.float32); _cuda(H, torch.float32)
         n, k = H.shape
         self.M, self.W, self.H, self.U, self.lam = M, W, H, U, lam
         self.max_iters = max_iters
         l = U.shape[1] if U is not None else 0
         mref = M.ref() if M is not None else None
-        pre = (mref, n, _p(W), _p(H), k, float(alpha), _MODE[mode] | _RULE[rule], _PREC[precision], int(s), float(tau),
+        flags = _MODE[mode] | _RULE[rule] | (A.RECORD_PLANS if record_plans else 0)
+        pre = (mref, n, _p(W), _p(H), k, float(alpha), flags, _PREC[precision], int(s), float(tau),
                int(seed), int(first_iter), int(max_iters), _p(U), _p(lam), l, 1 if with_residual else 0)
         fn = lib().symnmf_solver_create
         size = C.c_size_t(0)
@@ -345,6 +346,20 @@ class Solver:
         A.check("symnmf_solver_last_plan",
                 lib().symnmf_solver_last_plan(self.h, _p(lev), _p(plan.uniq_idx), _p(plan.uniq_w), _p(plan.counts),
                                               _p(plan.mass), _stream()))
+        return lev, plan
+
+    def plan_history(self, t: int, side: int):
+        """(scores, plan) the LvS solver drew in half `side` of its iteration t (created with
+        record_plans=True; symnmf_solver_plan_history)."""
+        n, dev = self.W.shape[0], self.W.device
+        lev = torch.empty(n, dtype=torch.float32, device=dev)
+        plan = SamplingPlan(torch.empty(0, dtype=torch.int32, device=dev), torch.empty(0, dtype=torch.int32, device=dev),
+                            torch.empty(n, dtype=torch.int32, device=dev), torch.empty(n, dtype=torch.float64, device=dev),
+                            torch.empty(4, dtype=torch.int64, device=dev), torch.empty(2, dtype=torch.float64, device=dev),
+                            n)
+        A.check("symnmf_solver_plan_history",
+                lib().symnmf_solver_plan_history(self.h, int(t), int(side), _p(lev), _p(plan.uniq_idx),
+                                                 _p(plan.uniq_w), _p(plan.counts), _p(plan.mass), _stream()))
         return lev, plan
 
     def stats(self):
