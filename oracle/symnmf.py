@@ -55,8 +55,18 @@ def gram(F):
 
 # ----------------------------------------------------------------------- O-9
 def ah(A, F):
-    """O-9: Y = A F, the product the paper replaces (P:181 'X H')."""
-    return as_f64(A) @ np.asarray(F, dtype=np.float64)
+    """O-9: Y = A F, the product the paper replaces (P:181 'X H').
+
+    A dense fp32 A is promoted to fp64 4096 rows at a time (each output row still uses its whole
+    row of A; only the memory footprint changes: c5's A would be 28.8 GB in fp64)."""
+    F = np.asarray(F, dtype=np.float64)
+    if hasattr(A, "rowptr") or sp.issparse(A) or np.asarray(A).dtype == np.float64:
+        return as_f64(A) @ F
+    n = A.shape[0]
+    out = np.empty((n, F.shape[1]))
+    for r0 in range(0, n, 4096):
+        out[r0:r0 + 4096] = np.asarray(A[r0:r0 + 4096], dtype=np.float64) @ F
+    return out
 
 
 # ----------------------------------------------------------------------- O-3
@@ -288,7 +298,7 @@ def iterate(A, W0, H0, alpha: float, iters: int, mode: str = "exact", s: int = 0
     or the exact per-row NLS solution (rule "bpp", NEXT-1).
     Returns (W, H, trace); trace lists per-half plan statistics.
     """
-    A64 = as_f64(A)
+    A64 = as_f64(A) if mode != "lai" else None      # LAI never touches A (P:419-423)
     W = np.array(W0, dtype=np.float64, copy=True)
     H = np.array(H0, dtype=np.float64, copy=True)
     k = H.shape[1]
@@ -361,14 +371,13 @@ def rangefinder(A, l: int, q: int, seed: int, Omega=None):
     U = Q V, ordered by |lambda| descending (reading Z17).
     Returns (U, lam, Q).
     """
-    A64 = as_f64(A)
-    n = A64.shape[0]
+    n = A.n if hasattr(A, "rowptr") else A.shape[0]
     Om = gaussian_omega(n, l, seed) if Omega is None else np.asarray(Omega)
-    Q = orth(A64 @ Om.astype(np.float64))
+    Q = orth(ah(A, Om.astype(np.float64)))
     for _ in range(q):
-        Q = orth(A64 @ Q)
-        Q = orth(A64 @ Q)
-    Z = A64 @ Q
+        Q = orth(ah(A, Q))
+        Q = orth(ah(A, Q))
+    Z = ah(A, Q)
     T = Q.T @ Z
     T = 0.5 * (T + T.T)
     lam, V = np.linalg.eigh(T)
@@ -442,6 +451,17 @@ def lai_apply(U, lam, F):
 # ----------------------------------------------------------------------- O-14
 def residual(A, H) -> float:
     """O-14: ||A - H H^T||_F / ||A||_F (Eq. 2.2; reading Z20), direct definition."""
+    if not (hasattr(A, "rowptr") or sp.issparse(A)):
+        # dense: rows promoted to fp64 block by block (a 60,000^2 fp32 A would be 28.8 GB in fp64)
+        H = np.asarray(H, dtype=np.float64)
+        n = H.shape[0]
+        num = a2 = 0.0
+        for r0 in range(0, n, 2048):
+            blk = np.asarray(A[r0:r0 + 2048], dtype=np.float64)
+            D = blk - H[r0:r0 + 2048] @ H.T
+            num += float((D * D).sum())
+            a2 += float((blk * blk).sum())
+        return math.sqrt(num) / math.sqrt(a2)
     A64 = as_f64(A)
     H = np.asarray(H, dtype=np.float64)
     n = H.shape[0]
