@@ -615,6 +615,13 @@ struct symnmf_solver {
 
 namespace {
 
+// The streaming sweep (sweep.cu) for k in {8, 16, 32}; SYMNMF_SWEEP=fused selects the register-tile
+// sweep_fused instead (symnmf.h)
+bool sweep_stream_enabled() {
+  const char* e = getenv("SYMNMF_SWEEP");
+  return !(e && !strcmp(e, "fused"));
+}
+
 // Update(G + alpha I, Y + alpha F^T): one HALS sweep with the next half's Gram (and R) fused, or
 // (rule BPP) the exact per-row NLS followed by the Gram of the new factor.
 void enqueue_sweep(const symnmf_solver& S, const double* G, const float* F, float* X, bool zeroY, double* Gnext,
@@ -624,7 +631,10 @@ void enqueue_sweep(const symnmf_solver& S, const double* G, const float* F, floa
     launch_gram_fused(X, S.n, S.k, S.Gacc, Gnext, Rf32, S.counter, status, st);
     return;
   }
-  launch_sweep_fused(G, S.alpha, S.Y, F, X, S.n, S.k, zeroY, S.Gacc, Gnext, Rf32, S.counter, status, st);
+  if (sweep_stream_supported(S.k) && sweep_stream_enabled())
+    launch_sweep_stream(G, S.alpha, S.Y, F, X, S.n, S.k, zeroY, S.Gacc, Gnext, Rf32, S.counter, status, st);
+  else
+    launch_sweep_fused(G, S.alpha, S.Y, F, X, S.n, S.k, zeroY, S.Gacc, Gnext, Rf32, S.counter, status, st);
 }
 
 // LAI: the fused one-launch half (k = 64, l <= 80); SYMNMF_LAI_FUSED=never disables it (symnmf.h)
@@ -648,6 +658,13 @@ int64_t bucket_min_nnz() {
   if (e && !strcmp(e, "always")) return 0;
   if (e && !strcmp(e, "never")) return INT64_MAX;
   return 16ll << 20;
+}
+
+// LvS bucket path: the sampled product pulled into Y then the streaming sweep (default), or
+// (SYMNMF_BUCKET_FUSED=1) pulled inside the row-tile sweep kernel (tile.cu)
+bool bucket_fused() {
+  const char* e = getenv("SYMNMF_BUCKET_FUSED");
+  return e && !strcmp(e, "1");
 }
 
 // EXACT CSR tile path: column blocks so each pass's rows of F (n / nblk x 4k bytes) stay L2
@@ -695,7 +712,7 @@ void solver_layout(symnmf_solver& S, Carver& c) {
   S.bucket = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode == SYMNMF_LVS && !S.bpp &&
              S.A.nnz < (int64_t)INT32_MAX && S.A.nnz >= bucket_min_nnz();
   S.nonconv = c.take<int32_t>(1);
-  S.Y = c.take<float>((S.tile && S.nblk == 1) || S.bucket ? 0 : (size_t)n * k);
+  S.Y = c.take<float>((S.tile && S.nblk == 1) || (S.bucket && bucket_fused()) ? 0 : (size_t)n * k);
   S.stats = c.take<symnmf_half_stats>((size_t)2 * S.max_iters);
   S.resid = c.take<double>((size_t)S.max_iters);
   S.rgrid = residual_grid(n);
@@ -790,8 +807,16 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
       launch_bucket_build(S.A, S.plan.uniq_idx, S.plan.counts + 2, S.bk, S.counter + 1, status, st);
       mark(S, st, "bucket_build");
       cudaStreamWaitEvent(st, S.ev_join[side], 0);
-      launch_bucket_tile_sweep(S.bk, S.Zt, F, S.Gs, S.alpha, X, n, k, S.Gacc, Gnext, S.Rinv32, S.counter, status, st);
-      mark(S, st, "bucket_sweep");
+      if (bucket_fused()) {
+        launch_bucket_tile_sweep(S.bk, S.Zt, F, S.Gs, S.alpha, X, n, k, S.Gacc, Gnext, S.Rinv32, S.counter, status,
+                                 st);
+        mark(S, st, "bucket_sweep");
+        return true;
+      }
+      launch_bucket_pull(S.bk, S.Zt, n, k, S.Y, status, st);
+      mark(S, st, "bucket_pull");
+      enqueue_sweep(S, S.Gs, F, X, false, Gnext, S.Rinv32, status, st);
+      mark(S, st, "hals_sweep");
       return true;
     }
     if (S.A.kind == SYMNMF_CSR) {

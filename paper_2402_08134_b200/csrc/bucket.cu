@@ -4,7 +4,7 @@
 // consumes Y_s can pull each destination row's terms from one contiguous bucket and Y_s never
 // exists in HBM.  Steps (all on the solver's stream, after the plan):
 //
-//   plan_row_offsets  pre[t] = sum_{t' < t} nnz(u_t') over the plan's unique rows (one CTA), and
+//   plan_row_*        pre[t] = sum_{t' < t} nnz(u_t') over the plan's unique rows (two passes), and
 //                     rb[t] = rowptr[u_t] - pre[t], so entry j of the concatenated sampled rows is
 //                     nonzero e = rb[t] + j of A for the t with pre[t] <= j < pre[t+1].
 //   bucket_count      slot[e] = atomicAdd(&cnt[col[e]], 1) for every sampled nonzero e: the count
@@ -13,7 +13,8 @@
 //   bucket_scan_*     off = exclusive scan of cnt (two passes: tile sums + last-CTA scan of the
 //                     tile sums, then the tiles), cnt re-zeroed for the next plan.
 //   bucket_fill       ent[off[c] + slot[e]] = (t, a_e): the bucket entries.
-//   (tile sweep)      fused.cu: tile_sweep over (off, ent) with the gather table Z[t] = omega_t f_u_t.
+//   bucket_pull       Y_s[r] = sum over bucket r of a_e Z[t_e], Z[t] = omega_t f_{u_t} (the sampled
+//                     Gram kernel writes Z); or, fused, the row-tile sweep of tile.cu reads the buckets.
 //
 // The order of the entries inside a bucket follows the atomics (run to run it may differ), so the
 // fp32 sum of a bucket is compared by tolerance, like every other GPU product sum (reading Z29).
@@ -24,47 +25,81 @@ namespace symnmf {
 constexpr int kBucketChunk = 1024;   // sampled nonzeros per warp chunk (32 per lane)
 constexpr int kBucketUnroll = 4;     // independent entries in flight per lane
 
-// ---------------------------------------------------------------- plan_row_offsets (1 CTA)
-__global__ void __launch_bounds__(1024) plan_row_offsets(const int64_t* __restrict__ rowptr,
-                                                         const int32_t* __restrict__ uniq,
-                                                         const int64_t* __restrict__ n_uniq_dev,
-                                                         int64_t* __restrict__ pre, int64_t* __restrict__ rb,
-                                                         const int32_t* __restrict__ status) {
+// ---------------------------------------------------------------- plan_row_offsets (two passes)
+constexpr int kPlanTile = 1024;   // plan rows per CTA (256 threads x 4)
+
+__device__ __forceinline__ void plan_row_lens(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ uniq,
+                                              int64_t nu, int64_t t0, int64_t (&start)[4], int64_t (&len)[4]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int64_t t = t0 + q;
+    if (t < nu) {
+      const int64_t u = uniq[t];
+      start[q] = rowptr[u];
+      len[q] = rowptr[u + 1] - start[q];
+    } else {
+      start[q] = 0;
+      len[q] = 0;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) plan_row_sums(const int64_t* __restrict__ rowptr,
+                                                     const int32_t* __restrict__ uniq,
+                                                     const int64_t* __restrict__ n_uniq_dev,
+                                                     int64_t* __restrict__ tsum, int64_t* __restrict__ pre,
+                                                     unsigned int* counter, const int32_t* __restrict__ status) {
+  __shared__ int64_t sh[33];
+  __shared__ bool last;
+  if (dev_failed(status)) return;
+  const int64_t nu = *n_uniq_dev;
+  const int64_t nt = (nu + kPlanTile - 1) / kPlanTile;
+  if ((int64_t)blockIdx.x < nt) {
+    int64_t start[4], len[4];
+    plan_row_lens(rowptr, uniq, nu, (int64_t)blockIdx.x * kPlanTile + threadIdx.x * 4, start, len);
+    const int64_t s = block_sum(len[0] + len[1] + len[2] + len[3], sh);
+    if (threadIdx.x == 0) tsum[blockIdx.x] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) *counter = 0;
+  int64_t run = 0;
+  for (int64_t base = 0; base < nt; base += 256) {
+    const int64_t i = base + threadIdx.x;
+    const int64_t v = i < nt ? __ldcg(tsum + i) : 0;
+    int64_t tot;
+    const int64_t e = block_excl_scan(v, sh, &tot);
+    if (i < nt) tsum[i] = run + e;
+    run += tot;
+  }
+  if (threadIdx.x == 0) pre[nu] = run;
+}
+
+__global__ void __launch_bounds__(256) plan_row_write(const int64_t* __restrict__ rowptr,
+                                                      const int32_t* __restrict__ uniq,
+                                                      const int64_t* __restrict__ n_uniq_dev,
+                                                      const int64_t* __restrict__ tsum, int64_t* __restrict__ pre,
+                                                      int64_t* __restrict__ rb, const int32_t* __restrict__ status) {
   __shared__ int64_t sh[33];
   if (dev_failed(status)) return;
   const int64_t nu = *n_uniq_dev;
-  constexpr int PER = 8;
-  int64_t run = 0;
-  for (int64_t base = 0; base < nu; base += 1024 * PER) {
-    int64_t len[PER], start[PER];
-    int64_t tot = 0;
+  if ((int64_t)blockIdx.x * kPlanTile >= nu) return;
+  const int64_t t0 = (int64_t)blockIdx.x * kPlanTile + threadIdx.x * 4;
+  int64_t start[4], len[4];
+  plan_row_lens(rowptr, uniq, nu, t0, start, len);
+  int64_t p = block_excl_scan(len[0] + len[1] + len[2] + len[3], sh, (int64_t*)nullptr) + tsum[blockIdx.x];
 #pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int64_t t = base + (int64_t)threadIdx.x * PER + q;
-      if (t < nu) {
-        const int64_t u = uniq[t];
-        start[q] = rowptr[u];
-        len[q] = rowptr[u + 1] - start[q];
-      } else {
-        start[q] = 0;
-        len[q] = 0;
-      }
-      tot += len[q];
+  for (int q = 0; q < 4; ++q) {
+    if (t0 + q < nu) {
+      pre[t0 + q] = p;
+      rb[t0 + q] = start[q] - p;
     }
-    int64_t chunk_tot;
-    int64_t p = run + block_excl_scan(tot, sh, &chunk_tot);
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int64_t t = base + (int64_t)threadIdx.x * PER + q;
-      if (t < nu) {
-        pre[t] = p;
-        rb[t] = start[q] - p;
-      }
-      p += len[q];
-    }
-    run += chunk_tot;
+    p += len[q];
   }
-  if (threadIdx.x == 0) pre[nu] = run;
 }
 
 // Largest t in [lo, hi] with pre[t] <= j (pre non-decreasing, pre[lo] <= j).
@@ -241,6 +276,60 @@ __global__ void __launch_bounds__(256) bucket_fill(const int32_t* __restrict__ c
   });
 }
 
+// ---------------------------------------------------------------- bucket_pull
+// Y_s[r] = sum over bucket r of a_e Z[t_e] (Z[t] = omega_t f_{u_t}): one group of KP / 4 lanes per
+// destination row, float4 gathers of Z (|U| x 4k bytes, L2 resident), each row written once.
+template <int KP>
+__global__ void __launch_bounds__(256) bucket_pull(const int32_t* __restrict__ off, const int2* __restrict__ ent,
+                                                   const float4* __restrict__ Z, int64_t n, float4* __restrict__ Y,
+                                                   const int32_t* __restrict__ status) {
+  if (dev_failed(status)) return;
+  constexpr int LPR = KP / 4;
+  const int li = threadIdx.x % LPR;
+  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / LPR;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPR; r < n; r += ng) {
+    const int32_t e0 = __ldg(off + r), e1 = __ldg(off + r + 1);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int32_t e = e0;
+    for (; e + 4 <= e1; e += 4) {
+      int2 en[4];
+      float4 z[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) en[u] = __ldcs(ent + e + u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) z[u] = __ldg(Z + (int64_t)en[u].x * LPR + li);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float a = __int_as_float(en[u].y);
+        acc.x = fmaf(a, z[u].x, acc.x); acc.y = fmaf(a, z[u].y, acc.y);
+        acc.z = fmaf(a, z[u].z, acc.z); acc.w = fmaf(a, z[u].w, acc.w);
+      }
+    }
+    for (; e < e1; ++e) {
+      const int2 en = __ldcs(ent + e);
+      const float4 z = __ldg(Z + (int64_t)en.x * LPR + li);
+      const float a = __int_as_float(en.y);
+      acc.x = fmaf(a, z.x, acc.x); acc.y = fmaf(a, z.y, acc.y);
+      acc.z = fmaf(a, z.z, acc.z); acc.w = fmaf(a, z.w, acc.w);
+    }
+    Y[r * LPR + li] = acc;
+  }
+}
+
+void launch_bucket_pull(const BucketWs& b, const float* Z, int64_t n, int k, float* Y, const int32_t* status,
+                        cudaStream_t st) {
+  const int64_t thr = n * (k / 4);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((thr + 255) / 256, 148 * 8));
+  const float4* Z4 = reinterpret_cast<const float4*>(Z);
+  float4* Y4 = reinterpret_cast<float4*>(Y);
+  switch (k) {
+    case 8: launch_pdl(bucket_pull<8>, grid, 256, 0, st, b.off, b.ent, Z4, n, Y4, status); break;
+    case 16: launch_pdl(bucket_pull<16>, grid, 256, 0, st, b.off, b.ent, Z4, n, Y4, status); break;
+    case 32: launch_pdl(bucket_pull<32>, grid, 256, 0, st, b.off, b.ent, Z4, n, Y4, status); break;
+    default: launch_pdl(bucket_pull<64>, grid, 256, 0, st, b.off, b.ent, Z4, n, Y4, status); break;
+  }
+}
+
 // ---------------------------------------------------------------- launchers
 size_t bucket_ws_bytes(int64_t n, int64_t nnz, int64_t cap) {
   // pre, rb [cap + 1] int64; cnt, off [n + 1] int32; tsum; slot [nnz] int32; ent [nnz] int2
@@ -250,6 +339,8 @@ size_t bucket_ws_bytes(int64_t n, int64_t nnz, int64_t cap) {
 }
 
 void bucket_layout(Carver& c, int64_t n, int64_t nnz, int64_t cap, BucketWs* b) {
+  b->cap = cap;
+  b->ptsum = c.take<int64_t>((size_t)(cap + kPlanTile - 1) / kPlanTile + 4);
   b->pre = c.take<int64_t>((size_t)cap + 1);
   b->rb = c.take<int64_t>((size_t)cap + 1);
   b->cnt = c.take<int32_t>((size_t)n + 4);
@@ -267,7 +358,9 @@ static int bucket_grid(int64_t cap_entries) {
 void launch_bucket_build(const symnmf_matrix& A, const int32_t* uniq, const int64_t* n_uniq_dev, const BucketWs& b,
                          unsigned int* counter, int32_t* status, cudaStream_t st) {
   const int64_t n = A.n;
-  launch_pdl(plan_row_offsets, 1, 1024, 0, st, A.rowptr, uniq, n_uniq_dev, b.pre, b.rb, status);
+  const int ptiles = (int)std::max<int64_t>(1, (b.cap + kPlanTile - 1) / kPlanTile);
+  launch_pdl(plan_row_sums, ptiles, 256, 0, st, A.rowptr, uniq, n_uniq_dev, b.ptsum, b.pre, counter, status);
+  launch_pdl(plan_row_write, ptiles, 256, 0, st, A.rowptr, uniq, n_uniq_dev, b.ptsum, b.pre, b.rb, status);
   const int grid = bucket_grid(A.nnz);
   launch_pdl(bucket_count, grid, 256, 0, st, A.colidx, b.pre, b.rb, n_uniq_dev, b.cnt, b.slot, status);
   const int tiles = (int)bucket_scan_tiles(n);

@@ -118,15 +118,6 @@ constexpr int SDC = 128;    // output rows per CTA
 constexpr int SDS = 4;      // pipeline stages
 constexpr int SDUMAX = 2048;   // U entries per CTA (indices + weights in shared memory)
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool ok) {
-  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
-  const int sz = ok ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(sz) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
 template <int KP, int JB, int SDU>   // SDU sampled rows per stage
 struct SdSmem {
   static constexpr size_t a = 0;                                              // float [SDS][SDU][SDC]

@@ -112,10 +112,19 @@ void launch_sampled_csr_nozero(const symnmf_matrix& A, const float* F, int k, co
                                const int64_t* n_uniq_dev, int64_t cap, float* Y, const int32_t* status,
                                cudaStream_t st);
 
+// ---------------------------------------------------------------- sweep.cu
+// Streaming HALS sweep (k in {8, 16, 32}): cp.async-staged tiles, thread per row, fused Gram + Cholesky.
+bool sweep_stream_supported(int k);
+void launch_sweep_stream(const double* G, double alpha, float* Y, const float* F, float* X, int64_t n, int k,
+                         bool zeroY, double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
+                         cudaStream_t st);
+
 // ---------------------------------------------------------------- bucket.cu / tile.cu (sparse A)
 // Destination buckets of the sampled CSR product (bucket.cu): per plan, the sampled rows'
 // nonzeros counting-sorted by column.  cnt is kept zero between plans.
 struct BucketWs {
+  int64_t cap;       // plan capacity
+  int64_t* ptsum;    // plan-row scan tile sums
   int64_t* pre;      // [cap + 1] exclusive prefix of the plan rows' nnz
   int64_t* rb;       // [cap + 1] rowptr[u_t] - pre[t]
   int32_t* cnt;      // [n] bucket sizes (zero between plans)
@@ -127,6 +136,9 @@ struct BucketWs {
 void bucket_layout(Carver& c, int64_t n, int64_t nnz, int64_t cap, BucketWs* b);
 void launch_bucket_build(const symnmf_matrix& A, const int32_t* uniq, const int64_t* n_uniq_dev, const BucketWs& b,
                          unsigned int* counter, int32_t* status, cudaStream_t st);
+// Y_s (n x k, every row written) from the buckets with the gather table Z; kpad(k) == k.
+void launch_bucket_pull(const BucketWs& b, const float* Z, int64_t n, int k, float* Y, const int32_t* status,
+                        cudaStream_t st);
 // Sampled product from the buckets (gather table Z[t] = omega_t f_{u_t}, k floats per row) fused
 // with the sweep, X^T X and (Rf32 non-null) its Cholesky factor.  kpad(k) == k.
 void launch_bucket_tile_sweep(const BucketWs& b, const float* Z, const float* F, const double* G, double alpha,

@@ -1,0 +1,205 @@
+// (a11) The HALS sweep Update(G + alpha I, Y + alpha F^T) (Eq. 2.6; App. G)
+// as a streaming kernel, fused with the Gram of the updated factor (the next half's F^T F, P:420 /
+// P:690) and, in the last CTA, its Cholesky factor (CholeskyQR).
+//
+// sweep_stream<KP>: persistent CTAs of 256 threads, one 256-row tile per step, thread r owning row r.
+// The tile's rows of Y, F and X are brought into shared memory with cp.async (16 B chunks, coalesced,
+// in flight while the previous tile computes), stored with a 16 B-chunk XOR swizzle so that a thread
+// reading its own row is bank-conflict free; b = y + alpha f and x are then held in registers, the
+// Gauss-Seidel pass over the k columns runs on them with G (+alpha I) broadcast from shared memory,
+// and the new row goes through a swizzled output tile for coalesced stores and the tile Gram.
+// Bytes per row: Y, F, X read, X written (+ Y re-zeroed for the scatter paths): 16k (20k) B.
+#include "fused_common.cuh"
+
+namespace symnmf {
+
+template <int KP>
+struct SwL {
+  static constexpr int C = KP / 4;              // 16 B chunks per row
+  static constexpr int TR = 256;                // rows per tile = threads
+  static constexpr size_t arr = sizeof(float) * TR * KP;
+  static constexpr size_t y = 0, f = arr, x = 2 * arr, o = 3 * arr, gram = 4 * arr;
+  static constexpr size_t bytes = gram + sizeof(double) * TR * 16;
+  static constexpr int per_sm = bytes <= 70 * 1024 ? 3 : bytes <= 110 * 1024 ? 2 : 1;
+};
+
+// chunk c of row r lives at chunk position swz(c, r): the 8 rows a quarter-warp reads hit 8
+// distinct 16 B bank groups (rows are KP * 4 B; 128 B hold 8 / C rows)
+template <int KP>
+__device__ __forceinline__ int swz(int c, int r) {
+  constexpr int C = KP / 4, RPL = 8 / C;   // rows per 128 B line
+  return c ^ ((r / RPL) % C);
+}
+
+template <int KP>
+__global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
+    const double* __restrict__ G, double alpha, float* __restrict__ Y, const float* __restrict__ F,
+    float* __restrict__ X, int64_t n, int zeroY, double* Gacc, double* Gout, float* Rf32, unsigned int* counter,
+    int32_t* status) {
+  using L = SwL<KP>;
+  constexpr int C = L::C, TR = L::TR;
+  constexpr int NB = KP / 4, PAIRS = NB * (NB + 1) / 2, RG = TR / PAIRS;
+  __shared__ __align__(16) float sG[KP * KP];     // sG[i*KP + j] = G[j][i], 0 on the diagonal
+  __shared__ float sInv[KP];
+  __shared__ int sOk[KP];
+  extern __shared__ __align__(16) unsigned char sms[];
+  float* sY = reinterpret_cast<float*>(sms + L::y);
+  float* sF = reinterpret_cast<float*>(sms + L::f);
+  float* sX = reinterpret_cast<float*>(sms + L::x);
+  float* sO = reinterpret_cast<float*>(sms + L::o);
+  double* gslot = reinterpret_cast<double*>(sms + L::gram);
+  if (dev_failed(status)) return;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < KP * KP; e += TR) {
+    const int i = e / KP, j = e - i * KP;
+    sG[e] = (i != j) ? (float)G[j * KP + i] : 0.f;
+  }
+  for (int i = tid; i < KP; i += TR) {
+    const double den = G[i * KP + i] + alpha;
+    sOk[i] = den > 0.0;
+    sInv[i] = den > 0.0 ? (float)(1.0 / den) : 0.f;
+  }
+#pragma unroll
+  for (int e = 0; e < 16; ++e) gslot[tid * 16 + e] = 0.0;
+  // Gram role of this thread: upper 4x4 block (ai, bi) over row group g
+  const int gg = tid / PAIRS, gp = tid - gg * PAIRS;
+  int ai = 0, bi = 0;
+  {
+    int a = 0, rem = gp;
+    while (rem >= NB - a) { rem -= NB - a; ++a; }
+    ai = a; bi = a + rem;
+  }
+  const bool gactive = gg < RG;
+  const float a32 = (float)alpha;
+  const int64_t tiles = (n + TR - 1) / TR;
+
+  auto issue = [&](int64_t t) {
+    const int64_t r0 = t * TR;
+    const int rows = (int)min64(TR, n - r0);
+    for (int q = tid; q < TR * C; q += TR) {
+      const int r = q / C, c = q - r * C;
+      const bool ok = r < rows;
+      const int so = r * KP + 4 * swz<KP>(c, r);
+      const int64_t go = ok ? (r0 + r) * KP + 4 * c : 0;
+      cp_async16(sY + so, Y + go, ok);
+      cp_async16(sF + so, F + go, ok);
+      cp_async16(sX + so, X + go, ok);
+    }
+    cp_async_commit();
+  };
+
+  int64_t t = blockIdx.x;
+  if (t < tiles) issue(t);
+  for (; t < tiles; t += gridDim.x) {
+    const int64_t r0 = t * TR;
+    const int rows = (int)min64(TR, n - r0);
+    cp_async_wait<0>();
+    __syncthreads();
+    float b[KP], x[KP];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int so = tid * KP + 4 * swz<KP>(c, tid);
+      const float4 y4 = *reinterpret_cast<const float4*>(sY + so);
+      const float4 f4 = *reinterpret_cast<const float4*>(sF + so);
+      const float4 x4 = *reinterpret_cast<const float4*>(sX + so);
+      b[4 * c] = fmaf(a32, f4.x, y4.x); b[4 * c + 1] = fmaf(a32, f4.y, y4.y);
+      b[4 * c + 2] = fmaf(a32, f4.z, y4.z); b[4 * c + 3] = fmaf(a32, f4.w, y4.w);
+      x[4 * c] = x4.x; x[4 * c + 1] = x4.y; x[4 * c + 2] = x4.z; x[4 * c + 3] = x4.w;
+    }
+    __syncthreads();                                   // staging buffers of tile t consumed
+    if (t + gridDim.x < tiles) issue(t + gridDim.x);   // tile t + grid streams in while t computes
+    if (zeroY) {
+      float4* Y4 = reinterpret_cast<float4*>(Y) + r0 * C;
+      for (int q = tid; q < rows * C; q += TR) __stcs(Y4 + q, make_float4(0.f, 0.f, 0.f, 0.f));
+    }
+    // Gauss-Seidel over the columns of row tid: x_i <- [(b_i - sum_{j != i} G_ij x_j) / (G_ii + alpha)]_+
+#pragma unroll
+    for (int i = 0; i < KP; ++i) {
+      float s0 = b[i], s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+      for (int j = 0; j < KP; j += 4) {
+        const float4 g = *reinterpret_cast<const float4*>(sG + i * KP + j);
+        s0 = fmaf(-x[j], g.x, s0);
+        s1 = fmaf(-x[j + 1], g.y, s1);
+        s2 = fmaf(-x[j + 2], g.z, s2);
+        s3 = fmaf(-x[j + 3], g.w, s3);
+      }
+      const float sv = (s0 + s1) + (s2 + s3);
+      if (sOk[i]) x[i] = fmaxf(0.f, sv * sInv[i]);
+    }
+    const bool live = tid < rows;
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      *reinterpret_cast<float4*>(sO + tid * KP + 4 * swz<KP>(c, tid)) =
+          live ? make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    {
+      float4* X4 = reinterpret_cast<float4*>(X) + r0 * C;
+      for (int q = tid; q < rows * C; q += TR) {
+        const int r = q / C, c = q - r * C;
+        X4[q] = *reinterpret_cast<const float4*>(sO + r * KP + 4 * swz<KP>(c, r));
+      }
+    }
+    if (Gacc && gactive) {   // tile Gram of the new rows: fp32 over the tile, fp64 slot per thread
+      float acc[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+      for (int r = gg; r < rows; r += RG) {
+        const float4 a4 = *reinterpret_cast<const float4*>(sO + r * KP + 4 * swz<KP>(ai, r));
+        const float4 b4 = *reinterpret_cast<const float4*>(sO + r * KP + 4 * swz<KP>(bi, r));
+        const float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i * 4 + j] = fmaf(av[i], bv[j], acc[i * 4 + j]);
+      }
+#pragma unroll
+      for (int e = 0; e < 16; ++e) gslot[tid * 16 + e] += (double)acc[e];
+    }
+  }
+  cp_async_wait<0>();
+  if (!Gacc) return;
+  // commit: the row groups' slots summed in fixed order, one fp64 red.add per entry into a replica
+  __syncthreads();
+  double* rep = Gacc + (size_t)(blockIdx.x % kGramReplicas) * KP * KP;
+  for (int idx = tid; idx < PAIRS * 16; idx += TR) {
+    const int pp = idx >> 4, e = idx & 15;
+    double sum = 0.0;
+    for (int g2 = 0; g2 < RG; ++g2) sum += gslot[(size_t)(g2 * PAIRS + pp) * 16 + e];
+    int a0 = 0, rem = pp;
+    while (rem >= NB - a0) { rem -= NB - a0; ++a0; }
+    const int a = 4 * a0 + (e >> 2), bb = 4 * (a0 + rem) + (e & 3);
+    if (a <= bb && sum != 0.0) atomicAdd(rep + a * KP + bb, sum);
+  }
+  if (arrive_last(counter)) {
+    double* sa = reinterpret_cast<double*>(sms);
+    finalize_gram<KP>(Gacc, Gout, KP, Rf32, sa, sa + KP * (KP + 1), status);
+  }
+}
+
+template <int KP>
+static void sweep_stream_t(const double* G, double alpha, float* Y, const float* F, float* X, int64_t n, bool zeroY,
+                           double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
+                           cudaStream_t st) {
+  using L = SwL<KP>;
+  const size_t smem = std::max(L::bytes, sizeof(double) * 2 * KP * (KP + 1));
+  const int64_t tiles = (n + L::TR - 1) / L::TR;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * L::per_sm));
+  cudaFuncSetAttribute(sweep_stream<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  launch_pdl(sweep_stream<KP>, grid, L::TR, smem, st, G, alpha, Y, F, X, n, zeroY ? 1 : 0, Gacc, Gout, Rf32, counter,
+             status);
+}
+
+bool sweep_stream_supported(int k) { return k == 8 || k == 16 || k == 32; }
+
+void launch_sweep_stream(const double* G, double alpha, float* Y, const float* F, float* X, int64_t n, int k,
+                         bool zeroY, double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
+                         cudaStream_t st) {
+  switch (k) {
+    case 8: sweep_stream_t<8>(G, alpha, Y, F, X, n, zeroY, Gacc, Gout, Rf32, counter, status, st); break;
+    case 16: sweep_stream_t<16>(G, alpha, Y, F, X, n, zeroY, Gacc, Gout, Rf32, counter, status, st); break;
+    default: sweep_stream_t<32>(G, alpha, Y, F, X, n, zeroY, Gacc, Gout, Rf32, counter, status, st); break;
+  }
+}
+
+}  // namespace symnmf
