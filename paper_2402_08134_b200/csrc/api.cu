@@ -576,6 +576,9 @@ struct symnmf_solver {
   bool bpp;                // Update rule: exact per-row NLS by block principal pivoting (NEXT-1)
   int32_t* nonconv;        // BPP rows that hit the pivoting cap (device counter)
   bool tile;               // EXACT on a large CSR A (kpad(k) == k): product fused into the sweep
+  bool nnzsp;              // EXACT on CSR (kpad(k) == k): the nnz-balanced SpMM (spmm_nnz.cu)
+  int64_t* chunk_row;
+  float* carry;
   int nblk;                // tile path: column blocks of A per product (tile.cu); cuts (nblk - 1) x n
   int64_t* cuts;
   bool record;             // SYMNMF_RECORD_PLANS: per-half copies of the scores and plan
@@ -643,12 +646,16 @@ bool lai_enabled() {
   return !(e && !strcmp(e, "never"));
 }
 
-// EXACT CSR: the tile kernel from 16M nonzeros; SYMNMF_CSR_TILE=always|never overrides (symnmf.h)
+// EXACT CSR: the product fused with the sweep in row tiles only on request (SYMNMF_CSR_TILE=always,
+// symnmf.h); by default the nnz-balanced SpMM + streaming sweep (SYMNMF_CSR_SPMM=rows: row groups)
 int64_t tile_min_nnz() {
   const char* e = getenv("SYMNMF_CSR_TILE");
   if (e && !strcmp(e, "always")) return 0;
-  if (e && !strcmp(e, "never")) return INT64_MAX;
-  return 16ll << 20;
+  return INT64_MAX;
+}
+bool csr_spmm_nnz() {
+  const char* e = getenv("SYMNMF_CSR_SPMM");
+  return !(e && !strcmp(e, "rows"));
 }
 
 // LvS CSR: the destination-bucketed sampled product fused into the sweep from 16M nonzeros;
@@ -707,6 +714,9 @@ void solver_layout(symnmf_solver& S, Carver& c) {
   // the tile kernel balances hub rows; on small graphs the row-per-group SpMM + sweep is faster
   S.tile = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode == SYMNMF_EXACT && !S.bpp &&
            S.A.nnz >= tile_min_nnz();
+  S.nnzsp = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode == SYMNMF_EXACT && !S.tile && csr_spmm_nnz();
+  S.chunk_row = c.take<int64_t>(S.nnzsp ? (size_t)spmm_nnz_chunks(S.A.nnz) : 0);
+  S.carry = c.take<float>(S.nnzsp ? spmm_nnz_carry_floats(S.A.nnz, k) : 0);
   S.nblk = S.tile ? csr_blocks(n, k) : 1;
   S.cuts = c.take<int64_t>(S.tile ? (size_t)(S.nblk - 1) * n : 0);
   S.bucket = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode == SYMNMF_LVS && !S.bpp &&
@@ -775,6 +785,11 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     launch_csr_tile_passes(S.A, S.nblk, S.cuts, S.Y, F, Gf, S.alpha, X, n, k, S.Gacc, Gnext, nullptr, S.counter,
                            status, st);
     mark(S, st, "csr_tile_exact");
+  } else if (S.mode == SYMNMF_EXACT && S.nnzsp) {
+    launch_spmm_nnz(S.A, S.chunk_row, F, k, S.Y, S.carry, status, st);
+    mark(S, st, "spmm_csr");
+    enqueue_sweep(S, Gf, F, X, false, Gnext, nullptr, status, st);
+    mark(S, st, S.bpp ? "bpp_update" : "hals_sweep");
   } else if (S.mode == SYMNMF_EXACT) {
     if (!enqueue_product(S.A, F, k, S.Y, S.precision, S.tcs, S.tcs_bytes, status, st)) return false;
     mark(S, st, S.A.kind == SYMNMF_CSR ? "spmm_csr" : (S.precision == SYMNMF_3XTF32 ? "gemm_3xtf32" : "gemm_fp32"));
@@ -940,6 +955,7 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
     SYMNMF_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int32_t), st));
     if (hbad) return SYMNMF_ERR_ARG;
   }
+  if (S.nnzsp) launch_spmm_nnz_rows(S.A, S.chunk_row, st);
   set_i32<<<1, 1, 0, st>>>(S.iter_dev, first_iter);
   // H^T H (and its CholeskyQR factor for LvS) for the first W-half; later halves get
   // theirs from the fused Gram of the preceding sweep.

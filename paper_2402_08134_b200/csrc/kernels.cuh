@@ -112,6 +112,16 @@ void launch_sampled_csr_nozero(const symnmf_matrix& A, const float* F, int k, co
                                const int64_t* n_uniq_dev, int64_t cap, float* Y, const int32_t* status,
                                cudaStream_t st);
 
+// ---------------------------------------------------------------- spmm_nnz.cu
+// Exact CSR product balanced by nonzeros (k in {8,16,32,64}); chunk_row from launch_spmm_nnz_rows
+// (once per A), carry: spmm_nnz_carry_floats floats.
+int64_t spmm_nnz_chunks(int64_t nnz);
+size_t spmm_nnz_carry_floats(int64_t nnz, int k);
+bool spmm_nnz_supported(int k);
+void launch_spmm_nnz_rows(const symnmf_matrix& A, int64_t* chunk_row, cudaStream_t st);
+void launch_spmm_nnz(const symnmf_matrix& A, const int64_t* chunk_row, const float* F, int k, float* Y, float* carry,
+                     const int32_t* status, cudaStream_t st);
+
 // ---------------------------------------------------------------- sweep.cu
 // Streaming HALS sweep (k in {8, 16, 32}): cp.async-staged tiles, thread per row, fused Gram + Cholesky.
 bool sweep_stream_supported(int k);

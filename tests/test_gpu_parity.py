@@ -464,15 +464,18 @@ def _csr_case(cfgname, n, k, seed=7):
 
 @pytest.mark.parametrize("cfgname,n,k", [("c2", 20_000, 16), ("c2", 20_000, 8), ("c4", 40_000, 32),
                                          ("c4", 40_000, 64), ("c4", 40_032, 16), ("c2", 2_000, 32)])
-@pytest.mark.parametrize("tile", ["always", "never", "blocks3", "blocks7"])
+@pytest.mark.parametrize("tile", ["nnz", "rows", "always", "blocks3", "blocks7"])
 def test_csr_tile_exact_one_iteration(cfgname, n, k, tile, monkeypatch):
-    """Solver EXACT on CSR, both product forms: the tile kernel (A F per 256-row tile with
-    nnz-balanced slices, fused with the sweep and the next Gram; SYMNMF_CSR_TILE=always), also in
-    3 and 7 column-block passes (SYMNMF_CSR_BLOCKS: partial products through HBM, the last pass
-    fused with the sweep), and the row SpMM + sweep: W and H after one iteration vs the oracle's
-    fp64 iteration.  Covers ragged last tiles (n % 256 != 0), hub rows (power-law c4 recipe) and
-    k = 8..64."""
-    monkeypatch.setenv("SYMNMF_CSR_TILE", "never" if tile == "never" else "always")
+    """Solver EXACT on CSR, every product form: the nnz-balanced SpMM (chunks of 256 nonzeros with
+    carries, default) and the row-group SpMM (SYMNMF_CSR_SPMM=rows), each + the streaming sweep;
+    the tile kernel (A F per 256-row tile fused with the sweep and the next Gram;
+    SYMNMF_CSR_TILE=always), also in 3 and 7 column-block passes (SYMNMF_CSR_BLOCKS): W and H
+    after one iteration vs the oracle's fp64 iteration.  Covers ragged last tiles (n % 256 != 0),
+    hub rows (power-law c4 recipe) and k = 8..64."""
+    if tile == "rows":
+        monkeypatch.setenv("SYMNMF_CSR_SPMM", "rows")
+    if tile not in ("nnz", "rows"):
+        monkeypatch.setenv("SYMNMF_CSR_TILE", "always")
     if tile.startswith("blocks"):
         monkeypatch.setenv("SYMNMF_CSR_BLOCKS", tile[6:])
     A, H0, alpha = _csr_case(cfgname, n, k)
@@ -729,12 +732,15 @@ def _drop_vertices(A, frac, tail, seed=3):
     return CsrMatrix(A.n, rowptr, A.colidx[keep].copy(), A.val[keep].copy())
 
 
-@pytest.mark.parametrize("tile", ["always", "never", "blocks3"])
+@pytest.mark.parametrize("tile", ["nnz", "rows", "always", "blocks3"])
 def test_csr_empty_rows(tile, monkeypatch):
     """Isolated vertices (empty CSR rows, 10% random + an empty 300-row tail): the product, the
-    sampled product over all rows, one EXACT solver iteration (tile kernel in one or three
-    column-block passes, and row SpMM), and one LvS half of the bucketed solver path."""
-    monkeypatch.setenv("SYMNMF_CSR_TILE", "never" if tile == "never" else "always")
+    sampled product over all rows, one EXACT solver iteration (nnz-balanced SpMM, row SpMM, tile
+    kernel in one or three column-block passes), and one LvS half of the bucketed solver path."""
+    if tile == "rows":
+        monkeypatch.setenv("SYMNMF_CSR_SPMM", "rows")
+    if tile not in ("nnz", "rows"):
+        monkeypatch.setenv("SYMNMF_CSR_TILE", "always")
     if tile == "blocks3":
         monkeypatch.setenv("SYMNMF_CSR_BLOCKS", "3")
     A0, H0, alpha = _csr_case("c2", 20_000, 16)
@@ -777,7 +783,7 @@ def test_csr_zero_matrix():
     assert not Y.any()
     for mode, kw, env in (("exact", {}, "never"), ("lvs", dict(s=300, tau=1.0 / 300, seed=2), "never"),
                           ("exact", {}, "always"), ("lvs", dict(s=300, tau=1.0 / 300, seed=2), "always")):
-        os.environ["SYMNMF_CSR_TILE"] = os.environ["SYMNMF_BUCKET"] = env
+        os.environ["SYMNMF_CSR_TILE"] = os.environ["SYMNMF_BUCKET"] = env   # EXACT: nnz SpMM / tile
         W, H = cu(H0), cu(H0)
         sv = S.Solver(M, W, H, alpha, mode=mode, max_iters=1, **kw)
         sv.run(1)
