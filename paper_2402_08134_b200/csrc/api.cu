@@ -581,6 +581,8 @@ struct symnmf_solver {
   float* carry;
   int nblk;                // tile path: column blocks of A per product (tile.cu); cuts (nblk - 1) x n
   int64_t* cuts;
+  int cslot;               // constant-table slot of the streaming sweep (-1: G in shared memory)
+  float* ctab;             // scratch for the table copied to the constant bank
   bool record;             // SYMNMF_RECORD_PLANS: per-half copies of the scores and plan
   float* hlev;
   int32_t* huniq;
@@ -618,6 +620,27 @@ struct symnmf_solver {
 
 namespace {
 
+// Graph, exec, side stream, events and the constant-table slot of a solver (null-safe: used by
+// destroy and by every failure path of create).
+void release_solver_resources(symnmf_solver& S) {
+  if (S.exec) cudaGraphExecDestroy(S.exec);
+  if (S.graph) cudaGraphDestroy(S.graph);
+  if (S.side) cudaStreamDestroy(S.side);
+  for (int h = 0; h < 2; ++h) {
+    if (S.ev_fork[h]) cudaEventDestroy(S.ev_fork[h]);
+    if (S.ev_join[h]) cudaEventDestroy(S.ev_join[h]);
+  }
+  sweep_cslot_release(S.cslot);
+  S.exec = nullptr; S.graph = nullptr; S.side = nullptr; S.cslot = -1;
+  for (int h = 0; h < 2; ++h) S.ev_fork[h] = S.ev_join[h] = nullptr;
+}
+
+// The sweep's G through the constant bank (sweep.cu) unless SYMNMF_SWEEP_CMEM=0 (symnmf.h)
+bool sweep_cmem_enabled() {
+  const char* e = getenv("SYMNMF_SWEEP_CMEM");
+  return !(e && !strcmp(e, "0"));
+}
+
 // The streaming sweep (sweep.cu) for k in {8, 16, 32}; SYMNMF_SWEEP=fused selects the register-tile
 // sweep_fused instead (symnmf.h)
 bool sweep_stream_enabled() {
@@ -627,7 +650,7 @@ bool sweep_stream_enabled() {
 
 // Update(G + alpha I, Y + alpha F^T): one HALS sweep with the next half's Gram (and R) fused, or
 // (rule BPP) the exact per-row NLS followed by the Gram of the new factor.
-void enqueue_sweep(const symnmf_solver& S, const double* G, const float* F, float* X, bool zeroY, double* Gnext,
+void enqueue_sweep(const symnmf_solver& S, int side, const double* G, const float* F, float* X, bool zeroY, double* Gnext,
                    float* Rf32, int32_t* status, cudaStream_t st) {
   if (S.bpp) {
     launch_bpp(G, S.Y, F, X, S.n, S.k, S.alpha, zeroY, S.nonconv, status, st);
@@ -635,7 +658,8 @@ void enqueue_sweep(const symnmf_solver& S, const double* G, const float* F, floa
     return;
   }
   if (sweep_stream_supported(S.k) && sweep_stream_enabled())
-    launch_sweep_stream(G, S.alpha, S.Y, F, X, S.n, S.k, zeroY, S.Gacc, Gnext, Rf32, S.counter, status, st);
+    launch_sweep_stream(G, S.alpha, S.Y, F, X, S.n, S.k, zeroY, S.Gacc, Gnext, Rf32, S.counter, status, st,
+                        S.cslot >= 0 ? 2 * S.cslot + side : -1, S.ctab);
   else
     launch_sweep_fused(G, S.alpha, S.Y, F, X, S.n, S.k, zeroY, S.Gacc, Gnext, Rf32, S.counter, status, st);
 }
@@ -721,6 +745,7 @@ void solver_layout(symnmf_solver& S, Carver& c) {
   S.cuts = c.take<int64_t>(S.tile ? (size_t)(S.nblk - 1) * n : 0);
   S.bucket = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode == SYMNMF_LVS && !S.bpp &&
              S.A.nnz < (int64_t)INT32_MAX && S.A.nnz >= bucket_min_nnz();
+  S.ctab = c.take<float>(sweep_table_floats());
   S.nonconv = c.take<int32_t>(1);
   S.Y = c.take<float>((S.tile && S.nblk == 1) || (S.bucket && bucket_fused()) ? 0 : (size_t)n * k);
   S.stats = c.take<symnmf_half_stats>((size_t)2 * S.max_iters);
@@ -788,12 +813,12 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
   } else if (S.mode == SYMNMF_EXACT && S.nnzsp) {
     launch_spmm_nnz(S.A, S.chunk_row, F, k, S.Y, S.carry, status, st);
     mark(S, st, "spmm_csr");
-    enqueue_sweep(S, Gf, F, X, false, Gnext, nullptr, status, st);
+    enqueue_sweep(S, side, Gf, F, X, false, Gnext, nullptr, status, st);
     mark(S, st, S.bpp ? "bpp_update" : "hals_sweep");
   } else if (S.mode == SYMNMF_EXACT) {
     if (!enqueue_product(S.A, F, k, S.Y, S.precision, S.tcs, S.tcs_bytes, status, st)) return false;
     mark(S, st, S.A.kind == SYMNMF_CSR ? "spmm_csr" : (S.precision == SYMNMF_3XTF32 ? "gemm_3xtf32" : "gemm_fp32"));
-    enqueue_sweep(S, Gf, F, X, false, Gnext, nullptr, status, st);
+    enqueue_sweep(S, side, Gf, F, X, false, Gnext, nullptr, status, st);
     mark(S, st, S.bpp ? "bpp_update" : "hals_sweep");
   } else if (lvs) {
     // scores of F from R^{-1} (computed with F^T F) fused with sampler pass S1/S2
@@ -830,7 +855,7 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
       }
       launch_bucket_pull(S.bk, S.Zt, n, k, S.Y, status, st);
       mark(S, st, "bucket_pull");
-      enqueue_sweep(S, S.Gs, F, X, false, Gnext, S.Rinv32, status, st);
+      enqueue_sweep(S, side, S.Gs, F, X, false, Gnext, S.Rinv32, status, st);
       mark(S, st, "hals_sweep");
       return true;
     }
@@ -845,7 +870,7 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     }
     cudaStreamWaitEvent(st, S.ev_join[side], 0);
     // Update(G_s + alpha I, Y_s + alpha F^T); Y re-zeroed for the next scatter; X^T X and its R^{-1}
-    enqueue_sweep(S, S.Gs, F, X, true, Gnext, S.Rinv32, status, st);
+    enqueue_sweep(S, side, S.Gs, F, X, true, Gnext, S.Rinv32, status, st);
     mark(S, st, S.bpp ? "bpp_update" : "hals_sweep");
   } else if (S.lai_fused) {
     // Y = U (Lambda U^T F), sweep, X^T X and Lambda U^T X for the next half, in one launch
@@ -859,7 +884,7 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     launch_scale_rows(S.Z, S.l, k, S.lam, S.M32, status, st);
     launch_rowapply32(S.U, S.l, n, S.l, S.M32, k, S.Y, k, status, st);
     mark(S, st, "lai_uz");
-    enqueue_sweep(S, Gf, F, X, false, Gnext, nullptr, status, st);
+    enqueue_sweep(S, side, Gf, F, X, false, Gnext, nullptr, status, st);
     mark(S, st, S.bpp ? "bpp_update" : "hals_sweep");
   }
   return true;
@@ -962,34 +987,44 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
   launch_gram_fused(H, n, k, S.Gacc, S.Gbuf[0], mode == SYMNMF_LVS ? S.Rinv32 : nullptr, S.counter, S.status, st);
   if (finish() != SYMNMF_OK) return SYMNMF_ERR_CUDA;
   // Capture one iteration on a private stream (the caller's may be the legacy default stream).
-  SYMNMF_CUDA_TRY(cudaStreamCreateWithFlags(&S.side, cudaStreamNonBlocking));
-  for (int h = 0; h < 2; ++h) {
-    SYMNMF_CUDA_TRY(cudaEventCreateWithFlags(&S.ev_fork[h], cudaEventDisableTiming));
-    SYMNMF_CUDA_TRY(cudaEventCreateWithFlags(&S.ev_join[h], cudaEventDisableTiming));
-  }
-  cudaStream_t cs;
-  SYMNMF_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-  if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
-    cudaStreamDestroy(cs);
-    return SYMNMF_ERR_CUDA;
-  }
-  const bool ok = enqueue_iteration(S, cs);
+  // Every failure from here on releases what was created (release_solver_resources).
+  S.cslot = (sweep_stream_supported(k) && sweep_stream_enabled() && sweep_cmem_enabled()) ? sweep_cslot_acquire() : -1;
+  symnmf_status rs = SYMNMF_OK;
+  cudaStream_t cs = nullptr;
   cudaGraph_t g = nullptr;
-  const cudaError_t ce = cudaStreamEndCapture(cs, &g);
-  cudaStreamDestroy(cs);
-  if (!ok) { if (g) cudaGraphDestroy(g); return SYMNMF_ERR_UNSUPPORTED; }
-  if (ce != cudaSuccess || !g) { (void)cudaGetLastError(); return SYMNMF_ERR_CUDA; }
-  cudaGraphExec_t ex;
-  if (cudaGraphInstantiate(&ex, g, 0) != cudaSuccess) {
-    (void)cudaGetLastError();
-    cudaGraphDestroy(g);
-    return SYMNMF_ERR_CUDA;
+  bool ok = false;
+  cudaError_t ce = cudaSuccess;
+  if (cudaStreamCreateWithFlags(&S.side, cudaStreamNonBlocking) != cudaSuccess) rs = SYMNMF_ERR_CUDA;
+  for (int h = 0; h < 2 && rs == SYMNMF_OK; ++h) {
+    if (cudaEventCreateWithFlags(&S.ev_fork[h], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&S.ev_join[h], cudaEventDisableTiming) != cudaSuccess)
+      rs = SYMNMF_ERR_CUDA;
   }
+  if (rs == SYMNMF_OK && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) rs = SYMNMF_ERR_CUDA;
+  if (rs == SYMNMF_OK) {
+    if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+      rs = SYMNMF_ERR_CUDA;
+    } else {
+      ok = enqueue_iteration(S, cs);
+      ce = cudaStreamEndCapture(cs, &g);
+      if (!ok) rs = SYMNMF_ERR_UNSUPPORTED;
+      else if (ce != cudaSuccess || !g) rs = SYMNMF_ERR_CUDA;
+    }
+  }
+  if (cs) cudaStreamDestroy(cs);
+  if (rs == SYMNMF_OK && cudaGraphInstantiate(&S.exec, g, 0) != cudaSuccess) rs = SYMNMF_ERR_CUDA;
   S.graph = g;
-  S.exec = ex;
   S.iters_done = 0;
-  symnmf_solver* p = new (std::nothrow) symnmf_solver(S);
-  if (!p) { cudaGraphExecDestroy(ex); cudaGraphDestroy(g); return SYMNMF_ERR_ARG; }
+  symnmf_solver* p = nullptr;
+  if (rs == SYMNMF_OK) {
+    p = new (std::nothrow) symnmf_solver(S);
+    if (!p) rs = SYMNMF_ERR_ARG;
+  }
+  if (rs != SYMNMF_OK) {
+    (void)cudaGetLastError();
+    release_solver_resources(S);
+    return rs;
+  }
   *out = p;
   return SYMNMF_OK;
 }
@@ -1124,10 +1159,7 @@ extern "C" symnmf_status symnmf_solver_stats(symnmf_solver* S, int32_t* iters_do
 
 extern "C" symnmf_status symnmf_solver_destroy(symnmf_solver* S) {
   if (!S) return SYMNMF_ERR_ARG;
-  cudaGraphExecDestroy(S->exec);
-  cudaStreamDestroy(S->side);
-  for (int h = 0; h < 2; ++h) { cudaEventDestroy(S->ev_fork[h]); cudaEventDestroy(S->ev_join[h]); }
-  cudaGraphDestroy(S->graph);
+  release_solver_resources(*S);
   delete S;
   return SYMNMF_OK;
 }

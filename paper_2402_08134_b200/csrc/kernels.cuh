@@ -124,10 +124,15 @@ void launch_spmm_nnz(const symnmf_matrix& A, const int64_t* chunk_row, const flo
 
 // ---------------------------------------------------------------- sweep.cu
 // Streaming HALS sweep (k in {8, 16, 32}): cp.async-staged tiles, thread per row, fused Gram + Cholesky.
+// tab >= 0: G through constant table tab = 2 * slot + side (slot from sweep_cslot_acquire), built in
+// `scratch` (sweep_table_floats() floats); tab < 0: G in shared memory.
 bool sweep_stream_supported(int k);
 void launch_sweep_stream(const double* G, double alpha, float* Y, const float* F, float* X, int64_t n, int k,
                          bool zeroY, double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
-                         cudaStream_t st);
+                         cudaStream_t st, int tab = -1, float* scratch = nullptr);
+int sweep_cslot_acquire();
+void sweep_cslot_release(int slot);
+size_t sweep_table_floats();
 
 // ---------------------------------------------------------------- bucket.cu / tile.cu (sparse A)
 // Destination buckets of the sampled CSR product (bucket.cu): per plan, the sampled rows'

@@ -9,6 +9,7 @@
 // Gauss-Seidel pass over the k columns runs on them with G (+alpha I) broadcast from shared memory,
 // and the new row goes through a swizzled output tile for coalesced stores and the tile Gram.
 // Bytes per row: Y, F, X read, X written (+ Y re-zeroed for the scatter paths): 16k (20k) B.
+#include <atomic>
 #include "fused_common.cuh"
 
 namespace symnmf {
@@ -31,7 +32,33 @@ __device__ __forceinline__ int swz(int c, int r) {
   return c ^ ((r / RPL) % C);
 }
 
-template <int KP>
+// Constant-bank copies of the sweep's G (G_off^T, 1 / (G_ii + alpha), ok flags), one per (solver
+// slot, half): with G in the constant bank every FMA of the column loop takes its G operand
+// straight from the constant cache (no shared-memory loads, no load-to-use latency).  Written by
+// a D2D copy to the symbol (captured in the solver's graph) right before each sweep.
+constexpr int kCSlots = 4;
+constexpr int kCTab = 32 * 32 + 64;
+__constant__ float cSw[2 * kCSlots][kCTab];
+
+template <int KP, int TAB>
+struct SwG {   // G source: TAB < 0 -> shared memory, else constant table TAB
+  const float* s;
+  const float* inv;
+  const int* ok;
+  __device__ __forceinline__ float4 g4(int i, int j) const {
+    if constexpr (TAB < 0) return *reinterpret_cast<const float4*>(s + i * KP + j);
+    else return make_float4(cSw[TAB][i * KP + j], cSw[TAB][i * KP + j + 1], cSw[TAB][i * KP + j + 2],
+                            cSw[TAB][i * KP + j + 3]);
+  }
+  __device__ __forceinline__ float invd(int i) const {
+    if constexpr (TAB < 0) return inv[i]; else return cSw[TAB][KP * KP + i];
+  }
+  __device__ __forceinline__ bool okd(int i) const {
+    if constexpr (TAB < 0) return ok[i] != 0; else return cSw[TAB][KP * KP + KP + i] != 0.f;
+  }
+};
+
+template <int KP, int TAB = -1>
 __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
     const double* __restrict__ G, double alpha, float* __restrict__ Y, const float* __restrict__ F,
     float* __restrict__ X, int64_t n, int zeroY, double* Gacc, double* Gout, float* Rf32, unsigned int* counter,
@@ -71,6 +98,7 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
   }
   const bool gactive = gg < RG;
   const float a32 = (float)alpha;
+  const SwG<KP, TAB> gsrc{sG, sInv, sOk};
   const int64_t tiles = (n + TR - 1) / TR;
 
   auto issue = [&](int64_t t) {
@@ -118,14 +146,14 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
       float s0 = b[i], s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
       for (int j = 0; j < KP; j += 4) {
-        const float4 g = *reinterpret_cast<const float4*>(sG + i * KP + j);
+        const float4 g = gsrc.g4(i, j);
         s0 = fmaf(-x[j], g.x, s0);
         s1 = fmaf(-x[j + 1], g.y, s1);
         s2 = fmaf(-x[j + 2], g.z, s2);
         s3 = fmaf(-x[j + 3], g.w, s3);
       }
       const float sv = (s0 + s1) + (s2 + s3);
-      if (sOk[i]) x[i] = fmaxf(0.f, sv * sInv[i]);
+      if (gsrc.okd(i)) x[i] = fmaxf(0.f, sv * gsrc.invd(i));
     }
     const bool live = tid < rows;
 #pragma unroll
@@ -177,7 +205,23 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
   }
 }
 
+// fp32 table of the sweep's G for the constant bank: G_off^T (zero diagonal), 1 / (G_ii + alpha), ok
 template <int KP>
+__global__ void sweep_table(const double* __restrict__ G, double alpha, float* __restrict__ out,
+                            const int32_t* __restrict__ status) {
+  if (dev_failed(status)) return;
+  for (int e = threadIdx.x; e < KP * KP; e += blockDim.x) {
+    const int i = e / KP, j = e - i * KP;
+    out[e] = (i != j) ? (float)G[j * KP + i] : 0.f;
+  }
+  for (int i = threadIdx.x; i < KP; i += blockDim.x) {
+    const double den = G[i * KP + i] + alpha;
+    out[KP * KP + i] = den > 0.0 ? (float)(1.0 / den) : 0.f;
+    out[KP * KP + KP + i] = den > 0.0 ? 1.f : 0.f;
+  }
+}
+
+template <int KP, int TAB>
 static void sweep_stream_t(const double* G, double alpha, float* Y, const float* F, float* X, int64_t n, bool zeroY,
                            double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
                            cudaStream_t st) {
@@ -185,20 +229,60 @@ static void sweep_stream_t(const double* G, double alpha, float* Y, const float*
   const size_t smem = std::max(L::bytes, sizeof(double) * 2 * KP * (KP + 1));
   const int64_t tiles = (n + L::TR - 1) / L::TR;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * L::per_sm));
-  cudaFuncSetAttribute(sweep_stream<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  launch_pdl(sweep_stream<KP>, grid, L::TR, smem, st, G, alpha, Y, F, X, n, zeroY ? 1 : 0, Gacc, Gout, Rf32, counter,
-             status);
+  cudaFuncSetAttribute(sweep_stream<KP, TAB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  launch_pdl(sweep_stream<KP, TAB>, grid, L::TR, smem, st, G, alpha, Y, F, X, n, zeroY ? 1 : 0, Gacc, Gout, Rf32,
+             counter, status);
 }
 
 bool sweep_stream_supported(int k) { return k == 8 || k == 16 || k == 32; }
 
+// Constant-table slots: a solver takes one for its lifetime (two tables, one per half).
+static std::atomic<unsigned> g_cslots{0};
+int sweep_cslot_acquire() {
+  unsigned m = g_cslots.load();
+  for (;;) {
+    int b = 0;
+    while (b < kCSlots && (m >> b & 1u)) ++b;
+    if (b == kCSlots) return -1;
+    if (g_cslots.compare_exchange_weak(m, m | (1u << b))) return b;
+  }
+}
+void sweep_cslot_release(int slot) {
+  if (slot >= 0) g_cslots.fetch_and(~(1u << slot));
+}
+size_t sweep_table_floats() { return kCTab; }
+
+template <int KP>
+static void sweep_tab_dispatch(int tab, const double* G, double alpha, float* Y, const float* F, float* X, int64_t n,
+                               bool zeroY, double* Gacc, double* Gout, float* Rf32, unsigned int* counter,
+                               int32_t* status, cudaStream_t st) {
+#define SW_CASE(T) case T: sweep_stream_t<KP, T>(G, alpha, Y, F, X, n, zeroY, Gacc, Gout, Rf32, counter, status, st); break;
+  switch (tab) {
+    SW_CASE(0) SW_CASE(1) SW_CASE(2) SW_CASE(3) SW_CASE(4) SW_CASE(5) SW_CASE(6) SW_CASE(7)
+    default: sweep_stream_t<KP, -1>(G, alpha, Y, F, X, n, zeroY, Gacc, Gout, Rf32, counter, status, st); break;
+  }
+#undef SW_CASE
+}
+
+// tab >= 0: constant table 2 * slot + side, built from G into `scratch` (sweep_table_floats()) and
+// copied to the constant bank first; tab < 0: G staged in shared memory.
 void launch_sweep_stream(const double* G, double alpha, float* Y, const float* F, float* X, int64_t n, int k,
                          bool zeroY, double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
-                         cudaStream_t st) {
+                         cudaStream_t st, int tab, float* scratch) {
+  if (tab >= 0) {
+    const int kp = k;
+    switch (kp) {
+      case 8: sweep_table<8><<<1, 256, 0, st>>>(G, alpha, scratch, status); break;
+      case 16: sweep_table<16><<<1, 256, 0, st>>>(G, alpha, scratch, status); break;
+      default: sweep_table<32><<<1, 256, 0, st>>>(G, alpha, scratch, status); break;
+    }
+    cudaMemcpyToSymbolAsync(cSw, scratch, sizeof(float) * (kp * kp + 2 * kp), sizeof(float) * kCTab * tab,
+                            cudaMemcpyDeviceToDevice, st);
+  }
   switch (k) {
-    case 8: sweep_stream_t<8>(G, alpha, Y, F, X, n, zeroY, Gacc, Gout, Rf32, counter, status, st); break;
-    case 16: sweep_stream_t<16>(G, alpha, Y, F, X, n, zeroY, Gacc, Gout, Rf32, counter, status, st); break;
-    default: sweep_stream_t<32>(G, alpha, Y, F, X, n, zeroY, Gacc, Gout, Rf32, counter, status, st); break;
+    case 8: sweep_tab_dispatch<8>(tab, G, alpha, Y, F, X, n, zeroY, Gacc, Gout, Rf32, counter, status, st); break;
+    case 16: sweep_tab_dispatch<16>(tab, G, alpha, Y, F, X, n, zeroY, Gacc, Gout, Rf32, counter, status, st); break;
+    default: sweep_tab_dispatch<32>(tab, G, alpha, Y, F, X, n, zeroY, Gacc, Gout, Rf32, counter, status, st); break;
   }
 }
 
