@@ -592,6 +592,8 @@ struct symnmf_solver {
   bool bucket;             // LvS on a large CSR A (kpad(k) == k): destination-bucketed sampled product
   BucketWs bk;
   float* Zt;               // bucket gather table Z[t] = omega_t f_{u_t} (cap x k)
+  int64_t* bchunk;         // bucket product: chunk rows and carries of the nnz-balanced pull
+  float* bcarry;
   symnmf_half_stats* stats;
   double *resid, *rpart, *rout, *GH;
   double *pgrad, *ppart, *pout;   // NEXT-3: per-iteration projected-gradient norm (with_resid)
@@ -698,6 +700,13 @@ bool bucket_fused() {
   return e && !strcmp(e, "1");
 }
 
+// LvS bucket path: the pull as the nnz-balanced SpMM over the buckets (default) or one lane group
+// per destination row (SYMNMF_BUCKET_PULL=rows, symnmf.h)
+bool bucket_pull_rows() {
+  const char* e = getenv("SYMNMF_BUCKET_PULL");
+  return e && !strcmp(e, "rows");
+}
+
 // EXACT CSR tile path: column blocks so each pass's rows of F (n / nblk x 4k bytes) stay L2
 // resident: 4k n / 64 MB rounded up; SYMNMF_CSR_BLOCKS=<m> overrides (symnmf.h)
 int csr_blocks(int64_t n, int k) {
@@ -779,6 +788,8 @@ void solver_layout(symnmf_solver& S, Carver& c) {
     if (S.bucket) {
       bucket_layout(c, n, S.A.nnz, S.plan.cap, &S.bk);
       S.Zt = c.take<float>((size_t)S.plan.cap * k);
+      S.bchunk = c.take<int64_t>((size_t)spmm_nnz_chunks(S.A.nnz));
+      S.bcarry = c.take<float>(spmm_nnz_carry_floats(S.A.nnz, k));
     }
   }
   if (S.mode == SYMNMF_LAI) {
@@ -822,7 +833,8 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     mark(S, st, S.bpp ? "bpp_update" : "hals_sweep");
   } else if (lvs) {
     // scores of F from R^{-1} (computed with F^T F) fused with sampler pass S1/S2
-    launch_leverage_fused(F, n, k, S.Rinv32, S.lev, S.T, S.sw, S.s, S.plan, S.counter, status, st);
+    launch_leverage_fused(F, n, k, S.Rinv32, S.lev, S.T, S.sw, S.s, S.plan, S.counter, status, st,
+                          S.cslot >= 0 ? 2 * S.cslot + side : -1);
     mark(S, st, "leverage");
     launch_samp_prefix(S.lev, n, S.T, S.sw, S.plan, status, st);
     mark(S, st, "samp_prefix");
@@ -853,7 +865,10 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
         mark(S, st, "bucket_sweep");
         return true;
       }
-      launch_bucket_pull(S.bk, S.Zt, n, k, S.Y, status, st);
+      if (bucket_pull_rows())
+        launch_bucket_pull(S.bk, S.Zt, n, k, S.Y, status, st);
+      else
+        launch_bucket_spmm(S.bk.off, S.bk.ent, n, S.A.nnz, S.Zt, k, S.Y, S.bchunk, S.bcarry, status, st);
       mark(S, st, "bucket_pull");
       enqueue_sweep(S, side, S.Gs, F, X, false, Gnext, S.Rinv32, status, st);
       mark(S, st, "hals_sweep");

@@ -206,7 +206,28 @@ __global__ void __launch_bounds__(FT, KP <= 32 ? 2 : 1) sweep_fused(const double
 // ---------------------------------------------------------------- leverage_fused (+ S1, S2)
 constexpr double kTwo40f = 1099511627776.0;
 
-template <int KP>
+// Constant-bank copies of the CholeskyQR factor (R upper KP x KP | 1 / diag R), one per (solver
+// slot, half), as for the sweep's G (sweep.cu): the forward substitution's R operands come from
+// the constant cache into uniform registers instead of shared memory.
+constexpr int kLevTabs = 8;
+constexpr int kLevTab = 32 * 32 + 32;
+__constant__ float cLev[kLevTabs][kLevTab];
+
+template <int KP, int TAB>
+struct LevR {
+  const float* sR;
+  const float* sRd;
+  __device__ __forceinline__ float4 r4(int a, int c) const {
+    if constexpr (TAB < 0) return *reinterpret_cast<const float4*>(sR + a * KP + c);
+    else return make_float4(cLev[TAB][a * KP + c], cLev[TAB][a * KP + c + 1], cLev[TAB][a * KP + c + 2],
+                            cLev[TAB][a * KP + c + 3]);
+  }
+  __device__ __forceinline__ float rd(int a) const {
+    if constexpr (TAB < 0) return sRd[a]; else return cLev[TAB][KP * KP + a];
+  }
+};
+
+template <int KP, int TAB = -1>
 __global__ void __launch_bounds__(FT) leverage_fused(const float* __restrict__ F, int64_t n, int k,
                                                      const float* __restrict__ Rinv, float* __restrict__ lev,
                                                      double T, uint64_t* __restrict__ bw, uint32_t* __restrict__ bd,
@@ -274,14 +295,15 @@ __global__ void __launch_bounds__(FT) leverage_fused(const float* __restrict__ F
       // Row a of R is read as float4 groups from the aligned group holding column a: entries
       // c <= a of f are dead once q_a is formed, so updating them too is harmless (R is stored
       // with zeros below the diagonal), and the shared-memory loads drop fourfold.
+      const LevR<KP, TAB> rsrc{sR, sRd};
       float l = 0.f;
 #pragma unroll
       for (int a = 0; a < KP; ++a) {
-        const float q = f[a] * sRd[a];
+        const float q = f[a] * rsrc.rd(a);
         l = fmaf(q, q, l);
 #pragma unroll
         for (int c = (a + 1) & ~3; c < KP; c += 4) {
-          const float4 r4 = *reinterpret_cast<const float4*>(sR + a * KP + c);
+          const float4 r4 = rsrc.r4(a, c);
           f[c] = fmaf(-q, r4.x, f[c]); f[c + 1] = fmaf(-q, r4.y, f[c + 1]);
           f[c + 2] = fmaf(-q, r4.z, f[c + 2]); f[c + 3] = fmaf(-q, r4.w, f[c + 3]);
         }
@@ -771,24 +793,45 @@ void launch_sweep_fused(const double* G, double alpha, float* Y, const float* F,
   }
 }
 
-template <int KP>
+template <int KP, int TAB>
 static void leverage_fused_t(const float* F, int64_t n, int k, const float* Rinv, float* lev, double T,
                              const SamplerWs& w, int64_t s, const symnmf_plan& plan, unsigned int* counter,
                              int32_t* status, cudaStream_t st) {
   const size_t smem = sizeof(float) * FROWS * (KP + 4);
-  cudaFuncSetAttribute(leverage_fused<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  leverage_fused<KP><<<(unsigned)samp_blocks(n), FT, smem, st>>>(F, n, k, Rinv, lev, T, w.bw, w.bd, w.bt, s,
-                                                                 plan.cap, plan.counts, plan.mass, counter, status);
+  cudaFuncSetAttribute(leverage_fused<KP, TAB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  leverage_fused<KP, TAB><<<(unsigned)samp_blocks(n), FT, smem, st>>>(F, n, k, Rinv, lev, T, w.bw, w.bd, w.bt, s,
+                                                                      plan.cap, plan.counts, plan.mass, counter,
+                                                                      status);
 }
 
+template <int KP>
+static void leverage_tab_dispatch(int tab, const float* F, int64_t n, int k, const float* Rinv, float* lev, double T,
+                                  const SamplerWs& w, int64_t s, const symnmf_plan& plan, unsigned int* counter,
+                                  int32_t* status, cudaStream_t st) {
+#define LV_CASE(T_) case T_: leverage_fused_t<KP, T_>(F, n, k, Rinv, lev, T, w, s, plan, counter, status, st); break;
+  switch (tab) {
+    LV_CASE(0) LV_CASE(1) LV_CASE(2) LV_CASE(3) LV_CASE(4) LV_CASE(5) LV_CASE(6) LV_CASE(7)
+    default: leverage_fused_t<KP, -1>(F, n, k, Rinv, lev, T, w, s, plan, counter, status, st); break;
+  }
+#undef LV_CASE
+}
+
+// tab >= 0 (k == kpad(k) <= 32): R copied from Rinv to constant table tab first.
 void launch_leverage_fused(const float* F, int64_t n, int k, const float* Rinv, float* lev, double T,
                            const SamplerWs& w, int64_t s, const symnmf_plan& plan, unsigned int* counter,
-                           int32_t* status, cudaStream_t st) {
-  switch (kpad(k)) {
-    case 8: leverage_fused_t<8>(F, n, k, Rinv, lev, T, w, s, plan, counter, status, st); break;
-    case 16: leverage_fused_t<16>(F, n, k, Rinv, lev, T, w, s, plan, counter, status, st); break;
-    case 32: leverage_fused_t<32>(F, n, k, Rinv, lev, T, w, s, plan, counter, status, st); break;
-    default: leverage_fused_t<64>(F, n, k, Rinv, lev, T, w, s, plan, counter, status, st); break;
+                           int32_t* status, cudaStream_t st, int tab) {
+  const int kp = kpad(k);
+  if (tab >= 0 && kp == k && kp <= 32) {
+    cudaMemcpyToSymbolAsync(cLev, Rinv, sizeof(float) * (kp * kp + kp), sizeof(float) * kLevTab * tab,
+                            cudaMemcpyDeviceToDevice, st);
+  } else {
+    tab = -1;
+  }
+  switch (kp) {
+    case 8: leverage_tab_dispatch<8>(tab, F, n, k, Rinv, lev, T, w, s, plan, counter, status, st); break;
+    case 16: leverage_tab_dispatch<16>(tab, F, n, k, Rinv, lev, T, w, s, plan, counter, status, st); break;
+    case 32: leverage_tab_dispatch<32>(tab, F, n, k, Rinv, lev, T, w, s, plan, counter, status, st); break;
+    default: leverage_fused_t<64, -1>(F, n, k, Rinv, lev, T, w, s, plan, counter, status, st); break;
   }
 }
 

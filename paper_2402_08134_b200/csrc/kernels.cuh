@@ -85,9 +85,10 @@ void launch_gram_fused(const float* F, int64_t n, int k, double* Gacc, double* G
 void launch_sweep_fused(const double* G, double alpha, float* Y, const float* F, float* X, int64_t n, int k,
                         bool zeroY, double* Gacc, double* Gout, float* Rinv32, unsigned int* counter,
                         int32_t* status, cudaStream_t st);
+// tab >= 0 (kpad(k) == k <= 32): R through constant table tab (2 * sweep slot + side)
 void launch_leverage_fused(const float* F, int64_t n, int k, const float* Rinv, float* lev, double T,
                            const SamplerWs& w, int64_t s, const symnmf_plan& plan, unsigned int* counter,
-                           int32_t* status, cudaStream_t st);
+                           int32_t* status, cudaStream_t st, int tab = -1);
 void launch_uniq_count_fused(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
                              const int32_t* iter_dev, int32_t first_iter, int32_t max_iters, int side,
                              symnmf_half_stats* stats, unsigned int* counter, int32_t* status, cudaStream_t st);
@@ -121,6 +122,10 @@ bool spmm_nnz_supported(int k);
 void launch_spmm_nnz_rows(const symnmf_matrix& A, int64_t* chunk_row, cudaStream_t st);
 void launch_spmm_nnz(const symnmf_matrix& A, const int64_t* chunk_row, const float* F, int k, float* Y, float* carry,
                      const int32_t* status, cudaStream_t st);
+// The bucketed sampled product through the same nnz-balanced kernel (chunk_row: spmm_nnz_chunks(cap)
+// entries, carry: spmm_nnz_carry_floats(cap, k)); total entries read from off[n] on the device.
+void launch_bucket_spmm(const int32_t* off, const int2* ent, int64_t n, int64_t cap_entries, const float* Z, int k,
+                        float* Y, int64_t* chunk_row, float* carry, const int32_t* status, cudaStream_t st);
 
 // ---------------------------------------------------------------- sweep.cu
 // Streaming HALS sweep (k in {8, 16, 32}): cp.async-staged tiles, thread per row, fused Gram + Cholesky.

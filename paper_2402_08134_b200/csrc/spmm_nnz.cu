@@ -14,49 +14,72 @@ constexpr int kGather = 8;         // rows of F in flight per lane group
 
 int64_t spmm_nnz_chunks(int64_t nnz) { return (nnz + kChunk - 1) / kChunk; }
 
-// chunk_row[g] = the row holding nonzero g * kChunk (largest r with rowptr[r] <= g * kChunk)
-__global__ void spmm_nnz_rows_kernel(const int64_t* __restrict__ rowptr, int64_t n, int64_t nchunks,
-                                     int64_t* __restrict__ chunk_row) {
+struct NnzCsr {      // CSR A: rowptr int64, separate col / val
+  const int64_t* rowptr;
+  const int32_t* col;
+  const float* val;
+  __device__ __forceinline__ int64_t ptr(int64_t r) const { return rowptr[r]; }
+  __device__ __forceinline__ void load(int64_t e, int& c, float& a) const {
+    c = __ldcs(col + e);
+    a = __ldcs(val + e);
+  }
+};
+struct NnzBucket {   // destination buckets of the sampled product (bucket.cu): off int32, (t, a) pairs
+  const int32_t* off;
+  const int2* ent;
+  __device__ __forceinline__ int64_t ptr(int64_t r) const { return off[r]; }
+  __device__ __forceinline__ void load(int64_t e, int& c, float& a) const {
+    const int2 x = __ldcs(ent + e);
+    c = x.x;
+    a = __int_as_float(x.y);
+  }
+};
+
+// chunk_row[g] = the row holding entry g * kChunk (largest r with ptr(r) <= g * kChunk), for the
+// chunks of `total` entries (*total_dev when given)
+template <class Src>
+__global__ void spmm_nnz_rows_kernel(Src src, int64_t n, int64_t total, const int32_t* __restrict__ total_dev,
+                                     int64_t* __restrict__ chunk_row, const int32_t* __restrict__ status) {
+  if (status && dev_failed(status)) return;
+  const int64_t nnz = total_dev ? (int64_t)*total_dev : total;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= nchunks) return;
+  if (g * kChunk >= nnz) return;
   const int64_t s0 = g * kChunk;
   int64_t lo = 0, hi = n - 1;
   while (lo < hi) {
     const int64_t mid = (lo + hi + 1) >> 1;
-    if (rowptr[mid] <= s0) lo = mid; else hi = mid - 1;
+    if (src.ptr(mid) <= s0) lo = mid; else hi = mid - 1;
   }
   chunk_row[g] = lo;
 }
 
-template <int KP>
-__global__ void __launch_bounds__(256) spmm_nnz(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-                                                const float* __restrict__ val, int64_t nnz,
+template <int KP, class Src>
+__global__ void __launch_bounds__(256) spmm_nnz(Src src, int64_t total, const int32_t* __restrict__ total_dev,
                                                 const int64_t* __restrict__ chunk_row, const float4* __restrict__ F4,
                                                 float4* __restrict__ Y4, float4* __restrict__ carry,
                                                 const int32_t* __restrict__ status) {
   if (dev_failed(status)) return;
   constexpr int LPR = KP / 4;
   const int li = threadIdx.x % LPR;
+  const int64_t nnz = total_dev ? (int64_t)*total_dev : total;
   const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / LPR;
   const int64_t nchunks = (nnz + kChunk - 1) / kChunk;
   for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPR; g < nchunks; g += ng) {
     const int64_t s0 = g * kChunk, s1 = min64(nnz, s0 + kChunk);
     const int64_t rf = chunk_row[g];
     int64_t r = rf;
-    int64_t rstart = rowptr[r], rend = rowptr[r + 1];
+    int64_t rstart = src.ptr(r), rend = src.ptr(r + 1);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     auto emit = [&]() {
       if (rstart >= s0 && rend <= s1) Y4[r * LPR + li] = acc;                 // complete in this chunk
       else carry[(2 * g + (r == rf ? 0 : 1)) * LPR + li] = acc;               // shared with a neighbour
     };
-    // prefetched nonzeros of the next batch
+    // prefetched entries of the next batch
     int cn[kGather];
     float an[kGather];
 #pragma unroll
     for (int u = 0; u < kGather; ++u) {
-      const bool ok = s0 + u < s1;
-      cn[u] = ok ? __ldcs(col + s0 + u) : 0;
-      an[u] = ok ? __ldcs(val + s0 + u) : 0.f;
+      if (s0 + u < s1) src.load(s0 + u, cn[u], an[u]); else { cn[u] = 0; an[u] = 0.f; }
     }
     for (int64_t e = s0; e < s1; e += kGather) {
       int cc[kGather];
@@ -68,11 +91,9 @@ __global__ void __launch_bounds__(256) spmm_nnz(const int64_t* __restrict__ rowp
       for (int u = 0; u < kGather; ++u)
         ff[u] = (e + u < s1) ? __ldg(F4 + (int64_t)cc[u] * LPR + li) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int u = 0; u < kGather; ++u) {   // next batch's (col, val) in flight during this batch
+      for (int u = 0; u < kGather; ++u) {   // next batch's entries in flight during this batch
         const int64_t en = e + kGather + u;
-        const bool ok = en < s1;
-        cn[u] = ok ? __ldcs(col + en) : 0;
-        an[u] = ok ? __ldcs(val + en) : 0.f;
+        if (en < s1) src.load(en, cn[u], an[u]); else { cn[u] = 0; an[u] = 0.f; }
       }
 #pragma unroll
       for (int u = 0; u < kGather; ++u) {
@@ -81,7 +102,7 @@ __global__ void __launch_bounds__(256) spmm_nnz(const int64_t* __restrict__ rowp
           if (ei >= rend) {                 // row r ends: store it, move to the row holding ei
             emit();
             acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            do { ++r; rstart = rend; rend = rowptr[r + 1]; } while (rend <= ei);   // skips empty rows
+            do { ++r; rstart = rend; rend = src.ptr(r + 1); } while (rend <= ei);   // skips empty rows
           }
           acc.x = fmaf(aa[u], ff[u].x, acc.x); acc.y = fmaf(aa[u], ff[u].y, acc.y);
           acc.z = fmaf(aa[u], ff[u].z, acc.z); acc.w = fmaf(aa[u], ff[u].w, acc.w);
@@ -93,16 +114,15 @@ __global__ void __launch_bounds__(256) spmm_nnz(const int64_t* __restrict__ rowp
 }
 
 // Rows shared between chunks: the carries of every chunk they touch, in chunk order; empty rows: 0.
-template <int KP>
-__global__ void __launch_bounds__(256) spmm_nnz_fix(const int64_t* __restrict__ rowptr, int64_t n,
-                                                    const float4* __restrict__ carry, float4* __restrict__ Y4,
-                                                    const int32_t* __restrict__ status) {
+template <int KP, class Src>
+__global__ void __launch_bounds__(256) spmm_nnz_fix(Src src, int64_t n, const float4* __restrict__ carry,
+                                                    float4* __restrict__ Y4, const int32_t* __restrict__ status) {
   if (dev_failed(status)) return;
   constexpr int LPR = KP / 4;
   const int li = threadIdx.x % LPR;
   const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / LPR;
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPR; r < n; r += ng) {
-    const int64_t a = rowptr[r], b = rowptr[r + 1];
+    const int64_t a = src.ptr(r), b = src.ptr(r + 1);
     if (a == b) { Y4[r * LPR + li] = make_float4(0.f, 0.f, 0.f, 0.f); continue; }
     const int64_t c0 = a / kChunk, c1 = (b - 1) / kChunk;
     if (c0 == c1) continue;                                      // stored by its chunk
@@ -120,34 +140,54 @@ size_t spmm_nnz_carry_floats(int64_t nnz, int k) { return (size_t)2 * spmm_nnz_c
 
 void launch_spmm_nnz_rows(const symnmf_matrix& A, int64_t* chunk_row, cudaStream_t st) {
   const int64_t nc = spmm_nnz_chunks(A.nnz);
-  if (nc > 0) spmm_nnz_rows_kernel<<<(unsigned)((nc + 255) / 256), 256, 0, st>>>(A.rowptr, A.n, nc, chunk_row);
+  if (nc > 0)
+    spmm_nnz_rows_kernel<NnzCsr><<<(unsigned)((nc + 255) / 256), 256, 0, st>>>(
+        NnzCsr{A.rowptr, A.colidx, A.val}, A.n, A.nnz, nullptr, chunk_row, nullptr);
 }
 
-template <int KP>
-static void spmm_nnz_t(const symnmf_matrix& A, const int64_t* chunk_row, const float* F, float* Y, float* carry,
-                       const int32_t* status, cudaStream_t st) {
+template <int KP, class Src>
+static void spmm_nnz_t(Src src, int64_t n, int64_t total_cap, const int32_t* total_dev, const int64_t* chunk_row,
+                       const float* F, float* Y, float* carry, const int32_t* status, cudaStream_t st) {
   constexpr int LPR = KP / 4;
-  const int64_t groups = spmm_nnz_chunks(A.nnz);
+  const int64_t groups = spmm_nnz_chunks(total_cap);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((groups * LPR + 255) / 256, 148 * 16));
-  if (A.nnz > 0)
-    launch_pdl(spmm_nnz<KP>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, A.nnz, chunk_row,
+  if (total_cap > 0)
+    launch_pdl(spmm_nnz<KP, Src>, grid, 256, 0, st, src, total_cap, total_dev, chunk_row,
                reinterpret_cast<const float4*>(F), reinterpret_cast<float4*>(Y), reinterpret_cast<float4*>(carry),
                status);
-  const int gridf = (int)std::max<int64_t>(1, std::min<int64_t>((A.n * LPR + 255) / 256, 148 * 16));
-  launch_pdl(spmm_nnz_fix<KP>, gridf, 256, 0, st, A.rowptr, A.n, reinterpret_cast<const float4*>(carry),
+  const int gridf = (int)std::max<int64_t>(1, std::min<int64_t>((n * LPR + 255) / 256, 148 * 16));
+  launch_pdl(spmm_nnz_fix<KP, Src>, gridf, 256, 0, st, src, n, reinterpret_cast<const float4*>(carry),
              reinterpret_cast<float4*>(Y), status);
+}
+
+template <class Src>
+static void spmm_nnz_k(Src src, int64_t n, int64_t total_cap, const int32_t* total_dev, const int64_t* chunk_row,
+                       const float* F, int k, float* Y, float* carry, const int32_t* status, cudaStream_t st) {
+  switch (k) {
+    case 8: spmm_nnz_t<8>(src, n, total_cap, total_dev, chunk_row, F, Y, carry, status, st); break;
+    case 16: spmm_nnz_t<16>(src, n, total_cap, total_dev, chunk_row, F, Y, carry, status, st); break;
+    case 32: spmm_nnz_t<32>(src, n, total_cap, total_dev, chunk_row, F, Y, carry, status, st); break;
+    default: spmm_nnz_t<64>(src, n, total_cap, total_dev, chunk_row, F, Y, carry, status, st); break;
+  }
 }
 
 bool spmm_nnz_supported(int k) { return k == 8 || k == 16 || k == 32 || k == 64; }
 
 void launch_spmm_nnz(const symnmf_matrix& A, const int64_t* chunk_row, const float* F, int k, float* Y, float* carry,
                      const int32_t* status, cudaStream_t st) {
-  switch (k) {
-    case 8: spmm_nnz_t<8>(A, chunk_row, F, Y, carry, status, st); break;
-    case 16: spmm_nnz_t<16>(A, chunk_row, F, Y, carry, status, st); break;
-    case 32: spmm_nnz_t<32>(A, chunk_row, F, Y, carry, status, st); break;
-    default: spmm_nnz_t<64>(A, chunk_row, F, Y, carry, status, st); break;
-  }
+  spmm_nnz_k(NnzCsr{A.rowptr, A.colidx, A.val}, A.n, A.nnz, nullptr, chunk_row, F, k, Y, carry, status, st);
+}
+
+// The sampled product from the destination buckets (bucket.cu) as an nnz-balanced SpMM over
+// (off, ent) with gather table Z: chunk rows found per plan (total entries = off[n], on device).
+void launch_bucket_spmm(const int32_t* off, const int2* ent, int64_t n, int64_t cap_entries, const float* Z, int k,
+                        float* Y, int64_t* chunk_row, float* carry, const int32_t* status, cudaStream_t st) {
+  const NnzBucket src{off, ent};
+  const int64_t nc = spmm_nnz_chunks(cap_entries);
+  if (nc > 0)
+    launch_pdl(spmm_nnz_rows_kernel<NnzBucket>, (unsigned)((nc + 255) / 256), 256, 0, st, src, n, cap_entries,
+               off + n, chunk_row, status);
+  spmm_nnz_k(src, n, cap_entries, off + n, chunk_row, Z, k, Y, carry, status, st);
 }
 
 }  // namespace symnmf

@@ -19,9 +19,9 @@ struct SwL {
   static constexpr int C = KP / 4;              // 16 B chunks per row
   static constexpr int TR = 256;                // rows per tile = threads
   static constexpr size_t arr = sizeof(float) * TR * KP;
-  static constexpr size_t y = 0, f = arr, x = 2 * arr, o = 3 * arr, gram = 4 * arr;
-  static constexpr size_t bytes = gram + sizeof(double) * TR * 16;
-  static constexpr int per_sm = bytes <= 70 * 1024 ? 3 : bytes <= 110 * 1024 ? 2 : 1;
+  static constexpr size_t y = 0, f = arr, x = 2 * arr;
+  static constexpr size_t bytes = 3 * arr;      // Y, F, X staging (X rewritten in place)
+  static constexpr int per_sm = KP <= 8 ? 3 : 2;   // 128 registers per thread for k = 16, 32
 };
 
 // chunk c of row r lives at chunk position swz(c, r): the 8 rows a quarter-warp reads hit 8
@@ -66,29 +66,29 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
   using L = SwL<KP>;
   constexpr int C = L::C, TR = L::TR;
   constexpr int NB = KP / 4, PAIRS = NB * (NB + 1) / 2, RG = TR / PAIRS;
-  __shared__ __align__(16) float sG[KP * KP];     // sG[i*KP + j] = G[j][i], 0 on the diagonal
+  constexpr int RPL = 8 / C;                      // rows per 128 B line (swizzle period: C * RPL rows)
+  __shared__ __align__(16) float sG[TAB < 0 ? KP * KP : 4];   // sG[i*KP + j] = G[j][i], 0 on the diagonal
   __shared__ float sInv[KP];
   __shared__ int sOk[KP];
   extern __shared__ __align__(16) unsigned char sms[];
   float* sY = reinterpret_cast<float*>(sms + L::y);
   float* sF = reinterpret_cast<float*>(sms + L::f);
   float* sX = reinterpret_cast<float*>(sms + L::x);
-  float* sO = reinterpret_cast<float*>(sms + L::o);
-  double* gslot = reinterpret_cast<double*>(sms + L::gram);
   if (dev_failed(status)) return;
   const int tid = threadIdx.x;
-  for (int e = tid; e < KP * KP; e += TR) {
-    const int i = e / KP, j = e - i * KP;
-    sG[e] = (i != j) ? (float)G[j * KP + i] : 0.f;
+  if constexpr (TAB < 0) {
+    for (int e = tid; e < KP * KP; e += TR) {
+      const int i = e / KP, j = e - i * KP;
+      sG[e] = (i != j) ? (float)G[j * KP + i] : 0.f;
+    }
+    for (int i = tid; i < KP; i += TR) {
+      const double den = G[i * KP + i] + alpha;
+      sOk[i] = den > 0.0;
+      sInv[i] = den > 0.0 ? (float)(1.0 / den) : 0.f;
+    }
   }
-  for (int i = tid; i < KP; i += TR) {
-    const double den = G[i * KP + i] + alpha;
-    sOk[i] = den > 0.0;
-    sInv[i] = den > 0.0 ? (float)(1.0 / den) : 0.f;
-  }
-#pragma unroll
-  for (int e = 0; e < 16; ++e) gslot[tid * 16 + e] = 0.0;
-  // Gram role of this thread: upper 4x4 block (ai, bi) over row group g
+  // Gram role of this thread: upper 4x4 block (ai, bi) over the rows r = gg (mod RG) of each tile;
+  // fp32 over a tile, fp64 registers across tiles
   const int gg = tid / PAIRS, gp = tid - gg * PAIRS;
   int ai = 0, bi = 0;
   {
@@ -96,14 +96,19 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
     while (rem >= NB - a) { rem -= NB - a; ++a; }
     ai = a; bi = a + rem;
   }
-  const bool gactive = gg < RG;
+  const bool gactive = Gacc && gg < RG;
+  double acc64[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) acc64[e] = 0.0;
   const float a32 = (float)alpha;
   const SwG<KP, TAB> gsrc{sG, sInv, sOk};
   const int64_t tiles = (n + TR - 1) / TR;
+  __syncthreads();
 
-  auto issue = [&](int64_t t) {
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
     const int64_t r0 = t * TR;
     const int rows = (int)min64(TR, n - r0);
+    // stage the tile's rows of Y, F, X (coalesced 16 B chunks, swizzled)
     for (int q = tid; q < TR * C; q += TR) {
       const int r = q / C, c = q - r * C;
       const bool ok = r < rows;
@@ -114,67 +119,64 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
       cp_async16(sX + so, X + go, ok);
     }
     cp_async_commit();
-  };
-
-  int64_t t = blockIdx.x;
-  if (t < tiles) issue(t);
-  for (; t < tiles; t += gridDim.x) {
-    const int64_t r0 = t * TR;
-    const int rows = (int)min64(TR, n - r0);
     cp_async_wait<0>();
     __syncthreads();
-    float b[KP], x[KP];
+    if (zeroY) {
+      float4* Y4 = reinterpret_cast<float4*>(Y) + r0 * C;
+      for (int q = tid; q < rows * C; q += TR) __stcs(Y4 + q, make_float4(0.f, 0.f, 0.f, 0.f));
+    }
+    float x[KP];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const float4 x4 = *reinterpret_cast<const float4*>(sX + tid * KP + 4 * swz<KP>(c, tid));
+      x[4 * c] = x4.x; x[4 * c + 1] = x4.y; x[4 * c + 2] = x4.z; x[4 * c + 3] = x4.w;
+    }
+    // Gauss-Seidel over the columns of row tid: x_i <- [(b_i - sum_{j != i} G_ij x_j) / (G_ii + alpha)]_+,
+    // b = y + alpha f read a 16 B chunk at a time
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       const int so = tid * KP + 4 * swz<KP>(c, tid);
       const float4 y4 = *reinterpret_cast<const float4*>(sY + so);
       const float4 f4 = *reinterpret_cast<const float4*>(sF + so);
-      const float4 x4 = *reinterpret_cast<const float4*>(sX + so);
-      b[4 * c] = fmaf(a32, f4.x, y4.x); b[4 * c + 1] = fmaf(a32, f4.y, y4.y);
-      b[4 * c + 2] = fmaf(a32, f4.z, y4.z); b[4 * c + 3] = fmaf(a32, f4.w, y4.w);
-      x[4 * c] = x4.x; x[4 * c + 1] = x4.y; x[4 * c + 2] = x4.z; x[4 * c + 3] = x4.w;
-    }
-    __syncthreads();                                   // staging buffers of tile t consumed
-    if (t + gridDim.x < tiles) issue(t + gridDim.x);   // tile t + grid streams in while t computes
-    if (zeroY) {
-      float4* Y4 = reinterpret_cast<float4*>(Y) + r0 * C;
-      for (int q = tid; q < rows * C; q += TR) __stcs(Y4 + q, make_float4(0.f, 0.f, 0.f, 0.f));
-    }
-    // Gauss-Seidel over the columns of row tid: x_i <- [(b_i - sum_{j != i} G_ij x_j) / (G_ii + alpha)]_+
+      const float bc[4] = {fmaf(a32, f4.x, y4.x), fmaf(a32, f4.y, y4.y), fmaf(a32, f4.z, y4.z),
+                           fmaf(a32, f4.w, y4.w)};
 #pragma unroll
-    for (int i = 0; i < KP; ++i) {
-      float s0 = b[i], s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      for (int u = 0; u < 4; ++u) {
+        const int i = 4 * c + u;
+        float s0 = bc[u], s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
-      for (int j = 0; j < KP; j += 4) {
-        const float4 g = gsrc.g4(i, j);
-        s0 = fmaf(-x[j], g.x, s0);
-        s1 = fmaf(-x[j + 1], g.y, s1);
-        s2 = fmaf(-x[j + 2], g.z, s2);
-        s3 = fmaf(-x[j + 3], g.w, s3);
+        for (int j = 0; j < KP; j += 4) {
+          const float4 g = gsrc.g4(i, j);
+          s0 = fmaf(-x[j], g.x, s0);
+          s1 = fmaf(-x[j + 1], g.y, s1);
+          s2 = fmaf(-x[j + 2], g.z, s2);
+          s3 = fmaf(-x[j + 3], g.w, s3);
+        }
+        const float sv = (s0 + s1) + (s2 + s3);
+        if (gsrc.okd(i)) x[i] = fmaxf(0.f, sv * gsrc.invd(i));
       }
-      const float sv = (s0 + s1) + (s2 + s3);
-      if (gsrc.okd(i)) x[i] = fmaxf(0.f, sv * gsrc.invd(i));
     }
     const bool live = tid < rows;
 #pragma unroll
-    for (int c = 0; c < C; ++c)
-      *reinterpret_cast<float4*>(sO + tid * KP + 4 * swz<KP>(c, tid)) =
+    for (int c = 0; c < C; ++c)   // the new row replaces the old one in the staging tile
+      *reinterpret_cast<float4*>(sX + tid * KP + 4 * swz<KP>(c, tid)) =
           live ? make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
     {
       float4* X4 = reinterpret_cast<float4*>(X) + r0 * C;
       for (int q = tid; q < rows * C; q += TR) {
         const int r = q / C, c = q - r * C;
-        X4[q] = *reinterpret_cast<const float4*>(sO + r * KP + 4 * swz<KP>(c, r));
+        X4[q] = *reinterpret_cast<const float4*>(sX + r * KP + 4 * swz<KP>(c, r));
       }
     }
-    if (Gacc && gactive) {   // tile Gram of the new rows: fp32 over the tile, fp64 slot per thread
+    if (gactive) {   // tile Gram of the new rows
       float acc[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) acc[e] = 0.f;
       for (int r = gg; r < rows; r += RG) {
-        const float4 a4 = *reinterpret_cast<const float4*>(sO + r * KP + 4 * swz<KP>(ai, r));
-        const float4 b4 = *reinterpret_cast<const float4*>(sO + r * KP + 4 * swz<KP>(bi, r));
+        const int xr = (r / RPL) % C;                 // swizzle of row r (swz)
+        const float4 a4 = *reinterpret_cast<const float4*>(sX + r * KP + 4 * (ai ^ xr));
+        const float4 b4 = *reinterpret_cast<const float4*>(sX + r * KP + 4 * (bi ^ xr));
         const float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -182,18 +184,24 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
           for (int j = 0; j < 4; ++j) acc[i * 4 + j] = fmaf(av[i], bv[j], acc[i * 4 + j]);
       }
 #pragma unroll
-      for (int e = 0; e < 16; ++e) gslot[tid * 16 + e] += (double)acc[e];
+      for (int e = 0; e < 16; ++e) acc64[e] += (double)acc[e];
     }
+    __syncthreads();   // staging tile free for the next tile
   }
-  cp_async_wait<0>();
   if (!Gacc) return;
-  // commit: the row groups' slots summed in fixed order, one fp64 red.add per entry into a replica
+  // commit: the row groups' partials reduced in shared memory in fixed order, one fp64 red.add per
+  // entry into a replica of the global accumulator; the last CTA forms X^T X and its Cholesky factor
+  double* red = reinterpret_cast<double*>(sms);       // RG * PAIRS * 16 doubles (<= 32 KB)
+  if (gg < RG) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) red[(size_t)tid * 16 + e] = acc64[e];
+  }
   __syncthreads();
   double* rep = Gacc + (size_t)(blockIdx.x % kGramReplicas) * KP * KP;
   for (int idx = tid; idx < PAIRS * 16; idx += TR) {
     const int pp = idx >> 4, e = idx & 15;
     double sum = 0.0;
-    for (int g2 = 0; g2 < RG; ++g2) sum += gslot[(size_t)(g2 * PAIRS + pp) * 16 + e];
+    for (int g2 = 0; g2 < RG; ++g2) sum += red[(size_t)(g2 * PAIRS + pp) * 16 + e];
     int a0 = 0, rem = pp;
     while (rem >= NB - a0) { rem -= NB - a0; ++a0; }
     const int a = 4 * a0 + (e >> 2), bb = 4 * (a0 + rem) + (e & 3);
@@ -226,7 +234,7 @@ static void sweep_stream_t(const double* G, double alpha, float* Y, const float*
                            double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
                            cudaStream_t st) {
   using L = SwL<KP>;
-  const size_t smem = std::max(L::bytes, sizeof(double) * 2 * KP * (KP + 1));
+  const size_t smem = std::max({L::bytes, sizeof(double) * 2 * KP * (KP + 1), sizeof(double) * 256 * 16});
   const int64_t tiles = (n + L::TR - 1) / L::TR;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * L::per_sm));
   cudaFuncSetAttribute(sweep_stream<KP, TAB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
