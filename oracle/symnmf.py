@@ -20,7 +20,7 @@ __all__ = [
     "draw_indices", "build_plan", "sampled_products", "hals_sweep", "hals_sweep_explicit",
     "surrogate_objective", "iterate", "gaussian_omega", "orth", "rangefinder", "lai_apply",
     "residual", "residual_fast", "nls_bruteforce", "frob_sq", "projected_gradient", "stop_index", "solve",
-    "rangefinder_adaptive", "solve_lai_ir", "bpp_nnls", "bpp_update",
+    "rangefinder_adaptive", "solve_lai_ir", "bpp_nnls", "bpp_update", "half_step",
 ]
 
 TWO40 = float(2 ** 40)
@@ -301,37 +301,43 @@ def iterate(A, W0, H0, alpha: float, iters: int, mode: str = "exact", s: int = 0
     A64 = as_f64(A) if mode != "lai" else None      # LAI never touches A
     W = np.array(W0, dtype=np.float64, copy=True)
     H = np.array(H0, dtype=np.float64, copy=True)
-    k = H.shape[1]
     trace = []
     for t in range(iters):
         it = first_iter + t
         for side in (0, 1):
-            F, X = (H, W) if side == 0 else (W, H)
-            if mode == "exact":
-                G, Y = gram(F), ah(A64, F)
-                st = {}
-            elif mode == "lai":
-                G, Y = gram(F), lai_apply(U, lam, F)
-                st = {}
-            elif mode == "lvs":
-                if plans is not None:
-                    pl = plans[(it, side)]
-                else:
-                    lev32 = leverage_scores(F).astype(np.float32)
-                    pl = build_plan(lev32, k, s, tau, seed, it, side)
-                G, Y = sampled_products(A64, F, pl["uniq_idx"], pl["uniq_w"])
-                st = {"s_D": pl["s_D"], "s_R": pl["s_R"], "n_uniq": pl["n_uniq"], "theta": pl["theta"]}
-                if record:
-                    st["plan"] = pl
-            else:
-                raise ValueError(mode)
-            Xn = hals_sweep(G, Y, F, X, alpha) if rule == "hals" else bpp_update(G, Y, F, alpha)
-            if side == 0:
-                W = Xn
-            else:
-                H = Xn
+            W, H, st = half_step(A64, W, H, alpha, it, side, mode, s=s, tau=tau, seed=seed, U=U, lam=lam,
+                                 plans=plans, record=record, rule=rule)
             trace.append(dict(it=it, side=side, **st))
     return W, H, trace
+
+
+def half_step(A64, W, H, alpha: float, it: int, side: int, mode: str = "exact", s: int = 0, tau: float = 1.0,
+              seed: int = 0, U=None, lam=None, plans=None, record=False, rule: str = "hals"):
+    """One half of O-11 / O-13 (Alg. LvS-SymNMF lines 682-689 for side 0, 690-696 for side 1;
+    LAI-SymNMF P:417-424): F = H, X = W (side 0) or F = W, X = H (side 1); X <- Update(G + alpha I,
+    Y + alpha F^T).  A64 is the fp64 A of as_f64 (None for LAI).  Returns (W, H, stats)."""
+    F, X = (H, W) if side == 0 else (W, H)
+    k = F.shape[1]
+    if mode == "exact":
+        G, Y = gram(F), ah(A64, F)
+        st = {}
+    elif mode == "lai":
+        G, Y = gram(F), lai_apply(U, lam, F)
+        st = {}
+    elif mode == "lvs":
+        if plans is not None:
+            pl = plans[(it, side)]
+        else:
+            lev32 = leverage_scores(F).astype(np.float32)
+            pl = build_plan(lev32, k, s, tau, seed, it, side)
+        G, Y = sampled_products(A64, F, pl["uniq_idx"], pl["uniq_w"])
+        st = {"s_D": pl["s_D"], "s_R": pl["s_R"], "n_uniq": pl["n_uniq"], "theta": pl["theta"]}
+        if record:
+            st["plan"] = pl
+    else:
+        raise ValueError(mode)
+    Xn = hals_sweep(G, Y, F, X, alpha) if rule == "hals" else bpp_update(G, Y, F, alpha)
+    return (Xn, H, st) if side == 0 else (W, Xn, st)
 
 
 # ----------------------------------------------------------------------- O-12
