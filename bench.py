@@ -5,8 +5,9 @@ python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--mode lvs|ex
                 [--impl ours|reference]
 
 A step is one full iteration (W-half + H-half) of the solver of config
-`--config` (default configs[1] = c2, mode LvS: CholeskyQR scores, hybrid plan,
-sampled Gram, sampled product, HALS sweep with the next Gram fused), replayed
+`--config` (default c4 -- the largest single-GPU configuration of BASELINE.json with both modes of the
+metric -- mode LvS: CholeskyQR scores, hybrid plan, sampled Gram, sampled product, HALS sweep with
+the next Gram fused), replayed
 from the solver's captured CUDA graph with inputs resident in HBM.  L2 is
 flushed (256 MiB write) before every timed step.  N > 1 runs N independent
 replicas (the single-GPU north star does not shard; weak
@@ -38,7 +39,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c4")
     ap.add_argument("--mode", default=None, choices=[None, "lvs", "exact", "lai"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rule", default="hals", choices=["hals", "bpp"], help="Update(): HALS sweep or BPP (NEXT-1)")
@@ -151,8 +152,8 @@ def kernel_cost(name, n, k, nnz=0, nnz_u=0, n_u=0, l=0, zeroY=False):
         return 8 * nnz_u + 16 * n_u + 4 * n_u * k + 12 * n * k, 2 * nnz_u * k + 2 * n * k * k
     if name == "bpp_update":   # read Y, F, write X (+ Y re-zero in LvS); pivoting solves are fp64 ALU work
         return (20 if zeroY else 16) * n * k, None
-    if name == "hals_sweep":
-        return (20 if zeroY else 16) * n * k, 2 * n * k * k
+    if name == "hals_sweep":   # read Y, X, F, write X (a re-zero of Y is not method bytes)
+        return 16 * n * k, 2 * n * k * k
     if name == "leverage":
         return 4 * n * k + 4 * n, n * k * k
     if name == "sampled_gram":
@@ -172,57 +173,90 @@ def kernel_cost(name, n, k, nnz=0, nnz_u=0, n_u=0, l=0, zeroY=False):
     return None, None
 
 
+# ------------------------------------------------------------------ workload description (both arms)
+def precision_of(d):
+    A = d["A"]
+    dense = not hasattr(A, "rowptr")
+    return "3xtf32" if dense and d["n"] % 4 == 0 else "fp32"
+
+
+def config_dict(args, d, ws):
+    """The `config` object of the JSON line; identical in our arm and the reference arm."""
+    cfg, A, n = d["cfg"], d["A"], d["n"]
+    dense = not hasattr(A, "rowptr")
+    lvs = args.mode == "lvs"
+    return {"workload": args.config, "n": n, "nnz": int(n * n if dense else A.nnz), "k": cfg.k, "mode": args.mode,
+            "rule": args.rule, "precision": precision_of(d), "s": cfg.s if lvs else None,
+            "tau": cfg.tau if lvs else None, "l": cfg.l or None, "q": cfg.q or None,
+            "l2": "flushed (256 MiB write) before every timed step", "parallelism": f"replicas{ws}",
+            "graph": "per-iteration CUDA graph replay (PDL edges)"}
+
+
 # ------------------------------------------------------------------ reference arm: the oracle on host cores
-def oracle_steps(args, d, steps, warmup, budget_s=None):
-    import numpy as np
-    import oracle as O
-    cfg = d["cfg"]
-    A, alpha = d["A"], d["alpha"]
-    kw = {}
-    if args.mode == "lvs":
-        kw = dict(s=cfg.s, tau=cfg.tau, seed=cfg.seed)
-    elif args.mode == "lai":
-        U, lam, _ = O.rangefinder(A, cfg.l, cfg.q, seed=cfg.seed)
-        kw = dict(U=U, lam=lam)
-    W = H = d["H0"].astype(np.float64)
-    it = 0
-    for _ in range(warmup):
-        W, H, _ = O.iterate(A, W, H, alpha, 1, args.mode, first_iter=it, rule=args.rule, **kw)
-        it += 1
-    t0 = time.perf_counter()
-    done = 0
-    while done < steps:
-        W, H, _ = O.iterate(A, W, H, alpha, 1, args.mode, first_iter=it, rule=args.rule, **kw)
-        it += 1
-        done += 1
-        if budget_s is not None and time.perf_counter() - t0 > budget_s:
-            break
-    return done, time.perf_counter() - t0
+class OracleRun:
+    """The fp64 oracle (oracle/) advanced one half-iteration at a time (oracle.half_step, the body of
+    oracle.iterate), so that a bounded sample of the workload can be timed."""
+
+    def __init__(self, args, d):
+        import numpy as np
+        import oracle as O
+        self.O, self.args, self.d = O, args, d
+        cfg = d["cfg"]
+        self.kw = {}
+        if args.mode == "lvs":
+            self.kw = dict(s=cfg.s, tau=cfg.tau, seed=cfg.seed)
+        elif args.mode == "lai":
+            U, lam, _ = O.rangefinder(d["A"], cfg.l, cfg.q, seed=cfg.seed)
+            self.kw = dict(U=U, lam=lam)
+        self.A64 = O.as_f64(d["A"]) if args.mode != "lai" else None
+        self.W = d["H0"].astype(np.float64)
+        self.H = d["H0"].astype(np.float64)
+        self.halves = 0
+
+    def half(self):
+        it, side = divmod(self.halves, 2)
+        self.W, self.H, _ = self.O.half_step(self.A64, self.W, self.H, self.d["alpha"], it, side, self.args.mode,
+                                             rule=self.args.rule, **self.kw)
+        self.halves += 1
 
 
 def run_reference(args, rank, ws):
+    """The oracle as it stands, on this host's cores: one step = one half-iteration (W- or H-update,
+    alternating), so value = steps / 2 / seconds iterations per second."""
     from synth import make_input
     if rank != 0:
         return None
     d = make_input(args.config)
-    cfg = d["cfg"]
-    done, dt = oracle_steps(args, d, args.steps, args.warmup)
-    v = done / dt
-    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": done,
-            "warmup": args.warmup, "ms_per_step": 1e3 * dt / done, "higher_is_better": True,
+    run = OracleRun(args, d)
+    for _ in range(args.warmup):
+        run.half()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run.half()
+    dt = time.perf_counter() - t0
+    v = args.steps / 2 / dt
+    sample = (f"{args.steps} oracle half-iterations (after {args.warmup} untimed) of {args.config} {args.mode} "
+              f"at full n; one step = one half-iteration")
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "n": d["n"], "k": cfg.k, "mode": args.mode,
-                       "s": cfg.s if args.mode == "lvs" else None, "tau": cfg.tau if args.mode == "lvs" else None},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-                             "sample": f"{done} full oracle {args.mode} iterations of {args.config}"},
+            "config": config_dict(args, d, ws),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
 def cpu_baseline(args, d):
-    steps = 10 ** 6
-    done, dt = oracle_steps(args, d, steps, 0, budget_s=args.cpu_budget)
-    return {"value": done / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-            "sample": f"first {done} oracle {args.mode} iterations of {args.config} (full n), "
+    """The oracle on a bounded sample: as many half-iterations of the full workload as fit in
+    --cpu-budget seconds (at least one)."""
+    run = OracleRun(args, d)
+    t0 = time.perf_counter()
+    while True:
+        run.half()
+        if time.perf_counter() - t0 > args.cpu_budget:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": run.halves / 2 / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"first {run.halves} oracle half-iterations of {args.config} {args.mode} (full n), "
                       f"~{args.cpu_budget:.0f} s budget"}
 
 
@@ -240,7 +274,7 @@ def run_ours(args, ws, rank, local, pg):
     A, H0, alpha = d["A"], d["H0"], d["alpha"]
     n, k = d["n"], cfg.k
     dense = not hasattr(A, "rowptr")
-    precision = "3xtf32" if dense and n % 4 == 0 else "fp32"
+    precision = precision_of(d)
     M = S.DeviceMatrix.from_host(A)
     W = torch.from_numpy(H0).to(dev)
     H = torch.from_numpy(H0).to(dev)
@@ -409,11 +443,7 @@ def run_ours(args, ws, rank, local, pg):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": args.config, "n": n, "nnz": int(nnz), "k": k, "mode": args.mode, "rule": args.rule,
-                       "precision": precision, "s": cfg.s if args.mode == "lvs" else None,
-                       "tau": cfg.tau if args.mode == "lvs" else None, "l": cfg.l or None, "q": cfg.q or None,
-                       "l2": "flushed (256 MiB write) before every timed step", "parallelism": f"replicas{ws}",
-                       "graph": "per-iteration CUDA graph replay (PDL edges)"},
+            "config": config_dict(args, d, ws),
             **extra,
             "lvs_stats_mean": ({"s_D": statistics.mean(h["s_D"] for h in halves),
                                 "n_uniq": statistics.mean(h["n_uniq"] for h in halves), "nnz_U": nnz_u}
@@ -421,6 +451,10 @@ def run_ours(args, ws, rank, local, pg):
             "roofline": roof, "kernels": kernels, "clocks": clk, "e2e": e2e,
             "gpu_launches": kernels_per_iter * args.steps, "kernels_per_step": kernels_per_iter,
             "memsets_per_step": memsets_per_iter}
+    if "exact_iters_per_s" in extra:   # LvS vs deterministic per iteration, next to the paper's CPU figure
+        line["lvs_over_exact"] = {"ratio": value / extra["exact_iters_per_s"], "paper": 5.5,
+                                  "paper_context": "LvS-HALS vs HALS per iteration, OAG n=37.7M k=16, 8x Xeon "
+                                                   "6226 CPU, MATLAB (P:1214); context, not a target"}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, d)
     solver.close()

@@ -857,7 +857,6 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     if (S.bucket) {
       // sampled nonzeros counting-sorted by destination row; the sweep pulls Y_s from the buckets
       launch_bucket_build(S.A, S.plan.uniq_idx, S.plan.counts + 2, S.bk, S.counter + 1, status, st);
-      mark(S, st, "bucket_build");
       cudaStreamWaitEvent(st, S.ev_join[side], 0);
       if (bucket_fused()) {
         launch_bucket_tile_sweep(S.bk, S.Zt, F, S.Gs, S.alpha, X, n, k, S.Gacc, Gnext, S.Rinv32, S.counter, status,
@@ -869,7 +868,7 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
         launch_bucket_pull(S.bk, S.Zt, n, k, S.Y, status, st);
       else
         launch_bucket_spmm(S.bk.off, S.bk.ent, n, S.A.nnz, S.Zt, k, S.Y, S.bchunk, S.bcarry, status, st);
-      mark(S, st, "bucket_pull");
+      mark(S, st, "sampled_ah_csr");   // bucket build + pull: the sampled product (a9)
       enqueue_sweep(S, side, S.Gs, F, X, false, Gnext, S.Rinv32, status, st);
       mark(S, st, "hals_sweep");
       return true;

@@ -22,8 +22,8 @@
 
 namespace symnmf {
 
-constexpr int kBucketChunk = 1024;   // sampled nonzeros per warp chunk (32 per lane)
-constexpr int kBucketUnroll = 4;     // independent entries in flight per lane
+constexpr int kBucketChunk = 2048;   // sampled nonzeros per warp chunk (64 per lane)
+constexpr int kBucketUnroll = 8;     // independent entries in flight per lane
 
 // ---------------------------------------------------------------- plan_row_offsets (two passes)
 constexpr int kPlanTile = 1024;   // plan rows per CTA (256 threads x 4)
@@ -111,6 +111,23 @@ __device__ __forceinline__ int64_t row_of_entry(const int64_t* __restrict__ pre,
   return lo;
 }
 
+// The same search by a whole warp: 32-ary steps (each lane probes one split point), so a chunk's
+// bounds cost ~log32(nu) dependent loads instead of log2(nu).  Largest t < cnt with pre[t] <= j.
+__device__ __forceinline__ int64_t warp_row_of_entry(const int64_t* __restrict__ pre, int64_t cnt, int64_t j,
+                                                     int lane) {
+  int64_t lo = 0, len = cnt;                          // answer in [lo, lo + len)
+  while (len > 1) {
+    const int64_t step = (len + 31) / 32;
+    const int64_t p = lo + (int64_t)lane * step;      // lane probes the start of its segment
+    const bool le = p < lo + len && __ldg(pre + p) <= j;
+    const unsigned m = __ballot_sync(0xffffffffu, le);
+    const int last = 31 - __clz(m);                   // the last segment whose start is <= j (lane 0 always)
+    lo += (int64_t)last * step;
+    len = min64(step, len - (int64_t)last * step);
+  }
+  return lo;
+}
+
 // Visit every sampled nonzero in nnz-balanced warp chunks: fn(t, e) with t the plan slot and e the
 // nonzero of A.  Each lane keeps kBucketUnroll entries in flight.
 template <class Fn>
@@ -122,8 +139,8 @@ __device__ __forceinline__ void for_sampled_nonzeros(const int64_t* __restrict__
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t ch = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; ch < nchunks; ch += nw) {
     const int64_t j0 = ch * kBucketChunk, j1 = min64(total, j0 + kBucketChunk);
-    const int64_t thi = row_of_entry(pre, 0, nu - 1, j1 - 1);
-    int64_t tcur = row_of_entry(pre, 0, thi, j0);
+    const int64_t thi = warp_row_of_entry(pre, nu, j1 - 1, lane);
+    int64_t tcur = warp_row_of_entry(pre, thi + 1, j0, lane);
     for (int64_t jb = j0; jb < j1; jb += 32 * kBucketUnroll) {
       int64_t t[kBucketUnroll], e[kBucketUnroll];
 #pragma unroll
