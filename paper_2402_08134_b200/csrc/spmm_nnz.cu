@@ -54,13 +54,16 @@ __global__ void spmm_nnz_rows_kernel(Src src, int64_t n, int64_t total, const in
 }
 
 template <int KP, class Src>
-__global__ void __launch_bounds__(256) spmm_nnz(Src src, int64_t total, const int32_t* __restrict__ total_dev,
-                                                const int64_t* __restrict__ chunk_row, const float4* __restrict__ F4,
-                                                float4* __restrict__ Y4, float4* __restrict__ carry,
-                                                const int32_t* __restrict__ status) {
+__global__ void __launch_bounds__(256, 4) spmm_nnz(Src src, int64_t total, const int32_t* __restrict__ total_dev,
+                                                   const int64_t* __restrict__ chunk_row,
+                                                   const float4* __restrict__ F4, float4* __restrict__ Y4,
+                                                   float4* __restrict__ carry, const int32_t* __restrict__ status) {
   if (dev_failed(status)) return;
-  constexpr int LPR = KP / 4;
-  const int li = threadIdx.x % LPR;
+  constexpr int LPR = KP / 4;                        // lanes per group (float4 each)
+  constexpr int LG = LPR < kGather ? LPR : kGather;  // lanes that load a batch's entries
+  constexpr int PER = kGather / LG;                  // entries each loading lane holds
+  const int lane = threadIdx.x & 31, li = lane % LPR;
+  const unsigned gmask = (LPR == 32 ? 0xffffffffu : ((1u << LPR) - 1u) << (lane - li));
   const int64_t nnz = total_dev ? (int64_t)*total_dev : total;
   const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / LPR;
   const int64_t nchunks = (nnz + kChunk - 1) / kChunk;
@@ -74,27 +77,26 @@ __global__ void __launch_bounds__(256) spmm_nnz(Src src, int64_t total, const in
       if (rstart >= s0 && rend <= s1) Y4[r * LPR + li] = acc;                 // complete in this chunk
       else carry[(2 * g + (r == rf ? 0 : 1)) * LPR + li] = acc;               // shared with a neighbour
     };
-    // prefetched entries of the next batch
-    int cn[kGather];
-    float an[kGather];
-#pragma unroll
-    for (int u = 0; u < kGather; ++u) {
-      if (s0 + u < s1) src.load(s0 + u, cn[u], an[u]); else { cn[u] = 0; an[u] = 0.f; }
-    }
     for (int64_t e = s0; e < s1; e += kGather) {
+      // the batch's entries: lane li < LG loads entries e + li + LG p (coalesced), shared by shuffles
+      int cm[PER];
+      float am[PER];
+#pragma unroll
+      for (int p = 0; p < PER; ++p) {
+        const int64_t ej = e + li + LG * p;
+        if (li < LG && ej < s1) src.load(ej, cm[p], am[p]); else { cm[p] = 0; am[p] = 0.f; }
+      }
       int cc[kGather];
       float aa[kGather];
-      float4 ff[kGather];
 #pragma unroll
-      for (int u = 0; u < kGather; ++u) { cc[u] = cn[u]; aa[u] = an[u]; }
+      for (int u = 0; u < kGather; ++u) {
+        cc[u] = __shfl_sync(gmask, cm[u / LG], u % LG, LPR);
+        aa[u] = __shfl_sync(gmask, am[u / LG], u % LG, LPR);
+      }
+      float4 ff[kGather];
 #pragma unroll
       for (int u = 0; u < kGather; ++u)
         ff[u] = (e + u < s1) ? __ldg(F4 + (int64_t)cc[u] * LPR + li) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int u = 0; u < kGather; ++u) {   // next batch's entries in flight during this batch
-        const int64_t en = e + kGather + u;
-        if (en < s1) src.load(en, cn[u], an[u]); else { cn[u] = 0; an[u] = 0.f; }
-      }
 #pragma unroll
       for (int u = 0; u < kGather; ++u) {
         const int64_t ei = e + u;

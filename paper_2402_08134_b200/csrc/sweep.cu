@@ -3,11 +3,13 @@
 // P:690) and, in the last CTA, its Cholesky factor (CholeskyQR).
 //
 // sweep_stream<KP>: persistent CTAs of 256 threads, one 256-row tile per step, thread r owning row r.
-// The tile's rows of Y, F and X are brought into shared memory with cp.async (16 B chunks, coalesced,
-// in flight while the previous tile computes), stored with a 16 B-chunk XOR swizzle so that a thread
-// reading its own row is bank-conflict free; b = y + alpha f and x are then held in registers, the
-// Gauss-Seidel pass over the k columns runs on them with G (+alpha I) broadcast from shared memory,
-// and the new row goes through a swizzled output tile for coalesced stores and the tile Gram.
+// The tile's rows of Y, F and X are brought into shared memory with cp.async (16 B chunks, coalesced),
+// stored with a padded row stride (k + 4 floats) so that a thread reading its own row and a row group
+// reading one row are bank-conflict free; x is held in registers, b = y + alpha f read a chunk at a
+// time, and the Gauss-Seidel pass over the k columns takes G (+alpha I) from the constant bank (or
+// shared memory).  The new row replaces the old one in the tile, which is then stored coalesced and
+// accumulated into the tile Gram (fp32 per tile, fp64 registers across tiles).  Two CTAs per SM:
+// one stages its next tile while the other computes.
 // Bytes per row: Y, F, X read, X written (+ Y re-zeroed for the scatter paths): 16k (20k) B.
 #include <atomic>
 #include "fused_common.cuh"
@@ -18,19 +20,13 @@ template <int KP>
 struct SwL {
   static constexpr int C = KP / 4;              // 16 B chunks per row
   static constexpr int TR = 256;                // rows per tile = threads
-  static constexpr size_t arr = sizeof(float) * TR * KP;
+  static constexpr int ST = KP + 4;             // padded row stride (floats): a thread reading its own
+                                                // row and a row group reading one row are conflict free
+  static constexpr size_t arr = sizeof(float) * TR * ST;
   static constexpr size_t y = 0, f = arr, x = 2 * arr;
   static constexpr size_t bytes = 3 * arr;      // Y, F, X staging (X rewritten in place)
   static constexpr int per_sm = KP <= 8 ? 3 : 2;   // 128 registers per thread for k = 16, 32
 };
-
-// chunk c of row r lives at chunk position swz(c, r): the 8 rows a quarter-warp reads hit 8
-// distinct 16 B bank groups (rows are KP * 4 B; 128 B hold 8 / C rows)
-template <int KP>
-__device__ __forceinline__ int swz(int c, int r) {
-  constexpr int C = KP / 4, RPL = 8 / C;   // rows per 128 B line
-  return c ^ ((r / RPL) % C);
-}
 
 // Constant-bank copies of the sweep's G (G_off^T, 1 / (G_ii + alpha), ok flags), one per (solver
 // slot, half): with G in the constant bank every FMA of the column loop takes its G operand
@@ -66,7 +62,7 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
   using L = SwL<KP>;
   constexpr int C = L::C, TR = L::TR;
   constexpr int NB = KP / 4, PAIRS = NB * (NB + 1) / 2, RG = TR / PAIRS;
-  constexpr int RPL = 8 / C;                      // rows per 128 B line (swizzle period: C * RPL rows)
+  constexpr int ST = L::ST;
   __shared__ __align__(16) float sG[TAB < 0 ? KP * KP : 4];   // sG[i*KP + j] = G[j][i], 0 on the diagonal
   __shared__ float sInv[KP];
   __shared__ int sOk[KP];
@@ -112,7 +108,7 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
     for (int q = tid; q < TR * C; q += TR) {
       const int r = q / C, c = q - r * C;
       const bool ok = r < rows;
-      const int so = r * KP + 4 * swz<KP>(c, r);
+      const int so = r * ST + 4 * c;
       const int64_t go = ok ? (r0 + r) * KP + 4 * c : 0;
       cp_async16(sY + so, Y + go, ok);
       cp_async16(sF + so, F + go, ok);
@@ -128,14 +124,14 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
     float x[KP];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-      const float4 x4 = *reinterpret_cast<const float4*>(sX + tid * KP + 4 * swz<KP>(c, tid));
+      const float4 x4 = *reinterpret_cast<const float4*>(sX + tid * ST + 4 * c);
       x[4 * c] = x4.x; x[4 * c + 1] = x4.y; x[4 * c + 2] = x4.z; x[4 * c + 3] = x4.w;
     }
     // Gauss-Seidel over the columns of row tid: x_i <- [(b_i - sum_{j != i} G_ij x_j) / (G_ii + alpha)]_+,
     // b = y + alpha f read a 16 B chunk at a time
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-      const int so = tid * KP + 4 * swz<KP>(c, tid);
+      const int so = tid * ST + 4 * c;
       const float4 y4 = *reinterpret_cast<const float4*>(sY + so);
       const float4 f4 = *reinterpret_cast<const float4*>(sF + so);
       const float bc[4] = {fmaf(a32, f4.x, y4.x), fmaf(a32, f4.y, y4.y), fmaf(a32, f4.z, y4.z),
@@ -159,30 +155,36 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
     const bool live = tid < rows;
 #pragma unroll
     for (int c = 0; c < C; ++c)   // the new row replaces the old one in the staging tile
-      *reinterpret_cast<float4*>(sX + tid * KP + 4 * swz<KP>(c, tid)) =
+      *reinterpret_cast<float4*>(sX + tid * ST + 4 * c) =
           live ? make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
     {
       float4* X4 = reinterpret_cast<float4*>(X) + r0 * C;
       for (int q = tid; q < rows * C; q += TR) {
         const int r = q / C, c = q - r * C;
-        X4[q] = *reinterpret_cast<const float4*>(sX + r * KP + 4 * swz<KP>(c, r));
+        X4[q] = *reinterpret_cast<const float4*>(sX + r * ST + 4 * c);
       }
     }
     if (gactive) {   // tile Gram of the new rows
       float acc[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) acc[e] = 0.f;
-      for (int r = gg; r < rows; r += RG) {
-        const int xr = (r / RPL) % C;                 // swizzle of row r (swz)
-        const float4 a4 = *reinterpret_cast<const float4*>(sX + r * KP + 4 * (ai ^ xr));
-        const float4 b4 = *reinterpret_cast<const float4*>(sX + r * KP + 4 * (bi ^ xr));
+      const float* pa = sX + gg * ST + 4 * ai;
+      const float* pb = sX + gg * ST + 4 * bi;
+      int r = gg;
+      auto step = [&](int o) {
+        const float4 a4 = *reinterpret_cast<const float4*>(pa + o);
+        const float4 b4 = *reinterpret_cast<const float4*>(pb + o);
         const float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
           for (int j = 0; j < 4; ++j) acc[i * 4 + j] = fmaf(av[i], bv[j], acc[i * 4 + j]);
+      };
+      for (; r + 3 * RG < rows; r += 4 * RG, pa += 4 * RG * ST, pb += 4 * RG * ST) {
+        step(0); step(RG * ST); step(2 * RG * ST); step(3 * RG * ST);
       }
+      for (; r < rows; r += RG, pa += RG * ST, pb += RG * ST) step(0);
 #pragma unroll
       for (int e = 0; e < 16; ++e) acc64[e] += (double)acc[e];
     }
