@@ -119,7 +119,11 @@ typedef struct {
  *                                  partial products through an n x k buffer, the last pass fused
  *                                  with the sweep); default ceil(4 n k / 64 MB), so the rows of F a
  *                                  pass gathers stay resident in L2.
- *   SYMNMF_BUCKET=always|never     LvS solver on CSR (k in {8,16,32,64}): force / forbid the
+ *   SYMNMF_SAMPLED=scatter|bucket|mark  LvS solver on CSR (k in {8,16,32,64}): the sampled product as the
+ *                                  vector-atomic scatter (default below 16M nonzeros), destination
+ *                                  buckets, or mirror marks (default from 16M: each sampled nonzero
+ *                                  flags its mirror position, destination rows pull the flags).
+ *   SYMNMF_BUCKET=always|never     (older knob) LvS solver on CSR: force / forbid the
  *                                  destination-bucketed sampled product (counting sort by
  *                                  destination row, then a pull); default: used from 16M nonzeros.
  *   SYMNMF_BUCKET_FUSED=1          bucketed LvS: pull inside the row-tile sweep kernel.

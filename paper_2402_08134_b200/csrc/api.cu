@@ -589,6 +589,10 @@ struct symnmf_solver {
   double* hw;
   int64_t* hcounts;
   double* hmass;
+  bool markp;              // LvS on a large CSR A (kpad(k) == k): mirror-marked sampled product (default)
+  int32_t* mirror;         // [nnz] position of (c, r) in row c
+  uint32_t* bits;          // flagged mirror positions (kept zero between plans)
+  int32_t* slot_of;        // [n] plan slot of a sampled row
   bool bucket;             // LvS on a large CSR A (kpad(k) == k): destination-bucketed sampled product
   BucketWs bk;
   float* Zt;               // bucket gather table Z[t] = omega_t f_{u_t} (cap x k)
@@ -684,13 +688,18 @@ bool csr_spmm_nnz() {
   return !(e && !strcmp(e, "rows"));
 }
 
-// LvS CSR: the destination-bucketed sampled product fused into the sweep from 16M nonzeros;
-// SYMNMF_BUCKET=always|never overrides (symnmf.h)
-int64_t bucket_min_nnz() {
-  const char* e = getenv("SYMNMF_BUCKET");
-  if (e && !strcmp(e, "always")) return 0;
-  if (e && !strcmp(e, "never")) return INT64_MAX;
-  return 16ll << 20;
+// LvS CSR sampled product (symnmf.h SYMNMF_SAMPLED=scatter|bucket|mark): 0 = vector-atomic scatter
+// (default below 16M nonzeros), 1 = destination buckets, 2 = mirror marks (default from 16M)
+int sampled_path(int64_t nnz) {
+  if (nnz < 0) return 0;
+  const char* e = getenv("SYMNMF_SAMPLED");
+  if (e && !strcmp(e, "scatter")) return 0;
+  if (e && !strcmp(e, "bucket")) return 1;
+  if (e && !strcmp(e, "mark")) return 2;
+  const char* b = getenv("SYMNMF_BUCKET");   // older knob: always -> bucket, never -> scatter
+  if (b && !strcmp(b, "always")) return 1;
+  if (b && !strcmp(b, "never")) return 0;
+  return nnz >= (16ll << 20) ? 2 : 0;
 }
 
 // LvS bucket path: the sampled product pulled into Y then the streaming sweep (default), or
@@ -752,8 +761,13 @@ void solver_layout(symnmf_solver& S, Carver& c) {
   S.carry = c.take<float>(S.nnzsp ? spmm_nnz_carry_floats(S.A.nnz, k) : 0);
   S.nblk = S.tile ? csr_blocks(n, k) : 1;
   S.cuts = c.take<int64_t>(S.tile ? (size_t)(S.nblk - 1) * n : 0);
-  S.bucket = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode == SYMNMF_LVS && !S.bpp &&
-             S.A.nnz < (int64_t)INT32_MAX && S.A.nnz >= bucket_min_nnz();
+  {
+    const bool big = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode == SYMNMF_LVS && !S.bpp &&
+                     S.A.nnz < (int64_t)INT32_MAX;
+    const int path = sampled_path(big ? S.A.nnz : -1);
+    S.markp = big && path == 2;
+    S.bucket = big && path == 1;
+  }
   S.ctab = c.take<float>(sweep_table_floats());
   S.nonconv = c.take<int32_t>(1);
   S.Y = c.take<float>((S.tile && S.nblk == 1) || (S.bucket && bucket_fused()) ? 0 : (size_t)n * k);
@@ -785,6 +799,15 @@ void solver_layout(symnmf_solver& S, Carver& c) {
     S.hw = c.take<double>(halves * S.plan.cap);
     S.hcounts = c.take<int64_t>(halves * 4);
     S.hmass = c.take<double>(halves * 2);
+    if (S.markp) {
+      mark_layout(c, n, S.A.nnz, S.plan.cap, &S.bk);
+      S.Zt = c.take<float>((size_t)S.plan.cap * k);
+      S.mirror = c.take<int32_t>((size_t)S.A.nnz);
+      S.bits = c.take<uint32_t>((size_t)spmm_nnz_chunks(S.A.nnz) * 8 + 8);
+      S.slot_of = c.take<int32_t>((size_t)n);
+      S.bchunk = c.take<int64_t>((size_t)spmm_nnz_chunks(S.A.nnz));
+      S.bcarry = c.take<float>(spmm_nnz_carry_floats(S.A.nnz, k));
+    }
     if (S.bucket) {
       bucket_layout(c, n, S.A.nnz, S.plan.cap, &S.bk);
       S.Zt = c.take<float>((size_t)S.plan.cap * k);
@@ -852,8 +875,20 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     // G_s and Y_s only read the plan: G_s runs on a second branch of the graph, concurrently
     cudaEventRecord(S.ev_fork[side], st);
     cudaStreamWaitEvent(S.side, S.ev_fork[side], 0);
-    launch_sampled_gram_fused(F, k, S.plan, S.Gacc, S.Gs, S.counter, status, S.side, S.bucket ? S.Zt : nullptr);
+    launch_sampled_gram_fused(F, k, S.plan, S.Gacc, S.Gs, S.counter, status, S.side,
+                              (S.bucket || S.markp) ? S.Zt : nullptr);
     cudaEventRecord(S.ev_join[side], S.side);
+    if (S.markp) {
+      // sampled nonzeros flag their mirror positions; each destination row pulls its flagged entries
+      launch_mark_sampled(S.A, S.plan.uniq_idx, S.plan.counts + 2, S.bk, S.mirror, S.bits, S.slot_of,
+                          S.counter + 1, status, st);
+      cudaStreamWaitEvent(st, S.ev_join[side], 0);
+      launch_mark_pull(S.A, S.bchunk, S.bits, S.slot_of, S.Zt, k, S.Y, S.bcarry, status, st);
+      mark(S, st, "sampled_ah_csr");
+      enqueue_sweep(S, side, S.Gs, F, X, false, Gnext, S.Rinv32, status, st);
+      mark(S, st, S.bpp ? "bpp_update" : "hals_sweep");
+      return true;
+    }
     if (S.bucket) {
       // sampled nonzeros counting-sorted by destination row; the sweep pulls Y_s from the buckets
       launch_bucket_build(S.A, S.plan.uniq_idx, S.plan.counts + 2, S.bk, S.counter + 1, status, st);
@@ -995,6 +1030,17 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
     if (hbad) return SYMNMF_ERR_ARG;
   }
   if (S.nnzsp) launch_spmm_nnz_rows(S.A, S.chunk_row, st);
+  if (S.markp) {
+    int32_t* bad = S.nonconv;
+    launch_mirror(S.A, S.mirror, bad, st);
+    int32_t hbad = 0;
+    SYMNMF_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    SYMNMF_CUDA_TRY(cudaStreamSynchronize(st));
+    SYMNMF_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int32_t), st));
+    if (hbad) return SYMNMF_ERR_ARG;   // the pattern of A is not symmetric
+    launch_spmm_nnz_rows(S.A, S.bchunk, st);
+    SYMNMF_CUDA_TRY(cudaMemsetAsync(S.bits, 0, sizeof(uint32_t) * ((size_t)spmm_nnz_chunks(S.A.nnz) * 8 + 8), st));
+  }
   set_i32<<<1, 1, 0, st>>>(S.iter_dev, first_iter);
   // H^T H (and its CholeskyQR factor for LvS) for the first W-half; later halves get
   // theirs from the fused Gram of the preceding sweep.

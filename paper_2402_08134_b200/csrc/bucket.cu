@@ -83,7 +83,8 @@ __global__ void __launch_bounds__(256) plan_row_write(const int64_t* __restrict_
                                                       const int32_t* __restrict__ uniq,
                                                       const int64_t* __restrict__ n_uniq_dev,
                                                       const int64_t* __restrict__ tsum, int64_t* __restrict__ pre,
-                                                      int64_t* __restrict__ rb, const int32_t* __restrict__ status) {
+                                                      int64_t* __restrict__ rb, int32_t* __restrict__ slot_of,
+                                                      const int32_t* __restrict__ status) {
   __shared__ int64_t sh[33];
   if (dev_failed(status)) return;
   const int64_t nu = *n_uniq_dev;
@@ -97,6 +98,7 @@ __global__ void __launch_bounds__(256) plan_row_write(const int64_t* __restrict_
     if (t0 + q < nu) {
       pre[t0 + q] = p;
       rb[t0 + q] = start[q] - p;
+      if (slot_of) slot_of[uniq[t0 + q]] = (int32_t)(t0 + q);
     }
     p += len[q];
   }
@@ -347,12 +349,76 @@ void launch_bucket_pull(const BucketWs& b, const float* Z, int64_t n, int k, flo
   }
 }
 
+static int bucket_grid(int64_t cap_entries);
+
+// ---------------------------------------------------------------- mirror marks (the default sampled product)
+// Each sampled nonzero e = (i, c) of A (i in U) flags its mirror position m(e) -- the place of (c, i)
+// in row c, precomputed once per A -- in a bitmap over the nonzeros; a pull over the rows of A then
+// reads, in each destination row c, exactly the flagged entries (c, i), i in U, in column order:
+// Y_s[c] = sum_i A[c, i] Z[slot(i)], deterministic and free of float atomics (spmm_nnz.cu).
+__global__ void __launch_bounds__(256) mark_sampled(const int32_t* __restrict__ mirror, const int64_t* __restrict__ pre,
+                                                    const int64_t* __restrict__ rb,
+                                                    const int64_t* __restrict__ n_uniq_dev, uint32_t* __restrict__ bits,
+                                                    const int32_t* __restrict__ status) {
+  if (dev_failed(status)) return;
+  const int64_t nu = *n_uniq_dev;
+  if (nu <= 0) return;
+  for_sampled_nonzeros(pre, rb, nu, [&](const int64_t (&t)[kBucketUnroll], const int64_t (&e)[kBucketUnroll]) {
+    int32_t m[kBucketUnroll];
+#pragma unroll
+    for (int u = 0; u < kBucketUnroll; ++u) m[u] = t[u] >= 0 ? __ldcs(mirror + e[u]) : 0;
+#pragma unroll
+    for (int u = 0; u < kBucketUnroll; ++u)
+      if (t[u] >= 0) atomicOr(bits + (m[u] >> 5), 1u << (m[u] & 31));
+  });
+}
+
+// mirror[e] = position of (c, r) in row c for e = (r, c); *bad = 1 if A's pattern is not symmetric
+__global__ void mirror_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, int64_t n,
+                              int32_t* __restrict__ mirror, int32_t* __restrict__ bad) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (r >= n) return;
+  const int lane = threadIdx.x & 31;
+  for (int64_t e = rowptr[r] + lane; e < rowptr[r + 1]; e += 32) {
+    const int64_t c = col[e];
+    int64_t lo = rowptr[c], hi = rowptr[c + 1];
+    while (lo < hi) {
+      const int64_t m = (lo + hi) >> 1;
+      if (col[m] < r) lo = m + 1; else hi = m;
+    }
+    if (lo < rowptr[c + 1] && col[lo] == r) mirror[e] = (int32_t)lo;
+    else { mirror[e] = 0; atomicExch(bad, 1); }
+  }
+}
+
+void launch_mirror(const symnmf_matrix& A, int32_t* mirror, int32_t* bad, cudaStream_t st) {
+  if (A.n > 0) mirror_kernel<<<(unsigned)((A.n + 7) / 8), 256, 0, st>>>(A.rowptr, A.colidx, A.n, mirror, bad);
+}
+
+void launch_mark_sampled(const symnmf_matrix& A, const int32_t* uniq, const int64_t* n_uniq_dev, const BucketWs& b,
+                         const int32_t* mirror, uint32_t* bits, int32_t* slot_of, unsigned int* counter,
+                         int32_t* status, cudaStream_t st) {
+  const int ptiles = (int)std::max<int64_t>(1, (b.cap + kPlanTile - 1) / kPlanTile);
+  launch_pdl(plan_row_sums, ptiles, 256, 0, st, A.rowptr, uniq, n_uniq_dev, b.ptsum, b.pre, counter, status);
+  launch_pdl(plan_row_write, ptiles, 256, 0, st, A.rowptr, uniq, n_uniq_dev, b.ptsum, b.pre, b.rb, slot_of, status);
+  launch_pdl(mark_sampled, bucket_grid(A.nnz), 256, 0, st, mirror, b.pre, b.rb, n_uniq_dev, bits, status);
+}
+
 // ---------------------------------------------------------------- launchers
 size_t bucket_ws_bytes(int64_t n, int64_t nnz, int64_t cap) {
   // pre, rb [cap + 1] int64; cnt, off [n + 1] int32; tsum; slot [nnz] int32; ent [nnz] int2
   return sizeof(int64_t) * 2 * (size_t)(cap + 1) + sizeof(int32_t) * 2 * (size_t)(n + 4) +
          sizeof(int32_t) * (size_t)(bucket_scan_tiles(n) + 4) + sizeof(int32_t) * (size_t)nnz +
          sizeof(int2) * (size_t)nnz + 6 * 256;
+}
+
+void mark_layout(Carver& c, int64_t n, int64_t nnz, int64_t cap, BucketWs* b) {   // plan-row offsets only
+  (void)n; (void)nnz;
+  *b = BucketWs{};
+  b->cap = cap;
+  b->ptsum = c.take<int64_t>((size_t)(cap + kPlanTile - 1) / kPlanTile + 4);
+  b->pre = c.take<int64_t>((size_t)cap + 1);
+  b->rb = c.take<int64_t>((size_t)cap + 1);
 }
 
 void bucket_layout(Carver& c, int64_t n, int64_t nnz, int64_t cap, BucketWs* b) {
@@ -377,7 +443,8 @@ void launch_bucket_build(const symnmf_matrix& A, const int32_t* uniq, const int6
   const int64_t n = A.n;
   const int ptiles = (int)std::max<int64_t>(1, (b.cap + kPlanTile - 1) / kPlanTile);
   launch_pdl(plan_row_sums, ptiles, 256, 0, st, A.rowptr, uniq, n_uniq_dev, b.ptsum, b.pre, counter, status);
-  launch_pdl(plan_row_write, ptiles, 256, 0, st, A.rowptr, uniq, n_uniq_dev, b.ptsum, b.pre, b.rb, status);
+  launch_pdl(plan_row_write, ptiles, 256, 0, st, A.rowptr, uniq, n_uniq_dev, b.ptsum, b.pre, b.rb,
+             (int32_t*)nullptr, status);
   const int grid = bucket_grid(A.nnz);
   launch_pdl(bucket_count, grid, 256, 0, st, A.colidx, b.pre, b.rb, n_uniq_dev, b.cnt, b.slot, status);
   const int tiles = (int)bucket_scan_tiles(n);

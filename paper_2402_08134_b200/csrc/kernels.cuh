@@ -154,8 +154,18 @@ struct BucketWs {
   int2* ent;         // [nnz] bucket entries (plan slot t, a_e)
 };
 void bucket_layout(Carver& c, int64_t n, int64_t nnz, int64_t cap, BucketWs* b);
+void mark_layout(Carver& c, int64_t n, int64_t nnz, int64_t cap, BucketWs* b);
 void launch_bucket_build(const symnmf_matrix& A, const int32_t* uniq, const int64_t* n_uniq_dev, const BucketWs& b,
                          unsigned int* counter, int32_t* status, cudaStream_t st);
+// Mirror marks (default LvS CSR sampled product): mirror[e] = position of (c, r) in row c (once per A;
+// *bad = 1 if the pattern is not symmetric); per plan, plan-row offsets, slot_of[u_t] = t and the
+// bitmap of flagged mirror positions; launch_mark_pull (spmm_nnz.cu) forms Y_s and clears the bitmap.
+void launch_mirror(const symnmf_matrix& A, int32_t* mirror, int32_t* bad, cudaStream_t st);
+void launch_mark_sampled(const symnmf_matrix& A, const int32_t* uniq, const int64_t* n_uniq_dev, const BucketWs& b,
+                         const int32_t* mirror, uint32_t* bits, int32_t* slot_of, unsigned int* counter,
+                         int32_t* status, cudaStream_t st);
+void launch_mark_pull(const symnmf_matrix& A, const int64_t* chunk_row, uint32_t* bits, const int32_t* slot_of,
+                      const float* Z, int k, float* Y, float* carry, const int32_t* status, cudaStream_t st);
 // Y_s (n x k, every row written) from the buckets with the gather table Z; kpad(k) == k.
 void launch_bucket_pull(const BucketWs& b, const float* Z, int64_t n, int k, float* Y, const int32_t* status,
                         cudaStream_t st);

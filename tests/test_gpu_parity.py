@@ -491,13 +491,13 @@ def test_csr_tile_exact_one_iteration(cfgname, n, k, tile, monkeypatch):
 
 
 @pytest.mark.parametrize("cfgname,n,k,s", [("c4", 40_000, 32, 800), ("c2", 20_000, 16, 400), ("c4", 40_000, 8, 2000)])
-@pytest.mark.parametrize("slice_mb", ["", "1", "bucket"])
+@pytest.mark.parametrize("slice_mb", ["", "1", "bucket", "mark"])
 def test_csr_lvs_solver_equals_abi_composition(cfgname, n, k, s, slice_mb, monkeypatch):
-    """Solver LvS on CSR graphs with hubs (destination-range scatter passes, fused Gram) equals
-    the composition of the ABI calls on the same device data; slice_mb = 1 forces several
-    destination-range passes of the sampled scatter; "bucket" the destination-bucketed sampled
-    product fused into the sweep (bucket.cu + tile.cu)."""
-    monkeypatch.setenv("SYMNMF_BUCKET", "always" if slice_mb == "bucket" else "never")
+    """Solver LvS on CSR graphs with hubs equals the composition of the ABI calls on the same device
+    data, for every form of the sampled product: the vector-atomic scatter ("", and slice_mb = 1:
+    several destination-range passes), the destination buckets ("bucket") and the mirror marks
+    ("mark", the default for large graphs)."""
+    monkeypatch.setenv("SYMNMF_SAMPLED", {"bucket": "bucket", "mark": "mark"}.get(slice_mb, "scatter"))
     if slice_mb == "1":
         monkeypatch.setenv("SYMNMF_SCATTER_SLICE_MB", slice_mb)
     A, H0, alpha = _csr_case(cfgname, n, k)
@@ -523,11 +523,11 @@ def test_csr_lvs_solver_equals_abi_composition(cfgname, n, k, s, slice_mb, monke
     assert rel(H1.cpu().numpy(), H2.cpu().numpy()) < 1e-5
 
 
-@pytest.mark.parametrize("bucket", ["always", "never"])
-def test_csr_lvs_replayed_plan_vs_oracle(bucket, monkeypatch):
+@pytest.mark.parametrize("path", ["mark", "bucket", "scatter"])
+def test_csr_lvs_replayed_plan_vs_oracle(path, monkeypatch):
     """One LvS half through the solver vs the oracle's sampled products + sweep fed the plan the
     GPU drew (the same plan is recomputed by the ABI sampler from the same device scores)."""
-    monkeypatch.setenv("SYMNMF_BUCKET", bucket)
+    monkeypatch.setenv("SYMNMF_SAMPLED", path)
     A, H0, alpha = _csr_case("c4", 30_016, 32)
     s, tau = 600, 1.0 / 600
     M = S.DeviceMatrix.from_host(A)
@@ -758,17 +758,18 @@ def test_csr_empty_rows(tile, monkeypatch):
     Wr, Hr, _ = O.iterate(A, H0, H0, alpha, 1, "exact")
     assert rel(W.cpu().numpy(), Wr) < 1e-5
     assert rel(H.cpu().numpy(), Hr) < 1e-5
-    # LvS, bucketed sampled product: W-half vs the oracle fed the plan the GPU draws
-    monkeypatch.setenv("SYMNMF_BUCKET", "always")
+    # LvS, bucketed and mirror-marked sampled products: W-half vs the oracle fed the plan the GPU draws
     s_, tau = 800, 1.0 / 800
-    W, H = cu(H0), cu(H0)
-    sv = S.Solver(M, W, H, alpha, mode="lvs", s=s_, tau=tau, seed=5, max_iters=1)
-    sv.run(1)
-    assert sv.stats()["status"] == 0
-    sv.close()
     ph = S.hybrid_sample(S.leverage_scores(cu(H0)), 16, s_, tau, 5, 0, 0).to_host()
     Gs, Ys = O.sampled_products(A, H0, ph["uniq_idx"], ph["uniq_w"])
-    assert rel(W.cpu().numpy(), O.hals_sweep(Gs, Ys, H0, H0, alpha)) < 1e-5
+    for path in ("bucket", "mark"):
+        monkeypatch.setenv("SYMNMF_SAMPLED", path)
+        W, H = cu(H0), cu(H0)
+        sv = S.Solver(M, W, H, alpha, mode="lvs", s=s_, tau=tau, seed=5, max_iters=1)
+        sv.run(1)
+        assert sv.stats()["status"] == 0
+        sv.close()
+        assert rel(W.cpu().numpy(), O.hals_sweep(Gs, Ys, H0, H0, alpha)) < 1e-5, path
 
 
 def test_csr_zero_matrix():
@@ -781,9 +782,11 @@ def test_csr_zero_matrix():
     M = S.DeviceMatrix.from_host(A)
     Y = S.ah(M, cu(H0)).cpu().numpy()
     assert not Y.any()
-    for mode, kw, env in (("exact", {}, "never"), ("lvs", dict(s=300, tau=1.0 / 300, seed=2), "never"),
-                          ("exact", {}, "always"), ("lvs", dict(s=300, tau=1.0 / 300, seed=2), "always")):
-        os.environ["SYMNMF_CSR_TILE"] = os.environ["SYMNMF_BUCKET"] = env   # EXACT: nnz SpMM / tile
+    lvs = dict(s=300, tau=1.0 / 300, seed=2)
+    for mode, kw, env, path in (("exact", {}, "never", ""), ("exact", {}, "always", ""), ("lvs", lvs, "", "scatter"),
+                                ("lvs", lvs, "", "bucket"), ("lvs", lvs, "", "mark")):
+        os.environ["SYMNMF_CSR_TILE"] = env   # EXACT: nnz SpMM / tile kernel
+        os.environ["SYMNMF_SAMPLED"] = path or "scatter"
         W, H = cu(H0), cu(H0)
         sv = S.Solver(M, W, H, alpha, mode=mode, max_iters=1, **kw)
         sv.run(1)
@@ -794,4 +797,4 @@ def test_csr_zero_matrix():
             Wr, Hr, _ = O.iterate(A, H0, H0, alpha, 1, "exact")
             assert rel(Wg, Wr) < 1e-5 and rel(H.cpu().numpy(), Hr) < 1e-5
         assert np.isfinite(Wg).all() and (Wg >= 0).all()
-    os.environ.pop("SYMNMF_CSR_TILE"); os.environ.pop("SYMNMF_BUCKET")
+    os.environ.pop("SYMNMF_CSR_TILE"); os.environ.pop("SYMNMF_SAMPLED")
