@@ -101,7 +101,11 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
   const int64_t tiles = (n + TR - 1) / TR;
   __syncthreads();
 
-  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+  // tiles last to first: the product that wrote Y finished with its highest rows, which are the
+  // ones still resident in L2; the sweep then ends on the lowest rows, where the next half's
+  // leverage / product kernels start
+  for (int64_t tt = blockIdx.x; tt < tiles; tt += gridDim.x) {
+    const int64_t t = tiles - 1 - tt;
     const int64_t r0 = t * TR;
     const int rows = (int)min64(TR, n - r0);
     // stage the tile's rows of Y, F, X (coalesced 16 B chunks, swizzled)
