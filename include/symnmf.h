@@ -111,22 +111,11 @@ typedef struct {
  * the same up to fp32 summation order):
  *   SYMNMF_CSR_SPMM=rows           EXACT solver on CSR (k in {8,16,32,64}): the row-group SpMM
  *                                  instead of the default nnz-balanced one (chunks of 256 nonzeros).
- *   SYMNMF_CSR_TILE=always         EXACT solver on CSR: the row-tile kernel (product fused with the
- *                                  sweep) instead of SpMM + streaming sweep.
  *   SYMNMF_SWEEP=fused             k in {8,16,32}: the register-tile sweep instead of the streaming
  *                                  (cp.async-staged) sweep.
- *   SYMNMF_CSR_BLOCKS=<m>          EXACT row-tile kernel: column blocks of A per product (m passes, the
- *                                  partial products through an n x k buffer, the last pass fused
- *                                  with the sweep); default ceil(4 n k / 64 MB), so the rows of F a
- *                                  pass gathers stay resident in L2.
- *   SYMNMF_SAMPLED=scatter|bucket|mark  LvS solver on CSR (k in {8,16,32,64}): the sampled product as the
- *                                  vector-atomic scatter (default below 16M nonzeros), destination
- *                                  buckets, or mirror marks (default from 16M: each sampled nonzero
- *                                  flags its mirror position, destination rows pull the flags).
- *   SYMNMF_BUCKET=always|never     (older knob) LvS solver on CSR: force / forbid the
- *                                  destination-bucketed sampled product (counting sort by
- *                                  destination row, then a pull); default: used from 16M nonzeros.
- *   SYMNMF_BUCKET_FUSED=1          bucketed LvS: pull inside the row-tile sweep kernel.
+ *   SYMNMF_SWEEP_CMEM=0            streaming sweep and leverage scores: G / R from shared memory
+ *                                  instead of the constant bank (a solver holds one of 4 constant
+ *                                  slots; beyond 4 live solvers the shared-memory form is used).
  *   SYMNMF_SCATTER_SLICE_MB=<mb>   sampled CSR scatter product: rows of Y per destination-range
  *                                  pass (default 86 MB, so each pass's slice of Y stays in L2).
  *   SYMNMF_LAI_FUSED=never         LAI solver (k = 64, l <= 80): use the four-kernel half (U^T F,

@@ -575,12 +575,9 @@ struct symnmf_solver {
   float* Y;
   bool bpp;                // Update rule: exact per-row NLS by block principal pivoting (NEXT-1)
   int32_t* nonconv;        // BPP rows that hit the pivoting cap (device counter)
-  bool tile;               // EXACT on a large CSR A (kpad(k) == k): product fused into the sweep
   bool nnzsp;              // EXACT on CSR (kpad(k) == k): the nnz-balanced SpMM (spmm_nnz.cu)
   int64_t* chunk_row;
   float* carry;
-  int nblk;                // tile path: column blocks of A per product (tile.cu); cuts (nblk - 1) x n
-  int64_t* cuts;
   int cslot;               // constant-table slot of the streaming sweep (-1: G in shared memory)
   float* ctab;             // scratch for the table copied to the constant bank
   bool record;             // SYMNMF_RECORD_PLANS: per-half copies of the scores and plan
@@ -589,15 +586,6 @@ struct symnmf_solver {
   double* hw;
   int64_t* hcounts;
   double* hmass;
-  bool markp;              // LvS on a large CSR A (kpad(k) == k): mirror-marked sampled product (default)
-  int32_t* mirror;         // [nnz] position of (c, r) in row c
-  uint32_t* bits;          // flagged mirror positions (kept zero between plans)
-  int32_t* slot_of;        // [n] plan slot of a sampled row
-  bool bucket;             // LvS on a large CSR A (kpad(k) == k): destination-bucketed sampled product
-  BucketWs bk;
-  float* Zt;               // bucket gather table Z[t] = omega_t f_{u_t} (cap x k)
-  int64_t* bchunk;         // bucket product: chunk rows and carries of the nnz-balanced pull
-  float* bcarry;
   symnmf_half_stats* stats;
   double *resid, *rpart, *rout, *GH;
   double *pgrad, *ppart, *pout;   // NEXT-3: per-iteration projected-gradient norm (with_resid)
@@ -676,54 +664,11 @@ bool lai_enabled() {
   return !(e && !strcmp(e, "never"));
 }
 
-// EXACT CSR: the product fused with the sweep in row tiles only on request (SYMNMF_CSR_TILE=always,
-// symnmf.h); by default the nnz-balanced SpMM + streaming sweep (SYMNMF_CSR_SPMM=rows: row groups)
-int64_t tile_min_nnz() {
-  const char* e = getenv("SYMNMF_CSR_TILE");
-  if (e && !strcmp(e, "always")) return 0;
-  return INT64_MAX;
-}
+// EXACT CSR (kpad(k) == k): the nnz-balanced SpMM by default, the row-group SpMM with
+// SYMNMF_CSR_SPMM=rows (symnmf.h)
 bool csr_spmm_nnz() {
   const char* e = getenv("SYMNMF_CSR_SPMM");
   return !(e && !strcmp(e, "rows"));
-}
-
-// LvS CSR sampled product (symnmf.h SYMNMF_SAMPLED=scatter|bucket|mark): 0 = vector-atomic scatter
-// (default below 16M nonzeros), 1 = destination buckets, 2 = mirror marks (default from 16M)
-int sampled_path(int64_t nnz) {
-  if (nnz < 0) return 0;
-  const char* e = getenv("SYMNMF_SAMPLED");
-  if (e && !strcmp(e, "scatter")) return 0;
-  if (e && !strcmp(e, "bucket")) return 1;
-  if (e && !strcmp(e, "mark")) return 2;
-  const char* b = getenv("SYMNMF_BUCKET");   // older knob: always -> bucket, never -> scatter
-  if (b && !strcmp(b, "always")) return 1;
-  if (b && !strcmp(b, "never")) return 0;
-  return nnz >= (16ll << 20) ? 2 : 0;
-}
-
-// LvS bucket path: the sampled product pulled into Y then the streaming sweep (default), or
-// (SYMNMF_BUCKET_FUSED=1) pulled inside the row-tile sweep kernel (tile.cu)
-bool bucket_fused() {
-  const char* e = getenv("SYMNMF_BUCKET_FUSED");
-  return e && !strcmp(e, "1");
-}
-
-// LvS bucket path: the pull as the nnz-balanced SpMM over the buckets (default) or one lane group
-// per destination row (SYMNMF_BUCKET_PULL=rows, symnmf.h)
-bool bucket_pull_rows() {
-  const char* e = getenv("SYMNMF_BUCKET_PULL");
-  return e && !strcmp(e, "rows");
-}
-
-// EXACT CSR tile path: column blocks so each pass's rows of F (n / nblk x 4k bytes) stay L2
-// resident: 4k n / 64 MB rounded up; SYMNMF_CSR_BLOCKS=<m> overrides (symnmf.h)
-int csr_blocks(int64_t n, int k) {
-  const char* e = getenv("SYMNMF_CSR_BLOCKS");
-  const int64_t v = e ? atoll(e) : 0;
-  if (v > 0) return (int)std::min<int64_t>(v, 64);
-  const int64_t fb = 4ll * k * n;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(64, (fb + (64ll << 20) - 1) / (64ll << 20)));
 }
 
 // Profiling hook: records an event after the launch site just enqueued (no-op unless profiling).
@@ -753,24 +698,12 @@ void solver_layout(symnmf_solver& S, Carver& c) {
   S.Gs = c.take<double>((size_t)k * k);
   S.GH = c.take<double>((size_t)k * k);
   S.gpart = c.take<double>(gram_partial_doubles(k, k, true, S.ggrid));
-  // the tile kernel balances hub rows; on small graphs the row-per-group SpMM + sweep is faster
-  S.tile = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode == SYMNMF_EXACT && !S.bpp &&
-           S.A.nnz >= tile_min_nnz();
-  S.nnzsp = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode == SYMNMF_EXACT && !S.tile && csr_spmm_nnz();
+  S.nnzsp = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode == SYMNMF_EXACT && csr_spmm_nnz();
   S.chunk_row = c.take<int64_t>(S.nnzsp ? (size_t)spmm_nnz_chunks(S.A.nnz) : 0);
   S.carry = c.take<float>(S.nnzsp ? spmm_nnz_carry_floats(S.A.nnz, k) : 0);
-  S.nblk = S.tile ? csr_blocks(n, k) : 1;
-  S.cuts = c.take<int64_t>(S.tile ? (size_t)(S.nblk - 1) * n : 0);
-  {
-    const bool big = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode == SYMNMF_LVS && !S.bpp &&
-                     S.A.nnz < (int64_t)INT32_MAX;
-    const int path = sampled_path(big ? S.A.nnz : -1);
-    S.markp = big && path == 2;
-    S.bucket = big && path == 1;
-  }
   S.ctab = c.take<float>(sweep_table_floats());
   S.nonconv = c.take<int32_t>(1);
-  S.Y = c.take<float>((S.tile && S.nblk == 1) || (S.bucket && bucket_fused()) ? 0 : (size_t)n * k);
+  S.Y = c.take<float>((size_t)n * k);
   S.stats = c.take<symnmf_half_stats>((size_t)2 * S.max_iters);
   S.resid = c.take<double>((size_t)S.max_iters);
   S.rgrid = residual_grid(n);
@@ -799,21 +732,6 @@ void solver_layout(symnmf_solver& S, Carver& c) {
     S.hw = c.take<double>(halves * S.plan.cap);
     S.hcounts = c.take<int64_t>(halves * 4);
     S.hmass = c.take<double>(halves * 2);
-    if (S.markp) {
-      mark_layout(c, n, S.A.nnz, S.plan.cap, &S.bk);
-      S.Zt = c.take<float>((size_t)S.plan.cap * k);
-      S.mirror = c.take<int32_t>((size_t)S.A.nnz);
-      S.bits = c.take<uint32_t>((size_t)spmm_nnz_chunks(S.A.nnz) * 8 + 8);
-      S.slot_of = c.take<int32_t>((size_t)n);
-      S.bchunk = c.take<int64_t>((size_t)spmm_nnz_chunks(S.A.nnz));
-      S.bcarry = c.take<float>(spmm_nnz_carry_floats(S.A.nnz, k));
-    }
-    if (S.bucket) {
-      bucket_layout(c, n, S.A.nnz, S.plan.cap, &S.bk);
-      S.Zt = c.take<float>((size_t)S.plan.cap * k);
-      S.bchunk = c.take<int64_t>((size_t)spmm_nnz_chunks(S.A.nnz));
-      S.bcarry = c.take<float>(spmm_nnz_carry_floats(S.A.nnz, k));
-    }
   }
   if (S.mode == SYMNMF_LAI) {
     S.Zpart = c.take<double>(gram_partial_doubles(S.l, k, false, S.ggrid));
@@ -840,11 +758,7 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
   const double* Gf = S.Gbuf[side];
   double* Gnext = S.Gbuf[side ^ 1];
   const bool lvs = S.mode == SYMNMF_LVS;
-  if (S.mode == SYMNMF_EXACT && S.tile) {
-    launch_csr_tile_passes(S.A, S.nblk, S.cuts, S.Y, F, Gf, S.alpha, X, n, k, S.Gacc, Gnext, nullptr, S.counter,
-                           status, st);
-    mark(S, st, "csr_tile_exact");
-  } else if (S.mode == SYMNMF_EXACT && S.nnzsp) {
+  if (S.mode == SYMNMF_EXACT && S.nnzsp) {
     launch_spmm_nnz(S.A, S.chunk_row, F, k, S.Y, S.carry, status, st);
     mark(S, st, "spmm_csr");
     enqueue_sweep(S, side, Gf, F, X, false, Gnext, nullptr, status, st);
@@ -875,39 +789,8 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     // G_s and Y_s only read the plan: G_s runs on a second branch of the graph, concurrently
     cudaEventRecord(S.ev_fork[side], st);
     cudaStreamWaitEvent(S.side, S.ev_fork[side], 0);
-    launch_sampled_gram_fused(F, k, S.plan, S.Gacc, S.Gs, S.counter, status, S.side,
-                              (S.bucket || S.markp) ? S.Zt : nullptr);
+    launch_sampled_gram_fused(F, k, S.plan, S.Gacc, S.Gs, S.counter, status, S.side);
     cudaEventRecord(S.ev_join[side], S.side);
-    if (S.markp) {
-      // sampled nonzeros flag their mirror positions; each destination row pulls its flagged entries
-      launch_mark_sampled(S.A, S.plan.uniq_idx, S.plan.counts + 2, S.bk, S.mirror, S.bits, S.slot_of,
-                          S.counter + 1, status, st);
-      cudaStreamWaitEvent(st, S.ev_join[side], 0);
-      launch_mark_pull(S.A, S.bchunk, S.bits, S.slot_of, S.Zt, k, S.Y, S.bcarry, status, st);
-      mark(S, st, "sampled_ah_csr");
-      enqueue_sweep(S, side, S.Gs, F, X, false, Gnext, S.Rinv32, status, st);
-      mark(S, st, S.bpp ? "bpp_update" : "hals_sweep");
-      return true;
-    }
-    if (S.bucket) {
-      // sampled nonzeros counting-sorted by destination row; the sweep pulls Y_s from the buckets
-      launch_bucket_build(S.A, S.plan.uniq_idx, S.plan.counts + 2, S.bk, S.counter + 1, status, st);
-      cudaStreamWaitEvent(st, S.ev_join[side], 0);
-      if (bucket_fused()) {
-        launch_bucket_tile_sweep(S.bk, S.Zt, F, S.Gs, S.alpha, X, n, k, S.Gacc, Gnext, S.Rinv32, S.counter, status,
-                                 st);
-        mark(S, st, "bucket_sweep");
-        return true;
-      }
-      if (bucket_pull_rows())
-        launch_bucket_pull(S.bk, S.Zt, n, k, S.Y, status, st);
-      else
-        launch_bucket_spmm(S.bk.off, S.bk.ent, n, S.A.nnz, S.Zt, k, S.Y, S.bchunk, S.bcarry, status, st);
-      mark(S, st, "sampled_ah_csr");   // bucket build + pull: the sampled product (a9)
-      enqueue_sweep(S, side, S.Gs, F, X, false, Gnext, S.Rinv32, status, st);
-      mark(S, st, "hals_sweep");
-      return true;
-    }
     if (S.A.kind == SYMNMF_CSR) {
       launch_sampled_csr_nozero(S.A, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap, S.Y,
                                 status, st);
@@ -1016,13 +899,12 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
     launch_scale_rows(S.Z, S.l, k, S.lam, S.Mside[0], S.status, st);
   }
   if (mode == SYMNMF_LVS && S.Y) SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Y, 0, sizeof(float) * n * k, st));
-  if (S.bucket) SYMNMF_CUDA_TRY(cudaMemsetAsync(S.bk.cnt, 0, sizeof(int32_t) * n, st));
   if (S.hasA && S.A.kind == SYMNMF_CSR) {
-    // every sparse path assumes each row's columns sorted, unique and in range (the column cuts of
-    // the EXACT tile passes and the destination ranges of the sampled scatter search them)
+    // every sparse path assumes each row's columns sorted, unique and in range (the destination
+    // ranges of the sampled scatter binary-search them)
     int32_t* bad = S.nonconv;
     SYMNMF_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int32_t), st));
-    launch_csr_cuts(S.A, S.tile ? S.nblk : 1, S.cuts, bad, st);
+    launch_csr_check(S.A, bad, st);
     int32_t hbad = 0;
     SYMNMF_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     SYMNMF_CUDA_TRY(cudaStreamSynchronize(st));
@@ -1030,17 +912,6 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
     if (hbad) return SYMNMF_ERR_ARG;
   }
   if (S.nnzsp) launch_spmm_nnz_rows(S.A, S.chunk_row, st);
-  if (S.markp) {
-    int32_t* bad = S.nonconv;
-    launch_mirror(S.A, S.mirror, bad, st);
-    int32_t hbad = 0;
-    SYMNMF_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    SYMNMF_CUDA_TRY(cudaStreamSynchronize(st));
-    SYMNMF_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int32_t), st));
-    if (hbad) return SYMNMF_ERR_ARG;   // the pattern of A is not symmetric
-    launch_spmm_nnz_rows(S.A, S.bchunk, st);
-    SYMNMF_CUDA_TRY(cudaMemsetAsync(S.bits, 0, sizeof(uint32_t) * ((size_t)spmm_nnz_chunks(S.A.nnz) * 8 + 8), st));
-  }
   set_i32<<<1, 1, 0, st>>>(S.iter_dev, first_iter);
   // H^T H (and its CholeskyQR factor for LvS) for the first W-half; later halves get
   // theirs from the fused Gram of the preceding sweep.

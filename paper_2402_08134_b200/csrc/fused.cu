@@ -405,8 +405,7 @@ __global__ void __launch_bounds__(FT) sampled_gram_fused(const float* __restrict
                                                          const int32_t* __restrict__ uniq,
                                                          const double* __restrict__ w,
                                                          const int64_t* __restrict__ n_uniq_dev, double* Gacc,
-                                                         double* Gout, unsigned int* counter, int32_t* status,
-                                                         float* __restrict__ Z) {
+                                                         double* Gout, unsigned int* counter, int32_t* status) {
   constexpr int ST = KP + 4;
   constexpr int ROWS = 64;
   __shared__ __align__(16) float s[ROWS * ST];
@@ -439,10 +438,6 @@ __global__ void __launch_bounds__(FT) sampled_gram_fused(const float* __restrict
       for (int q = 0; q < Q; ++q) {
         const int e = threadIdx.x + q * FT, r = e / (KP / 4), c = e - r * (KP / 4);
         if (e < NV) *reinterpret_cast<float4*>(s + r * ST + 4 * c) = v[q];
-        if (Z && e < NV && r < rows) {   // Z[t] = omega_t f_{u_t}: the bucketed product's gather table
-          const float om = sw[r];
-          reinterpret_cast<float4*>(Z)[(r0 + r) * (KP / 4) + c] = make_float4(om * v[q].x, om * v[q].y, om * v[q].z, om * v[q].w);
-        }
       }
     } else {
       for (int e = threadIdx.x; e < ROWS * KP; e += FT) {
@@ -455,297 +450,6 @@ __global__ void __launch_bounds__(FT) sampled_gram_fused(const float* __restrict
   }
   gt.commit(Gacc, k, red);
   if (arrive_last(counter)) finalize_gram<KP>(Gacc, Gout, k, nullptr, nullptr, nullptr, status);
-}
-
-// ---------------------------------------------------------------- csr_tile_sweep
-// Exact CSR product fused with the sweep, for graphs with hub rows: one 256-row tile of
-// Y = A F is computed in shared memory, then swept.  The tile's nonzeros are split into
-// 32 equal slices, one per lane group; a group accumulates a row in registers and stores it once
-// (rows interior to its slice are its own); the first / last row of a slice go to carry slots
-// that are combined in slice order afterwards -- no atomics, deterministic, and a hub row is
-// spread over many groups instead of serialising one.  Then thread r sweeps row r (Eq. 2.6,
-// P:170-175) with G (+alpha I) and b = y + alpha f_r (formed in shared memory), writes X, and the
-// updated rows of the tile are accumulated into X^T X (fp32 per tile, fp64 per-thread slots in
-// shared memory), committed once per CTA; the last CTA forms X^T X and its Cholesky factor.
-constexpr int TR = 256;          // rows per tile = threads per CTA
-constexpr int TUE = 8;           // gathers in flight per lane group (exact)
-
-__device__ __forceinline__ int tile_row_of(const int* sOff, int rows, int e) {   // sOff[r] <= e < sOff[r+1]
-  int lo = 0, hi = rows - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (sOff[mid] <= e) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-
-// Per-thread upper 4x4 block (ai <= bi) of the tile Gram over row groups g: fp32 over one tile,
-// added into this thread's own fp64 slot in shared memory (no atomics, no fp64 registers).
-template <int KP>
-struct GramTile {
-  static constexpr int NB = KP / 4, PAIRS = NB * (NB + 1) / 2;
-  int ai, bi, g, RG, p;
-  bool active;
-  __device__ void init(int t) {
-    RG = TR / PAIRS;
-    g = t / PAIRS;
-    p = t - g * PAIRS;
-    active = g < RG;
-    int a = 0, rem = p;
-    while (rem >= NB - a) { rem -= NB - a; ++a; }
-    ai = a; bi = a + rem;
-  }
-  __device__ void tile(const float* s, int stride, int rows, double* slot) const {
-    if (!active) return;
-    float acc[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) acc[e] = 0.f;
-    for (int r = g; r < rows; r += RG) {
-      const float4 a4 = *reinterpret_cast<const float4*>(s + r * stride + 4 * ai);
-      const float4 b4 = *reinterpret_cast<const float4*>(s + r * stride + 4 * bi);
-      const float a[4] = {a4.x, a4.y, a4.z, a4.w}, b[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i * 4 + j] = fmaf(a[i], b[j], acc[i * 4 + j]);
-    }
-    double* my = slot + (size_t)threadIdx.x * 16;
-#pragma unroll
-    for (int e = 0; e < 16; ++e) my[e] += (double)acc[e];
-  }
-  // CTA commit: the row groups' slots summed in fixed order, one fp64 red.add per entry into a
-  // replica of the global accumulator.  All threads must call.
-  __device__ void commit(const double* slot, double* Gacc) const {
-    __syncthreads();
-    double* rep = Gacc + (size_t)(blockIdx.x % kGramReplicas) * KP * KP;
-    for (int idx = threadIdx.x; idx < PAIRS * 16; idx += TR) {
-      const int pp = idx >> 4, e = idx & 15;
-      double sum = 0.0;
-      for (int gg = 0; gg < TR / PAIRS; ++gg) sum += slot[(size_t)(gg * PAIRS + pp) * 16 + e];
-      int a0 = 0, rem = pp;
-      while (rem >= NB - a0) { rem -= NB - a0; ++a0; }
-      const int a = 4 * a0 + (e >> 2), b = 4 * (a0 + rem) + (e & 3);
-      if (a <= b && sum != 0.0) atomicAdd(rep + a * KP + b, sum);
-    }
-  }
-};
-
-template <int KP>
-struct TileSmem {
-  static constexpr int ST = KP + 4;
-  static constexpr int NSLICE = (TR / 32) * (32 / (KP / 4));   // lane groups
-  static constexpr int NCARRY = 2 * NSLICE;
-  static constexpr size_t y = 0;                                               // float [TR][ST]
-  static constexpr size_t carry = y + sizeof(float) * TR * ST;                 // float [NCARRY][KP]
-  static constexpr size_t crow = carry + sizeof(float) * NCARRY * KP;          // int [NCARRY]
-  static constexpr size_t gram = crow + sizeof(int) * NCARRY;                  // double [TR][16]
-  static constexpr size_t bytes = gram + sizeof(double) * TR * 16;
-};
-
-template <int KP>
-__global__ void __launch_bounds__(TR, 2) csr_tile_sweep(
-    const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, const float* __restrict__ val, int64_t n,
-    const float* __restrict__ F, const double* __restrict__ G, double alpha, float* __restrict__ X, double* Gacc,
-    double* Gout, float* Rf32, unsigned int* counter, int32_t* status) {
-  using L = TileSmem<KP>;
-  constexpr int ST = L::ST, LPR = KP / 4, NG = 32 / LPR;
-  __shared__ __align__(16) float sG[KP * KP];     // sG[i*KP + j] = G[j][i], 0 on the diagonal
-  __shared__ float sInv[KP];
-  __shared__ int sOk[KP];
-  __shared__ int sOff[TR + 1];
-  extern __shared__ __align__(16) unsigned char smt[];
-  float* sY = reinterpret_cast<float*>(smt + L::y);
-  float* sC = reinterpret_cast<float*>(smt + L::carry);
-  int* sCr = reinterpret_cast<int*>(smt + L::crow);
-  if (dev_failed(status)) return;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, grp = lane / LPR, li = lane % LPR;
-  for (int e = tid; e < KP * KP; e += TR) {
-    const int i = e / KP, j = e - i * KP;
-    sG[e] = (i != j) ? (float)G[j * KP + i] : 0.f;
-  }
-  for (int i = tid; i < KP; i += TR) {
-    const double den = G[i * KP + i] + alpha;
-    sOk[i] = den > 0.0;
-    sInv[i] = den > 0.0 ? (float)(1.0 / den) : 0.f;
-  }
-  double* gslot = reinterpret_cast<double*>(smt + L::gram);
-#pragma unroll
-  for (int e = 0; e < 16; ++e) gslot[tid * 16 + e] = 0.0;
-  GramTile<KP> gt;
-  gt.init(tid);
-  const float a32 = (float)alpha;
-  const float4* F4 = reinterpret_cast<const float4*>(F);
-  const int64_t tiles = (n + TR - 1) / TR;
-  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-    const int64_t r0 = t * TR;
-    const int rows = (int)min64(TR, n - r0);
-    const int64_t eb = rowptr[r0];
-    if (tid < rows) {   // the sweep's X and F rows: fetched into L2 while the product runs
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(X + (r0 + tid) * KP));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(F + (r0 + tid) * KP));
-      if (KP == 64) {
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(X + (r0 + tid) * KP + 32));
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(F + (r0 + tid) * KP + 32));
-      }
-    }
-    __syncthreads();   // previous tile's Gram reads of sY are done
-    {
-      const int64_t ep = rowptr[r0 + min(tid, rows)];
-      sOff[tid] = (int)(ep - eb);
-      if (tid == 0) sOff[TR] = (int)(rowptr[r0 + rows] - eb);
-#pragma unroll
-      for (int c = 0; c < KP; c += 4) *reinterpret_cast<float4*>(sY + tid * ST + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int e = tid; e < L::NCARRY * KP; e += TR) sC[e] = 0.f;
-      if (tid < L::NCARRY) sCr[tid] = -1;
-    }
-    __syncthreads();
-    const int total = sOff[TR];
-    {
-      // ---- nnz-balanced slices, one per lane group; rows owned or carried
-      const int sl = wid * NG + grp;
-      const int Ls = (total + L::NSLICE - 1) / L::NSLICE;
-      const int s0 = min(total, sl * Ls), s1 = min(total, s0 + Ls);
-      if (s0 < s1) {
-        const int rfirst = tile_row_of(sOff, rows, s0), rlast = tile_row_of(sOff, rows, s1 - 1);
-        int row = rfirst;
-        int rend = sOff[row + 1];
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        auto put = [&](int r, float4 v) {   // one write per (slice, row)
-          float* dst = (r == rfirst) ? sC + (2 * sl) * KP : (r == rlast) ? sC + (2 * sl + 1) * KP : sY + r * ST;
-          *reinterpret_cast<float4*>(dst + 4 * li) = v;
-        };
-        if (li == 0) { sCr[2 * sl] = rfirst; sCr[2 * sl + 1] = rlast != rfirst ? rlast : -1; }
-        for (int e = s0; e < s1; e += TUE) {
-          int cc[TUE];
-          float aa[TUE];
-          float4 ff[TUE];
-#pragma unroll
-          for (int u = 0; u < TUE; ++u) {
-            const bool ok = e + u < s1;
-            cc[u] = ok ? __ldg(col + eb + e + u) : 0;
-            aa[u] = ok ? __ldg(val + eb + e + u) : 0.f;
-          }
-#pragma unroll
-          for (int u = 0; u < TUE; ++u)
-            ff[u] = (e + u < s1) ? __ldg(F4 + (int64_t)cc[u] * LPR + li) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-          for (int u = 0; u < TUE; ++u) {
-            if (e + u < s1) {
-              if (e + u >= rend) {
-                put(row, acc);
-                acc = make_float4(0.f, 0.f, 0.f, 0.f);
-                row = tile_row_of(sOff, rows, e + u);
-                rend = sOff[row + 1];
-              }
-              acc.x = fmaf(aa[u], ff[u].x, acc.x); acc.y = fmaf(aa[u], ff[u].y, acc.y);
-              acc.z = fmaf(aa[u], ff[u].z, acc.z); acc.w = fmaf(aa[u], ff[u].w, acc.w);
-            }
-          }
-        }
-        put(row, acc);
-      }
-    }
-    __syncthreads();
-    // ---- carries: runs of equal rows (consecutive slices) summed in slice order, added once
-    for (int e = tid; e < L::NCARRY * LPR; e += TR) {
-      const int c = e / LPR, q = e - c * LPR;
-      const int r = sCr[c];
-      if (r < 0) continue;
-      int prev = c - 1;
-      while (prev >= 0 && sCr[prev] < 0) --prev;
-      if (prev >= 0 && sCr[prev] == r) continue;   // not the head of its run
-      float4 s = *reinterpret_cast<const float4*>(sC + c * KP + 4 * q);
-      for (int c2 = c + 1; c2 < L::NCARRY; ++c2) {
-        const int r2 = sCr[c2];
-        if (r2 < 0) continue;
-        if (r2 != r) break;
-        const float4 v = *reinterpret_cast<const float4*>(sC + c2 * KP + 4 * q);
-        s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
-      }
-      float4* d4 = reinterpret_cast<float4*>(sY + r * ST + 4 * q);
-      float4 cur = *d4;
-      cur.x += s.x; cur.y += s.y; cur.z += s.z; cur.w += s.w;
-      *d4 = cur;
-    }
-    __syncthreads();
-    // ---- b = y + alpha f for the tile (coalesced: the tile's F rows are contiguous)
-    {
-      const float4* Ft = F4 + r0 * LPR;
-      for (int q = tid; q < rows * LPR; q += TR) {
-        const int r = q / LPR, c = q - r * LPR;
-        const float4 fv = __ldg(Ft + q);
-        float4* d4 = reinterpret_cast<float4*>(sY + r * ST + 4 * c);
-        float4 y = *d4;
-        y.x = fmaf(a32, fv.x, y.x); y.y = fmaf(a32, fv.y, y.y); y.z = fmaf(a32, fv.z, y.z); y.w = fmaf(a32, fv.w, y.w);
-        *d4 = y;
-      }
-    }
-    __syncthreads();
-    // ---- HALS sweep of row tid, Gauss-Seidel over the KP columns (x in registers, b in smem)
-    if (tid < rows) {
-      const int64_t r = r0 + tid;
-      float x[KP];
-      const float4* X4 = reinterpret_cast<const float4*>(X + r * KP);
-#pragma unroll
-      for (int j = 0; j < KP; j += 4) {
-        const float4 xv = X4[j / 4];
-        x[j] = xv.x; x[j + 1] = xv.y; x[j + 2] = xv.z; x[j + 3] = xv.w;
-      }
-      const float* brow = sY + tid * ST;
-#pragma unroll
-      for (int i = 0; i < KP; ++i) {
-        float s0 = brow[i], s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll
-        for (int j = 0; j < KP; j += 4) {
-          const float4 g = *reinterpret_cast<const float4*>(sG + i * KP + j);
-          s0 = fmaf(-x[j], g.x, s0);
-          s1 = fmaf(-x[j + 1], g.y, s1);
-          s2 = fmaf(-x[j + 2], g.z, s2);
-          s3 = fmaf(-x[j + 3], g.w, s3);
-        }
-        const float sv = (s0 + s1) + (s2 + s3);
-        if (sOk[i]) x[i] = fmaxf(0.f, sv * sInv[i]);
-      }
-      float4* Xw = reinterpret_cast<float4*>(X + r * KP);
-#pragma unroll
-      for (int j = 0; j < KP; j += 4) {
-        const float4 v = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
-        Xw[j / 4] = v;
-        *reinterpret_cast<float4*>(sY + tid * ST + j) = v;
-      }
-    }
-    __syncthreads();
-    gt.tile(sY, ST, rows, gslot);
-  }
-  // ---- commit the CTA's X^T X into a replica of the global accumulator; last CTA finalizes
-  gt.commit(gslot, Gacc);
-  if (arrive_last(counter)) {
-    double* sa = reinterpret_cast<double*>(smt);
-    finalize_gram<KP>(Gacc, Gout, KP, Rf32, sa, sa + KP * (KP + 1), status);
-  }
-}
-
-template <int KP>
-static void csr_tile_sweep_t(const symnmf_matrix& A, const float* F, const double* G, double alpha, float* X, int64_t n,
-                             double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
-                             cudaStream_t st) {
-  const size_t smem = std::max({TileSmem<KP>::bytes, sizeof(double) * 2 * KP * (KP + 1), kRedBytes});
-  const int64_t tiles = (n + TR - 1) / TR;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 2));
-  cudaFuncSetAttribute(csr_tile_sweep<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  launch_pdl(csr_tile_sweep<KP>, grid, TR, smem, st, A.rowptr, A.colidx, A.val, n, F, G, alpha, X, Gacc, Gout, Rf32,
-             counter, status);
-}
-
-void launch_csr_tile_sweep(const symnmf_matrix& A, const float* F, const double* G, double alpha, float* X, int64_t n,
-                           int k, double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
-                           cudaStream_t st) {
-  switch (k) {
-    case 8: csr_tile_sweep_t<8>(A, F, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
-    case 16: csr_tile_sweep_t<16>(A, F, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
-    case 32: csr_tile_sweep_t<32>(A, F, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
-    default: csr_tile_sweep_t<64>(A, F, G, alpha, X, n, Gacc, Gout, Rf32, counter, status, st); break;
-  }
 }
 
 // ---------------------------------------------------------------- launchers
@@ -844,13 +548,13 @@ void launch_uniq_count_fused(const float* lev, int64_t n, double T, const Sample
 }
 
 void launch_sampled_gram_fused(const float* F, int k, const symnmf_plan& plan, double* Gacc, double* Gout,
-                               unsigned int* counter, int32_t* status, cudaStream_t st, float* Z) {
+                               unsigned int* counter, int32_t* status, cudaStream_t st) {
   const int grid = fused_grid((plan.cap + 63) / 64, 1);
   switch (kpad(k)) {
-    case 8: launch_pdl(sampled_gram_fused<8>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status, Z); break;
-    case 16: launch_pdl(sampled_gram_fused<16>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status, Z); break;
-    case 32: launch_pdl(sampled_gram_fused<32>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status, Z); break;
-    default: launch_pdl(sampled_gram_fused<64>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status, Z); break;
+    case 8: launch_pdl(sampled_gram_fused<8>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
+    case 16: launch_pdl(sampled_gram_fused<16>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
+    case 32: launch_pdl(sampled_gram_fused<32>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
+    default: launch_pdl(sampled_gram_fused<64>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
   }
 }
 

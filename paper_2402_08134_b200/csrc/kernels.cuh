@@ -92,15 +92,8 @@ void launch_leverage_fused(const float* F, int64_t n, int k, const float* Rinv, 
 void launch_uniq_count_fused(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
                              const int32_t* iter_dev, int32_t first_iter, int32_t max_iters, int side,
                              symnmf_half_stats* stats, unsigned int* counter, int32_t* status, cudaStream_t st);
-// Z (nullable): the gather table Z[t] = (float) omega_t * f_{u_t} of the bucketed product (k floats per row)
 void launch_sampled_gram_fused(const float* F, int k, const symnmf_plan& plan, double* Gacc, double* Gout,
-                               unsigned int* counter, int32_t* status, cudaStream_t st, float* Z = nullptr);
-// Exact CSR product fused with the sweep (csr_tile_sweep): 256-row tiles of Y = A F in shared
-// memory with nnz-balanced slices (hub rows spread over lane groups), the HALS sweep of the tile,
-// the Gram of the updated rows and (last CTA) its Cholesky factor.  Requires kpad(k) == k.
-void launch_csr_tile_sweep(const symnmf_matrix& A, const float* F, const double* G, double alpha, float* X, int64_t n,
-                           int k, double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
-                           cudaStream_t st);
+                               unsigned int* counter, int32_t* status, cudaStream_t st);
 // sampler.cu passes used by the fused path
 void launch_samp_prefix(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
                         int32_t* status, cudaStream_t st);
@@ -122,10 +115,8 @@ bool spmm_nnz_supported(int k);
 void launch_spmm_nnz_rows(const symnmf_matrix& A, int64_t* chunk_row, cudaStream_t st);
 void launch_spmm_nnz(const symnmf_matrix& A, const int64_t* chunk_row, const float* F, int k, float* Y, float* carry,
                      const int32_t* status, cudaStream_t st);
-// The bucketed sampled product through the same nnz-balanced kernel (chunk_row: spmm_nnz_chunks(cap)
-// entries, carry: spmm_nnz_carry_floats(cap, k)); total entries read from off[n] on the device.
-void launch_bucket_spmm(const int32_t* off, const int2* ent, int64_t n, int64_t cap_entries, const float* Z, int k,
-                        float* Y, int64_t* chunk_row, float* carry, const int32_t* status, cudaStream_t st);
+// *bad = 1 if a row's column indices are not sorted, unique and in [0, n) (caller zeroes *bad).
+void launch_csr_check(const symnmf_matrix& A, int32_t* bad, cudaStream_t st);
 
 // ---------------------------------------------------------------- sweep.cu
 // Streaming HALS sweep (k in {8, 16, 32}): cp.async-staged tiles, thread per row, fused Gram + Cholesky.
@@ -138,50 +129,6 @@ void launch_sweep_stream(const double* G, double alpha, float* Y, const float* F
 int sweep_cslot_acquire();
 void sweep_cslot_release(int slot);
 size_t sweep_table_floats();
-
-// ---------------------------------------------------------------- bucket.cu / tile.cu (sparse A)
-// Destination buckets of the sampled CSR product (bucket.cu): per plan, the sampled rows'
-// nonzeros counting-sorted by column.  cnt is kept zero between plans.
-struct BucketWs {
-  int64_t cap;       // plan capacity
-  int64_t* ptsum;    // plan-row scan tile sums
-  int64_t* pre;      // [cap + 1] exclusive prefix of the plan rows' nnz
-  int64_t* rb;       // [cap + 1] rowptr[u_t] - pre[t]
-  int32_t* cnt;      // [n] bucket sizes (zero between plans)
-  int32_t* off;      // [n + 1] bucket offsets
-  int32_t* tsum;     // scan tile sums
-  int32_t* slot;     // [nnz] place of a sampled nonzero in its bucket
-  int2* ent;         // [nnz] bucket entries (plan slot t, a_e)
-};
-void bucket_layout(Carver& c, int64_t n, int64_t nnz, int64_t cap, BucketWs* b);
-void mark_layout(Carver& c, int64_t n, int64_t nnz, int64_t cap, BucketWs* b);
-void launch_bucket_build(const symnmf_matrix& A, const int32_t* uniq, const int64_t* n_uniq_dev, const BucketWs& b,
-                         unsigned int* counter, int32_t* status, cudaStream_t st);
-// Mirror marks (default LvS CSR sampled product): mirror[e] = position of (c, r) in row c (once per A;
-// *bad = 1 if the pattern is not symmetric); per plan, plan-row offsets, slot_of[u_t] = t and the
-// bitmap of flagged mirror positions; launch_mark_pull (spmm_nnz.cu) forms Y_s and clears the bitmap.
-void launch_mirror(const symnmf_matrix& A, int32_t* mirror, int32_t* bad, cudaStream_t st);
-void launch_mark_sampled(const symnmf_matrix& A, const int32_t* uniq, const int64_t* n_uniq_dev, const BucketWs& b,
-                         const int32_t* mirror, uint32_t* bits, int32_t* slot_of, unsigned int* counter,
-                         int32_t* status, cudaStream_t st);
-void launch_mark_pull(const symnmf_matrix& A, const int64_t* chunk_row, uint32_t* bits, const int32_t* slot_of,
-                      const float* Z, int k, float* Y, float* carry, const int32_t* status, cudaStream_t st);
-// Y_s (n x k, every row written) from the buckets with the gather table Z; kpad(k) == k.
-void launch_bucket_pull(const BucketWs& b, const float* Z, int64_t n, int k, float* Y, const int32_t* status,
-                        cudaStream_t st);
-// Sampled product from the buckets (gather table Z[t] = omega_t f_{u_t}, k floats per row) fused
-// with the sweep, X^T X and (Rf32 non-null) its Cholesky factor.  kpad(k) == k.
-void launch_bucket_tile_sweep(const BucketWs& b, const float* Z, const float* F, const double* G, double alpha,
-                              float* X, int64_t n, int k, double* Gacc, double* Gout, float* Rf32,
-                              unsigned int* counter, int32_t* status, cudaStream_t st);
-// Exact CSR product in nb column-block passes (cuts: (nb - 1) x n, launch_csr_cuts), the last fused
-// with the sweep; Ypart (n x k) holds the partial sums between passes (unused for nb = 1).
-void launch_csr_tile_passes(const symnmf_matrix& A, int nb, const int64_t* cuts, float* Ypart, const float* F,
-                            const double* G, double alpha, float* X, int64_t n, int k, double* Gacc, double* Gout,
-                            float* Rf32, unsigned int* counter, int32_t* status, cudaStream_t st);
-// cuts[(b-1) n + r] = first nonzero of row r with column >= b n / nb; *bad = 1 if some row's columns
-// are not sorted, unique and in [0, n) (caller zeroes *bad).
-void launch_csr_cuts(const symnmf_matrix& A, int nb, int64_t* cuts, int32_t* bad, cudaStream_t st);
 
 // ---------------------------------------------------------------- bpp.cu (NEXT-1)
 // X <- exact per-row NLS with (G + alpha I, Y + alpha F) (block principal pivoting, k <= 32);

@@ -8,7 +8,6 @@
 // sampled row; groups of k/4 lanes scatter-add omega_i a_ic f_i into row c of
 // Y_s with 128-bit vector atomics (red.global.add.v4.f32).
 #include <cstdlib>
-#include <cstring>
 #include "kernels.cuh"
 
 namespace symnmf {
@@ -82,12 +81,6 @@ static int64_t scatter_slice_bytes() {
   return mb > 0 ? (mb << 20) : (86ll << 20);
 }
 
-// SYMNMF_SCATTER_BULK=1: TMA bulk reductions instead of vector atomics (symnmf.h)
-static bool scatter_bulk() {
-  const char* e = getenv("SYMNMF_SCATTER_BULK");
-  return e && !strcmp(e, "1");
-}
-
 static int grid_for(int64_t work_threads) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((work_threads + 255) / 256, 148 * 16));
 }
@@ -146,70 +139,6 @@ __global__ void __launch_bounds__(256) sampled_csr_v4(const int64_t* __restrict_
   }
 }
 
-// Same scatter with TMA bulk reductions: each group writes omega_i a_ic f_i (k floats) into a
-// per-warp shared-memory staging slot and one lane issues cp.reduce.async.bulk .add.f32 of the whole
-// row into Y_s[c] -- one L2 reduction request per (entry, 4k bytes) instead of k/4 vector atomics.
-template <int LPR>
-__global__ void __launch_bounds__(256) sampled_csr_bulk(const int64_t* __restrict__ rowptr,
-                                                        const int32_t* __restrict__ col, const float* __restrict__ val,
-                                                        const float4* __restrict__ F4, const int32_t* __restrict__ uniq,
-                                                        const double* __restrict__ w,
-                                                        const int64_t* __restrict__ n_uniq_dev, float4* __restrict__ Y4,
-                                                        int32_t c_lo, int32_t c_hi, int ranged,
-                                                        const int32_t* __restrict__ status) {
-  constexpr int NPW = 32 / LPR;   // entries per warp step
-  constexpr int NBUF = 4;         // staging slots per warp (ring)
-  __shared__ __align__(128) float4 stage[8][NBUF][NPW][LPR];
-  if (dev_failed(status)) return;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, sub = lane / LPR, li = lane % LPR;
-  const int64_t nu = *n_uniq_dev;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int buf = 0;
-  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < nu; u += nw) {
-    const int64_t i = uniq[u];
-    const float om = (float)w[u];
-    float4 f = __ldg(F4 + i * LPR + li);
-    f.x *= om; f.y *= om; f.z *= om; f.w *= om;
-    int64_t e0 = rowptr[i], e1 = rowptr[i + 1];
-    if (ranged) {
-      int64_t a = e0, b = e1;
-      while (a < b) { const int64_t m = (a + b) >> 1; if (__ldg(col + m) < c_lo) a = m + 1; else b = m; }
-      int64_t c = a, d = e1;
-      while (c < d) { const int64_t m = (c + d) >> 1; if (__ldg(col + m) < c_hi) c = m + 1; else d = m; }
-      e0 = a; e1 = c;
-    }
-    for (int64_t eb = e0; eb < e1; eb += NPW) {
-      const int64_t e = eb + sub;
-      const bool ok = e < e1;
-      const int64_t c = ok ? __ldg(col + e) : 0;
-      const float a = ok ? __ldg(val + e) : 0.f;
-      // the slot is free once the bulk reductions issued NBUF steps ago have read it
-      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NBUF - 1) : "memory");
-      __syncwarp();
-      stage[wid][buf][sub][li] = make_float4(a * f.x, a * f.y, a * f.z, a * f.w);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      const unsigned okm = __ballot_sync(0xffffffffu, ok && li == 0);
-      // each entry's destination from its group's first lane
-      int64_t cd[NPW];
-#pragma unroll
-      for (int q = 0; q < NPW; ++q) cd[q] = __shfl_sync(0xffffffffu, c, q * LPR);
-      if (lane == 0) {
-#pragma unroll
-        for (int q = 0; q < NPW; ++q) {
-          if (!((okm >> (q * LPR)) & 1u)) continue;
-          const uint32_t src = (uint32_t)__cvta_generic_to_shared(&stage[wid][buf][q][0]);
-          asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;"
-                       ::"l"(Y4 + cd[q] * LPR), "r"(src), "r"(LPR * 16) : "memory");
-        }
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-      buf = (buf + 1) % NBUF;
-    }
-  }
-  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-
 __global__ void __launch_bounds__(256) sampled_csr_scalar(const int64_t* __restrict__ rowptr,
                                                           const int32_t* __restrict__ col,
                                                           const float* __restrict__ val, const float* __restrict__ F,
@@ -257,11 +186,6 @@ void launch_sampled_csr_nozero(const symnmf_matrix& A, const float* F, int k, co
     for (int p = 0; p < passes; ++p) {
       const int32_t lo = (int32_t)(A.n * p / passes), hi = (int32_t)(A.n * (p + 1) / passes);
       const int ranged = passes > 1;
-      if (scatter_bulk() && (k / 4 == 4 || k / 4 == 8)) {
-        if (k / 4 == 4) launch_pdl(sampled_csr_bulk<4>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, status);
-        else launch_pdl(sampled_csr_bulk<8>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, status);
-        continue;
-      }
       switch (k / 4) {
         case 1: launch_pdl(sampled_csr_v4<1>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, status); break;
         case 2: launch_pdl(sampled_csr_v4<2>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, status); break;

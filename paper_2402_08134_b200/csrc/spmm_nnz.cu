@@ -1,4 +1,4 @@
-// (a10) The exact CSR product Y = A F for graphs with hub rows, balanced by
+// (a10) The exact CSR product Y = A F, balanced by
 // nonzeros: the nnz range is cut into equal chunks of kChunk nonzeros, one per group of k/4 lanes
 // (float4 per lane), so a hub row is spread over many groups and every group gathers the same
 // number of rows of F.  Rows complete inside a chunk are stored by its group; the partial sums of
@@ -24,17 +24,6 @@ struct NnzCsr {      // CSR A: rowptr int64, separate col / val
     a = __ldcs(val + e);
   }
 };
-struct NnzBucket {   // destination buckets of the sampled product (bucket.cu): off int32, (t, a) pairs
-  const int32_t* off;
-  const int2* ent;
-  __device__ __forceinline__ int64_t ptr(int64_t r) const { return off[r]; }
-  __device__ __forceinline__ void load(int64_t e, int& c, float& a) const {
-    const int2 x = __ldcs(ent + e);
-    c = x.x;
-    a = __int_as_float(x.y);
-  }
-};
-
 // chunk_row[g] = the row holding entry g * kChunk (largest r with ptr(r) <= g * kChunk), for the
 // chunks of `total` entries (*total_dev when given)
 template <class Src>
@@ -138,125 +127,6 @@ __global__ void __launch_bounds__(256) spmm_nnz_fix(Src src, int64_t n, const fl
   }
 }
 
-// The sampled product from the mirror marks (bucket.cu: mark_sampled): chunk g of A's nonzeros is 8
-// words of the bitmap; its flagged entries (c, i), i in U, are taken in order and
-// Y_s[c] += A[c, i] Z[slot_of[i]]; rows are stored / carried exactly as in spmm_nnz (rows without a
-// flagged entry get 0), and the chunk's words are cleared for the next plan.
-template <int KP>
-__global__ void __launch_bounds__(256, 4) mark_pull(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-                                                    const float* __restrict__ val, int64_t nnz,
-                                                    const int64_t* __restrict__ chunk_row, uint32_t* __restrict__ bits,
-                                                    const int32_t* __restrict__ slot_of,
-                                                    const float4* __restrict__ Z4, float4* __restrict__ Y4,
-                                                    float4* __restrict__ carry, const int32_t* __restrict__ status) {
-  if (dev_failed(status)) return;
-  constexpr int LPR = KP / 4;
-  constexpr int W = kChunk / 32;                     // bitmap words per chunk
-  const int lane = threadIdx.x & 31, li = lane % LPR;
-  const unsigned gmask = (LPR == 32 ? 0xffffffffu : ((1u << LPR) - 1u) << (lane - li));
-  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / LPR;
-  const int64_t nchunks = (nnz + kChunk - 1) / kChunk;
-  for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPR; g < nchunks; g += ng) {
-    const int64_t s0 = g * kChunk, s1 = min64(nnz, s0 + kChunk);
-    const int64_t rf = chunk_row[g];
-    int64_t r = rf;
-    int64_t rstart = rowptr[r], rend = rowptr[r + 1];
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    auto emit = [&]() {
-      if (rstart >= s0 && rend <= s1) Y4[r * LPR + li] = acc;
-      else carry[(2 * g + (r == rf ? 0 : 1)) * LPR + li] = acc;
-    };
-    // the chunk's words: lane li < LG holds words li + LG q, shared by shuffles; cleared for the next plan
-    constexpr int LG = LPR < W ? LPR : W, WPL = W / LG;
-    uint32_t wm[WPL];
-    const int64_t w0 = s0 >> 5;
-#pragma unroll
-    for (int q = 0; q < WPL; ++q) {
-      const int wi = li + LG * q;
-      wm[q] = 0u;
-      if (li < LG && s0 + 32 * wi < s1) {
-        wm[q] = bits[w0 + wi];
-        if (wm[q]) bits[w0 + wi] = 0u;
-      }
-    }
-#pragma unroll
-    for (int wi = 0; wi < W; ++wi) {
-      uint32_t wd = __shfl_sync(gmask, wm[wi / LG], wi % LG, LPR);
-      while (wd) {
-        // up to 8 flagged positions of this word per batch: gathers in flight together
-        int64_t pos[8];
-        int cnt = 0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (wd) {
-            const int b = __ffs(wd) - 1;
-            wd &= wd - 1;
-            pos[u] = s0 + 32 * wi + b;
-            ++cnt;
-          } else {
-            pos[u] = -1;
-          }
-        }
-        int cc[8];
-        float aa[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (pos[u] >= 0) { cc[u] = __ldg(col + pos[u]); aa[u] = __ldg(val + pos[u]); }
-          else { cc[u] = 0; aa[u] = 0.f; }
-        }
-        int tt[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) tt[u] = pos[u] >= 0 ? __ldg(slot_of + cc[u]) : 0;
-        float4 zz[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          zz[u] = pos[u] >= 0 ? __ldg(Z4 + (int64_t)tt[u] * LPR + li) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (pos[u] >= 0) {
-            const int64_t p = pos[u];
-            if (p >= rend) {
-              do { emit(); acc = make_float4(0.f, 0.f, 0.f, 0.f); ++r; rstart = rend; rend = rowptr[r + 1]; }
-              while (rend <= p);
-            }
-            acc.x = fmaf(aa[u], zz[u].x, acc.x); acc.y = fmaf(aa[u], zz[u].y, acc.y);
-            acc.z = fmaf(aa[u], zz[u].z, acc.z); acc.w = fmaf(aa[u], zz[u].w, acc.w);
-          }
-        }
-        (void)cnt;
-      }
-    }
-    // every remaining row of the chunk: stored (0 if nothing flagged) or carried
-    while (rend < s1) { emit(); acc = make_float4(0.f, 0.f, 0.f, 0.f); ++r; rstart = rend; rend = rowptr[r + 1]; }
-    emit();
-  }
-}
-
-template <int KP>
-static void mark_pull_t(const symnmf_matrix& A, const int64_t* chunk_row, uint32_t* bits, const int32_t* slot_of,
-                        const float* Z, float* Y, float* carry, const int32_t* status, cudaStream_t st) {
-  constexpr int LPR = KP / 4;
-  const int64_t groups = spmm_nnz_chunks(A.nnz);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((groups * LPR + 255) / 256, 148 * 16));
-  if (A.nnz > 0)
-    launch_pdl(mark_pull<KP>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, A.nnz, chunk_row, bits, slot_of,
-               reinterpret_cast<const float4*>(Z), reinterpret_cast<float4*>(Y), reinterpret_cast<float4*>(carry),
-               status);
-  const int gridf = (int)std::max<int64_t>(1, std::min<int64_t>((A.n * LPR + 255) / 256, 148 * 16));
-  launch_pdl(spmm_nnz_fix<KP, NnzCsr>, gridf, 256, 0, st, NnzCsr{A.rowptr, A.colidx, A.val}, A.n,
-             reinterpret_cast<const float4*>(carry), reinterpret_cast<float4*>(Y), status);
-}
-
-void launch_mark_pull(const symnmf_matrix& A, const int64_t* chunk_row, uint32_t* bits, const int32_t* slot_of,
-                      const float* Z, int k, float* Y, float* carry, const int32_t* status, cudaStream_t st) {
-  switch (k) {
-    case 8: mark_pull_t<8>(A, chunk_row, bits, slot_of, Z, Y, carry, status, st); break;
-    case 16: mark_pull_t<16>(A, chunk_row, bits, slot_of, Z, Y, carry, status, st); break;
-    case 32: mark_pull_t<32>(A, chunk_row, bits, slot_of, Z, Y, carry, status, st); break;
-    default: mark_pull_t<64>(A, chunk_row, bits, slot_of, Z, Y, carry, status, st); break;
-  }
-}
-
 size_t spmm_nnz_carry_floats(int64_t nnz, int k) { return (size_t)2 * spmm_nnz_chunks(nnz) * k; }
 
 void launch_spmm_nnz_rows(const symnmf_matrix& A, int64_t* chunk_row, cudaStream_t st) {
@@ -299,16 +169,22 @@ void launch_spmm_nnz(const symnmf_matrix& A, const int64_t* chunk_row, const flo
   spmm_nnz_k(NnzCsr{A.rowptr, A.colidx, A.val}, A.n, A.nnz, nullptr, chunk_row, F, k, Y, carry, status, st);
 }
 
-// The sampled product from the destination buckets (bucket.cu) as an nnz-balanced SpMM over
-// (off, ent) with gather table Z: chunk rows found per plan (total entries = off[n], on device).
-void launch_bucket_spmm(const int32_t* off, const int2* ent, int64_t n, int64_t cap_entries, const float* Z, int k,
-                        float* Y, int64_t* chunk_row, float* carry, const int32_t* status, cudaStream_t st) {
-  const NnzBucket src{off, ent};
-  const int64_t nc = spmm_nnz_chunks(cap_entries);
-  if (nc > 0)
-    launch_pdl(spmm_nnz_rows_kernel<NnzBucket>, (unsigned)((nc + 255) / 256), 256, 0, st, src, n, cap_entries,
-               off + n, chunk_row, status);
-  spmm_nnz_k(src, n, cap_entries, off + n, chunk_row, Z, k, Y, carry, status, st);
+// ---------------------------------------------------------------- CSR input check (once per A)
+// *bad = 1 if some row's column indices are not sorted, unique and in [0, n) (caller zeroes *bad).
+__global__ void csr_check_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, int64_t n,
+                                 int32_t* __restrict__ bad) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (r >= n) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t e0 = rowptr[r], e1 = rowptr[r + 1];
+  for (int64_t e = e0 + lane; e < e1; e += 32) {
+    const int32_t c = col[e];
+    if (c < 0 || c >= n || (e > e0 && c <= col[e - 1])) atomicExch(bad, 1);
+  }
+}
+
+void launch_csr_check(const symnmf_matrix& A, int32_t* bad, cudaStream_t st) {
+  if (A.n > 0) csr_check_kernel<<<(unsigned)((A.n + 7) / 8), 256, 0, st>>>(A.rowptr, A.colidx, A.n, bad);
 }
 
 }  // namespace symnmf

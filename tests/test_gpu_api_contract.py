@@ -142,21 +142,3 @@ def test_solver_rejects_malformed_csr(defect):
     sv = S.Solver(S.DeviceMatrix.from_host(A), cu(H0), cu(H0), alpha, mode="exact", max_iters=1)
     sv.close()
 
-
-def test_mark_path_rejects_nonsymmetric_pattern(monkeypatch):
-    """The mirror-marked sampled product needs every (r, c) to have its mirror (c, r) (both triangles
-    stored): a pattern with a one-sided entry is refused at solver creation."""
-    from synth.configs import CsrMatrix
-    monkeypatch.setenv("SYMNMF_SAMPLED", "mark")
-    d = make_input("c2", n_override=4_000)
-    A, H0, alpha = d["A"], d["H0"], d["alpha"]
-    rows = np.repeat(np.arange(A.n), np.diff(A.rowptr))
-    drop = int(np.nonzero(rows < A.colidx)[0][0])                   # remove one upper-triangle entry only
-    keep = np.ones(A.nnz, dtype=bool)
-    keep[drop] = False
-    rowptr = np.zeros(A.n + 1, dtype=np.int64)
-    np.cumsum(np.bincount(rows[keep], minlength=A.n), out=rowptr[1:])
-    B = CsrMatrix(A.n, rowptr, A.colidx[keep].copy(), A.val[keep].copy())
-    with pytest.raises(S.A.SymNMFError):
-        S.Solver(S.DeviceMatrix.from_host(B), cu(H0), cu(H0), alpha, mode="lvs", s=200, tau=1.0 / 200, seed=1,
-                 max_iters=1)

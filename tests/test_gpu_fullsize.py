@@ -183,7 +183,7 @@ def test_c3_full_size_lvs_solver_half_vs_oracle(c3):
 def test_c4_full_size_sampled_parity(c4):
     """c4 (CSR n = 2,000,000, 1e8 nonzeros, k = 32): SpMM rows, scores, plan (s = 20,000, with a
     non-empty deterministic set), sampled-product rows, and W rows after one EXACT solver
-    iteration (the tile kernel with the sweep fused, as bench.py times it)."""
+    iteration (the nnz-balanced SpMM + streaming sweep, as bench.py times it)."""
     M, idx = check_product_scores_plan_sampled(c4, "fp32", seed=41, tile=256, stride=7)
     check_solver_exact_w_rows(c4, M, idx, "fp32", 1e-5)
 
@@ -299,7 +299,7 @@ def test_c3_full_size_10_iterations_lvs(c3):
 
 
 def test_c4_full_size_10_iterations_exact(c4):
-    """c4 EXACT (the tile kernel in column-block passes, as bench.py times it), 10 iterations."""
+    """c4 EXACT (nnz-balanced SpMM + streaming sweep, as bench.py times it), 10 iterations."""
     run_exact(c4, S.DeviceMatrix.from_host(c4["A"]), "fp32")
 
 

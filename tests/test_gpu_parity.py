@@ -464,20 +464,14 @@ def _csr_case(cfgname, n, k, seed=7):
 
 @pytest.mark.parametrize("cfgname,n,k", [("c2", 20_000, 16), ("c2", 20_000, 8), ("c4", 40_000, 32),
                                          ("c4", 40_000, 64), ("c4", 40_032, 16), ("c2", 2_000, 32)])
-@pytest.mark.parametrize("tile", ["nnz", "rows", "always", "blocks3", "blocks7"])
+@pytest.mark.parametrize("tile", ["nnz", "rows"])
 def test_csr_tile_exact_one_iteration(cfgname, n, k, tile, monkeypatch):
-    """Solver EXACT on CSR, every product form: the nnz-balanced SpMM (chunks of 256 nonzeros with
-    carries, default) and the row-group SpMM (SYMNMF_CSR_SPMM=rows), each + the streaming sweep;
-    the tile kernel (A F per 256-row tile fused with the sweep and the next Gram;
-    SYMNMF_CSR_TILE=always), also in 3 and 7 column-block passes (SYMNMF_CSR_BLOCKS): W and H
-    after one iteration vs the oracle's fp64 iteration.  Covers ragged last tiles (n % 256 != 0),
-    hub rows (power-law c4 recipe) and k = 8..64."""
+    """Solver EXACT on CSR, both SpMM forms: the nnz-balanced SpMM (chunks of 256 nonzeros with
+    carries, default) and the row-group SpMM (SYMNMF_CSR_SPMM=rows), each followed by the streaming
+    sweep: W and H after one iteration vs the oracle's fp64 iteration.  Covers ragged last tiles
+    (n % 256 != 0), hub rows (power-law c4 recipe) and k = 8..64."""
     if tile == "rows":
         monkeypatch.setenv("SYMNMF_CSR_SPMM", "rows")
-    if tile not in ("nnz", "rows"):
-        monkeypatch.setenv("SYMNMF_CSR_TILE", "always")
-    if tile.startswith("blocks"):
-        monkeypatch.setenv("SYMNMF_CSR_BLOCKS", tile[6:])
     A, H0, alpha = _csr_case(cfgname, n, k)
     M = S.DeviceMatrix.from_host(A)
     W, H = cu(H0), cu(H0)
@@ -491,14 +485,12 @@ def test_csr_tile_exact_one_iteration(cfgname, n, k, tile, monkeypatch):
 
 
 @pytest.mark.parametrize("cfgname,n,k,s", [("c4", 40_000, 32, 800), ("c2", 20_000, 16, 400), ("c4", 40_000, 8, 2000)])
-@pytest.mark.parametrize("slice_mb", ["", "1", "bucket", "mark"])
+@pytest.mark.parametrize("slice_mb", ["", "1"])
 def test_csr_lvs_solver_equals_abi_composition(cfgname, n, k, s, slice_mb, monkeypatch):
-    """Solver LvS on CSR graphs with hubs equals the composition of the ABI calls on the same device
-    data, for every form of the sampled product: the vector-atomic scatter ("", and slice_mb = 1:
-    several destination-range passes), the destination buckets ("bucket") and the mirror marks
-    ("mark", the default for large graphs)."""
-    monkeypatch.setenv("SYMNMF_SAMPLED", {"bucket": "bucket", "mark": "mark"}.get(slice_mb, "scatter"))
-    if slice_mb == "1":
+    """Solver LvS on CSR graphs with hubs (vector-atomic scatter of the sampled product, fused Gram)
+    equals the composition of the ABI calls on the same device data; slice_mb = 1 forces several
+    destination-range passes of the sampled scatter."""
+    if slice_mb:
         monkeypatch.setenv("SYMNMF_SCATTER_SLICE_MB", slice_mb)
     A, H0, alpha = _csr_case(cfgname, n, k)
     tau = 1.0 / s
@@ -523,11 +515,9 @@ def test_csr_lvs_solver_equals_abi_composition(cfgname, n, k, s, slice_mb, monke
     assert rel(H1.cpu().numpy(), H2.cpu().numpy()) < 1e-5
 
 
-@pytest.mark.parametrize("path", ["mark", "bucket", "scatter"])
-def test_csr_lvs_replayed_plan_vs_oracle(path, monkeypatch):
+def test_csr_lvs_replayed_plan_vs_oracle():
     """One LvS half through the solver vs the oracle's sampled products + sweep fed the plan the
     GPU drew (the same plan is recomputed by the ABI sampler from the same device scores)."""
-    monkeypatch.setenv("SYMNMF_SAMPLED", path)
     A, H0, alpha = _csr_case("c4", 30_016, 32)
     s, tau = 600, 1.0 / 600
     M = S.DeviceMatrix.from_host(A)
@@ -732,17 +722,13 @@ def _drop_vertices(A, frac, tail, seed=3):
     return CsrMatrix(A.n, rowptr, A.colidx[keep].copy(), A.val[keep].copy())
 
 
-@pytest.mark.parametrize("tile", ["nnz", "rows", "always", "blocks3"])
+@pytest.mark.parametrize("tile", ["nnz", "rows"])
 def test_csr_empty_rows(tile, monkeypatch):
     """Isolated vertices (empty CSR rows, 10% random + an empty 300-row tail): the product, the
-    sampled product over all rows, one EXACT solver iteration (nnz-balanced SpMM, row SpMM, tile
-    kernel in one or three column-block passes), and one LvS half of the bucketed solver path."""
+    sampled product over all rows, one EXACT solver iteration (nnz-balanced and row SpMM), and one
+    LvS half of the solver."""
     if tile == "rows":
         monkeypatch.setenv("SYMNMF_CSR_SPMM", "rows")
-    if tile not in ("nnz", "rows"):
-        monkeypatch.setenv("SYMNMF_CSR_TILE", "always")
-    if tile == "blocks3":
-        monkeypatch.setenv("SYMNMF_CSR_BLOCKS", "3")
     A0, H0, alpha = _csr_case("c2", 20_000, 16)
     A = _drop_vertices(A0, 0.1, 300)
     assert (np.diff(A.rowptr) == 0).sum() >= 2000
@@ -758,18 +744,16 @@ def test_csr_empty_rows(tile, monkeypatch):
     Wr, Hr, _ = O.iterate(A, H0, H0, alpha, 1, "exact")
     assert rel(W.cpu().numpy(), Wr) < 1e-5
     assert rel(H.cpu().numpy(), Hr) < 1e-5
-    # LvS, bucketed and mirror-marked sampled products: W-half vs the oracle fed the plan the GPU draws
+    # LvS: W-half vs the oracle fed the plan the GPU draws
     s_, tau = 800, 1.0 / 800
     ph = S.hybrid_sample(S.leverage_scores(cu(H0)), 16, s_, tau, 5, 0, 0).to_host()
     Gs, Ys = O.sampled_products(A, H0, ph["uniq_idx"], ph["uniq_w"])
-    for path in ("bucket", "mark"):
-        monkeypatch.setenv("SYMNMF_SAMPLED", path)
-        W, H = cu(H0), cu(H0)
-        sv = S.Solver(M, W, H, alpha, mode="lvs", s=s_, tau=tau, seed=5, max_iters=1)
-        sv.run(1)
-        assert sv.stats()["status"] == 0
-        sv.close()
-        assert rel(W.cpu().numpy(), O.hals_sweep(Gs, Ys, H0, H0, alpha)) < 1e-5, path
+    W, H = cu(H0), cu(H0)
+    sv = S.Solver(M, W, H, alpha, mode="lvs", s=s_, tau=tau, seed=5, max_iters=1)
+    sv.run(1)
+    assert sv.stats()["status"] == 0
+    sv.close()
+    assert rel(W.cpu().numpy(), O.hals_sweep(Gs, Ys, H0, H0, alpha)) < 1e-5
 
 
 def test_csr_zero_matrix():
@@ -783,10 +767,8 @@ def test_csr_zero_matrix():
     Y = S.ah(M, cu(H0)).cpu().numpy()
     assert not Y.any()
     lvs = dict(s=300, tau=1.0 / 300, seed=2)
-    for mode, kw, env, path in (("exact", {}, "never", ""), ("exact", {}, "always", ""), ("lvs", lvs, "", "scatter"),
-                                ("lvs", lvs, "", "bucket"), ("lvs", lvs, "", "mark")):
-        os.environ["SYMNMF_CSR_TILE"] = env   # EXACT: nnz SpMM / tile kernel
-        os.environ["SYMNMF_SAMPLED"] = path or "scatter"
+    for mode, kw, spmm in (("exact", {}, "nnz"), ("exact", {}, "rows"), ("lvs", lvs, "nnz")):
+        os.environ["SYMNMF_CSR_SPMM"] = spmm
         W, H = cu(H0), cu(H0)
         sv = S.Solver(M, W, H, alpha, mode=mode, max_iters=1, **kw)
         sv.run(1)
@@ -797,4 +779,4 @@ def test_csr_zero_matrix():
             Wr, Hr, _ = O.iterate(A, H0, H0, alpha, 1, "exact")
             assert rel(Wg, Wr) < 1e-5 and rel(H.cpu().numpy(), Hr) < 1e-5
         assert np.isfinite(Wg).all() and (Wg >= 0).all()
-    os.environ.pop("SYMNMF_CSR_TILE"); os.environ.pop("SYMNMF_SAMPLED")
+    os.environ.pop("SYMNMF_CSR_SPMM")
