@@ -137,6 +137,7 @@ def _scores(n, k, seed, power=3):
     (1, 1, 1, 1.0, 0, 0, 0),
     (2_000_000, 32, 20_000, 1 / 20_000, 0, 1, 1),
     ((1 << 20) + 17, 4, 30_000, 1 / 30_000, 9, 5, 0),
+    (6_500_003, 4, 20_000, 1 / 20_000, 2, 3, 1),   # > 6144 prefix blocks: the one-level draw search
 ])
 def test_hybrid_plan_bit_exact(n, k, s, tau, seed, it, side):
     lev = _scores(n, k, seed + 11)
