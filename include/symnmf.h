@@ -116,6 +116,10 @@ typedef struct {
  *   SYMNMF_SWEEP_CMEM=0            streaming sweep and leverage scores: G / R from shared memory
  *                                  instead of the constant bank (a solver holds one of 4 constant
  *                                  slots; beyond 4 live solvers the shared-memory form is used).
+ *   SYMNMF_SAMPLED=scatter|coarse  LvS solver on CSR: the sampled product as the vector-atomic
+ *                                  scatter (default below 16M nonzeros) or the two-level sort of the
+ *                                  sampled nonzeros by destination row (default from 16M; k in
+ *                                  {8,16,32,64}, n <= 2^25).
  *   SYMNMF_SCATTER_SLICE_MB=<mb>   sampled CSR scatter product: rows of Y per destination-range
  *                                  pass (default 86 MB, so each pass's slice of Y stays in L2).
  *   SYMNMF_LAI_FUSED=never         LAI solver (k = 64, l <= 80): use the four-kernel half (U^T F,

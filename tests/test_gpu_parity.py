@@ -486,12 +486,14 @@ def test_csr_tile_exact_one_iteration(cfgname, n, k, tile, monkeypatch):
 
 
 @pytest.mark.parametrize("cfgname,n,k,s", [("c4", 40_000, 32, 800), ("c2", 20_000, 16, 400), ("c4", 40_000, 8, 2000)])
-@pytest.mark.parametrize("slice_mb", ["", "1"])
+@pytest.mark.parametrize("slice_mb", ["", "1", "coarse"])
 def test_csr_lvs_solver_equals_abi_composition(cfgname, n, k, s, slice_mb, monkeypatch):
-    """Solver LvS on CSR graphs with hubs (vector-atomic scatter of the sampled product, fused Gram)
-    equals the composition of the ABI calls on the same device data; slice_mb = 1 forces several
-    destination-range passes of the sampled scatter."""
-    if slice_mb:
+    """Solver LvS on CSR graphs with hubs equals the composition of the ABI calls on the same device
+    data, for both forms of the sampled product: the vector-atomic scatter ("", and slice_mb = 1:
+    several destination-range passes) and the two-level destination sort ("coarse", coarse.cu, the
+    default from 16M nonzeros)."""
+    monkeypatch.setenv("SYMNMF_SAMPLED", "coarse" if slice_mb == "coarse" else "scatter")
+    if slice_mb == "1":
         monkeypatch.setenv("SYMNMF_SCATTER_SLICE_MB", slice_mb)
     A, H0, alpha = _csr_case(cfgname, n, k)
     tau = 1.0 / s
@@ -516,9 +518,11 @@ def test_csr_lvs_solver_equals_abi_composition(cfgname, n, k, s, slice_mb, monke
     assert rel(H1.cpu().numpy(), H2.cpu().numpy()) < 1e-5
 
 
-def test_csr_lvs_replayed_plan_vs_oracle():
+@pytest.mark.parametrize("path", ["coarse", "scatter"])
+def test_csr_lvs_replayed_plan_vs_oracle(path, monkeypatch):
     """One LvS half through the solver vs the oracle's sampled products + sweep fed the plan the
     GPU drew (the same plan is recomputed by the ABI sampler from the same device scores)."""
+    monkeypatch.setenv("SYMNMF_SAMPLED", path)
     A, H0, alpha = _csr_case("c4", 30_016, 32)
     s, tau = 600, 1.0 / 600
     M = S.DeviceMatrix.from_host(A)
@@ -749,12 +753,14 @@ def test_csr_empty_rows(tile, monkeypatch):
     s_, tau = 800, 1.0 / 800
     ph = S.hybrid_sample(S.leverage_scores(cu(H0)), 16, s_, tau, 5, 0, 0).to_host()
     Gs, Ys = O.sampled_products(A, H0, ph["uniq_idx"], ph["uniq_w"])
-    W, H = cu(H0), cu(H0)
-    sv = S.Solver(M, W, H, alpha, mode="lvs", s=s_, tau=tau, seed=5, max_iters=1)
-    sv.run(1)
-    assert sv.stats()["status"] == 0
-    sv.close()
-    assert rel(W.cpu().numpy(), O.hals_sweep(Gs, Ys, H0, H0, alpha)) < 1e-5
+    for path in ("scatter", "coarse"):
+        monkeypatch.setenv("SYMNMF_SAMPLED", path)
+        W, H = cu(H0), cu(H0)
+        sv = S.Solver(M, W, H, alpha, mode="lvs", s=s_, tau=tau, seed=5, max_iters=1)
+        sv.run(1)
+        assert sv.stats()["status"] == 0
+        sv.close()
+        assert rel(W.cpu().numpy(), O.hals_sweep(Gs, Ys, H0, H0, alpha)) < 1e-5, path
 
 
 def test_csr_zero_matrix():
@@ -768,8 +774,10 @@ def test_csr_zero_matrix():
     Y = S.ah(M, cu(H0)).cpu().numpy()
     assert not Y.any()
     lvs = dict(s=300, tau=1.0 / 300, seed=2)
-    for mode, kw, spmm in (("exact", {}, "nnz"), ("exact", {}, "rows"), ("lvs", lvs, "nnz")):
+    for mode, kw, spmm in (("exact", {}, "nnz"), ("exact", {}, "rows"), ("lvs", lvs, "scatter"),
+                           ("lvs", lvs, "coarse")):
         os.environ["SYMNMF_CSR_SPMM"] = spmm
+        os.environ["SYMNMF_SAMPLED"] = spmm
         W, H = cu(H0), cu(H0)
         sv = S.Solver(M, W, H, alpha, mode=mode, max_iters=1, **kw)
         sv.run(1)
@@ -780,4 +788,4 @@ def test_csr_zero_matrix():
             Wr, Hr, _ = O.iterate(A, H0, H0, alpha, 1, "exact")
             assert rel(Wg, Wr) < 1e-5 and rel(H.cpu().numpy(), Hr) < 1e-5
         assert np.isfinite(Wg).all() and (Wg >= 0).all()
-    os.environ.pop("SYMNMF_CSR_SPMM")
+    os.environ.pop("SYMNMF_CSR_SPMM"); os.environ.pop("SYMNMF_SAMPLED")
