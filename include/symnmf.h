@@ -109,17 +109,15 @@ typedef struct {
 
 /* Tuning knobs read from the environment when a call is enqueued (host only; results are
  * the same up to fp32 summation order):
- *   SYMNMF_CSR_SPMM=rows           EXACT solver on CSR (k in {8,16,32,64}): the row-group SpMM
- *                                  instead of the default nnz-balanced one (chunks of 256 nonzeros).
- *   SYMNMF_SWEEP=fused             k in {8,16,32}: the register-tile sweep instead of the streaming
- *                                  (cp.async-staged) sweep.
+ *   SYMNMF_CSR_SPMM=rows|nnz       EXACT solver on CSR: the row-group SpMM or (k in {8,16,32,64})
+ *                                  the nnz-balanced one (chunks of 256 nonzeros); default: nnz-
+ *                                  balanced from 16M nonzeros.
+ *   SYMNMF_SWEEP=fused|stream      k in {8,16,32}: the register-tile sweep or the streaming
+ *                                  (cp.async-staged, two CTAs/SM) sweep; default: streaming from
+ *                                  2^20 rows.
  *   SYMNMF_SWEEP_CMEM=0            streaming sweep and leverage scores: G / R from shared memory
  *                                  instead of the constant bank (a solver holds one of 4 constant
  *                                  slots; beyond 4 live solvers the shared-memory form is used).
- *   SYMNMF_SAMPLED=scatter|coarse  LvS solver on CSR: the sampled product as the vector-atomic
- *                                  scatter (default below 16M nonzeros) or the two-level sort of the
- *                                  sampled nonzeros by destination row (default from 16M; k in
- *                                  {8,16,32,64}, n <= 2^25).
  *   SYMNMF_SCATTER_SLICE_MB=<mb>   sampled CSR scatter product: rows of Y per destination-range
  *                                  pass (default 86 MB, so each pass's slice of Y stays in L2).
  *   SYMNMF_LAI_FUSED=never         LAI solver (k = 64, l <= 80): use the four-kernel half (U^T F,

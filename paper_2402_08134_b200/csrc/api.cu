@@ -580,9 +580,6 @@ struct symnmf_solver {
   float* carry;
   int cslot;               // constant-table slot of the streaming sweep (-1: G in shared memory)
   float* ctab;             // scratch for the table copied to the constant bank
-  bool coarse;             // LvS on a large CSR A: the sampled product by a two-level sort (coarse.cu)
-  CoarseWs cw;
-  float* Zt;               // its gather table Z[t] = omega_t f_{u_t} (cap x k)
   bool record;             // SYMNMF_RECORD_PLANS: per-half copies of the scores and plan
   float* hlev;
   int32_t* huniq;
@@ -640,9 +637,11 @@ bool sweep_cmem_enabled() {
 
 // The streaming sweep (sweep.cu) for k in {8, 16, 32}; SYMNMF_SWEEP=fused selects the register-tile
 // sweep_fused instead (symnmf.h)
-bool sweep_stream_enabled() {
+bool sweep_stream_enabled(int64_t n) {
   const char* e = getenv("SYMNMF_SWEEP");
-  return !(e && !strcmp(e, "fused"));
+  if (e && !strcmp(e, "fused")) return false;
+  if (e && !strcmp(e, "stream")) return true;
+  return n >= (1ll << 20);   // c4: 0.33 vs 0.43 ms; c2 (n = 100k, L2 resident): 31 vs 29 us
 }
 
 // Update(G + alpha I, Y + alpha F^T): one HALS sweep with the next half's Gram (and R) fused, or
@@ -654,7 +653,7 @@ void enqueue_sweep(const symnmf_solver& S, int side, const double* G, const floa
     launch_gram_fused(X, S.n, S.k, S.Gacc, Gnext, Rf32, S.counter, status, st);
     return;
   }
-  if (sweep_stream_supported(S.k) && sweep_stream_enabled())
+  if (sweep_stream_supported(S.k) && sweep_stream_enabled(S.n))
     launch_sweep_stream(G, S.alpha, S.Y, F, X, S.n, S.k, zeroY, S.Gacc, Gnext, Rf32, S.counter, status, st,
                         S.cslot >= 0 ? 2 * S.cslot + side : -1, S.ctab);
   else
@@ -669,18 +668,11 @@ bool lai_enabled() {
 
 // EXACT CSR (kpad(k) == k): the nnz-balanced SpMM by default, the row-group SpMM with
 // SYMNMF_CSR_SPMM=rows (symnmf.h)
-bool csr_spmm_nnz() {
+bool csr_spmm_nnz(int64_t nnz) {
   const char* e = getenv("SYMNMF_CSR_SPMM");
-  return !(e && !strcmp(e, "rows"));
-}
-
-// LvS CSR sampled product: the two-level destination sort (coarse.cu) from 16M nonzeros, else the
-// vector-atomic scatter; SYMNMF_SAMPLED=scatter|coarse overrides (symnmf.h)
-bool sampled_coarse(int64_t nnz) {
-  const char* e = getenv("SYMNMF_SAMPLED");
-  if (e && !strcmp(e, "scatter")) return false;
-  if (e && !strcmp(e, "coarse")) return true;
-  return nnz >= (16ll << 20);
+  if (e && !strcmp(e, "rows")) return false;
+  if (e && !strcmp(e, "nnz")) return true;
+  return nnz >= (16ll << 20);   // c2 (2M nonzeros): row groups 26 us vs 60 us; c4: 5.4 ms vs 1.8 ms
 }
 
 // Profiling hook: records an event after the launch site just enqueued (no-op unless profiling).
@@ -710,12 +702,10 @@ void solver_layout(symnmf_solver& S, Carver& c) {
   S.Gs = c.take<double>((size_t)k * k);
   S.GH = c.take<double>((size_t)k * k);
   S.gpart = c.take<double>(gram_partial_doubles(k, k, true, S.ggrid));
-  S.nnzsp = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode == SYMNMF_EXACT && csr_spmm_nnz();
+  S.nnzsp = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && S.mode == SYMNMF_EXACT && csr_spmm_nnz(S.A.nnz);
   S.chunk_row = c.take<int64_t>(S.nnzsp ? (size_t)spmm_nnz_chunks(S.A.nnz) : 0);
   S.carry = c.take<float>(S.nnzsp ? spmm_nnz_carry_floats(S.A.nnz, k) : 0);
   S.ctab = c.take<float>(sweep_table_floats());
-  S.coarse = S.hasA && S.A.kind == SYMNMF_CSR && S.mode == SYMNMF_LVS && !S.bpp &&
-             coarse_supported(n, S.A.nnz, k) && sampled_coarse(S.A.nnz);
   S.nonconv = c.take<int32_t>(1);
   S.Y = c.take<float>((size_t)n * k);
   S.stats = c.take<symnmf_half_stats>((size_t)2 * S.max_iters);
@@ -740,10 +730,6 @@ void solver_layout(symnmf_solver& S, Carver& c) {
     S.plan.uniq_w = c.take<double>(n);
     S.plan.counts = c.take<int64_t>(4);
     S.plan.mass = c.take<double>(2);
-    if (S.coarse) {
-      coarse_layout(c, n, S.A.nnz, S.plan.cap, &S.cw);
-      S.Zt = c.take<float>((size_t)S.plan.cap * k);
-    }
     const size_t halves = S.record ? (size_t)2 * S.max_iters : 0;
     S.hlev = c.take<float>(halves * n);
     S.huniq = c.take<int32_t>(halves * S.plan.cap);
@@ -807,18 +793,8 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     // G_s and Y_s only read the plan: G_s runs on a second branch of the graph, concurrently
     cudaEventRecord(S.ev_fork[side], st);
     cudaStreamWaitEvent(S.side, S.ev_fork[side], 0);
-    launch_sampled_gram_fused(F, k, S.plan, S.Gacc, S.Gs, S.counter, status, S.side, S.coarse ? S.Zt : nullptr);
+    launch_sampled_gram_fused(F, k, S.plan, S.Gacc, S.Gs, S.counter, status, S.side);
     cudaEventRecord(S.ev_join[side], S.side);
-    if (S.coarse) {
-      // the sampled nonzeros sorted by destination row in two levels; each row of Y_s written once
-      launch_coarse_partition(S.A, S.plan.uniq_idx, S.plan.counts + 2, S.cw, S.counter + 1, status, st);
-      cudaStreamWaitEvent(st, S.ev_join[side], 0);
-      launch_coarse_rows(S.cw, n, S.Zt, k, S.Y, status, st);
-      mark(S, st, "sampled_ah_csr");
-      enqueue_sweep(S, side, S.Gs, F, X, false, Gnext, S.Rinv32, status, st);
-      mark(S, st, S.bpp ? "bpp_update" : "hals_sweep");
-      return true;
-    }
     if (S.A.kind == SYMNMF_CSR) {
       launch_sampled_csr_nozero(S.A, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap, S.Y,
                                 status, st);
@@ -927,7 +903,6 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
     launch_scale_rows(S.Z, S.l, k, S.lam, S.Mside[0], S.status, st);
   }
   if (mode == SYMNMF_LVS && S.Y) SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Y, 0, sizeof(float) * n * k, st));
-  if (S.coarse) SYMNMF_CUDA_TRY(cudaMemsetAsync(S.cw.gcnt, 0, sizeof(int32_t) * (S.cw.nb + 1), st));
   if (S.hasA && S.A.kind == SYMNMF_CSR) {
     // every sparse path assumes each row's columns sorted, unique and in range (the destination
     // ranges of the sampled scatter binary-search them)
@@ -948,7 +923,7 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
   if (finish() != SYMNMF_OK) return SYMNMF_ERR_CUDA;
   // Capture one iteration on a private stream (the caller's may be the legacy default stream).
   // Every failure from here on releases what was created (release_solver_resources).
-  S.cslot = (sweep_stream_supported(k) && sweep_stream_enabled() && sweep_cmem_enabled()) ? sweep_cslot_acquire() : -1;
+  S.cslot = (sweep_stream_supported(k) && sweep_stream_enabled(n) && sweep_cmem_enabled()) ? sweep_cslot_acquire() : -1;
   symnmf_status rs = SYMNMF_OK;
   cudaStream_t cs = nullptr;
   cudaGraph_t g = nullptr;

@@ -405,8 +405,7 @@ __global__ void __launch_bounds__(FT) sampled_gram_fused(const float* __restrict
                                                          const int32_t* __restrict__ uniq,
                                                          const double* __restrict__ w,
                                                          const int64_t* __restrict__ n_uniq_dev, double* Gacc,
-                                                         double* Gout, unsigned int* counter, int32_t* status,
-                                                         float* __restrict__ Z) {
+                                                         double* Gout, unsigned int* counter, int32_t* status) {
   constexpr int ST = KP + 4;
   constexpr int ROWS = 64;
   __shared__ __align__(16) float s[ROWS * ST];
@@ -439,11 +438,6 @@ __global__ void __launch_bounds__(FT) sampled_gram_fused(const float* __restrict
       for (int q = 0; q < Q; ++q) {
         const int e = threadIdx.x + q * FT, r = e / (KP / 4), c = e - r * (KP / 4);
         if (e < NV) *reinterpret_cast<float4*>(s + r * ST + 4 * c) = v[q];
-        if (Z && e < NV && r < rows) {   // Z[t] = omega_t f_{u_t}: the gather table of the sorted product
-          const float om = sw[r];
-          reinterpret_cast<float4*>(Z)[(r0 + r) * (KP / 4) + c] =
-              make_float4(om * v[q].x, om * v[q].y, om * v[q].z, om * v[q].w);
-        }
       }
     } else {
       for (int e = threadIdx.x; e < ROWS * KP; e += FT) {
@@ -554,13 +548,13 @@ void launch_uniq_count_fused(const float* lev, int64_t n, double T, const Sample
 }
 
 void launch_sampled_gram_fused(const float* F, int k, const symnmf_plan& plan, double* Gacc, double* Gout,
-                               unsigned int* counter, int32_t* status, cudaStream_t st, float* Z) {
+                               unsigned int* counter, int32_t* status, cudaStream_t st) {
   const int grid = fused_grid((plan.cap + 63) / 64, 1);
   switch (kpad(k)) {
-    case 8: launch_pdl(sampled_gram_fused<8>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status, Z); break;
-    case 16: launch_pdl(sampled_gram_fused<16>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status, Z); break;
-    case 32: launch_pdl(sampled_gram_fused<32>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status, Z); break;
-    default: launch_pdl(sampled_gram_fused<64>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status, Z); break;
+    case 8: launch_pdl(sampled_gram_fused<8>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
+    case 16: launch_pdl(sampled_gram_fused<16>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
+    case 32: launch_pdl(sampled_gram_fused<32>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
+    default: launch_pdl(sampled_gram_fused<64>, grid, FT, kRedBytes, st, F, k, plan.uniq_idx, plan.uniq_w, plan.counts + 2, Gacc, Gout, counter, status); break;
   }
 }
 

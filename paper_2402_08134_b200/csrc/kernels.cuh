@@ -92,9 +92,8 @@ void launch_leverage_fused(const float* F, int64_t n, int k, const float* Rinv, 
 void launch_uniq_count_fused(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
                              const int32_t* iter_dev, int32_t first_iter, int32_t max_iters, int side,
                              symnmf_half_stats* stats, unsigned int* counter, int32_t* status, cudaStream_t st);
-// Z (nullable, kpad(k) == k): the gather table Z[t] = (float) omega_t f_{u_t} of the sorted product
 void launch_sampled_gram_fused(const float* F, int k, const symnmf_plan& plan, double* Gacc, double* Gout,
-                               unsigned int* counter, int32_t* status, cudaStream_t st, float* Z = nullptr);
+                               unsigned int* counter, int32_t* status, cudaStream_t st);
 // sampler.cu passes used by the fused path
 void launch_samp_prefix(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
                         int32_t* status, cudaStream_t st);
@@ -130,25 +129,6 @@ void launch_sweep_stream(const double* G, double alpha, float* Y, const float* F
 int sweep_cslot_acquire();
 void sweep_cslot_release(int slot);
 size_t sweep_table_floats();
-
-// ---------------------------------------------------------------- coarse.cu (sampled CSR product, large graphs)
-struct CoarseWs {
-  int lb, nb;          // 2^lb destination rows per coarse bucket, nb buckets
-  int64_t cap;         // plan capacity
-  int64_t *ptsum, *pre, *rb;          // plan-row offsets
-  int32_t *gcnt, *gstart, *cursor;    // bucket counts (zero between plans), starts, cursors
-  int2* key;           // [nnz] (plan slot, row in bucket)
-  float* kval;         // [nnz] a_e
-  int2* sorted;        // [nnz] (plan slot, a_e) sorted by destination row within each bucket
-};
-bool coarse_supported(int64_t n, int64_t nnz, int k);
-void coarse_layout(Carver& c, int64_t n, int64_t nnz, int64_t cap, CoarseWs* w);
-// Plan-row offsets and the coarse partition of the sampled nonzeros; then (after the sampled Gram
-// wrote the gather table Z) every row of Y_s written once.
-void launch_coarse_partition(const symnmf_matrix& A, const int32_t* uniq, const int64_t* n_uniq_dev,
-                             const CoarseWs& w, unsigned int* counter, int32_t* status, cudaStream_t st);
-void launch_coarse_rows(const CoarseWs& w, int64_t n, const float* Z, int k, float* Y, int32_t* status,
-                        cudaStream_t st);
 
 // ---------------------------------------------------------------- bpp.cu (NEXT-1)
 // X <- exact per-row NLS with (G + alpha I, Y + alpha F) (block principal pivoting, k <= 32);

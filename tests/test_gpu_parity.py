@@ -471,8 +471,8 @@ def test_csr_tile_exact_one_iteration(cfgname, n, k, tile, monkeypatch):
     carries, default) and the row-group SpMM (SYMNMF_CSR_SPMM=rows), each followed by the streaming
     sweep: W and H after one iteration vs the oracle's fp64 iteration.  Covers ragged last tiles
     (n % 256 != 0), hub rows (power-law c4 recipe) and k = 8..64."""
-    if tile == "rows":
-        monkeypatch.setenv("SYMNMF_CSR_SPMM", "rows")
+    monkeypatch.setenv("SYMNMF_CSR_SPMM", tile)
+    monkeypatch.setenv("SYMNMF_SWEEP", "stream")
     A, H0, alpha = _csr_case(cfgname, n, k)
     M = S.DeviceMatrix.from_host(A)
     W, H = cu(H0), cu(H0)
@@ -486,13 +486,14 @@ def test_csr_tile_exact_one_iteration(cfgname, n, k, tile, monkeypatch):
 
 
 @pytest.mark.parametrize("cfgname,n,k,s", [("c4", 40_000, 32, 800), ("c2", 20_000, 16, 400), ("c4", 40_000, 8, 2000)])
-@pytest.mark.parametrize("slice_mb", ["", "1", "coarse"])
+@pytest.mark.parametrize("slice_mb", ["", "1", "stream"])
 def test_csr_lvs_solver_equals_abi_composition(cfgname, n, k, s, slice_mb, monkeypatch):
-    """Solver LvS on CSR graphs with hubs equals the composition of the ABI calls on the same device
-    data, for both forms of the sampled product: the vector-atomic scatter ("", and slice_mb = 1:
-    several destination-range passes) and the two-level destination sort ("coarse", coarse.cu, the
-    default from 16M nonzeros)."""
-    monkeypatch.setenv("SYMNMF_SAMPLED", "coarse" if slice_mb == "coarse" else "scatter")
+    """Solver LvS on CSR graphs with hubs (vector-atomic scatter of the sampled product, fused Gram)
+    equals the composition of the ABI calls on the same device data; slice_mb = 1 forces several
+    destination-range passes of the sampled scatter, "stream" the streaming sweep with G and R in
+    the constant bank (the default from 2^20 rows)."""
+    if slice_mb == "stream":
+        monkeypatch.setenv("SYMNMF_SWEEP", "stream")
     if slice_mb == "1":
         monkeypatch.setenv("SYMNMF_SCATTER_SLICE_MB", slice_mb)
     A, H0, alpha = _csr_case(cfgname, n, k)
@@ -518,11 +519,11 @@ def test_csr_lvs_solver_equals_abi_composition(cfgname, n, k, s, slice_mb, monke
     assert rel(H1.cpu().numpy(), H2.cpu().numpy()) < 1e-5
 
 
-@pytest.mark.parametrize("path", ["coarse", "scatter"])
-def test_csr_lvs_replayed_plan_vs_oracle(path, monkeypatch):
+@pytest.mark.parametrize("sweep", ["stream", "fused"])
+def test_csr_lvs_replayed_plan_vs_oracle(sweep, monkeypatch):
     """One LvS half through the solver vs the oracle's sampled products + sweep fed the plan the
     GPU drew (the same plan is recomputed by the ABI sampler from the same device scores)."""
-    monkeypatch.setenv("SYMNMF_SAMPLED", path)
+    monkeypatch.setenv("SYMNMF_SWEEP", sweep)
     A, H0, alpha = _csr_case("c4", 30_016, 32)
     s, tau = 600, 1.0 / 600
     M = S.DeviceMatrix.from_host(A)
@@ -732,8 +733,8 @@ def test_csr_empty_rows(tile, monkeypatch):
     """Isolated vertices (empty CSR rows, 10% random + an empty 300-row tail): the product, the
     sampled product over all rows, one EXACT solver iteration (nnz-balanced and row SpMM), and one
     LvS half of the solver."""
-    if tile == "rows":
-        monkeypatch.setenv("SYMNMF_CSR_SPMM", "rows")
+    monkeypatch.setenv("SYMNMF_CSR_SPMM", tile)
+    monkeypatch.setenv("SYMNMF_SWEEP", "stream")
     A0, H0, alpha = _csr_case("c2", 20_000, 16)
     A = _drop_vertices(A0, 0.1, 300)
     assert (np.diff(A.rowptr) == 0).sum() >= 2000
@@ -753,8 +754,8 @@ def test_csr_empty_rows(tile, monkeypatch):
     s_, tau = 800, 1.0 / 800
     ph = S.hybrid_sample(S.leverage_scores(cu(H0)), 16, s_, tau, 5, 0, 0).to_host()
     Gs, Ys = O.sampled_products(A, H0, ph["uniq_idx"], ph["uniq_w"])
-    for path in ("scatter", "coarse"):
-        monkeypatch.setenv("SYMNMF_SAMPLED", path)
+    for path in ("stream", "fused"):
+        monkeypatch.setenv("SYMNMF_SWEEP", path)
         W, H = cu(H0), cu(H0)
         sv = S.Solver(M, W, H, alpha, mode="lvs", s=s_, tau=tau, seed=5, max_iters=1)
         sv.run(1)
@@ -774,10 +775,10 @@ def test_csr_zero_matrix():
     Y = S.ah(M, cu(H0)).cpu().numpy()
     assert not Y.any()
     lvs = dict(s=300, tau=1.0 / 300, seed=2)
-    for mode, kw, spmm in (("exact", {}, "nnz"), ("exact", {}, "rows"), ("lvs", lvs, "scatter"),
-                           ("lvs", lvs, "coarse")):
+    for mode, kw, spmm in (("exact", {}, "nnz"), ("exact", {}, "rows"), ("lvs", lvs, "stream"),
+                           ("lvs", lvs, "fused")):
         os.environ["SYMNMF_CSR_SPMM"] = spmm
-        os.environ["SYMNMF_SAMPLED"] = spmm
+        os.environ["SYMNMF_SWEEP"] = spmm
         W, H = cu(H0), cu(H0)
         sv = S.Solver(M, W, H, alpha, mode=mode, max_iters=1, **kw)
         sv.run(1)
@@ -788,4 +789,4 @@ def test_csr_zero_matrix():
             Wr, Hr, _ = O.iterate(A, H0, H0, alpha, 1, "exact")
             assert rel(Wg, Wr) < 1e-5 and rel(H.cpu().numpy(), Hr) < 1e-5
         assert np.isfinite(Wg).all() and (Wg >= 0).all()
-    os.environ.pop("SYMNMF_CSR_SPMM"); os.environ.pop("SYMNMF_SAMPLED")
+    os.environ.pop("SYMNMF_CSR_SPMM"); os.environ.pop("SYMNMF_SWEEP")
