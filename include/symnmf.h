@@ -56,7 +56,7 @@ enum { SYMNMF_DENSE = 0, SYMNMF_CSR = 1 };        /* symnmf_matrix.kind         
 enum { SYMNMF_FP32 = 0, SYMNMF_3XTF32 = 1 };      /* precision of a dense product     */
 enum { SYMNMF_EXACT = 0, SYMNMF_LVS = 1, SYMNMF_LAI = 2 };  /* symnmf_iterate mode     */
 /* OR-ed into a mode: Update() by exact per-row NLS with block principal pivoting (ANLS-BPP,
- * P:155, App. G) instead of one HALS sweep (NEXT-1; k <= 32, else SYMNMF_ERR_UNSUPPORTED). */
+ * P:155, App. G) instead of one HALS sweep (NEXT-1; k <= 64, else SYMNMF_ERR_UNSUPPORTED). */
 enum { SYMNMF_RULE_BPP = 16 };
 /* Solver mode flag (LvS): keep the scores and plan of every half in device memory for
  * symnmf_solver_plan_history (costs ~20 n bytes per half; for parity tests, not for timing). */
@@ -203,7 +203,7 @@ symnmf_status symnmf_hals_sweep(const double* G, const float* Y, const float* F,
 
 /* NEXT-1 Update by block principal pivoting (App. G; Kim & Park full exchange
  * with the backup rule): X[r,:] = argmin_{x >= 0} x^T (G + alpha I) x - 2 (Y[r,:] + alpha F[r,:])^T x
- * for every row r, fp64 solves (G fp64 k x k, Y F X n x k fp32, k <= 32); X is overwritten
+ * for every row r, fp64 solves (G fp64 k x k, Y F X n x k fp32, k <= 64); X is overwritten
  * (its entry value is not used).  G_new (nullable)
  * receives X^T X.  nonconv_host (nullable; host-synchronising) receives the number of rows that
  * hit the 256-step pivoting cap (their last iterate, clipped at 0, is written). */

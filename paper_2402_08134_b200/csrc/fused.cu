@@ -227,74 +227,80 @@ struct LevR {
   }
 };
 
+// Scores of the sampler block's 1024 rows in four 256-row sub-tiles, staged with cp.async into a
+// double-buffered shared-memory ring (16 B chunks XOR-swizzled by row, so a thread reading its own
+// row is conflict free); with R in the constant bank three CTAs fit an SM.
+template <int KP>
+__device__ __forceinline__ int lev_swz(int c, int r) {
+  constexpr int C = KP / 4, RPL = 8 / (C < 8 ? C : 8);
+  return c ^ ((r / RPL) % C);
+}
+
 template <int KP, int TAB = -1>
-__global__ void __launch_bounds__(FT) leverage_fused(const float* __restrict__ F, int64_t n, int k,
-                                                     const float* __restrict__ Rinv, float* __restrict__ lev,
-                                                     double T, uint64_t* __restrict__ bw, uint32_t* __restrict__ bd,
-                                                     double* __restrict__ bt, int64_t s, int64_t cap,
-                                                     int64_t* __restrict__ counts, double* __restrict__ mass,
-                                                     unsigned int* counter, int32_t* status) {
-  constexpr int ST = KP + 4;
-  __shared__ __align__(16) float sR[KP * KP];
-  __shared__ float sRd[KP];
+__global__ void __launch_bounds__(FT, TAB >= 0 && KP <= 32 ? 3 : 1) leverage_fused(
+    const float* __restrict__ F, int64_t n, int k, const float* __restrict__ Rinv, float* __restrict__ lev, double T,
+    uint64_t* __restrict__ bw, uint32_t* __restrict__ bd, double* __restrict__ bt, int64_t s, int64_t cap,
+    int64_t* __restrict__ counts, double* __restrict__ mass, unsigned int* counter, int32_t* status) {
+  constexpr int C = KP / 4;
+  __shared__ __align__(16) float sR[TAB < 0 ? KP * KP : 4];
+  __shared__ float sRd[TAB < 0 ? KP : 1];
   __shared__ uint64_t shw[33];
   __shared__ uint32_t shd[33];
   __shared__ double sht[33];
   extern __shared__ __align__(16) unsigned char sml[];
-  float* sF = reinterpret_cast<float*>(sml);          // [256][ST]
+  float* sF = reinterpret_cast<float*>(sml);          // k == KP: [2][256][KP] swizzled; else [256][KP + 4]
   if (dev_failed(status)) return;
   const int tid = threadIdx.x;
-  for (int e = tid; e < KP * KP + KP; e += FT) {   // Rf = [R (KP x KP upper) | 1 / diag(R)]
-    if (e < KP * KP) sR[e] = Rinv[e]; else sRd[e - KP * KP] = Rinv[e];
+  if constexpr (TAB < 0) {
+    for (int e = tid; e < KP * KP + KP; e += FT) {   // Rf = [R (KP x KP upper) | 1 / diag(R)]
+      if (e < KP * KP) sR[e] = Rinv[e]; else sRd[e - KP * KP] = Rinv[e];
+    }
   }
   const int64_t b = blockIdx.x;                       // sampler block: rows [1024 b, 1024 b + 1024)
   uint64_t sw = 0;
   uint32_t sd = 0;
   double stt = 0.0;
-  constexpr int Q = FROWS * KP / 4 / FT;   // float4 per thread per 256-row sub-tile
-  float4 v[Q];                              // next sub-tile, loaded while the current one computes
-  auto load_sub = [&](int sub) {
+  constexpr int NSUB = kSampBlock / FROWS;
+  const bool full = k == KP;
+  auto issue = [&](int sub) {                         // cp.async of sub-tile `sub` into buffer sub & 1
     const int64_t r0 = b * kSampBlock + sub * FROWS;
     const int rows = (int)max64(0, min64(FROWS, n - r0));
-    const float4* src = reinterpret_cast<const float4*>(F + r0 * k);
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const int e = tid + q * FT;
-      v[q] = (e < rows * (KP / 4)) ? __ldg(src + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float* dst = sF + (sub & 1) * FROWS * KP;
+    for (int q = tid; q < FROWS * C; q += FT) {
+      const int r = q / C, c = q - r * C;
+      const bool ok = r < rows;
+      cp_async16(dst + r * KP + 4 * lev_swz<KP>(c, r), ok ? F + (r0 + r) * KP + 4 * c : F, ok);
     }
+    cp_async_commit();
   };
-  if (k == KP) load_sub(0);
-  for (int sub = 0; sub < kSampBlock / FROWS; ++sub) {
+  if (full) { issue(0); issue(1); }
+  for (int sub = 0; sub < NSUB; ++sub) {
     const int64_t r0 = b * kSampBlock + sub * FROWS;
     const int rows = (int)max64(0, min64(FROWS, n - r0));
-    __syncthreads();
-    if (rows > 0) {
-      if (k == KP) {
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          const int e = tid + q * FT, r = e / (KP / 4), c = e - r * (KP / 4);
-          *reinterpret_cast<float4*>(sF + r * ST + 4 * c) = v[q];
-        }
-        if (sub + 1 < kSampBlock / FROWS) load_sub(sub + 1);
-      } else {
-        for (int e = tid; e < FROWS * KP; e += FT) {
-          const int r = e / KP, c = e - r * KP;
-          sF[r * ST + c] = (r < rows && c < k) ? F[(r0 + r) * k + c] : 0.f;
-        }
+    const float* cur = sF + (full ? (sub & 1) * FROWS * KP : 0);
+    if (full) {
+      cp_async_wait<1>();                             // this sub-tile's group has landed
+      __syncthreads();
+    } else {
+      __syncthreads();
+      for (int e = tid; e < FROWS * KP; e += FT) {
+        const int r = e / KP, c = e - r * KP;
+        sF[r * (KP + 4) + c] = (r < rows && c < k) ? F[(r0 + r) * k + c] : 0.f;
       }
+      __syncthreads();
     }
-    __syncthreads();
     if (tid < rows) {
       float f[KP];
 #pragma unroll
       for (int a = 0; a < KP; a += 4) {
-        const float4 v = *reinterpret_cast<const float4*>(sF + tid * ST + a);
+        const float4 v = full ? *reinterpret_cast<const float4*>(cur + tid * KP + 4 * lev_swz<KP>(a / 4, tid))
+                              : *reinterpret_cast<const float4*>(sF + tid * (KP + 4) + a);
         f[a] = v.x; f[a + 1] = v.y; f[a + 2] = v.z; f[a + 3] = v.w;
       }
       // q = f R^{-1} by forward substitution q R = f (R upper, rd = 1 / diag R), l = ||q||^2.
       // Row a of R is read as float4 groups from the aligned group holding column a: entries
       // c <= a of f are dead once q_a is formed, so updating them too is harmless (R is stored
-      // with zeros below the diagonal), and the shared-memory loads drop fourfold.
+      // with zeros below the diagonal).
       const LevR<KP, TAB> rsrc{sR, sRd};
       float l = 0.f;
 #pragma unroll
@@ -314,6 +320,10 @@ __global__ void __launch_bounds__(FT) leverage_fused(const float* __restrict__ F
       sw += det ? 0ull : (uint64_t)__double2ull_rd(ld * kTwo40f);  // reading Z6
       sd += det ? 1u : 0u;
       stt += det ? ld : 0.0;
+    }
+    if (full) {
+      __syncthreads();                                // buffer sub & 1 free
+      if (sub + 2 < NSUB) issue(sub + 2); else cp_async_commit();   // keep one group per step
     }
   }
   sw = block_sum(sw, shw);
@@ -501,7 +511,7 @@ template <int KP, int TAB>
 static void leverage_fused_t(const float* F, int64_t n, int k, const float* Rinv, float* lev, double T,
                              const SamplerWs& w, int64_t s, const symnmf_plan& plan, unsigned int* counter,
                              int32_t* status, cudaStream_t st) {
-  const size_t smem = sizeof(float) * FROWS * (KP + 4);
+  const size_t smem = k == KP ? sizeof(float) * 2 * FROWS * KP : sizeof(float) * FROWS * (KP + 4);
   cudaFuncSetAttribute(leverage_fused<KP, TAB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   leverage_fused<KP, TAB><<<(unsigned)samp_blocks(n), FT, smem, st>>>(F, n, k, Rinv, lev, T, w.bw, w.bd, w.bt, s,
                                                                       plan.cap, plan.counts, plan.mass, counter,

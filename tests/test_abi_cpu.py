@@ -122,9 +122,10 @@ def test_next_items_argument_validation_without_gpu(lib):
     from paper_2402_08134_b200._abi import Matrix, RULE_BPP
     sz = C.c_size_t(0)
     G, Y, F, X = (C.c_void_p(256),) * 4
-    # BPP: alpha < 0, k > 32 unsupported, query ok
+    # BPP: alpha < 0, k > 64 rejected, query ok
     assert lib.symnmf_bpp_update(G, Y, F, X, 100, 8, -1.0, None, None, None, C.byref(sz), None) == 1
-    assert lib.symnmf_bpp_update(G, Y, F, X, 100, 40, 1.0, None, None, None, C.byref(sz), None) == 5
+    assert lib.symnmf_bpp_update(G, Y, F, X, 100, 40, 1.0, None, None, None, C.byref(sz), None) == 0   # k <= 64
+    assert lib.symnmf_bpp_update(G, Y, F, X, 100, 65, 1.0, None, None, None, C.byref(sz), None) == 1   # k > 64
     assert lib.symnmf_bpp_update(G, Y, F, X, 100, 16, 1.0, None, None, None, C.byref(sz), None) == 0
     dense = Matrix(0, 0, 1000, 256, 1000, None, None, 0)
     csr = Matrix(1, 0, 1000, 256, 0, 256, 256, 5000)
@@ -154,4 +155,4 @@ def test_next_items_argument_validation_without_gpu(lib):
     assert lib.symnmf_solve(C.byref(dense), 1000, W, H, 8, 1.0, 0 | RULE_BPP, 0, 0, 1.0, 0, None, None, 0, 50, 1e-4,
                             4, 1, its, None, None, C.byref(sz), None) == 0
     assert lib.symnmf_solver_create(None, C.byref(dense), 1000, W, H, 40, 1.0, RULE_BPP, 0, 0, 1.0, 0, 0, 5,
-                                    None, None, 0, 0, None, C.byref(sz), None) == 5     # BPP needs k <= 32
+                                    None, None, 0, 0, None, C.byref(sz), None) == 0     # BPP: k <= 64

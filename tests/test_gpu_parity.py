@@ -673,7 +673,7 @@ def test_solve_lai_with_iterative_refinement_vs_oracle(c1):
 
 
 # ------------------------------------------------------------------ NEXT-1 BPP update
-@pytest.mark.parametrize("n,k", [(3000, 8), (2049, 16), (1500, 32), (777, 5), (40, 3)])
+@pytest.mark.parametrize("n,k", [(3000, 8), (2049, 16), (1500, 32), (777, 5), (40, 3), (900, 64), (513, 48)])
 def test_bpp_update_vs_oracle(n, k):
     """Exact per-row NLS by block principal pivoting (App. G) vs the fp64 oracle BPP on the
     same (G, Y, F): regularised problems from a random factor, right-hand sides with mixed signs
@@ -712,6 +712,26 @@ def test_solver_bpp_rule_vs_oracle(mode, c1):
             assert (g["s_D"], g["s_R"], g["n_uniq"]) == (o["s_D"], o["s_R"], o["n_uniq"])
     rg, ro = O.residual(A, H.cpu().numpy()), O.residual(A, Hr)
     assert abs(rg - ro) <= 1e-4 * ro
+
+
+def test_solver_lai_bpp_k64_vs_oracle():
+    """LAI-BPP (the LAI variant of the paper's BPP runs) at k = 64, the c5 rank: a c5-shaped
+    Gaussian-kernel problem at n = 3,000 (l = 74, q = 2), 3 LAI iterations with the exact per-row
+    NLS update (k = 64: two variables per lane) vs the oracle's iterate(rule="bpp") on the GPU's
+    U, Lambda: residual against the full A within 1e-4 relative."""
+    d = make_input("c5", n_override=3_000)
+    A, H0, alpha, cfg = d["A"], d["H0"], d["alpha"], d["cfg"]
+    M = S.DeviceMatrix.from_host(A)
+    U, lam = S.rangefinder(M, cfg.l, cfg.q, cfg.seed, precision="3xtf32")
+    W, H = cu(H0), cu(H0)
+    sv = S.Solver(M, W, H, alpha, mode="lai", precision="3xtf32", max_iters=3, U=U, lam=lam, rule="bpp")
+    sv.run(3)
+    assert sv.stats()["status"] == 0
+    sv.close()
+    Ug, lg = U.cpu().numpy().astype(np.float64), lam.cpu().numpy()
+    _, Hr, _ = O.iterate(A, H0, H0, alpha, 3, "lai", U=Ug, lam=lg, rule="bpp")
+    rg, ro = O.residual(A, H.cpu().numpy()), O.residual(A, Hr)
+    assert abs(rg - ro) <= 1e-4 * ro, (rg, ro)
 
 
 def _drop_vertices(A, frac, tail, seed=3):
