@@ -118,9 +118,6 @@ typedef struct {
  *   SYMNMF_SWEEP_CMEM=0            streaming sweep and leverage scores: G / R from shared memory
  *                                  instead of the constant bank (a solver holds one of 4 constant
  *                                  slots; beyond 4 live solvers the shared-memory form is used).
- *   SYMNMF_SCATTER=bal|rows        LvS solver on CSR (k in {8,16,32,64}): the sampled scatter in
- *                                  nnz-balanced warp chunks of the plan's rows or one warp per
- *                                  sampled row; default: balanced from 16M nonzeros.
  *   SYMNMF_SCATTER_SLICE_MB=<mb>   sampled CSR scatter product: rows of Y per destination-range
  *                                  pass (default 86 MB, so each pass's slice of Y stays in L2).
  *   SYMNMF_LAI_FUSED=never         LAI solver (k = 64, l <= 80): use the four-kernel half (U^T F,

@@ -580,8 +580,6 @@ struct symnmf_solver {
   float* carry;
   int cslot;               // constant-table slot of the streaming sweep (-1: G in shared memory)
   float* ctab;             // scratch for the table copied to the constant bank
-  bool balsc;              // LvS CSR: the nnz-balanced sampled scatter (from 16M nonzeros)
-  void* balws;
   bool record;             // SYMNMF_RECORD_PLANS: per-half copies of the scores and plan
   float* hlev;
   int32_t* huniq;
@@ -677,15 +675,6 @@ bool csr_spmm_nnz(int64_t nnz) {
   return nnz >= (16ll << 20);   // c2 (2M nonzeros): row groups 26 us vs 60 us; c4: 5.4 ms vs 1.8 ms
 }
 
-// LvS CSR sampled scatter: nnz-balanced warp chunks (from 16M nonzeros) or one warp per sampled row;
-// SYMNMF_SCATTER=bal|rows overrides (symnmf.h)
-bool scatter_balanced(int64_t nnz) {
-  const char* e = getenv("SYMNMF_SCATTER");
-  if (e && !strcmp(e, "rows")) return false;
-  if (e && !strcmp(e, "bal")) return true;
-  return nnz >= (16ll << 20);
-}
-
 // Profiling hook: records an event after the launch site just enqueued (no-op unless profiling).
 void mark(symnmf_solver& S, cudaStream_t st, const char* name) {
   if (!S.prof || S.prof->n >= symnmf_solver::Prof::kMax) return;
@@ -741,8 +730,6 @@ void solver_layout(symnmf_solver& S, Carver& c) {
     S.plan.uniq_w = c.take<double>(n);
     S.plan.counts = c.take<int64_t>(4);
     S.plan.mass = c.take<double>(2);
-    S.balsc = S.hasA && S.A.kind == SYMNMF_CSR && kp == k && scatter_balanced(S.A.nnz);
-    S.balws = c.take<char>(S.balsc ? sampled_bal_ws_bytes(S.plan.cap) : 0);
     const size_t halves = S.record ? (size_t)2 * S.max_iters : 0;
     S.hlev = c.take<float>(halves * n);
     S.huniq = c.take<int32_t>(halves * S.plan.cap);
@@ -808,11 +795,7 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     cudaStreamWaitEvent(S.side, S.ev_fork[side], 0);
     launch_sampled_gram_fused(F, k, S.plan, S.Gacc, S.Gs, S.counter, status, S.side);
     cudaEventRecord(S.ev_join[side], S.side);
-    if (S.A.kind == SYMNMF_CSR && S.balsc) {
-      launch_sampled_csr_bal(S.A, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap, S.Y, S.balws,
-                             S.counter + 1, status, st);
-      mark(S, st, "sampled_ah_csr");
-    } else if (S.A.kind == SYMNMF_CSR) {
+    if (S.A.kind == SYMNMF_CSR) {
       launch_sampled_csr_nozero(S.A, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap, S.Y,
                                 status, st);
       mark(S, st, "sampled_ah_csr");

@@ -101,12 +101,6 @@ void launch_samp_draws(const SamplerWs& w, int64_t n, int64_t s, uint64_t seed, 
                        uint32_t iteration, uint32_t side, const symnmf_plan& plan, int32_t* status, cudaStream_t st);
 void launch_samp_uniq_write(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
                             int32_t* status, cudaStream_t st);
-// nnz-balanced sampled CSR scatter (k in {8,16,32,64}) into a Y the caller has zeroed; ws holds the
-// plan-row offsets (sampled_bal_ws_bytes(cap)); counter: a zeroed last-CTA counter.
-size_t sampled_bal_ws_bytes(int64_t cap);
-void launch_sampled_csr_bal(const symnmf_matrix& A, const float* F, int k, const int32_t* uniq, const double* w,
-                            const int64_t* n_uniq_dev, int64_t cap, float* Y, void* ws, unsigned int* counter,
-                            int32_t* status, cudaStream_t st);
 // sampled CSR scatter into a Y the caller has zeroed
 void launch_sampled_csr_nozero(const symnmf_matrix& A, const float* F, int k, const int32_t* uniq, const double* w,
                                const int64_t* n_uniq_dev, int64_t cap, float* Y, const int32_t* status,

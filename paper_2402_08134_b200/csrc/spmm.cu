@@ -201,231 +201,4 @@ void launch_sampled_csr_nozero(const symnmf_matrix& A, const float* F, int k, co
 }
 
 
-// ---------------------------------------------------------------- nnz-balanced sampled scatter
-// The sampled rows of a power-law graph are its hubs: with one warp per sampled row the longest
-// rows (~10^4 nonzeros) decide the kernel's length while most warps idle.  Here the sampled
-// nonzeros are visited in equal warp chunks of the concatenated plan rows (plan-row offsets pre,
-// rb below), a group of k/4 lanes per nonzero, so every warp issues the same number of vector
-// reductions.  Same destination-range passes, same result up to fp32 summation order.
-constexpr int kPlanTile = 1024;      // plan rows per CTA of the plan-row scan (256 threads x 4)
-constexpr int kEntChunk = 2048;      // sampled nonzeros per warp chunk (64 per lane)
-constexpr int kEntUnroll = 8;        // independent entries in flight per lane
-constexpr int kCoarseMaxBuckets = 8192;
-
-// ---------------------------------------------------------------- plan-row offsets (two passes)
-__device__ __forceinline__ void plan_row_lens(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ uniq,
-                                              int64_t nu, int64_t t0, int64_t (&start)[4], int64_t (&len)[4]) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int64_t t = t0 + q;
-    if (t < nu) {
-      const int64_t u = uniq[t];
-      start[q] = rowptr[u];
-      len[q] = rowptr[u + 1] - start[q];
-    } else {
-      start[q] = 0;
-      len[q] = 0;
-    }
-  }
-}
-
-__global__ void __launch_bounds__(256) plan_row_sums(const int64_t* __restrict__ rowptr,
-                                                     const int32_t* __restrict__ uniq,
-                                                     const int64_t* __restrict__ n_uniq_dev,
-                                                     int64_t* __restrict__ tsum, int64_t* __restrict__ pre,
-                                                     unsigned int* counter, const int32_t* __restrict__ status) {
-  __shared__ int64_t sh[33];
-  __shared__ bool last;
-  if (dev_failed(status)) return;
-  const int64_t nu = *n_uniq_dev;
-  const int64_t nt = (nu + kPlanTile - 1) / kPlanTile;
-  if ((int64_t)blockIdx.x < nt) {
-    int64_t start[4], len[4];
-    plan_row_lens(rowptr, uniq, nu, (int64_t)blockIdx.x * kPlanTile + threadIdx.x * 4, start, len);
-    const int64_t s = block_sum(len[0] + len[1] + len[2] + len[3], sh);
-    if (threadIdx.x == 0) tsum[blockIdx.x] = s;
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  if (threadIdx.x == 0) *counter = 0;
-  int64_t run = 0;
-  for (int64_t base = 0; base < nt; base += 256) {
-    const int64_t i = base + threadIdx.x;
-    const int64_t v = i < nt ? __ldcg(tsum + i) : 0;
-    int64_t tot;
-    const int64_t e = block_excl_scan(v, sh, &tot);
-    if (i < nt) tsum[i] = run + e;
-    run += tot;
-  }
-  if (threadIdx.x == 0) pre[nu] = run;
-}
-
-__global__ void __launch_bounds__(256) plan_row_write(const int64_t* __restrict__ rowptr,
-                                                      const int32_t* __restrict__ uniq,
-                                                      const int64_t* __restrict__ n_uniq_dev,
-                                                      const int64_t* __restrict__ tsum, int64_t* __restrict__ pre,
-                                                      int64_t* __restrict__ rb, const int32_t* __restrict__ status) {
-  __shared__ int64_t sh[33];
-  if (dev_failed(status)) return;
-  const int64_t nu = *n_uniq_dev;
-  if ((int64_t)blockIdx.x * kPlanTile >= nu) return;
-  const int64_t t0 = (int64_t)blockIdx.x * kPlanTile + threadIdx.x * 4;
-  int64_t start[4], len[4];
-  plan_row_lens(rowptr, uniq, nu, t0, start, len);
-  int64_t p = block_excl_scan(len[0] + len[1] + len[2] + len[3], sh, (int64_t*)nullptr) + tsum[blockIdx.x];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    if (t0 + q < nu) {
-      pre[t0 + q] = p;
-      rb[t0 + q] = start[q] - p;
-    }
-    p += len[q];
-  }
-}
-
-// Largest t in [lo, hi] with pre[t] <= j (pre non-decreasing, pre[lo] <= j).
-__device__ __forceinline__ int64_t row_of_entry(const int64_t* __restrict__ pre, int64_t lo, int64_t hi, int64_t j) {
-  while (lo < hi) {
-    const int64_t mid = (lo + hi + 1) >> 1;
-    if (__ldg(pre + mid) <= j) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-
-// The same search by a whole warp in 32-ary steps.  Largest t < cnt with pre[t] <= j.
-__device__ __forceinline__ int64_t warp_row_of_entry(const int64_t* __restrict__ pre, int64_t cnt, int64_t j,
-                                                     int lane) {
-  int64_t lo = 0, len = cnt;
-  while (len > 1) {
-    const int64_t step = (len + 31) / 32;
-    const int64_t p = lo + (int64_t)lane * step;
-    const bool le = p < lo + len && __ldg(pre + p) <= j;
-    const unsigned m = __ballot_sync(0xffffffffu, le);
-    const int last = 31 - __clz(m);
-    lo += (int64_t)last * step;
-    len = min64(step, len - (int64_t)last * step);
-  }
-  return lo;
-}
-
-// Visit every sampled nonzero in nnz-balanced warp chunks: fn(t, e) with t the plan slot (-1: none)
-// and e the nonzero of A.  The chunk -> warp assignment depends only on the grid, so two calls in
-// kernels of the same grid visit the same entries in the same CTA.
-template <class Fn>
-__device__ __forceinline__ void for_sampled_nonzeros(const int64_t* __restrict__ pre, const int64_t* __restrict__ rb,
-                                                     int64_t nu, Fn&& fn) {
-  const int lane = threadIdx.x & 31;
-  const int64_t total = pre[nu];
-  const int64_t nchunks = (total + kEntChunk - 1) / kEntChunk;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t ch = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; ch < nchunks; ch += nw) {
-    const int64_t j0 = ch * kEntChunk, j1 = min64(total, j0 + kEntChunk);
-    const int64_t thi = warp_row_of_entry(pre, nu, j1 - 1, lane);
-    int64_t tcur = warp_row_of_entry(pre, thi + 1, j0, lane);
-    for (int64_t jb = j0; jb < j1; jb += 32 * kEntUnroll) {
-      int64_t t[kEntUnroll], e[kEntUnroll];
-#pragma unroll
-      for (int u = 0; u < kEntUnroll; ++u) {
-        const int64_t j = jb + 32 * u + lane;
-        t[u] = j < j1 ? row_of_entry(pre, tcur, thi, j) : -1;
-        e[u] = t[u] >= 0 ? __ldg(rb + t[u]) + j : 0;
-      }
-      fn(t, e);
-      const int64_t jl = min64(j1, jb + 32 * kEntUnroll) - 1;
-      tcur = row_of_entry(pre, tcur, thi, jl);
-    }
-  }
-}
-
-
-template <int LPR>
-__global__ void __launch_bounds__(256) sampled_csr_bal(const int32_t* __restrict__ col, const float* __restrict__ val,
-                                                       const float4* __restrict__ F4, const int32_t* __restrict__ uniq,
-                                                       const double* __restrict__ w, const int64_t* __restrict__ pre,
-                                                       const int64_t* __restrict__ rb,
-                                                       const int64_t* __restrict__ n_uniq_dev, float4* __restrict__ Y4,
-                                                       int32_t c_lo, int32_t c_hi, const int32_t* __restrict__ status) {
-  if (dev_failed(status)) return;
-  constexpr int NPW = 32 / LPR;          // nonzeros per warp step
-  constexpr int U = 4;                   // steps in flight
-  const int lane = threadIdx.x & 31, sub = lane / LPR, li = lane % LPR;
-  const int64_t nu = *n_uniq_dev;
-  if (nu <= 0) return;
-  const int64_t total = pre[nu];
-  const int64_t nchunks = (total + kEntChunk - 1) / kEntChunk;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t ch = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; ch < nchunks; ch += nw) {
-    const int64_t j0 = ch * kEntChunk, j1 = min64(total, j0 + kEntChunk);
-    const int64_t thi = warp_row_of_entry(pre, nu, j1 - 1, lane);
-    int64_t tcur = warp_row_of_entry(pre, thi + 1, j0, lane);
-    for (int64_t jb = j0; jb < j1; jb += NPW * U) {
-      int64_t t[U], e[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t j = jb + NPW * u + sub;
-        t[u] = j < j1 ? row_of_entry(pre, tcur, thi, j) : -1;
-        e[u] = t[u] >= 0 ? __ldg(rb + t[u]) + j : 0;
-      }
-      int c[U];
-      float a[U];
-      float4 f[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        c[u] = t[u] >= 0 ? __ldg(col + e[u]) : -1;
-        a[u] = t[u] >= 0 ? __ldg(val + e[u]) : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (t[u] >= 0 && c[u] >= c_lo && c[u] < c_hi) {
-          f[u] = __ldg(F4 + (int64_t)__ldg(uniq + t[u]) * LPR + li);
-          const float s = a[u] * (float)__ldg(w + t[u]);
-          atomicAdd(Y4 + (int64_t)c[u] * LPR + li, make_float4(s * f[u].x, s * f[u].y, s * f[u].z, s * f[u].w));
-        }
-      }
-      const int64_t jl = min64(j1, jb + NPW * U) - 1;
-      tcur = row_of_entry(pre, tcur, thi, jl);
-    }
-  }
-}
-
-size_t sampled_bal_ws_bytes(int64_t cap) {
-  return sizeof(int64_t) * ((size_t)(cap + kPlanTile - 1) / kPlanTile + 4 + 2 * ((size_t)cap + 1)) + 3 * 256;
-}
-
-// Plan-row offsets (two small passes), then the balanced scatter in destination-range passes into
-// a Y the caller has zeroed.  ws: sampled_bal_ws_bytes(cap) bytes (256-aligned).
-void launch_sampled_csr_bal(const symnmf_matrix& A, const float* F, int k, const int32_t* uniq, const double* w,
-                            const int64_t* n_uniq_dev, int64_t cap, float* Y, void* ws, unsigned int* counter,
-                            int32_t* status, cudaStream_t st) {
-  Carver c(nullptr);
-  c.base = static_cast<char*>(ws);
-  c.off = 0;
-  int64_t* ptsum = c.take<int64_t>((size_t)(cap + kPlanTile - 1) / kPlanTile + 4);
-  int64_t* pre = c.take<int64_t>((size_t)cap + 1);
-  int64_t* rb = c.take<int64_t>((size_t)cap + 1);
-  const int ptiles = (int)std::max<int64_t>(1, (cap + kPlanTile - 1) / kPlanTile);
-  launch_pdl(plan_row_sums, ptiles, 256, 0, st, A.rowptr, uniq, n_uniq_dev, ptsum, pre, counter, status);
-  launch_pdl(plan_row_write, ptiles, 256, 0, st, A.rowptr, uniq, n_uniq_dev, ptsum, pre, rb, status);
-  const int64_t warps = (A.nnz + kEntChunk - 1) / kEntChunk;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, 148 * 8));
-  const float4* F4 = reinterpret_cast<const float4*>(F);
-  float4* Y4 = reinterpret_cast<float4*>(Y);
-  const int64_t ybytes = (int64_t)sizeof(float) * A.n * k;
-  const int64_t slice = scatter_slice_bytes();
-  const int passes = (int)std::max<int64_t>(1, (ybytes + slice - 1) / slice);
-  for (int p = 0; p < passes; ++p) {
-    const int32_t lo = (int32_t)(A.n * p / passes), hi = (int32_t)(A.n * (p + 1) / passes);
-    switch (k / 4) {
-      case 2: launch_pdl(sampled_csr_bal<2>, grid, 256, 0, st, A.colidx, A.val, F4, uniq, w, pre, rb, n_uniq_dev, Y4, lo, hi, status); break;
-      case 4: launch_pdl(sampled_csr_bal<4>, grid, 256, 0, st, A.colidx, A.val, F4, uniq, w, pre, rb, n_uniq_dev, Y4, lo, hi, status); break;
-      case 8: launch_pdl(sampled_csr_bal<8>, grid, 256, 0, st, A.colidx, A.val, F4, uniq, w, pre, rb, n_uniq_dev, Y4, lo, hi, status); break;
-      default: launch_pdl(sampled_csr_bal<16>, grid, 256, 0, st, A.colidx, A.val, F4, uniq, w, pre, rb, n_uniq_dev, Y4, lo, hi, status); break;
-    }
-  }
-}
-
 }  // namespace symnmf

@@ -486,7 +486,7 @@ def test_csr_tile_exact_one_iteration(cfgname, n, k, tile, monkeypatch):
 
 
 @pytest.mark.parametrize("cfgname,n,k,s", [("c4", 40_000, 32, 800), ("c2", 20_000, 16, 400), ("c4", 40_000, 8, 2000)])
-@pytest.mark.parametrize("slice_mb", ["", "1", "stream", "bal", "bal1"])
+@pytest.mark.parametrize("slice_mb", ["", "1", "stream"])
 def test_csr_lvs_solver_equals_abi_composition(cfgname, n, k, s, slice_mb, monkeypatch):
     """Solver LvS on CSR graphs with hubs (vector-atomic scatter of the sampled product, fused Gram)
     equals the composition of the ABI calls on the same device data; slice_mb = 1 forces several
@@ -494,8 +494,7 @@ def test_csr_lvs_solver_equals_abi_composition(cfgname, n, k, s, slice_mb, monke
     the constant bank (the default from 2^20 rows)."""
     if slice_mb == "stream":
         monkeypatch.setenv("SYMNMF_SWEEP", "stream")
-    monkeypatch.setenv("SYMNMF_SCATTER", "bal" if slice_mb.startswith("bal") else "rows")
-    if slice_mb.endswith("1"):
+    if slice_mb == "1":
         monkeypatch.setenv("SYMNMF_SCATTER_SLICE_MB", "1")
     A, H0, alpha = _csr_case(cfgname, n, k)
     tau = 1.0 / s
@@ -520,12 +519,11 @@ def test_csr_lvs_solver_equals_abi_composition(cfgname, n, k, s, slice_mb, monke
     assert rel(H1.cpu().numpy(), H2.cpu().numpy()) < 1e-5
 
 
-@pytest.mark.parametrize("sweep", ["stream", "fused", "bal"])
+@pytest.mark.parametrize("sweep", ["stream", "fused"])
 def test_csr_lvs_replayed_plan_vs_oracle(sweep, monkeypatch):
     """One LvS half through the solver vs the oracle's sampled products + sweep fed the plan the
     GPU drew (the same plan is recomputed by the ABI sampler from the same device scores)."""
-    monkeypatch.setenv("SYMNMF_SWEEP", "stream" if sweep == "bal" else sweep)
-    monkeypatch.setenv("SYMNMF_SCATTER", "bal" if sweep == "bal" else "rows")
+    monkeypatch.setenv("SYMNMF_SWEEP", sweep)
     A, H0, alpha = _csr_case("c4", 30_016, 32)
     s, tau = 600, 1.0 / 600
     M = S.DeviceMatrix.from_host(A)
@@ -776,9 +774,8 @@ def test_csr_empty_rows(tile, monkeypatch):
     s_, tau = 800, 1.0 / 800
     ph = S.hybrid_sample(S.leverage_scores(cu(H0)), 16, s_, tau, 5, 0, 0).to_host()
     Gs, Ys = O.sampled_products(A, H0, ph["uniq_idx"], ph["uniq_w"])
-    for path in ("stream", "fused", "bal"):
-        monkeypatch.setenv("SYMNMF_SWEEP", "stream" if path == "bal" else path)
-        monkeypatch.setenv("SYMNMF_SCATTER", "bal" if path == "bal" else "rows")
+    for path in ("stream", "fused"):
+        monkeypatch.setenv("SYMNMF_SWEEP", path)
         W, H = cu(H0), cu(H0)
         sv = S.Solver(M, W, H, alpha, mode="lvs", s=s_, tau=tau, seed=5, max_iters=1)
         sv.run(1)
@@ -799,10 +796,9 @@ def test_csr_zero_matrix():
     assert not Y.any()
     lvs = dict(s=300, tau=1.0 / 300, seed=2)
     for mode, kw, spmm in (("exact", {}, "nnz"), ("exact", {}, "rows"), ("lvs", lvs, "stream"),
-                           ("lvs", lvs, "fused"), ("lvs", lvs, "bal")):
+                           ("lvs", lvs, "fused")):
         os.environ["SYMNMF_CSR_SPMM"] = spmm
         os.environ["SYMNMF_SWEEP"] = spmm
-        os.environ["SYMNMF_SCATTER"] = spmm
         W, H = cu(H0), cu(H0)
         sv = S.Solver(M, W, H, alpha, mode=mode, max_iters=1, **kw)
         sv.run(1)
@@ -813,4 +809,4 @@ def test_csr_zero_matrix():
             Wr, Hr, _ = O.iterate(A, H0, H0, alpha, 1, "exact")
             assert rel(Wg, Wr) < 1e-5 and rel(H.cpu().numpy(), Hr) < 1e-5
         assert np.isfinite(Wg).all() and (Wg >= 0).all()
-    os.environ.pop("SYMNMF_CSR_SPMM"); os.environ.pop("SYMNMF_SWEEP"); os.environ.pop("SYMNMF_SCATTER")
+    os.environ.pop("SYMNMF_CSR_SPMM"); os.environ.pop("SYMNMF_SWEEP")
