@@ -316,6 +316,43 @@ symnmf_status symnmf_solver_last_plan(const symnmf_solver* solver, float* lev_ou
 symnmf_status symnmf_solver_plan_history(const symnmf_solver* solver, int32_t t, int32_t side, float* lev_out,
                                          int32_t* uniq_idx_out, double* uniq_w_out, int64_t* counts_out,
                                          double* mass_out, cudaStream_t st);
+/* ---------------------------------------------------------------- NEXT-4 row sharding
+ * Building blocks of the row-sharded solver (driver: paper_2402_08134_b200/shard.py).
+ * A shard owns the row block [row0, row0 + n) of A (CSR rows, global column indices), W and H.
+ * The collectives between the calls (allreduce of k x k Grams, allgather of the shards' masses and
+ * plan rows) are the caller's.  All pointers are device pointers unless stated; enqueue only. */
+
+/* lev = scores of the rows of F (n x k block) given G = F_all^T F_all of the whole factor (fp64
+ * k x k): l_i = f_i G^{-1} f_i^T by CholeskyQR.  SYMNMF_ERR_NOT_PD on the status word. */
+symnmf_status symnmf_leverage_scores_gram(const float* F, int64_t n, int32_t k, const double* G, float* lev,
+                                          void* ws, size_t* ws_bytes, cudaStream_t st);
+/* The block's share of the sampler totals (readings Z1-Z6): *W_out = sum floor(l 2^40)
+ * over its rows outside I_D (uint64, exact), *sD_out = |I_D ∩ block|, *theta_out = sum_{I_D} l. */
+symnmf_status symnmf_hybrid_shard_sums(const float* lev, int64_t n, int32_t k, double tau, uint64_t* W_out,
+                                       int64_t* sD_out, double* theta_out, void* ws, size_t* ws_bytes,
+                                       cudaStream_t st);
+/* The block's part of the global plan, given (host values) the exclusive prefix W_offset of the
+ * shards' masses before this one, the global W_total and sD_total: its I_D rows and the global
+ * draws j < s_R = s - sD_total whose target mulhi(u_j, W_total) falls in [W_offset, W_offset + W_b),
+ * weights omega = c W_total / (s_R w) (the same IEEE operations as symnmf_hybrid_sample).
+ * plan->uniq_idx holds global row ids; counts = {s_D of the block, s_R, n_uniq of the block, W_total};
+ * det_idx holds block-local rows; draw_idx is not written.  The shards' uniq_idx / uniq_w
+ * concatenated in row order equal symnmf_hybrid_sample's on the whole score vector, bit for bit. */
+symnmf_status symnmf_hybrid_shard_plan(const float* lev, int64_t n, int64_t row0, int32_t k, int64_t s, double tau,
+                                       uint64_t seed, uint32_t iteration, uint32_t side, uint64_t W_offset,
+                                       uint64_t W_total, int64_t sD_total, const symnmf_plan* plan, void* ws,
+                                       size_t* ws_bytes, cudaStream_t st);
+/* Z[t] = omega_t f_{u_t} (fp32, n_uniq x k) for the block's plan rows (F = the block's rows, u_t
+ * global), and (G_s nullable) the block's share of the sampled Gram sum_t omega_t f_t^T f_t (fp64). */
+symnmf_status symnmf_plan_rows_scaled(const float* F, int64_t row0, int32_t k, const symnmf_plan* plan, float* Z,
+                                      double* G_s, void* ws, size_t* ws_bytes, cudaStream_t st);
+/* Rows of the sampled product for the block as a pull: Y[c] = sum_{i in U} a_ci Z[slot(i)]
+ * over the block's CSR rows (a_ci = a_ic by symmetry), U = uniq[0 .. *n_uniq_dev) global row
+ * ids of the whole plan, Z their scaled rows in plan order (n_uniq x k); Y is the block's n x k. */
+symnmf_status symnmf_sampled_ah_rows(const symnmf_matrix* A_block, int64_t n_total, const int32_t* uniq,
+                                     const int64_t* n_uniq_dev, int64_t cap, const float* Z, int32_t k, float* Y,
+                                     void* ws, size_t* ws_bytes, cudaStream_t st);
+
 /* Kernel and memset node counts of the captured per-iteration graph (host only). */
 symnmf_status symnmf_solver_graph_nodes(const symnmf_solver* solver, int32_t* kernels_host, int32_t* memsets_host);
 

@@ -73,6 +73,11 @@ SIGNATURES = {
     "symnmf_solver_plan_history": (I32, [P, I32, I32, P, P, P, P, P, P]),
     "symnmf_solver_graph_nodes": (I32, [P, C.POINTER(I32), C.POINTER(I32)]),
     "symnmf_solver_profile": (I32, [P, I32, I32, C.c_void_p, C.POINTER(C.c_float), C.POINTER(I32), P]),
+    "symnmf_leverage_scores_gram": (I32, [P, I64, I32, P, P, P, PSZ, P]),
+    "symnmf_hybrid_shard_sums": (I32, [P, I64, I32, F64, P, P, P, P, PSZ, P]),
+    "symnmf_hybrid_shard_plan": (I32, [P, I64, I64, I32, I64, F64, U64, U32, U32, U64, U64, I64, PP, P, PSZ, P]),
+    "symnmf_plan_rows_scaled": (I32, [P, I64, I32, PP, P, P, P, PSZ, P]),
+    "symnmf_sampled_ah_rows": (I32, [PM, I64, P, P, I64, P, I32, P, P, PSZ, P]),
 }
 
 _lib = None

@@ -196,6 +196,116 @@ extern "C" symnmf_status symnmf_hybrid_sample(const float* lev, int64_t n, int32
   return finish();
 }
 
+// ---------------------------------------------------------------- NEXT-4 row-sharded building blocks (shard.cu)
+extern "C" symnmf_status symnmf_leverage_scores_gram(const float* F, int64_t n, int32_t k, const double* G, float* lev,
+                                                     void* ws, size_t* ws_bytes, cudaStream_t st) {
+  if (!F || !G || !lev || n < 1 || bad_k(k)) return SYMNMF_ERR_ARG;
+  const int kp = kpad(k);
+  Carver c(nullptr);
+  c.take<float>((size_t)kp * kp);
+  bool q;
+  symnmf_status r = ws_protocol(ws, ws_bytes, c.bytes(), &q);
+  if (r != SYMNMF_OK || q) return r;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  float* R = w.take<float>((size_t)kp * kp);
+  int32_t* status = ws_status(ws);
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
+  launch_chol_inv(G, k, R, kp, kp, nullptr, 0, status, st);
+  launch_leverage(F, n, k, R, lev, status, st);
+  return finish();
+}
+
+extern "C" symnmf_status symnmf_hybrid_shard_sums(const float* lev, int64_t n, int32_t k, double tau, uint64_t* W_out,
+                                                  int64_t* sD_out, double* theta_out, void* ws, size_t* ws_bytes,
+                                                  cudaStream_t st) {
+  if (!lev || n < 1 || bad_k(k) || !(tau > 0.0 && tau <= 1.0) || !W_out || !sD_out || !theta_out)
+    return SYMNMF_ERR_ARG;
+  SamplerWs sw;
+  Carver c(nullptr);
+  sampler_layout(c, n, &sw);
+  bool q;
+  symnmf_status r = ws_protocol(ws, ws_bytes, c.bytes(), &q);
+  if (r != SYMNMF_OK || q) return r;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  sampler_layout(w, n, &sw);
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
+  launch_shard_sums(lev, n, tau * (double)k, sw, W_out, sD_out, theta_out, ws_status(ws), st);
+  return finish();
+}
+
+extern "C" symnmf_status symnmf_hybrid_shard_plan(const float* lev, int64_t n, int64_t row0, int32_t k, int64_t s,
+                                                  double tau, uint64_t seed, uint32_t iteration, uint32_t side,
+                                                  uint64_t W_offset, uint64_t W_total, int64_t sD_total,
+                                                  const symnmf_plan* plan, void* ws, size_t* ws_bytes,
+                                                  cudaStream_t st) {
+  if (!lev || n < 1 || row0 < 0 || bad_k(k) || s < 1 || !(tau > 0.0 && tau <= 1.0) || side > 1 || bad_plan(plan) ||
+      sD_total < 0)
+    return SYMNMF_ERR_ARG;
+  SamplerWs sw;
+  auto layout = [&](Carver& c, uint64_t** wloc) {
+    sampler_layout(c, n, &sw);
+    *wloc = c.take<uint64_t>(1);
+  };
+  uint64_t* wloc;
+  Carver c(nullptr);
+  layout(c, &wloc);
+  bool q;
+  symnmf_status r = ws_protocol(ws, ws_bytes, c.bytes(), &q);
+  if (r != SYMNMF_OK || q) return r;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  layout(w, &wloc);
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(sw.cnt, 0, sizeof(int32_t) * n, st));
+  launch_shard_plan(lev, n, row0, k, s, tau * (double)k, seed, iteration, side, W_offset, W_total, sD_total, *plan, sw,
+                    wloc, ws_status(ws), st);
+  return finish();
+}
+
+extern "C" symnmf_status symnmf_plan_rows_scaled(const float* F, int64_t row0, int32_t k, const symnmf_plan* plan,
+                                                 float* Z, double* G_s, void* ws, size_t* ws_bytes, cudaStream_t st) {
+  if (!F || row0 < 0 || bad_k(k) || bad_plan(plan) || !Z) return SYMNMF_ERR_ARG;
+  const int grid = gram_grid(plan->cap);
+  Carver c(nullptr);
+  c.take<double>(gram_partial_doubles(k, k, true, grid));
+  bool q;
+  symnmf_status r = ws_protocol(ws, ws_bytes, c.bytes(), &q);
+  if (r != SYMNMF_OK || q) return r;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  double* part = w.take<double>(gram_partial_doubles(k, k, true, grid));
+  int32_t* status = ws_status(ws);
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
+  launch_plan_rows_scaled(F, row0, k, *plan, Z, status, st);
+  // the block's share of G_s = sum_t omega_t f_t^T f_t (rows u_t - row0 of the block's F)
+  if (G_s)
+    launch_cross_gram(F - row0 * k, k, k, F - row0 * k, k, k, true, plan->cap, plan->counts + 2, plan->uniq_idx,
+                      plan->uniq_w, part, grid, G_s, k, status, st);
+  return finish();
+}
+
+extern "C" symnmf_status symnmf_sampled_ah_rows(const symnmf_matrix* A_block, int64_t n_total, const int32_t* uniq,
+                                                const int64_t* n_uniq_dev, int64_t cap, const float* Z, int32_t k,
+                                                float* Y, void* ws, size_t* ws_bytes, cudaStream_t st) {
+  if (!A_block || A_block->kind != SYMNMF_CSR || A_block->n < 1 || !A_block->rowptr || n_total < 1 || !uniq ||
+      !n_uniq_dev || cap < 1 || !Z || bad_k(k) || !Y)
+    return SYMNMF_ERR_ARG;
+  Carver c(nullptr);
+  c.take<int32_t>((size_t)n_total);
+  bool q;
+  symnmf_status r = ws_protocol(ws, ws_bytes, c.bytes(), &q);
+  if (r != SYMNMF_OK || q) return r;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  int32_t* slot = w.take<int32_t>((size_t)n_total);
+  int32_t* status = ws_status(ws);
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
+  launch_sampled_rows_pull(*A_block, n_total, uniq, n_uniq_dev, cap, Z, k, Y, slot, status, st);
+  return finish();
+}
+
 // ---------------------------------------------------------------- (a8), (a9)
 extern "C" symnmf_status symnmf_sampled_ah(const symnmf_matrix* A, const float* F, int32_t k, const symnmf_plan* plan,
                                            float* Y, double* G_s, void* ws, size_t* ws_bytes, cudaStream_t st) {

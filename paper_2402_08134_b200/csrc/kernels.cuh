@@ -40,6 +40,27 @@ void launch_hybrid_sample(const float* lev, int64_t n, int k, int64_t s, double 
                           const int32_t* iter_dev, uint32_t iteration, uint32_t side, const symnmf_plan& plan,
                           const SamplerWs& w, int32_t* status, cudaStream_t st);
 
+// sampler passes used by the sharded sampler (shard.cu)
+void launch_samp_block_sums(const float* lev, int64_t n, double T, const SamplerWs& w, int32_t* status,
+                            cudaStream_t st);
+void launch_samp_scan_blocks(int64_t n, int64_t s, int k, const symnmf_plan& plan, const SamplerWs& w,
+                             int32_t* status, cudaStream_t st);
+void launch_samp_uniq(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
+                      int32_t* status, cudaStream_t st);
+
+// ---------------------------------------------------------------- shard.cu (NEXT-4)
+void launch_shard_sums(const float* lev, int64_t n, double T, const SamplerWs& w, uint64_t* W_out, int64_t* sD_out,
+                       double* theta_out, int32_t* status, cudaStream_t st);
+void launch_shard_plan(const float* lev, int64_t n, int64_t row0, int k, int64_t s, double T, uint64_t seed,
+                       uint32_t iteration, uint32_t side, uint64_t W_off, uint64_t W_total, int64_t sD_total,
+                       const symnmf_plan& plan, const SamplerWs& w, uint64_t* wloc, int32_t* status,
+                       cudaStream_t st);
+void launch_plan_rows_scaled(const float* F, int64_t row0, int k, const symnmf_plan& plan, float* Z,
+                             const int32_t* status, cudaStream_t st);
+void launch_sampled_rows_pull(const symnmf_matrix& Ab, int64_t n_total, const int32_t* uniq,
+                              const int64_t* n_uniq_dev, int64_t cap, const float* Z, int k, float* Y, int32_t* slot,
+                              const int32_t* status, cudaStream_t st);
+
 // ---------------------------------------------------------------- spmm.cu / dense.cu
 void launch_spmm_csr(const symnmf_matrix& A, const float* F, int k, float* Y, const int32_t* status, cudaStream_t st);
 void launch_sampled_csr(const symnmf_matrix& A, const float* F, int k, const int32_t* uniq, const double* w,

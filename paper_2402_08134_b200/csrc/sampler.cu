@@ -332,6 +332,26 @@ void launch_samp_uniq_write(const float* lev, int64_t n, double T, const Sampler
                                                            plan.uniq_w, plan.cap, status);
 }
 
+void launch_samp_block_sums(const float* lev, int64_t n, double T, const SamplerWs& w, int32_t* status,
+                            cudaStream_t st) {
+  samp_block_sums<<<(unsigned)samp_blocks(n), ST, 0, st>>>(lev, n, T, w.bw, w.bd, w.bt, status);
+}
+
+void launch_samp_scan_blocks(int64_t n, int64_t s, int k, const symnmf_plan& plan, const SamplerWs& w,
+                             int32_t* status, cudaStream_t st) {
+  samp_scan_blocks<<<1, 1024, 0, st>>>(samp_blocks(n), w.bw, w.bd, w.bt, s, k, plan.cap, plan.counts, plan.mass,
+                                       status);
+}
+
+void launch_samp_uniq(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
+                      int32_t* status, cudaStream_t st) {
+  const int64_t nb = samp_blocks(n);
+  samp_uniq_counts<<<(unsigned)nb, ST, 0, st>>>(lev, n, T, w.cnt, w.bu, status);
+  samp_scan_uniq<<<1, 1024, 0, st>>>(nb, w.bu, plan.cap, plan.counts, status);
+  samp_uniq_write<<<(unsigned)nb, ST, 0, st>>>(lev, n, T, w.cnt, w.bu, plan.counts, plan.uniq_idx, plan.uniq_w,
+                                               plan.cap, status);
+}
+
 void launch_hybrid_sample(const float* lev, int64_t n, int k, int64_t s, double T, uint64_t seed,
                           const int32_t* iter_dev, uint32_t iteration, uint32_t side, const symnmf_plan& plan,
                           const SamplerWs& w, int32_t* status, cudaStream_t st) {

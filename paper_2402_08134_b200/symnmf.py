@@ -214,6 +214,66 @@ def sampled_ah(M: DeviceMatrix, F: torch.Tensor, plan: SamplingPlan, with_gram=T
     return Y, Gs
 
 
+# ------------------------------------------------------------------ NEXT-4 row-sharding blocks
+def leverage_scores_gram(F: torch.Tensor, G: torch.Tensor, check=True) -> torch.Tensor:
+    """Scores of the rows of F given the Gram G of the whole factor, symnmf_leverage_scores_gram."""
+    _cuda(F, torch.float32); _cuda(G, torch.float64)
+    n, k = F.shape
+    lev = torch.empty(n, dtype=torch.float32, device=F.device)
+    ws = _call("symnmf_leverage_scores_gram", (_p(F), n, k, _p(G), _p(lev)), (_stream(),))
+    if check:
+        check_ws(ws, "symnmf_leverage_scores_gram")
+    return lev
+
+
+def hybrid_shard_sums(lev: torch.Tensor, k: int, tau: float):
+    """(W_b, s_D_b, theta_b) of a row block's scores (host ints / float), symnmf_hybrid_shard_sums."""
+    _cuda(lev, torch.float32)
+    out = torch.zeros(3, dtype=torch.int64, device=lev.device)
+    th = torch.zeros(1, dtype=torch.float64, device=lev.device)
+    ws = _call("symnmf_hybrid_shard_sums", (_p(lev), lev.numel(), k, float(tau), C.c_void_p(out.data_ptr()),
+                                            C.c_void_p(out.data_ptr() + 8), _p(th)), (_stream(),))
+    check_ws(ws, "symnmf_hybrid_shard_sums")
+    w, sd = (int(x) for x in out[:2].cpu().tolist())
+    return w & ((1 << 64) - 1), sd, float(th.item())
+
+
+def hybrid_shard_plan(lev: torch.Tensor, row0: int, k: int, s: int, tau: float, seed: int, iteration: int, side: int,
+                      W_offset: int, W_total: int, sD_total: int, check=True) -> SamplingPlan:
+    """The row block's part of the global plan (global row ids), symnmf_hybrid_shard_plan."""
+    _cuda(lev, torch.float32)
+    n = lev.numel()
+    plan = new_plan(n, s, None, lev.device)
+    ps = plan.struct()
+    ws = _call("symnmf_hybrid_shard_plan", (_p(lev), n, int(row0), k, int(s), float(tau), int(seed), int(iteration),
+                                            int(side), C.c_uint64(int(W_offset)), C.c_uint64(int(W_total)),
+                                            int(sD_total), C.byref(ps)), (_stream(),))
+    if check:
+        check_ws(ws, "symnmf_hybrid_shard_plan")
+    return plan
+
+
+def plan_rows_scaled(F: torch.Tensor, row0: int, plan: SamplingPlan, with_gram=True):
+    """(Z, G_s part) for a row block's plan rows, symnmf_plan_rows_scaled."""
+    _cuda(F, torch.float32)
+    k = F.shape[1]
+    Z = torch.empty((plan.cap, k), dtype=torch.float32, device=F.device)
+    Gs = torch.empty((k, k), dtype=torch.float64, device=F.device) if with_gram else None
+    ps = plan.struct()
+    _call("symnmf_plan_rows_scaled", (_p(F), int(row0), k, C.byref(ps), _p(Z), _p(Gs)), (_stream(),))
+    return Z, Gs
+
+
+def sampled_ah_rows(Mb: DeviceMatrix, n_total: int, uniq: torch.Tensor, Z: torch.Tensor, k: int) -> torch.Tensor:
+    """Rows of the sampled product for a CSR row block (pull form), symnmf_sampled_ah_rows."""
+    _cuda(uniq, torch.int32); _cuda(Z, torch.float32)
+    nu = torch.tensor([uniq.numel()], dtype=torch.int64, device=Z.device)
+    Y = torch.empty((Mb.n, k), dtype=torch.float32, device=Z.device)
+    _call("symnmf_sampled_ah_rows", (Mb.ref(), int(n_total), _p(uniq), _p(nu), max(uniq.numel(), 1), _p(Z), k, _p(Y)),
+          (_stream(),))
+    return Y
+
+
 # ------------------------------------------------------------------ (a12, a13)
 def gaussian(n: int, l: int, seed: int, device="cuda") -> torch.Tensor:
     Om = torch.empty((n, l), dtype=torch.float32, device=device)

@@ -104,3 +104,34 @@ def test_row_sharded_plan_equals_single_process_plan(n, k, s, tau):
         draws[p[2]] = p[3]
     assert parts[0][4] == ref["W"] and parts[0][5] == ref["s_D"] and s_R == ref["s_R"]
     assert np.array_equal(draws, ref["draw_idx"])
+
+
+def _distcomm_worker(rank, ws, port, q):
+    from paper_2402_08134_b200.shard import DistComm, mass_offsets
+    _init(rank, ws, port)
+    c = DistComm()
+    # variable-length concatenation (plan rows of different sizes per shard), in rank order
+    x = torch.arange(3 + 2 * rank, dtype=torch.int32) + 100 * rank
+    cat = c.allgather_cat([x])[0]
+    # k x k Gram partials: fp64 sum
+    g = c.allreduce_sum([torch.full((2, 2), 1.5 * (rank + 1), dtype=torch.float64)])[0]
+    # the shards' exact integer masses (uint64 range), s_D and theta, and their exclusive scan
+    sums = c.allgather_obj([((1 << 62) + 7 * rank, 3 + rank, 0.25 * rank)])[0]
+    offs, W, sD = mass_offsets(sums)
+    q.put((rank, cat.tolist(), g.tolist(), offs, W, sD))
+    dist.destroy_process_group()
+
+
+def test_shard_distcomm_collectives_over_gloo():
+    """paper_2402_08134_b200.shard.DistComm (one shard per rank) over gloo, world size 2: the
+    variable-length all-gather the shards' plan rows go through, the Gram allreduce, and the exact
+    uint64 exclusive scan of the shards' masses."""
+    ws, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.spawn(_distcomm_worker, args=(ws, port, q), nprocs=ws, join=True)
+    out = sorted(q.get() for _ in range(ws))
+    for rank, cat, g, offs, W, sD in out:
+        assert cat == [0, 1, 2, 100, 101, 102, 103, 104]
+        assert g == [[4.5, 4.5], [4.5, 4.5]]
+        assert offs == [0, (1 << 62)] and W == (1 << 63) + 7 and sD == 7
