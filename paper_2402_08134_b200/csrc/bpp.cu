@@ -8,7 +8,8 @@
 // shared-memory block, factored by a lane-per-row Cholesky and solved by two substitutions -- so a
 // step costs O(|F|^2) lane work instead of a k x k refactorisation, and SymNMF rows have small
 // passive sets.  The dual y = Gh x - b of the active variables reads Gh's rows at the |F| passive
-// columns.  Optionally re-zeroes Y (the LvS scatter target) after reading it.
+// columns.  The pivoting starts from the support of one HALS sweep of the row (see below).
+// Optionally re-zeroes Y (the LvS scatter target) after reading it.
 #include "fused_common.cuh"
 
 namespace symnmf {
@@ -56,12 +57,97 @@ __global__ void __launch_bounds__(BppL<KP>::WPB * 32) bpp_rows(const double* __r
       const int v = lane + 32 * h;
       act[h] = v < k;
       bh[h] = act[h] ? (double)Y[r * k + v] + alpha * (double)F[r * k + v] : 0.0;
-      inF[h] = false;                 // cold start: F empty, x = 0, y = -b
-      x[h] = 0.0;
-      y[h] = -bh[h];
+      x[h] = act[h] ? (double)X[r * k + v] : 0.0;
     }
+    // Initial passive set: the support of one Gauss-Seidel (HALS) sweep of this row from the current
+    // X -- usually close to the NNLS support, so the pivoting starts from a small system.
+    // BPP converges to the unique NLS solution from any initial passive set (the backup rule
+    // guarantees termination), so the start changes the work, not the result.
+    for (int i = 0; i < k; ++i) {
+      double part = 0.0;
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const int v = lane + 32 * h;
+        if (act[h] && v != i) part = fma(sG[i * GS + v], x[h], part);
+      }
+      const double sum = warp_sum(part);
+      const double xi = fmax(0.0, (__shfl_sync(0xffffffffu, bh[i >> 5], i & 31) - sum) / sG[i * GS + i]);
+      if ((i & 31) == lane) x[i >> 5] = xi;
+    }
+    bool fail = false;
+    unsigned Fm[H];
+    int pos[H], nf = 0;
+    // x_F = Gh_FF^{-1} b_F on the passive set, y = Gh x - b on the active set
+    auto solve = [&]() {
+      int base = 0;
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        Fm[h] = __ballot_sync(0xffffffffu, inF[h]);
+        pos[h] = base + __popc(Fm[h] & ((1u << lane) - 1u));
+        if (inF[h]) {
+          idx[pos[h]] = lane + 32 * h;
+          rhs[pos[h]] = bh[h];
+        }
+        base += __popc(Fm[h]);
+      }
+      nf = base;
+      __syncwarp();
+      for (int e = lane; e < nf * nf; e += 32) {   // M = Gh_FF (lower part)
+        const int a = e / nf, c = e - a * nf;
+        if (c <= a) M[a * GS + c] = sG[idx[a] * GS + idx[c]];
+      }
+      __syncwarp();
+      for (int j = 0; j < nf; ++j) {               // Cholesky M = L L^T, lane-per-row updates
+        const double d = M[j * GS + j];
+        if (!(d > 0.0) || !isfinite(d)) { fail = true; return; }
+        const double rj = sqrt(d), rinv = 1.0 / rj;
+        __syncwarp();
+        for (int a = j + 1 + lane; a < nf; a += 32) M[a * GS + j] *= rinv;
+        if (lane == 0) M[j * GS + j] = rj;
+        __syncwarp();
+        for (int a = j + 1 + lane; a < nf; a += 32) {
+          const double laj = M[a * GS + j];
+          for (int c = j + 1; c <= a; ++c) M[a * GS + c] = fma(-laj, M[c * GS + j], M[a * GS + c]);
+        }
+        __syncwarp();
+      }
+      for (int a = lane; a < nf; a += 32) zz[a] = rhs[a];   // forward L z = rhs
+      __syncwarp();
+      for (int j = 0; j < nf; ++j) {
+        const double zj = zz[j] / M[j * GS + j];
+        __syncwarp();
+        if (lane == 0) zz[j] = zj;
+        for (int a = j + 1 + lane; a < nf; a += 32) zz[a] = fma(-M[a * GS + j], zj, zz[a]);
+        __syncwarp();
+      }
+      for (int j = nf - 1; j >= 0; --j) {                   // backward L^T x = z
+        const double xj = zz[j] / M[j * GS + j];
+        __syncwarp();
+        if (lane == 0) xs[j] = xj;
+        for (int a = lane; a < j; a += 32) zz[a] = fma(-M[j * GS + a], xj, zz[a]);
+        __syncwarp();
+      }
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const int v = lane + 32 * h;
+        if (inF[h]) {
+          x[h] = xs[pos[h]];
+          y[h] = 0.0;
+        } else {
+          x[h] = 0.0;
+          double yy = -bh[h];
+          if (act[h])
+            for (int q = 0; q < nf; ++q) yy = fma(sG[v * GS + idx[q]], xs[q], yy);
+          y[h] = yy;
+        }
+      }
+      __syncwarp();
+    };
+#pragma unroll
+    for (int h = 0; h < H; ++h) inF[h] = act[h] && x[h] > 0.0;
+    solve();
     int ninf = k + 1, p = 3, it = 0;
-    for (; it < kBppMaxIt; ++it) {
+    for (; it < kBppMaxIt && !fail; ++it) {
       unsigned V[H];
       int nv = 0;
 #pragma unroll
@@ -79,89 +165,14 @@ __global__ void __launch_bounds__(BppL<KP>::WPB * 32) bpp_rows(const double* __r
 #pragma unroll
         for (int h = 0; h < H; ++h) V[h] = h == hmax ? top : 0u;
       }
-      unsigned Fm[H];
-      int nf = 0;
 #pragma unroll
-      for (int h = 0; h < H; ++h) {
+      for (int h = 0; h < H; ++h)
         if ((V[h] >> lane) & 1u) inF[h] = !inF[h];
-        Fm[h] = __ballot_sync(0xffffffffu, inF[h]);
-      }
-      // compact passive list: idx[pos] = variable, rhs[pos] = b
-      int pos[H];
-      {
-        int base = 0;
-#pragma unroll
-        for (int h = 0; h < H; ++h) {
-          pos[h] = base + __popc(Fm[h] & ((1u << lane) - 1u));
-          if (inF[h]) {
-            idx[pos[h]] = lane + 32 * h;
-            rhs[pos[h]] = bh[h];
-          }
-          base += __popc(Fm[h]);
-        }
-        nf = base;
-      }
-      __syncwarp();
-      // M = Gh_FF (lower part used), lanes over entries
-      for (int e = lane; e < nf * nf; e += 32) {
-        const int a = e / nf, c = e - a * nf;
-        if (c <= a) M[a * GS + c] = sG[idx[a] * GS + idx[c]];
-      }
-      __syncwarp();
-      // Cholesky M = L L^T (lower, in place), lane-per-row updates
-      bool fail = false;
-      for (int j = 0; j < nf; ++j) {
-        const double d = M[j * GS + j];
-        if (!(d > 0.0) || !isfinite(d)) { fail = true; break; }
-        const double rj = sqrt(d), rinv = 1.0 / rj;
-        __syncwarp();
-        for (int a = j + 1 + lane; a < nf; a += 32) M[a * GS + j] *= rinv;
-        if (lane == 0) M[j * GS + j] = rj;
-        __syncwarp();
-        for (int a = j + 1 + lane; a < nf; a += 32) {
-          const double laj = M[a * GS + j];
-          for (int c = j + 1; c <= a; ++c) M[a * GS + c] = fma(-laj, M[c * GS + j], M[a * GS + c]);
-        }
-        __syncwarp();
-      }
-      if (fail) {                                 // Gh_FF not SPD (alpha = 0 and rank-deficient G)
-        if (lane == 0) dev_fail(status, SYMNMF_ERR_NOT_PD);
-        it = kBppMaxIt;
-        break;
-      }
-      // forward L z = rhs, backward L^T x = z (lane-parallel updates of the remaining entries)
-      for (int a = lane; a < nf; a += 32) zz[a] = rhs[a];
-      __syncwarp();
-      for (int j = 0; j < nf; ++j) {
-        const double zj = zz[j] / M[j * GS + j];
-        __syncwarp();
-        if (lane == 0) zz[j] = zj;
-        for (int a = j + 1 + lane; a < nf; a += 32) zz[a] = fma(-M[a * GS + j], zj, zz[a]);
-        __syncwarp();
-      }
-      for (int j = nf - 1; j >= 0; --j) {
-        const double xj = zz[j] / M[j * GS + j];
-        __syncwarp();
-        if (lane == 0) xs[j] = xj;
-        for (int a = lane; a < j; a += 32) zz[a] = fma(-M[j * GS + a], xj, zz[a]);
-        __syncwarp();
-      }
-      // x on the passive set, dual y = Gh x - b on the active set
-#pragma unroll
-      for (int h = 0; h < H; ++h) {
-        const int v = lane + 32 * h;
-        if (inF[h]) {
-          x[h] = xs[pos[h]];
-          y[h] = 0.0;
-        } else {
-          x[h] = 0.0;
-          double yy = -bh[h];
-          if (act[h])
-            for (int q = 0; q < nf; ++q) yy = fma(sG[v * GS + idx[q]], xs[q], yy);
-          y[h] = yy;
-        }
-      }
-      __syncwarp();
+      solve();
+    }
+    if (fail) {                                   // Gh_FF not SPD (alpha = 0 and rank-deficient G)
+      if (lane == 0) dev_fail(status, SYMNMF_ERR_NOT_PD);
+      it = kBppMaxIt;
     }
     if (it >= kBppMaxIt && lane == 0) atomicAdd(nonconv, 1);
 #pragma unroll
