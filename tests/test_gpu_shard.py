@@ -60,15 +60,22 @@ def _case(cfgname, n, k, seed=5):
 @pytest.mark.parametrize("cfgname,n,k,P", [("c2", 100_000, 16, 2), ("c2", 100_000, 16, 4), ("c4", 200_000, 32, 2),
                                            ("c4", 200_000, 32, 4)])
 def test_sharded_exact_iteration_matches_oracle(cfgname, n, k, P):
-    """EXACT: allgather F, block rows of A F, allreduced Gram, block sweeps; one iteration (both
-    halves) vs the oracle's fp64 iteration, 1e-5 relative -- the protocol of the unsharded solver's
-    test_csr_tile_exact_one_iteration."""
+    """EXACT: allgather F, block rows of A F, allreduced Gram, block sweeps.  Two iterations,
+    each half vs the oracle's fp64 half fed the GPU's own previous factors (1e-5 relative): the
+    per-half protocol isolates the sharded arithmetic from the fp32 amplification of earlier halves
+    (at c4 n = 200k the unsharded solver's H after one whole iteration is itself 1.2e-5 from the
+    oracle's -- DESIGN.md sec. 5)."""
     A, H0, alpha = _case(cfgname, n, k)
+    A64 = O.as_f64(A)
     sv = SH.ShardedSolver(A, H0, alpha, SH.LocalComm(P), mode="exact")
-    sv.run(1)
-    W, H = sv.factors()
-    Wr, Hr, _ = O.iterate(A, H0, H0, alpha, 1, "exact")
-    assert rel(W.cpu().numpy(), Wr) < 1e-5 and rel(H.cpu().numpy(), Hr) < 1e-5
+    for it in range(2):
+        for side in (0, 1):
+            W0, H0_ = (t.cpu().numpy().astype(np.float64) for t in sv.factors())
+            sv.half(it, side)
+            W, H = (t.cpu().numpy() for t in sv.factors())
+            Wr, Hr, _ = O.half_step(A64, W0, H0_, alpha, it, side, "exact")
+            got, ref = (W, Wr) if side == 0 else (H, Hr)
+            assert rel(got, ref) < 1e-5, (it, side, rel(got, ref))
 
 
 @pytest.mark.parametrize("cfgname,n,k,s,P", [("c2", 100_000, 16, 2000, 2), ("c2", 100_000, 16, 2000, 4),
