@@ -311,19 +311,28 @@ extern "C" symnmf_status symnmf_sampled_ah(const symnmf_matrix* A, const float* 
                                            float* Y, double* G_s, void* ws, size_t* ws_bytes, cudaStream_t st) {
   if (bad_matrix(A) || !F || !Y || bad_k(k) || bad_plan(plan)) return SYMNMF_ERR_ARG;
   const int grid = gram_grid(std::min<int64_t>(plan->cap, A->n));
+  const int64_t cap = std::min<int64_t>(plan->cap, A->n);
+  const size_t sbs_bytes = (A->kind == SYMNMF_DENSE && sampled_dense_tc_enabled() &&
+                            sampled_dense_tc_supported(A->val, A->lda, A->n, k))
+                               ? sampled_dense_tc_scratch(cap, k)
+                               : 0;
   Carver c(nullptr);
   c.take<double>(gram_partial_doubles(k, k, true, grid));
+  c.take<char>(sbs_bytes);
   bool q;
   symnmf_status r = ws_protocol(ws, ws_bytes, c.bytes(), &q);
   if (r != SYMNMF_OK || q) return r;
   if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
   Carver w(ws);
   double* part = w.take<double>(gram_partial_doubles(k, k, true, grid));
+  char* sbs = w.take<char>(sbs_bytes);
   int32_t* status = ws_status(ws);
   SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
-  const int64_t cap = std::min<int64_t>(plan->cap, A->n);
   if (A->kind == SYMNMF_CSR)
     launch_sampled_csr(*A, F, k, plan->uniq_idx, plan->uniq_w, plan->counts + 2, cap, Y, status, st);
+  else if (sbs_bytes)
+    launch_sampled_dense_tc(A->val, A->lda, A->n, F, k, plan->uniq_idx, plan->uniq_w, plan->counts + 2, cap, cap, Y,
+                            sbs, status, st);
   else
     launch_sampled_dense(A->val, A->lda, A->n, F, k, plan->uniq_idx, plan->uniq_w, plan->counts + 2, cap, Y, status, st);
   if (G_s)
@@ -685,6 +694,8 @@ struct symnmf_solver {
   float* Y;
   bool bpp;                // Update rule: exact per-row NLS by block principal pivoting (NEXT-1)
   int32_t* nonconv;        // BPP rows that hit the pivoting cap (device counter)
+  void* sbs;               // LvS on dense A: scratch of the tensor-core sampled product (tc_sampled.cu)
+  size_t sbs_bytes;
   bool nnzsp;              // EXACT on CSR (kpad(k) == k): the nnz-balanced SpMM (spmm_nnz.cu)
   int64_t* chunk_row;
   float* carry;
@@ -840,6 +851,11 @@ void solver_layout(symnmf_solver& S, Carver& c) {
     S.plan.uniq_w = c.take<double>(n);
     S.plan.counts = c.take<int64_t>(4);
     S.plan.mass = c.take<double>(2);
+    S.sbs_bytes = (S.hasA && S.A.kind == SYMNMF_DENSE && sampled_dense_tc_enabled() &&
+                   sampled_dense_tc_supported(S.A.val, S.A.lda, n, k))
+                      ? sampled_dense_tc_scratch(S.plan.cap, k)
+                      : 0;
+    S.sbs = c.take<char>(S.sbs_bytes);
     const size_t halves = S.record ? (size_t)2 * S.max_iters : 0;
     S.hlev = c.take<float>(halves * n);
     S.huniq = c.take<int32_t>(halves * S.plan.cap);
@@ -910,8 +926,12 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
                                 status, st);
       mark(S, st, "sampled_ah_csr");
     } else {
-      launch_sampled_dense(S.A.val, S.A.lda, n, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap,
-                           S.Y, status, st);
+      if (S.sbs_bytes)
+        launch_sampled_dense_tc(S.A.val, S.A.lda, n, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2,
+                                S.plan.cap, std::min<int64_t>(S.s, n), S.Y, S.sbs, status, st);
+      else
+        launch_sampled_dense(S.A.val, S.A.lda, n, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap,
+                             S.Y, status, st);
       mark(S, st, "sampled_ah_dense");
     }
     cudaStreamWaitEvent(st, S.ev_join[side], 0);

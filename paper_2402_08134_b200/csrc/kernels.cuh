@@ -74,6 +74,14 @@ void launch_sampled_dense(const float* A, int64_t lda, int64_t n, const float* F
 bool launch_dense_ah_tc(const float* A, int64_t lda, int64_t n, const float* F, int64_t ldf, int k, float* Y,
                         int64_t ldy, void* scratch, size_t scratch_bytes, const int32_t* status, cudaStream_t st);
 size_t dense_ah_tc_scratch(int64_t n, int k);
+// tcgen05 3xTF32 sampled dense product (tc_sampled.cu): k <= 64, lda % 4 == n % 4 == 0, A 16-B aligned;
+// scratch: sampled_dense_tc_scratch(cap, k) bytes.
+bool sampled_dense_tc_enabled();
+bool sampled_dense_tc_supported(const float* A, int64_t lda, int64_t n, int k);
+size_t sampled_dense_tc_scratch(int64_t cap, int k);
+void launch_sampled_dense_tc(const float* A, int64_t lda, int64_t n, const float* F, int k, const int32_t* uniq,
+                             const double* w, const int64_t* n_uniq_dev, int64_t cap, int64_t u_hint, float* Y,
+                             void* scratch, const int32_t* status, cudaStream_t st);
 
 // ---------------------------------------------------------------- hals.cu
 void launch_hals_sweep(const double* G, const float* Y, const float* F, float* X, int64_t n, int k, double alpha,

@@ -81,6 +81,13 @@ static int64_t scatter_slice_bytes() {
   return mb > 0 ? (mb << 20) : (86ll << 20);
 }
 
+// Warps per sampled row of the scatter; SYMNMF_SCATTER_SPLIT overrides (symnmf.h).
+static int scatter_split() {
+  const char* e = getenv("SYMNMF_SCATTER_SPLIT");
+  const int v = e ? atoi(e) : 0;
+  return v > 0 ? std::min(v, 64) : 2;   // c4 LvS it/s by split: 1 549, 2 555, 4 540, 8 437
+}
+
 static int grid_for(int64_t work_threads) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((work_threads + 255) / 256, 148 * 16));
 }
@@ -105,24 +112,30 @@ void launch_spmm_csr(const symnmf_matrix& A, const float* F, int k, float* Y, co
 }
 
 // ---------------------------------------------------------------- sampled (scatter) product
+// One warp per (sampled row u, part): the row's nonzeros in this pass's destination range are cut
+// into `split` contiguous parts, so a hub row (10^4 nonzeros at c4) is spread over several warps
+// instead of serialising one; each lane keeps SC_UNROLL entry loads in flight ahead of its vector
+// atomics (the per-step load -> red dependency bound the single-warp walk: ncu r2, long_scoreboard
+// 22 cycles per issued instruction, 20% warps active).
+constexpr int SC_UNROLL = 8;
+
 template <int LPR>
 __global__ void __launch_bounds__(256) sampled_csr_v4(const int64_t* __restrict__ rowptr,
                                                       const int32_t* __restrict__ col, const float* __restrict__ val,
                                                       const float4* __restrict__ F4, const int32_t* __restrict__ uniq,
                                                       const double* __restrict__ w,
                                                       const int64_t* __restrict__ n_uniq_dev, float4* __restrict__ Y4,
-                                                      int32_t c_lo, int32_t c_hi, int ranged,
+                                                      int32_t c_lo, int32_t c_hi, int ranged, int split,
                                                       const int32_t* __restrict__ status) {
   if (dev_failed(status)) return;
   constexpr int NPW = 32 / LPR;   // nonzeros per warp step
   const int lane = threadIdx.x & 31, sub = lane / LPR, li = lane % LPR;
   const int64_t nu = *n_uniq_dev;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < nu; u += nw) {
+  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nu * split; t += nw) {
+    const int64_t u = t / split;
+    const int part = (int)(t - u * split);
     const int64_t i = uniq[u];
-    const float om = (float)w[u];
-    float4 f = __ldg(F4 + i * LPR + li);
-    f.x *= om; f.y *= om; f.z *= om; f.w *= om;
     int64_t e0 = rowptr[i], e1 = rowptr[i + 1];
     if (ranged) {   // this pass's destination range [c_lo, c_hi): a sub-range of the sorted row
       int64_t a = e0, b = e1;
@@ -131,10 +144,26 @@ __global__ void __launch_bounds__(256) sampled_csr_v4(const int64_t* __restrict_
       while (c < d) { const int64_t m = (c + d) >> 1; if (__ldg(col + m) < c_hi) c = m + 1; else d = m; }
       e0 = a; e1 = c;
     }
-    for (int64_t e = e0 + sub; e < e1; e += NPW) {
-      const int64_t c = __ldg(col + e);
-      const float a = __ldg(val + e);
-      atomicAdd(Y4 + c * LPR + li, make_float4(a * f.x, a * f.y, a * f.z, a * f.w));
+    const int64_t len = e1 - e0;
+    const int64_t p0 = e0 + len * part / split, p1 = e0 + len * (part + 1) / split;
+    if (p0 >= p1) continue;
+    const float om = (float)w[u];
+    float4 f = __ldg(F4 + i * LPR + li);
+    f.x *= om; f.y *= om; f.z *= om; f.w *= om;
+    for (int64_t e = p0 + sub; e < p1; e += NPW * SC_UNROLL) {
+      int cc[SC_UNROLL];
+      float aa[SC_UNROLL];
+#pragma unroll
+      for (int j = 0; j < SC_UNROLL; ++j) {
+        const int64_t ej = e + (int64_t)j * NPW;
+        const bool ok = ej < p1;
+        cc[j] = ok ? __ldg(col + ej) : -1;
+        aa[j] = ok ? __ldg(val + ej) : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < SC_UNROLL; ++j)
+        if (cc[j] >= 0)
+          atomicAdd(Y4 + (int64_t)cc[j] * LPR + li, make_float4(aa[j] * f.x, aa[j] * f.y, aa[j] * f.z, aa[j] * f.w));
     }
   }
 }
@@ -183,15 +212,16 @@ void launch_sampled_csr_nozero(const symnmf_matrix& A, const float* F, int k, co
     const int64_t ybytes = (int64_t)sizeof(float) * A.n * k;
     const int64_t slice = scatter_slice_bytes();
     const int passes = (int)std::max<int64_t>(1, (ybytes + slice - 1) / slice);
+    const int split = scatter_split();
     for (int p = 0; p < passes; ++p) {
       const int32_t lo = (int32_t)(A.n * p / passes), hi = (int32_t)(A.n * (p + 1) / passes);
       const int ranged = passes > 1;
       switch (k / 4) {
-        case 1: launch_pdl(sampled_csr_v4<1>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, status); break;
-        case 2: launch_pdl(sampled_csr_v4<2>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, status); break;
-        case 4: launch_pdl(sampled_csr_v4<4>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, status); break;
-        case 8: launch_pdl(sampled_csr_v4<8>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, status); break;
-        case 16: launch_pdl(sampled_csr_v4<16>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, status); break;
+        case 1: launch_pdl(sampled_csr_v4<1>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, split, status); break;
+        case 2: launch_pdl(sampled_csr_v4<2>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, split, status); break;
+        case 4: launch_pdl(sampled_csr_v4<4>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, split, status); break;
+        case 8: launch_pdl(sampled_csr_v4<8>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, split, status); break;
+        case 16: launch_pdl(sampled_csr_v4<16>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, split, status); break;
         default: break;
       }
     }

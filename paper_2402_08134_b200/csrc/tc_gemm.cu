@@ -34,10 +34,8 @@
 // Measured (tools/tc_bias.py, uniform [0,1) A and X, n = 30,000): mean relative error -1.6e-6,
 // max 2.1e-6 with TC_DRAIN = 16 (fp32 SGEMM: max 1.4e-5); TC_DRAIN = 8 / 32: -8e-7 / -3.2e-6 at
 // 0.902 / 0.876 ms against 0.886 ms.
-#include <cstdio>
-#include <cuda.h>
 #include <cudaTypedefs.h>
-#include "kernels.cuh"
+#include "tc_common.cuh"
 
 namespace symnmf {
 
@@ -46,86 +44,6 @@ constexpr int TC_BK = 32;          // fp32 elements per 128-byte row
 template <int NP> constexpr int tc_stages() { return NP <= 32 ? 5 : NP <= 80 ? 4 : 3; }
 constexpr int TC_THREADS = 384;
 constexpr int TC_DRAIN = 16;       // k-blocks per accumulator chunk
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// Bounded wait: a pipeline that cannot make progress for ~10 s traps (a device
-// error the host sees) instead of hanging the GPU.
-// wait with a sleep between polls: for warps that are not on the critical path (the drain
-// warps share sub-partitions with the TMA producer and the MMA issuer)
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
-  for (;;) {
-    uint32_t ok;
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-    if (ok) return;
-    __nanosleep(200);
-  }
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
-  uint32_t ok = 0;
-  uint64_t spins = 0;
-  while (!ok) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-    if (!ok && ++spins > (1ull << 27)) {
-      printf("symnmf tc_gemm: mbarrier wait timeout block (%d,%d) thread %d bar %u parity %u\n", blockIdx.x,
-             blockIdx.y, threadIdx.x, a, parity);
-      __trap();
-    }
-  }
-}
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int x, int y) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-// K-major operand, 128-byte swizzle: rows of 128 B, 8-row core groups 1024 B apart.
-__device__ __forceinline__ uint64_t smem_desc_k128(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);          // start address
-  d |= (uint64_t)1 << 16;                           // leading byte offset (unused for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;                 // stride byte offset: 8 rows x 128 B
-  d |= (uint64_t)1 << 46;                           // descriptor version (sm_100)
-  d |= (uint64_t)2 << 61;                           // SWIZZLE_128B
-  return d;
-}
-
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t accum) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(
-          tmem_d),
-      "l"(ad), "l"(bd), "r"(idesc), "r"(accum)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
 
 template <int NP>
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -138,10 +56,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // accumulators: NACC independent chains per buffer, each 2 NP columns ([.. X_hi | .. X_lo]);
   // two buffers.  NACC = 4: {A_hi, A_lo} x {even, odd K=8 step}; 2: {A_hi, A_lo}; 1: shared.
   constexpr int NACC = NP <= 32 ? 4 : NP <= 64 ? 2 : 1;
-  constexpr uint32_t ACC_COLS = 2 * NP;
-  constexpr uint32_t BUF_COLS = NACC * ACC_COLS;
+  // NP > 64 with 2 x 3 NP TMEM columns available (NP = 80, the c5 range finder): three N = NP MMAs
+  // per K=8 step -- A_hi X_hi, A_hi X_lo, A_lo X_hi -- into three independent accumulators instead
+  // of two dependent N = 2 NP ones into one (A_lo X_lo, 1/4 of the tensor work, is dropped).
+  constexpr bool SPLIT3 = NP > 64 && 6 * NP <= 512;
+  constexpr uint32_t ACC_COLS = SPLIT3 ? NP : 2 * NP;
+  constexpr uint32_t BUF_COLS = SPLIT3 ? 3 * NP : NACC * ACC_COLS;
   constexpr uint32_t TMEM_COLS = 2 * BUF_COLS <= 128 ? 128 : 2 * BUF_COLS <= 256 ? 256 : 512;
-  constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)((2 * NP) >> 3) << 17) |
+  constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(ACC_COLS >> 3) << 17) |
                              ((uint32_t)(TC_BM >> 4) << 24);
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
@@ -199,6 +121,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t a_hi = smem_u32(sm + s * STAGE), a_lo = a_hi + A_BYTES;
         const uint32_t b_hi = a_hi + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
         const uint32_t td = tmem + (uint32_t)b * BUF_COLS;
+        if constexpr (SPLIT3) {
+#pragma unroll
+          for (int kk = 0; kk < TC_BK / 8; ++kk) {
+            const uint32_t off = kk * 32;
+            const uint32_t acc0 = ((i % TC_DRAIN) != 0 || kk > 0) ? 1u : 0u;
+            mma_tf32(td, smem_desc_k128(a_hi + off), smem_desc_k128(b_hi + off), IDESC, acc0);
+            mma_tf32(td + NP, smem_desc_k128(a_hi + off), smem_desc_k128(b_lo + off), IDESC, acc0);
+            mma_tf32(td + 2 * NP, smem_desc_k128(a_lo + off), smem_desc_k128(b_hi + off), IDESC, acc0);
+          }
+        } else
 #pragma unroll
         for (int kk = 0; kk < TC_BK / 8; ++kk) {
           const uint32_t off = kk * 32;   // 8 tf32 = 32 bytes along the swizzled row
@@ -247,7 +179,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_wait_sleep(acc_full + b, (c >> 1) & 1);
       tc_fence_after();
 #pragma unroll
-      for (int cc = 0; cc < NACC * 2 * NP; cc += 16) {
+      for (int cc = 0; cc < (int)BUF_COLS; cc += 16) {
         const int c0 = cc % NP;   // column block of Y; the NACC x {X_hi, X_lo} partial sums add up
         uint32_t r[16];
         const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)b * BUF_COLS + (uint32_t)cc;

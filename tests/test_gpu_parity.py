@@ -186,6 +186,38 @@ def test_sampled_dense(c1):
     assert rel(Y.cpu().numpy(), Yr) < 1e-5 and rel(Gs.cpu().numpy(), Gr) < 1e-6
 
 
+@pytest.mark.parametrize("n,k,s", [(1000, 8, 200), (3000, 32, 1500), (4100, 16, 900), (2052, 64, 700),
+                                   (1998, 32, 300), (5000, 3, 2000), (640, 32, 10), (12_000, 32, 3000)])
+@pytest.mark.parametrize("path", ["tc", "simt"])
+def test_sampled_dense_paths(n, k, s, path, monkeypatch):
+    """Sampled dense product Y_s = A[U,:]^T (Omega F[U]): the tcgen05 3xTF32 kernel
+    (tc_sampled.cu, default for n % 4 == 0, k <= 64) and the fp32 SIMT kernel (SYMNMF_SAMPLED_DENSE=
+    simt) vs the oracle.  Ragged output tiles (n % 128 != 0), n % 4 != 0 (SIMT fallback), |U| from
+    < 32 (one partial k-block) to the c3 budget (s = 3,000: U split over the grid)."""
+    if path == "simt":
+        monkeypatch.setenv("SYMNMF_SAMPLED_DENSE", "simt")
+    A = sym_dense(n, n + 7 * k)
+    F = random_factor(n, k, 11) ** 2
+    plan, o = _plan_for(F, k, s, 1.0 / s, seed=3, it=1, side=0)
+    Y, Gs = S.sampled_ah(S.DeviceMatrix.from_host(A), cu(F), plan)
+    Gr, Yr = O.sampled_products(A, F, o["uniq_idx"], o["uniq_w"])
+    assert rel(Y.cpu().numpy(), Yr) < 1e-5 and rel(Gs.cpu().numpy(), Gr) < 1e-6
+
+
+def test_sampled_dense_all_rows_equals_exact():
+    """Every row deterministic (tau below every p_i): U = all n rows, Omega = 1, so the tensor-core
+    sampled product is A F (P:716-719 with I_D = all rows)."""
+    n, k = 2_500, 16
+    A = sym_dense(n, 5)
+    F = random_factor(n, k, 12)
+    lev = S.leverage_scores(cu(F))
+    tau = float(lev.min().item()) / k * 0.5
+    plan = S.hybrid_sample(lev, k, 10, tau, 0, 0, 0)
+    Y, _ = S.sampled_ah(S.DeviceMatrix.from_host(A), cu(F), plan)
+    assert plan.to_host()["n_uniq"] == n
+    assert rel(Y.cpu().numpy(), O.ah(A, F)) < 1e-5
+
+
 @pytest.mark.parametrize("k", [3, 16, 32])
 def test_sampled_csr(c2small, k):
     A = c2small["A"]
