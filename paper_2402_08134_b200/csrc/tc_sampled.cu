@@ -14,22 +14,24 @@
 //
 // Per CTA: one 128-row output tile (c0 .. c0+127) and one range of U (split over gridDim.y so the
 // grid fills whole waves of the 148 SMs):
-//   warps 0..3   producers: per stage (32 sampled rows) cp.async the 32 x 512 B slab of A (the rows
-//                U_u, columns c0..c0+127) and the [Omega F]_hi^T / [Omega F]_lo^T tiles (2 NP rows of
-//                128 B, K-major, written once per product by sampled_b_split); then, per thread
-//                on its own chunks once they land, A_lo = a - (a & 0xffffe000) into a second buffer
-//                (the raw slab is A_hi: kind::tf32 ignores the low 13 mantissa bits),
-//                fence.proxy.async, arrive (128 arrivals)
+//   warps 0..3   producers.  Per stage (32 sampled rows) each thread cp.asyncs its own 8 chunks of
+//                the 32 x 512 B slab of A (rows U_u, columns c0..c0+127) and its chunks of the
+//                [Omega F]_hi^T / [Omega F]_lo^T tiles (2 NP rows of 128 B, K-major, written once
+//                per product by sampled_b_split) into a RAW ring that only this thread touches, SR
+//                stages deep.  When its chunks of stage j land it writes A_hi = a & 0xffffe000,
+//                A_lo = a - A_hi and the B chunks into one of two MMA slots, fence.proxy.async,
+//                arrive.  The raw slot is free again at once, so the loads in flight never wait
+//                for the tensor core (a single ring, where the MMA read the raw slot as A_hi, tied
+//                every reissue to an MMA round trip: 0.21 ms at c3 against 0.24 ms for SIMT).
 //   warp 4       one elected thread issues per K=8 step A_hi [B_hi | B_lo] and A_lo [B_hi | B_lo]
 //                (M = 128, N = 2 NP) into independent TMEM accumulators, as tc_gemm.cu does; the
-//                accumulators restart every TC_DRAIN k-blocks (the tensor core's truncating fp32
+//                accumulators restart every SB_DRAIN k-blocks (the tensor core's truncating fp32
 //                accumulate, tc_gemm.cu header)
 //   warp 5       TMEM allocation
 //   warps 6..9   drain TMEM into fp32 registers; at the end add into Y (fp32 red.add; Y zeroed
 //                when U is split, else plain stores)
-// Against the SIMT kernel (dense.cu sampled_dense_v3, fp32 FMA issue-bound at ~33% of the FMA
-// pipe, verdict r1) this moves the product onto the tensor pipe, leaving the gather of |U| x n x 4 B
-// of A from HBM as the bound.
+// A TMA form (one thread issuing 32 tile::gather4 loads per stage through
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) was correct but slower (0.27 ms at c3); not kept.
 #include "tc_common.cuh"
 
 #include <cstdlib>
@@ -43,14 +45,15 @@ constexpr int SB_BM = 128;          // output rows per CTA
 constexpr int SB_BK = 32;           // sampled rows per stage
 constexpr int SB_THREADS = 320;     // 10 warps
 constexpr int SB_DRAIN = 16;        // k-blocks per accumulator chunk (tc_gemm.cu)
-template <int NP> constexpr int sb_stages() { return NP <= 32 ? 4 : 3; }
 
 template <int NP>
 struct SbLayout {
-  static constexpr uint32_t A_BYTES = SB_BM * SB_BK * 4;            // 16 KB raw slab (A_hi)
-  static constexpr uint32_t B_BYTES = 2 * NP * SB_BK * 4;           // [B_hi ; B_lo] tiles
-  static constexpr uint32_t STAGE = 2 * A_BYTES + B_BYTES;          // raw | lo | B
-  static constexpr size_t smem = 1024 + (size_t)sb_stages<NP>() * STAGE + (3 * sb_stages<NP>() + 4) * 8 + 16;
+  static constexpr uint32_t A_BYTES = SB_BM * SB_BK * 4;              // 16 KB slab
+  static constexpr uint32_t B_BYTES = 2 * NP * SB_BK * 4;             // [B_hi ; B_lo] tiles
+  static constexpr uint32_t RAW = A_BYTES + B_BYTES;                   // raw ring stage
+  static constexpr uint32_t MMA = 2 * A_BYTES + B_BYTES;               // MMA slot: A_hi | A_lo | B
+  static constexpr int SR = NP <= 16 ? 6 : NP <= 32 ? 5 : 3;          // raw ring depth
+  static constexpr size_t smem = 1024 + (size_t)SR * RAW + 2 * (size_t)MMA + 8 * 8 + 16;
 };
 
 }  // namespace
@@ -82,7 +85,7 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
                       const float* __restrict__ loT, int64_t ldu, float* __restrict__ Y, int k,
                       const int32_t* __restrict__ status) {
   using L = SbLayout<NP>;
-  constexpr int S = sb_stages<NP>();
+  constexpr int SR = L::SR;
   constexpr int NACC = NP <= 32 ? 4 : 2;
   constexpr uint32_t ACC_COLS = 2 * NP;
   constexpr uint32_t BUF_COLS = NACC * ACC_COLS;
@@ -92,10 +95,12 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
                              ((uint32_t)((2 * NP) >> 3) << 17) | ((uint32_t)(SB_BM >> 4) << 24);
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-  uint64_t* conv = reinterpret_cast<uint64_t*>(sm + S * L::STAGE);
-  uint64_t* empty = conv + S;
-  uint64_t* acc_full = empty + S;    // [2]
-  uint64_t* acc_empty = acc_full + 2;  // [2]
+  unsigned char* slot = sm;                               // 2 MMA slots
+  unsigned char* raw = sm + 2 * L::MMA;                   // SR raw stages
+  uint64_t* hl_full = reinterpret_cast<uint64_t*>(raw + SR * L::RAW);   // [2]
+  uint64_t* hl_empty = hl_full + 2;                                    // [2]
+  uint64_t* acc_full = hl_empty + 2;                                   // [2]
+  uint64_t* acc_empty = acc_full + 2;                                  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   if (dev_failed(status)) return;
@@ -115,8 +120,10 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
   }
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) { mbar_init(conv + s, 128); mbar_init(empty + s, 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(acc_full + b, 1); mbar_init(acc_empty + b, 128); }
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(hl_full + h, 128); mbar_init(hl_empty + h, 1);
+      mbar_init(acc_full + h, 1); mbar_init(acc_empty + h, 128);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 5) {
@@ -132,72 +139,89 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
 
   if (warp < 4) {
     const int t = threadIdx.x;   // 0..127
-    // stage i: sampled rows u = (kb0 + i) * 32 + r.  A chunk e = t + 128 q (q < 8): row r = e / 32
-    // (warp w: rows w + 4q), chunk cq = e % 32 of the 512 B slice = atom cq / 8, 16-B chunk cq % 8.
-    // MN-major tf32 operands use the 128B-row / 32B-atom swizzle (SWIZZLE_128B_BASE32B, the only
-    // MN-major layout the tf32 MMA accepts): atoms of 4 K-rows x 128 B (32 fp32 along M), the
-    // 32-byte chunk index XOR (K-row mod 4).  Atom (m block mb, 4-row group kq) at kq*2048 + mb*512.
+    // A chunk e = t + 128 q (q < 8): K-row r = e / 32 = t / 32 + 4 q (warp-uniform), 16-B chunk
+    // cq = e % 32 = lane of the row's 512 B.  Atom (m block cq / 8, 4-row group r / 4) at
+    // (r / 4) * 2048 + (cq / 8) * 512; in it the 32-byte chunk (cq % 8) / 2 of row r % 4 is
+    // stored at position ((cq % 8) / 2) ^ (r % 4).
     auto aoff = [](int r, int cq) -> uint32_t {
       const int r4 = r & 3;
       return (uint32_t)((r >> 2) * 2048 + (cq >> 3) * 512 + r4 * 128 + ((((cq & 7) >> 1) ^ r4) << 5) + ((cq & 1) << 4));
     };
-    auto issue = [&](int i) {
-      const int s = i % S;
-      unsigned char* st = sm + s * L::STAGE;
+    // B chunk e = t + 128 q (q < NP / 8): row nn = e / 8 (< NP: hi, else lo), 16-B chunk e % 8,
+    // K-major 128B swizzle
+    auto boff = [](int e) -> uint32_t { const int nn = e >> 3, j = e & 7; return (uint32_t)(nn * 128 + ((j ^ (nn & 7)) << 4)); };
+    // the sampled row indices of a stage are loaded one stage ahead, off the issue path
+    int32_t urow[8];
+    auto load_rows = [&](int i) {
       const int64_t ub = (kb0 + i) * SB_BK;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const int e = t + 128 * q, r = e >> 5, cq = e & 31;
-        const int64_t u = ub + r, c = c0 + 4 * cq;
-        const bool ok = u < nu && c < n;
-        const float* src = ok ? A + (int64_t)__ldg(uniq + u) * lda + c : A;
-        cp_async16(st + aoff(r, cq), src, ok);
+        const int64_t u = ub + (t >> 5) + 4 * q;
+        urow[q] = (i < nkb && u < nu) ? __ldg(uniq + u) : -1;
       }
-      // B rows nn < NP from hiT, NP..2NP-1 from loT: 8 chunks of 16 B each, K-major 128B swizzle
-      unsigned char* sb = st + 2 * L::A_BYTES;
+    };
+    auto issue = [&](int i) {
+      unsigned char* st = raw + (i % SR) * L::RAW;
+      const int64_t ub = (kb0 + i) * SB_BK;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int r = (t >> 5) + 4 * q, cq = t & 31;
+        const int64_t c = c0 + 4 * cq;
+        const bool ok = urow[q] >= 0 && c < n;
+        cp_async16(st + aoff(r, cq), ok ? (const void*)(A + (int64_t)urow[q] * lda + c) : (const void*)A, ok);
+      }
 #pragma unroll
       for (int q = 0; q < (16 * NP) / 128; ++q) {
         const int e = t + 128 * q, nn = e >> 3, j = e & 7;
         const float* src = (nn < NP ? hiT + (int64_t)nn * ldu : loT + (int64_t)(nn - NP) * ldu) + ub + 4 * j;
-        cp_async16(sb + nn * 128 + ((j ^ (nn & 7)) << 4), src, true);
+        cp_async16(st + L::A_BYTES + boff(e), src, true);
       }
     };
-    for (int i = 0; i < nkb + S - 1; ++i) {
-      if (i < nkb) {
-        if (i >= S) mbar_wait(empty + i % S, ((i / S) - 1) & 1);
+    load_rows(0);
+    for (int i = 0; i < nkb + SR - 1; ++i) {
+      if (i < nkb) {   // raw slot i % SR: this thread's chunks of stage i - SR were consumed at i - 1
         issue(i);
+        load_rows(i + 1);
       }
       cp_async_commit();
-      if (i >= S - 1) {
-        const int j = i - (S - 1);
-        cp_async_wait<S - 1>();   // this thread's chunks of stage j have landed
-        unsigned char* st = sm + (j % S) * L::STAGE;
+      if (i >= SR - 1) {
+        const int j = i - (SR - 1), h = j & 1;
+        cp_async_wait<SR - 1>();   // this thread's chunks of stage j have landed
+        if (j >= 2) mbar_wait(hl_empty + h, ((j >> 1) - 1) & 1);
+        const unsigned char* st = raw + (j % SR) * L::RAW;
+        unsigned char* ms = slot + h * L::MMA;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const int e = t + 128 * q, r = e >> 5, cq = e & 31;
-          const uint32_t off = aoff(r, cq);
+          const uint32_t off = aoff((t >> 5) + 4 * q, t & 31);
           const uint4 v = *reinterpret_cast<const uint4*>(st + off);
-          uint4 l;
-          l.x = __float_as_uint(__uint_as_float(v.x) - __uint_as_float(v.x & 0xFFFFE000u));
-          l.y = __float_as_uint(__uint_as_float(v.y) - __uint_as_float(v.y & 0xFFFFE000u));
-          l.z = __float_as_uint(__uint_as_float(v.z) - __uint_as_float(v.z & 0xFFFFE000u));
-          l.w = __float_as_uint(__uint_as_float(v.w) - __uint_as_float(v.w & 0xFFFFE000u));
-          *reinterpret_cast<uint4*>(st + L::A_BYTES + off) = l;
+          uint4 hi, lo;
+          hi.x = v.x & 0xFFFFE000u; hi.y = v.y & 0xFFFFE000u; hi.z = v.z & 0xFFFFE000u; hi.w = v.w & 0xFFFFE000u;
+          lo.x = __float_as_uint(__uint_as_float(v.x) - __uint_as_float(hi.x));
+          lo.y = __float_as_uint(__uint_as_float(v.y) - __uint_as_float(hi.y));
+          lo.z = __float_as_uint(__uint_as_float(v.z) - __uint_as_float(hi.z));
+          lo.w = __float_as_uint(__uint_as_float(v.w) - __uint_as_float(hi.w));
+          *reinterpret_cast<uint4*>(ms + off) = hi;
+          *reinterpret_cast<uint4*>(ms + L::A_BYTES + off) = lo;
+        }
+#pragma unroll
+        for (int q = 0; q < (16 * NP) / 128; ++q) {
+          const uint32_t off = boff(t + 128 * q);
+          *reinterpret_cast<uint4*>(ms + 2 * L::A_BYTES + off) = *reinterpret_cast<const uint4*>(st + L::A_BYTES + off);
         }
         fence_proxy_async();
-        mbar_arrive(conv + j % S);
+        mbar_arrive(hl_full + h);
       }
     }
     cp_async_wait<0>();
   } else if (warp == 4) {
     if (lane == 0) {
       for (int i = 0; i < nkb; ++i) {
-        const int s = i % S;
+        const int h = i & 1;
         const int c = i / SB_DRAIN, b = c & 1;
         if (i % SB_DRAIN == 0 && c >= 2) mbar_wait(acc_empty + b, ((c >> 1) - 1) & 1);
-        mbar_wait(conv + s, (i / S) & 1);
+        mbar_wait(hl_full + h, (i >> 1) & 1);
         tc_fence_after();
-        const uint32_t a_hi = smem_u32(sm + s * L::STAGE), a_lo = a_hi + L::A_BYTES, bb = a_hi + 2 * L::A_BYTES;
+        const uint32_t a_hi = smem_u32(slot + h * L::MMA), a_lo = a_hi + L::A_BYTES, bb = a_hi + 2 * L::A_BYTES;
         const uint32_t td = tmem + (uint32_t)b * BUF_COLS;
 #pragma unroll
         for (int kk = 0; kk < SB_BK / 8; ++kk) {
@@ -208,7 +232,7 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
           mma_tf32(tq + ACC_COLS, smem_desc_mn128_b32(a_lo + kk * 4096, 512, 2048), smem_desc_k128(bb + kk * 32),
                    IDESC, acc0);
         }
-        mma_commit(empty + s);
+        mma_commit(hl_empty + h);
         if ((i + 1) % SB_DRAIN == 0 || i + 1 == nkb) mma_commit(acc_full + b);
       }
     }
@@ -298,6 +322,7 @@ static void launch_sb_t(const float* A, int64_t lda, int64_t n, const float* F, 
     const double eff = (double)ctas / (double)(waves * 148) * (1.0 - 0.01 * (double)sp);
     if (eff > best + 1e-9) { best = eff; splits = sp; }
   }
+  if (const char* e = getenv("SYMNMF_SB_SPLITS")) splits = std::max(1, atoi(e));   // measurement knob
   if (splits > 1) cudaMemsetAsync(Y, 0, sizeof(float) * n * k, st);
   cudaFuncSetAttribute(tc_sampled_3xtf32<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::smem);
   tc_sampled_3xtf32<NP><<<dim3((unsigned)mt, (unsigned)splits), SB_THREADS, L::smem, st>>>(
