@@ -43,7 +43,7 @@ __global__ void spmm_nnz_rows_kernel(Src src, int64_t n, int64_t total, const in
 }
 
 template <int KP, class Src>
-__global__ void __launch_bounds__(256, 4) spmm_nnz(Src src, int64_t total, const int32_t* __restrict__ total_dev,
+__global__ void __launch_bounds__(256, 3) spmm_nnz(Src src, int64_t total, const int32_t* __restrict__ total_dev,
                                                    const int64_t* __restrict__ chunk_row,
                                                    const float4* __restrict__ F4, float4* __restrict__ Y4,
                                                    float4* __restrict__ carry, const int32_t* __restrict__ status) {
@@ -66,15 +66,20 @@ __global__ void __launch_bounds__(256, 4) spmm_nnz(Src src, int64_t total, const
       if (rstart >= s0 && rend <= s1) Y4[r * LPR + li] = acc;                 // complete in this chunk
       else carry[(2 * g + (r == rf ? 0 : 1)) * LPR + li] = acc;               // shared with a neighbour
     };
-    for (int64_t e = s0; e < s1; e += kGather) {
-      // the batch's entries: lane li < LG loads entries e + li + LG p (coalesced), shared by shuffles
-      int cm[PER];
-      float am[PER];
+    // the batch's entries: lane li < LG loads entries e + li + LG p (coalesced), shared by shuffles;
+    // the next batch's are loaded before this batch's gathers, so the entry stream's latency
+    // overlaps the gathers' (ncu r2: the two dependent loads per batch were the top two stalls)
+    int cm[PER];
+    float am[PER];
+    auto load_batch = [&](int64_t e) {
 #pragma unroll
       for (int p = 0; p < PER; ++p) {
         const int64_t ej = e + li + LG * p;
         if (li < LG && ej < s1) src.load(ej, cm[p], am[p]); else { cm[p] = 0; am[p] = 0.f; }
       }
+    };
+    load_batch(s0);
+    for (int64_t e = s0; e < s1; e += kGather) {
       int cc[kGather];
       float aa[kGather];
 #pragma unroll
@@ -82,6 +87,7 @@ __global__ void __launch_bounds__(256, 4) spmm_nnz(Src src, int64_t total, const
         cc[u] = __shfl_sync(gmask, cm[u / LG], u % LG, LPR);
         aa[u] = __shfl_sync(gmask, am[u / LG], u % LG, LPR);
       }
+      load_batch(e + kGather);
       float4 ff[kGather];
 #pragma unroll
       for (int u = 0; u < kGather; ++u)
