@@ -121,7 +121,7 @@ typedef struct {
  *   SYMNMF_SCATTER_SLICE_MB=<mb>   sampled CSR scatter product: rows of Y per destination-range
  *                                  pass (default 86 MB, so each pass's slice of Y stays in L2).
  *   SYMNMF_SCATTER_SPLIT=<w>       sampled CSR scatter product: warps per sampled row and pass (each
- *                                  takes a contiguous part of the row's in-range nonzeros; default 2).
+ *                                  takes a contiguous part of the row's in-range nonzeros; default 4).
  *   SYMNMF_SAMPLED_DENSE=simt      sampled dense product: the fp32 SIMT kernel instead of the
  *                                  tcgen05 3xTF32 one (default when k <= 64, n % 4 == lda % 4 == 0).
  *   SYMNMF_LAI_FUSED=never         LAI solver (k = 64, l <= 80): use the four-kernel half (U^T F,

@@ -694,6 +694,7 @@ struct symnmf_solver {
   float* Y;
   bool bpp;                // Update rule: exact per-row NLS by block principal pivoting (NEXT-1)
   int32_t* nonconv;        // BPP rows that hit the pivoting cap (device counter)
+  int32_t* ppos;           // LvS on CSR: per-row boundaries of the scatter's destination passes
   void* sbs;               // LvS on dense A: scratch of the tensor-core sampled product (tc_sampled.cu)
   size_t sbs_bytes;
   bool nnzsp;              // EXACT on CSR (kpad(k) == k): the nnz-balanced SpMM (spmm_nnz.cu)
@@ -856,6 +857,8 @@ void solver_layout(symnmf_solver& S, Carver& c) {
                       ? sampled_dense_tc_scratch(S.plan.cap, k)
                       : 0;
     S.sbs = c.take<char>(S.sbs_bytes);
+    const int passes = (S.hasA && S.A.kind == SYMNMF_CSR) ? sampled_csr_passes(n, k) : 1;
+    S.ppos = c.take<int32_t>(passes > 1 ? (size_t)passes * n : 0);
     const size_t halves = S.record ? (size_t)2 * S.max_iters : 0;
     S.hlev = c.take<float>(halves * n);
     S.huniq = c.take<int32_t>(halves * S.plan.cap);
@@ -923,7 +926,7 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     cudaEventRecord(S.ev_join[side], S.side);
     if (S.A.kind == SYMNMF_CSR) {
       launch_sampled_csr_nozero(S.A, F, k, S.plan.uniq_idx, S.plan.uniq_w, S.plan.counts + 2, S.plan.cap, S.Y,
-                                status, st);
+                                status, st, S.ppos);
       mark(S, st, "sampled_ah_csr");
     } else {
       if (S.sbs_bytes)
@@ -1046,6 +1049,7 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
     if (hbad) return SYMNMF_ERR_ARG;
   }
   if (S.nnzsp) launch_spmm_nnz_rows(S.A, S.chunk_row, st);
+  if (S.ppos) launch_sampled_pass_bounds(S.A, k, S.ppos, st);
   set_i32<<<1, 1, 0, st>>>(S.iter_dev, first_iter);
   // H^T H (and its CholeskyQR factor for LvS) for the first W-half; later halves get
   // theirs from the fused Gram of the preceding sweep.

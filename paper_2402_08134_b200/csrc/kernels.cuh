@@ -131,9 +131,12 @@ void launch_samp_draws(const SamplerWs& w, int64_t n, int64_t s, uint64_t seed, 
 void launch_samp_uniq_write(const float* lev, int64_t n, double T, const SamplerWs& w, const symnmf_plan& plan,
                             int32_t* status, cudaStream_t st);
 // sampled CSR scatter into a Y the caller has zeroed
+// Scatter pass boundaries per row of A (once per A; (passes - 1) x n int32, see spmm.cu).
+int sampled_csr_passes(int64_t n, int k);
+void launch_sampled_pass_bounds(const symnmf_matrix& A, int k, int32_t* ppos, cudaStream_t st);
 void launch_sampled_csr_nozero(const symnmf_matrix& A, const float* F, int k, const int32_t* uniq, const double* w,
                                const int64_t* n_uniq_dev, int64_t cap, float* Y, const int32_t* status,
-                               cudaStream_t st);
+                               cudaStream_t st, const int32_t* ppos = nullptr);
 
 // ---------------------------------------------------------------- spmm_nnz.cu
 // Exact CSR product balanced by nonzeros (k in {8,16,32,64}); chunk_row from launch_spmm_nnz_rows

@@ -85,7 +85,8 @@ static int64_t scatter_slice_bytes() {
 static int scatter_split() {
   const char* e = getenv("SYMNMF_SCATTER_SPLIT");
   const int v = e ? atoi(e) : 0;
-  return v > 0 ? std::min(v, 64) : 2;   // c4 LvS it/s by split: 1 549, 2 555, 4 540, 8 437
+  // c4 LvS it/s by split (pass bounds precomputed): 1 565, 2 583, 4 614, 8 598, 16 545
+  return v > 0 ? std::min(v, 64) : 4;
 }
 
 static int grid_for(int64_t work_threads) {
@@ -126,6 +127,7 @@ __global__ void __launch_bounds__(256) sampled_csr_v4(const int64_t* __restrict_
                                                       const double* __restrict__ w,
                                                       const int64_t* __restrict__ n_uniq_dev, float4* __restrict__ Y4,
                                                       int32_t c_lo, int32_t c_hi, int ranged, int split,
+                                                      const int32_t* __restrict__ ppos, int pass, int64_t n,
                                                       const int32_t* __restrict__ status) {
   if (dev_failed(status)) return;
   constexpr int NPW = 32 / LPR;   // nonzeros per warp step
@@ -137,7 +139,11 @@ __global__ void __launch_bounds__(256) sampled_csr_v4(const int64_t* __restrict_
     const int part = (int)(t - u * split);
     const int64_t i = uniq[u];
     int64_t e0 = rowptr[i], e1 = rowptr[i + 1];
-    if (ranged) {   // this pass's destination range [c_lo, c_hi): a sub-range of the sorted row
+    if (ranged && ppos) {   // the pass boundaries of row i, found once per A (sampled_pass_bounds)
+      const int64_t base = e0;
+      if (pass > 0) e0 = base + ppos[(int64_t)(pass - 1) * n + i];
+      if (ppos[(int64_t)pass * n + i] >= 0) e1 = base + ppos[(int64_t)pass * n + i];
+    } else if (ranged) {   // this pass's destination range [c_lo, c_hi): a sub-range of the sorted row
       int64_t a = e0, b = e1;
       while (a < b) { const int64_t m = (a + b) >> 1; if (__ldg(col + m) < c_lo) a = m + 1; else b = m; }
       int64_t c = a, d = e1;
@@ -199,9 +205,41 @@ void launch_sampled_csr(const symnmf_matrix& A, const float* F, int k, const int
   launch_sampled_csr_nozero(A, F, k, uniq, w, n_uniq_dev, cap, Y, status, st);
 }
 
+// Destination-range passes of the scatter for this A and k (>= 1).
+int sampled_csr_passes(int64_t n, int k) {
+  const int64_t ybytes = (int64_t)sizeof(float) * n * k;
+  const int64_t slice = scatter_slice_bytes();
+  return (int)std::max<int64_t>(1, (ybytes + slice - 1) / slice);
+}
+
+// ppos[p][i] (p < passes - 1) = offset within row i of its first entry with column >= the start of
+// pass p + 1 (row columns sorted); the last pass ends at the row end (ppos row passes - 1 = -1).
+// Once per A: the scatter then reads a row's in-range sub-range instead of binary-searching it in
+// every pass (two dependent log2(deg) load chains per warp and pass, measured ~1/3 of the c4 scatter).
+__global__ void sampled_pass_bounds_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                           int64_t n, int passes, int32_t* __restrict__ ppos) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t e0 = rowptr[i], e1 = rowptr[i + 1];
+  int64_t a = e0;
+  for (int p = 0; p < passes; ++p) {
+    if (p == passes - 1) { ppos[(int64_t)p * n + i] = -1; break; }
+    const int32_t hi = (int32_t)(n * (p + 1) / passes);
+    int64_t b = e1;
+    while (a < b) { const int64_t m = (a + b) >> 1; if (col[m] < hi) a = m + 1; else b = m; }
+    ppos[(int64_t)p * n + i] = (int32_t)(a - e0);
+  }
+}
+
+void launch_sampled_pass_bounds(const symnmf_matrix& A, int k, int32_t* ppos, cudaStream_t st) {
+  const int passes = sampled_csr_passes(A.n, k);
+  if (passes > 1 && A.n > 0)
+    sampled_pass_bounds_kernel<<<(unsigned)((A.n + 255) / 256), 256, 0, st>>>(A.rowptr, A.colidx, A.n, passes, ppos);
+}
+
 void launch_sampled_csr_nozero(const symnmf_matrix& A, const float* F, int k, const int32_t* uniq, const double* w,
                                const int64_t* n_uniq_dev, int64_t cap, float* Y, const int32_t* status,
-                               cudaStream_t st) {
+                               cudaStream_t st, const int32_t* ppos) {
   const int grid = grid_for(std::max<int64_t>(cap, 1) * 32);
   if (k % 4 == 0) {
     const float4* F4 = reinterpret_cast<const float4*>(F);
@@ -209,19 +247,17 @@ void launch_sampled_csr_nozero(const symnmf_matrix& A, const float* F, int k, co
     // Destination-range passes: each pass scatters only into rows [c_lo, c_hi) of Y, a slice
     // small enough to stay resident in L2 (126 MB) while the pass's vector atomics land on it,
     // instead of read-modify-writes of random 128-byte lines of a Y larger than L2.
-    const int64_t ybytes = (int64_t)sizeof(float) * A.n * k;
-    const int64_t slice = scatter_slice_bytes();
-    const int passes = (int)std::max<int64_t>(1, (ybytes + slice - 1) / slice);
+    const int passes = sampled_csr_passes(A.n, k);
     const int split = scatter_split();
     for (int p = 0; p < passes; ++p) {
       const int32_t lo = (int32_t)(A.n * p / passes), hi = (int32_t)(A.n * (p + 1) / passes);
       const int ranged = passes > 1;
       switch (k / 4) {
-        case 1: launch_pdl(sampled_csr_v4<1>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, split, status); break;
-        case 2: launch_pdl(sampled_csr_v4<2>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, split, status); break;
-        case 4: launch_pdl(sampled_csr_v4<4>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, split, status); break;
-        case 8: launch_pdl(sampled_csr_v4<8>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, split, status); break;
-        case 16: launch_pdl(sampled_csr_v4<16>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, split, status); break;
+        case 1: launch_pdl(sampled_csr_v4<1>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, split, ppos, p, A.n, status); break;
+        case 2: launch_pdl(sampled_csr_v4<2>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, split, ppos, p, A.n, status); break;
+        case 4: launch_pdl(sampled_csr_v4<4>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, split, ppos, p, A.n, status); break;
+        case 8: launch_pdl(sampled_csr_v4<8>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, split, ppos, p, A.n, status); break;
+        case 16: launch_pdl(sampled_csr_v4<16>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, lo, hi, ranged, split, ppos, p, A.n, status); break;
         default: break;
       }
     }
