@@ -469,7 +469,11 @@ extern "C" symnmf_status symnmf_rangefinder_adaptive(const symnmf_matrix* A, int
   int32_t j = 0;
   for (;;) {
     ++j;
-    enqueue_dense_apply(*A, L.Q, l, L.Yb, precision, L, status, st);      // B^T = A^T Q = A Q
+    // B^T = A^T Q = A Q, always by the fp32 SIMT product: the residual trick subtracts ||B||^2 from
+    // ||A||^2, so a relative bias eps in B moves r by ~eps / r.  3xTF32 carries the tensor core's
+    // truncation bias (-1.6e-6, tc_gemm.cu), which at r = 5e-3 is a 3% error in r; round-to-
+    // nearest fp32 errors are unbiased and cancel in the fp64 sum of squares (reading R3).
+    enqueue_dense_apply(*A, L.Q, l, L.Yb, SYMNMF_FP32, L, status, st);
     launch_sumsq(L.Yb, n, l, l, sq_part, sq, status, st);                   // ||B||_F^2
     SYMNMF_CUDA_TRY(cudaMemcpyAsync(&b2, sq, sizeof(double), cudaMemcpyDeviceToHost, st));
     enqueue_orth(L, n, l, L.Yb, L.Q, status, st);                           // Q = qr(B^T)
@@ -939,7 +943,9 @@ bool enqueue_half(symnmf_solver& S, int side, cudaStream_t st) {
     }
     cudaStreamWaitEvent(st, S.ev_join[side], 0);
     // Update(G_s + alpha I, Y_s + alpha F^T); Y re-zeroed for the next scatter; X^T X and its R^{-1}
-    enqueue_sweep(S, side, S.Gs, F, X, true, Gnext, S.Rinv32, status, st);
+    // Y re-zeroed by the sweep for the next scatter (CSR); the dense sampled products write every
+    // row of Y themselves, so there the sweep leaves Y as is (k * 4 bytes per row less)
+    enqueue_sweep(S, side, S.Gs, F, X, S.A.kind == SYMNMF_CSR, Gnext, S.Rinv32, status, st);
     mark(S, st, S.bpp ? "bpp_update" : "hals_sweep");
   } else if (S.lai_fused) {
     // Y = U (Lambda U^T F), sweep, X^T X and Lambda U^T X for the next half, in one launch

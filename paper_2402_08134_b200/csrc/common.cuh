@@ -41,6 +41,19 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// ---------------------------------------------------------------- packed fp32 FMA (sm_100)
+// d = a * b + c on two lanes in one FFMA2 instruction (round to nearest, per lane identical to
+// fmaf).  The 3-register FFMA issues every other cycle per SM sub-partition (B300_MICROARCH.md:
+// rt_SMSP = 2), so the FMA-heavy SIMT loops (sweep, scores) double their FMA issue rate with it.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+
 // ---------------------------------------------------------------- cp.async (16 B, L2 only; zero-fill when !ok)
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool ok) {
   const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(FT, KP <= 32 ? 2 : 1) sweep_fused(const double
                                                   unsigned int* counter, int32_t* status) {
   constexpr int ST = KP + 4;
   constexpr int Q = KP / 4;       // float4 per lane per array (32-row warp tile)
-  __shared__ __align__(16) float sG[KP * KP];     // sG[i*KP + j] = G[j][i], 0 on the diagonal
+  __shared__ __align__(16) float sG[KP * KP];     // sG[i*KP + j] = -G[j][i], 0 on the diagonal
   __shared__ float sInv[KP];
   __shared__ int sOk[KP];
   extern __shared__ __align__(16) unsigned char smw[];
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(FT, KP <= 32 ? 2 : 1) sweep_fused(const double
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   for (int e = tid; e < KP * KP; e += FT) {
     const int i = e / KP, j = e - i * KP;
-    sG[e] = (i < k && j < k && i != j) ? (float)G[j * k + i] : 0.f;
+    sG[e] = (i < k && j < k && i != j) ? -(float)G[j * k + i] : 0.f;
   }
   for (int i = tid; i < KP; i += FT) {
     const double den = i < k ? G[i * k + i] + alpha : 0.0;
@@ -140,33 +140,34 @@ __global__ void __launch_bounds__(FT, KP <= 32 ? 2 : 1) sweep_fused(const double
     }
     __syncwarp();
     if (lane < cnt) {
-      float x[KP];   // b = Y + alpha F stays in shared memory (read once per column)
+      float2 x[KP / 2];   // column pairs (packed FFMA2); b = Y + alpha F stays in shared memory
       const float* brow = wB + lane * ST;
 #pragma unroll
       for (int j = 0; j < KP; j += 4) {
         const float4 xv = *reinterpret_cast<const float4*>(wX + lane * ST + j);
-        x[j] = xv.x; x[j + 1] = xv.y; x[j + 2] = xv.z; x[j + 3] = xv.w;
+        x[j / 2] = make_float2(xv.x, xv.y); x[j / 2 + 1] = make_float2(xv.z, xv.w);
       }
 #pragma unroll
       for (int i = 0; i < KP; ++i) {
         if (i < k) {
-          // four independent partial sums: the column update is a short dependency chain
-          float s0 = brow[i], s1 = 0.f, s2 = 0.f, s3 = 0.f;
+          // two independent packed partial sums: the column update is a short dependency chain
+          float2 s01 = make_float2(brow[i], 0.f), s23 = make_float2(0.f, 0.f);
 #pragma unroll
           for (int j = 0; j < KP; j += 4) {
             const float4 g = *reinterpret_cast<const float4*>(sG + i * KP + j);
-            s0 = fmaf(-x[j], g.x, s0);
-            s1 = fmaf(-x[j + 1], g.y, s1);
-            s2 = fmaf(-x[j + 2], g.z, s2);
-            s3 = fmaf(-x[j + 3], g.w, s3);
+            s01 = ffma2(x[j / 2], make_float2(g.x, g.y), s01);
+            s23 = ffma2(x[j / 2 + 1], make_float2(g.z, g.w), s23);
           }
-          const float s = (s0 + s1) + (s2 + s3);
-          if (sOk[i]) x[i] = fmaxf(0.f, s * sInv[i]);
+          const float s = (s01.x + s01.y) + (s23.x + s23.y);
+          if (sOk[i]) {
+            const float v = fmaxf(0.f, s * sInv[i]);
+            if (i & 1) x[i / 2].y = v; else x[i / 2].x = v;
+          }
         }
       }
 #pragma unroll
       for (int j = 0; j < KP; j += 4)
-        *reinterpret_cast<float4*>(wX + lane * ST + j) = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
+        *reinterpret_cast<float4*>(wX + lane * ST + j) = make_float4(x[j / 2].x, x[j / 2].y, x[j / 2 + 1].x, x[j / 2 + 1].y);
     } else {
 #pragma unroll
       for (int j = 0; j < KP; j += 4)
@@ -290,12 +291,12 @@ __global__ void __launch_bounds__(FT, TAB >= 0 && KP <= 32 ? 3 : 1) leverage_fus
       __syncthreads();
     }
     if (tid < rows) {
-      float f[KP];
+      float2 f[KP / 2];   // column pairs: the substitution runs on packed FFMA2
 #pragma unroll
       for (int a = 0; a < KP; a += 4) {
         const float4 v = full ? *reinterpret_cast<const float4*>(cur + tid * KP + 4 * lev_swz<KP>(a / 4, tid))
                               : *reinterpret_cast<const float4*>(sF + tid * (KP + 4) + a);
-        f[a] = v.x; f[a + 1] = v.y; f[a + 2] = v.z; f[a + 3] = v.w;
+        f[a / 2] = make_float2(v.x, v.y); f[a / 2 + 1] = make_float2(v.z, v.w);
       }
       // q = f R^{-1} by forward substitution q R = f (R upper, rd = 1 / diag R), l = ||q||^2.
       // Row a of R is read as float4 groups from the aligned group holding column a: entries
@@ -305,13 +306,14 @@ __global__ void __launch_bounds__(FT, TAB >= 0 && KP <= 32 ? 3 : 1) leverage_fus
       float l = 0.f;
 #pragma unroll
       for (int a = 0; a < KP; ++a) {
-        const float q = f[a] * rsrc.rd(a);
+        const float q = ((a & 1) ? f[a / 2].y : f[a / 2].x) * rsrc.rd(a);
         l = fmaf(q, q, l);
+        const float2 nq = make_float2(-q, -q);
 #pragma unroll
         for (int c = (a + 1) & ~3; c < KP; c += 4) {
           const float4 r4 = rsrc.r4(a, c);
-          f[c] = fmaf(-q, r4.x, f[c]); f[c + 1] = fmaf(-q, r4.y, f[c + 1]);
-          f[c + 2] = fmaf(-q, r4.z, f[c + 2]); f[c + 3] = fmaf(-q, r4.w, f[c + 3]);
+          f[c / 2] = ffma2(nq, make_float2(r4.x, r4.y), f[c / 2]);
+          f[c / 2 + 1] = ffma2(nq, make_float2(r4.z, r4.w), f[c / 2 + 1]);
         }
       }
       lev[r0 + tid] = l;

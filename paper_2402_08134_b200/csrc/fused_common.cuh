@@ -174,11 +174,14 @@ struct GramThread {
       const float4 b4 = *reinterpret_cast<const float4*>(s + r * stride + 4 * bi);
       const float wr = w ? w[r] : 1.f;
       const float a[4] = {a4.x * wr, a4.y * wr, a4.z * wr, a4.w * wr};
-      const float b[4] = {b4.x, b4.y, b4.z, b4.w};
+      const float2 b01 = make_float2(b4.x, b4.y), b23 = make_float2(b4.z, b4.w);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i * 4 + j] = fmaf(a[i], b[j], acc[i * 4 + j]);
+      for (int i = 0; i < 4; ++i) {   // packed FFMA2 over column pairs
+        float2 p0 = make_float2(acc[i * 4], acc[i * 4 + 1]), p1 = make_float2(acc[i * 4 + 2], acc[i * 4 + 3]);
+        p0 = ffma2(make_float2(a[i], a[i]), b01, p0);
+        p1 = ffma2(make_float2(a[i], a[i]), b23, p1);
+        acc[i * 4] = p0.x; acc[i * 4 + 1] = p0.y; acc[i * 4 + 2] = p1.x; acc[i * 4 + 3] = p1.y;
+      }
     }
     since += (rows + RG - 1) / RG;
     if (since >= 64) flush();

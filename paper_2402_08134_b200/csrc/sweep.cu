@@ -28,7 +28,7 @@ struct SwL {
   static constexpr int per_sm = KP <= 8 ? 3 : 2;   // 128 registers per thread for k = 16, 32
 };
 
-// Constant-bank copies of the sweep's G (G_off^T, 1 / (G_ii + alpha), ok flags), one per (solver
+// Constant-bank copies of the sweep's G (-G_off^T, 1 / (G_ii + alpha), ok flags), one per (solver
 // slot, half): with G in the constant bank every FMA of the column loop takes its G operand
 // straight from the constant cache (no shared-memory loads, no load-to-use latency).  Written by
 // a D2D copy to the symbol (captured in the solver's graph) right before each sweep.
@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
   constexpr int C = L::C, TR = L::TR;
   constexpr int NB = KP / 4, PAIRS = NB * (NB + 1) / 2, RG = TR / PAIRS;
   constexpr int ST = L::ST;
-  __shared__ __align__(16) float sG[TAB < 0 ? KP * KP : 4];   // sG[i*KP + j] = G[j][i], 0 on the diagonal
+  __shared__ __align__(16) float sG[TAB < 0 ? KP * KP : 4];   // sG[i*KP + j] = -G[j][i], 0 on the diagonal
   __shared__ float sInv[KP];
   __shared__ int sOk[KP];
   extern __shared__ __align__(16) unsigned char sms[];
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
   if constexpr (TAB < 0) {
     for (int e = tid; e < KP * KP; e += TR) {
       const int i = e / KP, j = e - i * KP;
-      sG[e] = (i != j) ? (float)G[j * KP + i] : 0.f;
+      sG[e] = (i != j) ? -(float)G[j * KP + i] : 0.f;
     }
     for (int i = tid; i < KP; i += TR) {
       const double den = G[i * KP + i] + alpha;
@@ -125,14 +125,15 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
       float4* Y4 = reinterpret_cast<float4*>(Y) + r0 * C;
       for (int q = tid; q < rows * C; q += TR) __stcs(Y4 + q, make_float4(0.f, 0.f, 0.f, 0.f));
     }
-    float x[KP];
+    // x in column pairs: the column loop runs on packed FFMA2 (two FMAs per instruction)
+    float2 x2[KP / 2];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       const float4 x4 = *reinterpret_cast<const float4*>(sX + tid * ST + 4 * c);
-      x[4 * c] = x4.x; x[4 * c + 1] = x4.y; x[4 * c + 2] = x4.z; x[4 * c + 3] = x4.w;
+      x2[2 * c] = make_float2(x4.x, x4.y); x2[2 * c + 1] = make_float2(x4.z, x4.w);
     }
     // Gauss-Seidel over the columns of row tid: x_i <- [(b_i - sum_{j != i} G_ij x_j) / (G_ii + alpha)]_+,
-    // b = y + alpha f read a 16 B chunk at a time
+    // b = y + alpha f read a 16 B chunk at a time; the table holds -G so every step is an FMA
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       const int so = tid * ST + 4 * c;
@@ -143,24 +144,26 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int i = 4 * c + u;
-        float s0 = bc[u], s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        float2 s01 = make_float2(bc[u], 0.f), s23 = make_float2(0.f, 0.f);
 #pragma unroll
         for (int j = 0; j < KP; j += 4) {
           const float4 g = gsrc.g4(i, j);
-          s0 = fmaf(-x[j], g.x, s0);
-          s1 = fmaf(-x[j + 1], g.y, s1);
-          s2 = fmaf(-x[j + 2], g.z, s2);
-          s3 = fmaf(-x[j + 3], g.w, s3);
+          s01 = ffma2(x2[j / 2], make_float2(g.x, g.y), s01);
+          s23 = ffma2(x2[j / 2 + 1], make_float2(g.z, g.w), s23);
         }
-        const float sv = (s0 + s1) + (s2 + s3);
-        if (gsrc.okd(i)) x[i] = fmaxf(0.f, sv * gsrc.invd(i));
+        const float sv = (s01.x + s01.y) + (s23.x + s23.y);
+        if (gsrc.okd(i)) {
+          const float v = fmaxf(0.f, sv * gsrc.invd(i));
+          if (i & 1) x2[i / 2].y = v; else x2[i / 2].x = v;
+        }
       }
     }
     const bool live = tid < rows;
 #pragma unroll
     for (int c = 0; c < C; ++c)   // the new row replaces the old one in the staging tile
       *reinterpret_cast<float4*>(sX + tid * ST + 4 * c) =
-          live ? make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+          live ? make_float4(x2[2 * c].x, x2[2 * c].y, x2[2 * c + 1].x, x2[2 * c + 1].y)
+               : make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
     {
       float4* X4 = reinterpret_cast<float4*>(X) + r0 * C;
@@ -170,27 +173,29 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
       }
     }
     if (gactive) {   // tile Gram of the new rows
-      float acc[16];
+      float2 acc[8];   // acc[i * 2 + p] = entries (4 ai + i, 4 bi + 2p .. 2p + 1)
 #pragma unroll
-      for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+      for (int e = 0; e < 8; ++e) acc[e] = make_float2(0.f, 0.f);
       const float* pa = sX + gg * ST + 4 * ai;
       const float* pb = sX + gg * ST + 4 * bi;
       int r = gg;
       auto step = [&](int o) {
         const float4 a4 = *reinterpret_cast<const float4*>(pa + o);
         const float4 b4 = *reinterpret_cast<const float4*>(pb + o);
-        const float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
+        const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+        const float2 b01 = make_float2(b4.x, b4.y), b23 = make_float2(b4.z, b4.w);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i * 4 + j] = fmaf(av[i], bv[j], acc[i * 4 + j]);
+        for (int i = 0; i < 4; ++i) {
+          acc[i * 2] = ffma2(make_float2(av[i], av[i]), b01, acc[i * 2]);
+          acc[i * 2 + 1] = ffma2(make_float2(av[i], av[i]), b23, acc[i * 2 + 1]);
+        }
       };
       for (; r + 3 * RG < rows; r += 4 * RG, pa += 4 * RG * ST, pb += 4 * RG * ST) {
         step(0); step(RG * ST); step(2 * RG * ST); step(3 * RG * ST);
       }
       for (; r < rows; r += RG, pa += RG * ST, pb += RG * ST) step(0);
 #pragma unroll
-      for (int e = 0; e < 16; ++e) acc64[e] += (double)acc[e];
+      for (int e = 0; e < 8; ++e) { acc64[2 * e] += (double)acc[e].x; acc64[2 * e + 1] += (double)acc[e].y; }
     }
     __syncthreads();   // staging tile free for the next tile
   }
@@ -219,14 +224,14 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
   }
 }
 
-// fp32 table of the sweep's G for the constant bank: G_off^T (zero diagonal), 1 / (G_ii + alpha), ok
+// fp32 table of the sweep's G for the constant bank: -G_off^T (zero diagonal), 1 / (G_ii + alpha), ok
 template <int KP>
 __global__ void sweep_table(const double* __restrict__ G, double alpha, float* __restrict__ out,
                             const int32_t* __restrict__ status) {
   if (dev_failed(status)) return;
   for (int e = threadIdx.x; e < KP * KP; e += blockDim.x) {
     const int i = e / KP, j = e - i * KP;
-    out[e] = (i != j) ? (float)G[j * KP + i] : 0.f;
+    out[e] = (i != j) ? -(float)G[j * KP + i] : 0.f;
   }
   for (int i = threadIdx.x; i < KP; i += blockDim.x) {
     const double den = G[i * KP + i] + alpha;

@@ -669,9 +669,10 @@ def test_adaptive_rangefinder_vs_oracle(precision):
     M = S.DeviceMatrix.from_host(A)
     U, lam, passes, res = S.rangefinder_adaptive(M, 40, 8, seed=4, tol=1e-3, precision=precision)
     Uo, lamo, Qo, po, reso = O.rangefinder_adaptive(A, 40, 8, seed=4, tol=1e-3)
-    # the trick r^2 = 1 - ||B||^2 / ||A||^2 cancels: a relative product error eps (<= 1e-5, the
-    # bound the 3xTF32 / fp32 product tests assert) moves r by about eps / r
-    dr = [max(1e-5, 1e-5 / b_) for b_ in reso]
+    # the trick r^2 = 1 - ||B||^2 / ||A||^2 cancels: a relative bias eps in ||B||^2 moves r by
+    # ~eps / (2 r).  B is formed by the fp32 SIMT product in both precisions (reading R3): its
+    # round-to-nearest errors are unbiased and cancel in the fp64 sum, so r is held to 0.2% relative
+    dr = [2e-3 * b_ for b_ in reso]
     margins = [abs((reso[i] - reso[i + 1]) - 1e-3) - dr[i] - dr[i + 1] for i in range(len(reso) - 1)]
     if not margins or min(margins) > 0:
         assert passes == po
