@@ -312,7 +312,7 @@ extern "C" symnmf_status symnmf_sampled_ah(const symnmf_matrix* A, const float* 
   if (bad_matrix(A) || !F || !Y || bad_k(k) || bad_plan(plan)) return SYMNMF_ERR_ARG;
   const int grid = gram_grid(std::min<int64_t>(plan->cap, A->n));
   const int64_t cap = std::min<int64_t>(plan->cap, A->n);
-  const size_t sbs_bytes = (A->kind == SYMNMF_DENSE && sampled_dense_tc_enabled() &&
+  const size_t sbs_bytes = (A->kind == SYMNMF_DENSE && sampled_dense_tc_enabled(A->n) &&
                             sampled_dense_tc_supported(A->val, A->lda, A->n, k))
                                ? sampled_dense_tc_scratch(cap, k)
                                : 0;
@@ -856,7 +856,7 @@ void solver_layout(symnmf_solver& S, Carver& c) {
     S.plan.uniq_w = c.take<double>(n);
     S.plan.counts = c.take<int64_t>(4);
     S.plan.mass = c.take<double>(2);
-    S.sbs_bytes = (S.hasA && S.A.kind == SYMNMF_DENSE && sampled_dense_tc_enabled() &&
+    S.sbs_bytes = (S.hasA && S.A.kind == SYMNMF_DENSE && sampled_dense_tc_enabled(n) &&
                    sampled_dense_tc_supported(S.A.val, S.A.lda, n, k))
                       ? sampled_dense_tc_scratch(S.plan.cap, k)
                       : 0;

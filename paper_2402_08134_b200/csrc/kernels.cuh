@@ -76,7 +76,7 @@ bool launch_dense_ah_tc(const float* A, int64_t lda, int64_t n, const float* F, 
 size_t dense_ah_tc_scratch(int64_t n, int k);
 // tcgen05 3xTF32 sampled dense product (tc_sampled.cu): k <= 64, lda % 4 == n % 4 == 0, A 16-B aligned;
 // scratch: sampled_dense_tc_scratch(cap, k) bytes.
-bool sampled_dense_tc_enabled();
+bool sampled_dense_tc_enabled(int64_t n);
 bool sampled_dense_tc_supported(const float* A, int64_t lda, int64_t n, int k);
 size_t sampled_dense_tc_scratch(int64_t cap, int k);
 void launch_sampled_dense_tc(const float* A, int64_t lda, int64_t n, const float* F, int k, const int32_t* uniq,

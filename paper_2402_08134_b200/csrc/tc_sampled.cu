@@ -287,10 +287,14 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
 static int sb_np(int k) { return k <= 16 ? 16 : k <= 32 ? 32 : 64; }
 static int64_t sb_ldu(int64_t cap) { return (cap + SB_BK - 1) / SB_BK * SB_BK; }
 
-// SYMNMF_SAMPLED_DENSE=simt selects the fp32 SIMT kernel (dense.cu) instead (symnmf.h).
-bool sampled_dense_tc_enabled() {
+// SYMNMF_SAMPLED_DENSE=simt selects the fp32 SIMT kernel (dense.cu), =tc this one wherever it applies;
+// by default this one from n = 16384 (c1, n = 1,000: the SIMT kernel's single launch is faster than the
+// split + zero + tensor-core launches, 10.4k vs 11.9k LvS it/s) (symnmf.h).
+bool sampled_dense_tc_enabled(int64_t n) {
   const char* e = getenv("SYMNMF_SAMPLED_DENSE");
-  return !(e && !strcmp(e, "simt"));
+  if (e && !strcmp(e, "simt")) return false;
+  if (e && !strcmp(e, "tc")) return true;
+  return n >= 16384;
 }
 
 size_t sampled_dense_tc_scratch(int64_t cap, int k) {

@@ -191,11 +191,10 @@ def test_sampled_dense(c1):
 @pytest.mark.parametrize("path", ["tc", "simt"])
 def test_sampled_dense_paths(n, k, s, path, monkeypatch):
     """Sampled dense product Y_s = A[U,:]^T (Omega F[U]): the tcgen05 3xTF32 kernel
-    (tc_sampled.cu, default for n % 4 == 0, k <= 64) and the fp32 SIMT kernel (SYMNMF_SAMPLED_DENSE=
-    simt) vs the oracle.  Ragged output tiles (n % 128 != 0), n % 4 != 0 (SIMT fallback), |U| from
+    (tc_sampled.cu, SYMNMF_SAMPLED_DENSE=tc; the default from n = 16384 when n % 4 == 0, k <= 64) and
+    the fp32 SIMT kernel (=simt) vs the oracle.  Ragged output tiles (n % 128 != 0), n % 4 != 0 (SIMT fallback), |U| from
     < 32 (one partial k-block) to the c3 budget (s = 3,000: U split over the grid)."""
-    if path == "simt":
-        monkeypatch.setenv("SYMNMF_SAMPLED_DENSE", "simt")
+    monkeypatch.setenv("SYMNMF_SAMPLED_DENSE", path)
     A = sym_dense(n, n + 7 * k)
     F = random_factor(n, k, 11) ** 2
     plan, o = _plan_for(F, k, s, 1.0 / s, seed=3, it=1, side=0)
@@ -208,12 +207,14 @@ def test_sampled_dense_all_rows_equals_exact():
     """Every row deterministic (tau below every p_i): U = all n rows, Omega = 1, so the tensor-core
     sampled product is A F (P:716-719 with I_D = all rows)."""
     n, k = 2_500, 16
+    os.environ["SYMNMF_SAMPLED_DENSE"] = "tc"
     A = sym_dense(n, 5)
     F = random_factor(n, k, 12)
     lev = S.leverage_scores(cu(F))
     tau = float(lev.min().item()) / k * 0.5
     plan = S.hybrid_sample(lev, k, 10, tau, 0, 0, 0)
     Y, _ = S.sampled_ah(S.DeviceMatrix.from_host(A), cu(F), plan)
+    os.environ.pop("SYMNMF_SAMPLED_DENSE")
     assert plan.to_host()["n_uniq"] == n
     assert rel(Y.cpu().numpy(), O.ah(A, F)) < 1e-5
 

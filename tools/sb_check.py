@@ -1,5 +1,5 @@
-"""Quick check of the tensor-core sampled dense product against the oracle (both descriptor
-readings of the MN-major atom strides), before the full parity tests."""
+"""Quick check of both sampled dense products (tensor-core and SIMT) against the oracle, before the
+full parity tests."""
 import os
 import sys
 
@@ -26,9 +26,7 @@ for n, k, s in [(1000, 8, 200), (3000, 32, 1500), (2052, 64, 700)]:
     o = O.build_plan(lev, k, s, 1.0 / s, 3, 1, 0)
     Gr, Yr = O.sampled_products(A, F, o["uniq_idx"], o["uniq_w"])
     M = S.DeviceMatrix.from_host(A)
-    for env in ({}, {"SYMNMF_SB_DESC_SWAP": "1"}, {"SYMNMF_SAMPLED_DENSE": "simt"}):
-        for kk in ("SYMNMF_SB_DESC_SWAP", "SYMNMF_SAMPLED_DENSE"):
-            os.environ.pop(kk, None)
+    for env in ({"SYMNMF_SAMPLED_DENSE": "tc"}, {"SYMNMF_SAMPLED_DENSE": "simt"}):
         os.environ.update(env)
         try:
             Y, _ = S.sampled_ah(M, torch.from_numpy(F).cuda(), plan)
