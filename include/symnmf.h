@@ -122,6 +122,9 @@ typedef struct {
  *                                  pass (default 86 MB, so each pass's slice of Y stays in L2).
  *   SYMNMF_SCATTER_SPLIT=<w>       sampled CSR scatter product: warps per sampled row and pass (each
  *                                  takes a contiguous part of the row's in-range nonzeros; default 4).
+ *   SYMNMF_YALPHA=0                LvS on CSR with the streaming sweep: re-zero Y for each scatter and
+ *                                  read F in the sweep, instead of the scatter accumulating onto
+ *                                  Y = alpha F left by the previous sweep (state kept across runs).
  *   SYMNMF_SAMPLED_DENSE=simt|tc   sampled dense product: the fp32 SIMT kernel, or the tcgen05 3xTF32
  *                                  one (k <= 64, n % 4 == lda % 4 == 0); default: tcgen05 from n = 16384.
  *   SYMNMF_LAI_FUSED=never         LAI solver (k = 64, l <= 80): use the four-kernel half (U^T F,

@@ -699,6 +699,7 @@ struct symnmf_solver {
   bool bpp;                // Update rule: exact per-row NLS by block principal pivoting (NEXT-1)
   int32_t* nonconv;        // BPP rows that hit the pivoting cap (device counter)
   int32_t* ppos;           // LvS on CSR: per-row boundaries of the scatter's destination passes
+  bool yalpha;             // LvS on CSR, streaming sweep: Y carries alpha F between halves (sweep.cu)
   void* sbs;               // LvS on dense A: scratch of the tensor-core sampled product (tc_sampled.cu)
   size_t sbs_bytes;
   bool nnzsp;              // EXACT on CSR (kpad(k) == k): the nnz-balanced SpMM (spmm_nnz.cu)
@@ -781,9 +782,15 @@ void enqueue_sweep(const symnmf_solver& S, int side, const double* G, const floa
   }
   if (sweep_stream_supported(S.k) && sweep_stream_enabled(S.n))
     launch_sweep_stream(G, S.alpha, S.Y, F, X, S.n, S.k, zeroY, S.Gacc, Gnext, Rf32, S.counter, status, st,
-                        S.cslot >= 0 ? 2 * S.cslot + side : -1, S.ctab);
+                        S.cslot >= 0 ? 2 * S.cslot + side : -1, S.ctab, S.yalpha && zeroY);
   else
     launch_sweep_fused(G, S.alpha, S.Y, F, X, S.n, S.k, zeroY, S.Gacc, Gnext, Rf32, S.counter, status, st);
+}
+
+// LvS on CSR: Y carries alpha F between halves (default) or is re-zeroed (SYMNMF_YALPHA=0, symnmf.h)
+bool yalpha_enabled() {
+  const char* e = getenv("SYMNMF_YALPHA");
+  return !(e && !strcmp(e, "0"));
 }
 
 // LAI: the fused one-launch half (k = 64, l <= 80); SYMNMF_LAI_FUSED=never disables it (symnmf.h)
@@ -1041,7 +1048,13 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
                       st);
     launch_scale_rows(S.Z, S.l, k, S.lam, S.Mside[0], S.status, st);
   }
-  if (mode == SYMNMF_LVS && S.Y) SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Y, 0, sizeof(float) * n * k, st));
+  // LvS on CSR with the streaming sweep: the scatter accumulates onto Y = alpha F (the first half's
+  // F is H) and each sweep leaves alpha X for the next half, so the sweep never reads F; the solver
+  // keeps this state across run calls, as it keeps F^T F (W and H are the solver's between runs)
+  S.yalpha = mode == SYMNMF_LVS && S.hasA && S.A.kind == SYMNMF_CSR && !S.bpp && sweep_stream_supported(k) &&
+             sweep_stream_enabled(n) && yalpha_enabled();
+  if (S.yalpha) launch_scale_copy(H, alpha, S.Y, n * k, st);
+  else if (mode == SYMNMF_LVS && S.Y) SYMNMF_CUDA_TRY(cudaMemsetAsync(S.Y, 0, sizeof(float) * n * k, st));
   if (S.hasA && S.A.kind == SYMNMF_CSR) {
     // every sparse path assumes each row's columns sorted, unique and in range (the destination
     // ranges of the sampled scatter binary-search them)

@@ -157,7 +157,9 @@ void launch_csr_check(const symnmf_matrix& A, int32_t* bad, cudaStream_t st);
 bool sweep_stream_supported(int k);
 void launch_sweep_stream(const double* G, double alpha, float* Y, const float* F, float* X, int64_t n, int k,
                          bool zeroY, double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
-                         cudaStream_t st, int tab = -1, float* scratch = nullptr);
+                         cudaStream_t st, int tab = -1, float* scratch = nullptr, bool yalpha = false);
+// Y = alpha F (count floats, count % 4 == 0)
+void launch_scale_copy(const float* F, double alpha, float* Y, int64_t count, cudaStream_t st);
 int sweep_cslot_acquire();
 void sweep_cslot_release(int slot);
 size_t sweep_table_floats();

@@ -57,8 +57,12 @@ struct SwG {   // G source: TAB < 0 -> shared memory, else constant table TAB
 template <int KP, int TAB = -1>
 __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
     const double* __restrict__ G, double alpha, float* __restrict__ Y, const float* __restrict__ F,
-    float* __restrict__ X, int64_t n, int zeroY, double* Gacc, double* Gout, float* Rf32, unsigned int* counter,
+    float* __restrict__ X, int64_t n, int ymode, double* Gacc, double* Gout, float* Rf32, unsigned int* counter,
     int32_t* status) {
+  // ymode 0: Y read only; 1: Y re-zeroed for the next scatter; 2: Y holds Y_s + alpha F already (the
+  // scatter accumulated onto alpha F), so F is not read, and Y is left as alpha X for the next half,
+  // whose fixed factor X is (LvS on CSR: 4nk bytes less per half)
+  const bool yalpha = ymode == 2;
   using L = SwL<KP>;
   constexpr int C = L::C, TR = L::TR;
   constexpr int NB = KP / 4, PAIRS = NB * (NB + 1) / 2, RG = TR / PAIRS;
@@ -115,13 +119,13 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
       const int so = r * ST + 4 * c;
       const int64_t go = ok ? (r0 + r) * KP + 4 * c : 0;
       cp_async16(sY + so, Y + go, ok);
-      cp_async16(sF + so, F + go, ok);
+      if (!yalpha) cp_async16(sF + so, F + go, ok);
       cp_async16(sX + so, X + go, ok);
     }
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    if (zeroY) {
+    if (ymode == 1) {
       float4* Y4 = reinterpret_cast<float4*>(Y) + r0 * C;
       for (int q = tid; q < rows * C; q += TR) __stcs(Y4 + q, make_float4(0.f, 0.f, 0.f, 0.f));
     }
@@ -138,7 +142,7 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
     for (int c = 0; c < C; ++c) {
       const int so = tid * ST + 4 * c;
       const float4 y4 = *reinterpret_cast<const float4*>(sY + so);
-      const float4 f4 = *reinterpret_cast<const float4*>(sF + so);
+      const float4 f4 = yalpha ? make_float4(0.f, 0.f, 0.f, 0.f) : *reinterpret_cast<const float4*>(sF + so);
       const float bc[4] = {fmaf(a32, f4.x, y4.x), fmaf(a32, f4.y, y4.y), fmaf(a32, f4.z, y4.z),
                            fmaf(a32, f4.w, y4.w)};
 #pragma unroll
@@ -167,9 +171,12 @@ __global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
     __syncthreads();
     {
       float4* X4 = reinterpret_cast<float4*>(X) + r0 * C;
+      float4* Y4 = reinterpret_cast<float4*>(Y) + r0 * C;
       for (int q = tid; q < rows * C; q += TR) {
         const int r = q / C, c = q - r * C;
-        X4[q] = *reinterpret_cast<const float4*>(sX + r * ST + 4 * c);
+        const float4 v = *reinterpret_cast<const float4*>(sX + r * ST + 4 * c);
+        X4[q] = v;
+        if (yalpha) __stcs(Y4 + q, make_float4(a32 * v.x, a32 * v.y, a32 * v.z, a32 * v.w));
       }
     }
     if (gactive) {   // tile Gram of the new rows
@@ -241,7 +248,7 @@ __global__ void sweep_table(const double* __restrict__ G, double alpha, float* _
 }
 
 template <int KP, int TAB>
-static void sweep_stream_t(const double* G, double alpha, float* Y, const float* F, float* X, int64_t n, bool zeroY,
+static void sweep_stream_t(const double* G, double alpha, float* Y, const float* F, float* X, int64_t n, int ymode,
                            double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
                            cudaStream_t st) {
   using L = SwL<KP>;
@@ -249,11 +256,25 @@ static void sweep_stream_t(const double* G, double alpha, float* Y, const float*
   const int64_t tiles = (n + L::TR - 1) / L::TR;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * L::per_sm));
   cudaFuncSetAttribute(sweep_stream<KP, TAB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  launch_pdl(sweep_stream<KP, TAB>, grid, L::TR, smem, st, G, alpha, Y, F, X, n, zeroY ? 1 : 0, Gacc, Gout, Rf32,
+  launch_pdl(sweep_stream<KP, TAB>, grid, L::TR, smem, st, G, alpha, Y, F, X, n, ymode, Gacc, Gout, Rf32,
              counter, status);
 }
 
 bool sweep_stream_supported(int k) { return k == 8 || k == 16 || k == 32; }
+
+// Y = alpha F (the invariant the yalpha sweep keeps for LvS on CSR, set at solver creation)
+__global__ void scale_copy_kernel(const float4* __restrict__ F4, float a, float4* __restrict__ Y4, int64_t n4) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = F4[i];
+    Y4[i] = make_float4(a * v.x, a * v.y, a * v.z, a * v.w);
+  }
+}
+void launch_scale_copy(const float* F, double alpha, float* Y, int64_t count, cudaStream_t st) {
+  const int64_t n4 = count / 4;
+  if (n4 > 0)
+    scale_copy_kernel<<<(unsigned)std::min<int64_t>((n4 + 255) / 256, 148 * 8), 256, 0, st>>>(
+        reinterpret_cast<const float4*>(F), (float)alpha, reinterpret_cast<float4*>(Y), n4);
+}
 
 // Constant-table slots: a solver takes one for its lifetime (two tables, one per half).
 static std::atomic<unsigned> g_cslots{0};
@@ -273,12 +294,12 @@ size_t sweep_table_floats() { return kCTab; }
 
 template <int KP>
 static void sweep_tab_dispatch(int tab, const double* G, double alpha, float* Y, const float* F, float* X, int64_t n,
-                               bool zeroY, double* Gacc, double* Gout, float* Rf32, unsigned int* counter,
+                               int ymode, double* Gacc, double* Gout, float* Rf32, unsigned int* counter,
                                int32_t* status, cudaStream_t st) {
-#define SW_CASE(T) case T: sweep_stream_t<KP, T>(G, alpha, Y, F, X, n, zeroY, Gacc, Gout, Rf32, counter, status, st); break;
+#define SW_CASE(T) case T: sweep_stream_t<KP, T>(G, alpha, Y, F, X, n, ymode, Gacc, Gout, Rf32, counter, status, st); break;
   switch (tab) {
     SW_CASE(0) SW_CASE(1) SW_CASE(2) SW_CASE(3) SW_CASE(4) SW_CASE(5) SW_CASE(6) SW_CASE(7)
-    default: sweep_stream_t<KP, -1>(G, alpha, Y, F, X, n, zeroY, Gacc, Gout, Rf32, counter, status, st); break;
+    default: sweep_stream_t<KP, -1>(G, alpha, Y, F, X, n, ymode, Gacc, Gout, Rf32, counter, status, st); break;
   }
 #undef SW_CASE
 }
@@ -287,7 +308,8 @@ static void sweep_tab_dispatch(int tab, const double* G, double alpha, float* Y,
 // copied to the constant bank first; tab < 0: G staged in shared memory.
 void launch_sweep_stream(const double* G, double alpha, float* Y, const float* F, float* X, int64_t n, int k,
                          bool zeroY, double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
-                         cudaStream_t st, int tab, float* scratch) {
+                         cudaStream_t st, int tab, float* scratch, bool yalpha) {
+  const int ymode = yalpha ? 2 : zeroY ? 1 : 0;
   if (tab >= 0) {
     const int kp = k;
     switch (kp) {
@@ -299,9 +321,9 @@ void launch_sweep_stream(const double* G, double alpha, float* Y, const float* F
                             cudaMemcpyDeviceToDevice, st);
   }
   switch (k) {
-    case 8: sweep_tab_dispatch<8>(tab, G, alpha, Y, F, X, n, zeroY, Gacc, Gout, Rf32, counter, status, st); break;
-    case 16: sweep_tab_dispatch<16>(tab, G, alpha, Y, F, X, n, zeroY, Gacc, Gout, Rf32, counter, status, st); break;
-    default: sweep_tab_dispatch<32>(tab, G, alpha, Y, F, X, n, zeroY, Gacc, Gout, Rf32, counter, status, st); break;
+    case 8: sweep_tab_dispatch<8>(tab, G, alpha, Y, F, X, n, ymode, Gacc, Gout, Rf32, counter, status, st); break;
+    case 16: sweep_tab_dispatch<16>(tab, G, alpha, Y, F, X, n, ymode, Gacc, Gout, Rf32, counter, status, st); break;
+    default: sweep_tab_dispatch<32>(tab, G, alpha, Y, F, X, n, ymode, Gacc, Gout, Rf32, counter, status, st); break;
   }
 }
 

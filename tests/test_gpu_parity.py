@@ -519,16 +519,20 @@ def test_csr_tile_exact_one_iteration(cfgname, n, k, tile, monkeypatch):
 
 
 @pytest.mark.parametrize("cfgname,n,k,s", [("c4", 40_000, 32, 800), ("c2", 20_000, 16, 400), ("c4", 40_000, 8, 2000)])
-@pytest.mark.parametrize("slice_mb", ["", "1", "stream"])
+@pytest.mark.parametrize("slice_mb", ["", "1", "stream", "stream1", "stream_zero"])
 def test_csr_lvs_solver_equals_abi_composition(cfgname, n, k, s, slice_mb, monkeypatch):
     """Solver LvS on CSR graphs with hubs (vector-atomic scatter of the sampled product, fused Gram)
     equals the composition of the ABI calls on the same device data; slice_mb = 1 forces several
     destination-range passes of the sampled scatter, "stream" the streaming sweep with G and R in
-    the constant bank (the default from 2^20 rows)."""
-    if slice_mb == "stream":
+    the constant bank (the default from 2^20 rows), where the scatter accumulates onto the alpha F the
+    previous sweep left in Y ("stream1": with several passes; "stream_zero": Y re-zeroed instead,
+    SYMNMF_YALPHA=0)."""
+    if slice_mb.startswith("stream"):
         monkeypatch.setenv("SYMNMF_SWEEP", "stream")
-    if slice_mb == "1":
+    if slice_mb in ("1", "stream1"):
         monkeypatch.setenv("SYMNMF_SCATTER_SLICE_MB", "1")
+    if slice_mb == "stream_zero":
+        monkeypatch.setenv("SYMNMF_YALPHA", "0")
     A, H0, alpha = _csr_case(cfgname, n, k)
     tau = 1.0 / s
     M = S.DeviceMatrix.from_host(A)
