@@ -23,9 +23,12 @@ struct SwL {
   static constexpr int ST = KP + 4;             // padded row stride (floats): a thread reading its own
                                                 // row and a row group reading one row are conflict free
   static constexpr size_t arr = sizeof(float) * TR * ST;
-  static constexpr size_t y = 0, f = arr, x = 2 * arr;
-  static constexpr size_t bytes = 3 * arr;      // Y, F, X staging (X rewritten in place)
-  static constexpr int per_sm = KP <= 8 ? 3 : 2;   // 128 registers per thread for k = 16, 32
+  static constexpr size_t y = 0, x = arr, f = 2 * arr;
+  static constexpr size_t bytes = 3 * arr;      // Y, X, F staging (X rewritten in place)
+  static constexpr size_t bytes_noF = 2 * arr;  // Y carries alpha F: F not staged
+  // CTAs per SM the register cap aims at: three when F is not staged (Y carries alpha F: 2 x 37 KB
+  // of staging), else two (3 x 110 KB of shared memory do not fit at k = 32)
+  static constexpr int per_sm(bool noF) { return noF ? 3 : (KP <= 8 ? 3 : 2); }
 };
 
 // Constant-bank copies of the sweep's G (-G_off^T, 1 / (G_ii + alpha), ok flags), one per (solver
@@ -54,15 +57,15 @@ struct SwG {   // G source: TAB < 0 -> shared memory, else constant table TAB
   }
 };
 
-template <int KP, int TAB = -1>
-__global__ void __launch_bounds__(256, SwL<KP>::per_sm) sweep_stream(
+template <int KP, int TAB, bool NOF>
+__global__ void __launch_bounds__(256, SwL<KP>::per_sm(NOF)) sweep_stream(
     const double* __restrict__ G, double alpha, float* __restrict__ Y, const float* __restrict__ F,
     float* __restrict__ X, int64_t n, int ymode, double* Gacc, double* Gout, float* Rf32, unsigned int* counter,
     int32_t* status) {
   // ymode 0: Y read only; 1: Y re-zeroed for the next scatter; 2: Y holds Y_s + alpha F already (the
   // scatter accumulated onto alpha F), so F is not read, and Y is left as alpha X for the next half,
   // whose fixed factor X is (LvS on CSR: 4nk bytes less per half)
-  const bool yalpha = ymode == 2;
+  const bool yalpha = NOF;   // == (ymode == 2)
   using L = SwL<KP>;
   constexpr int C = L::C, TR = L::TR;
   constexpr int NB = KP / 4, PAIRS = NB * (NB + 1) / 2, RG = TR / PAIRS;
@@ -252,12 +255,15 @@ static void sweep_stream_t(const double* G, double alpha, float* Y, const float*
                            double* Gacc, double* Gout, float* Rf32, unsigned int* counter, int32_t* status,
                            cudaStream_t st) {
   using L = SwL<KP>;
-  const size_t smem = std::max({L::bytes, sizeof(double) * 2 * KP * (KP + 1), sizeof(double) * 256 * 16});
+  const size_t smem = std::max({ymode == 2 ? L::bytes_noF : L::bytes, sizeof(double) * 2 * KP * (KP + 1),
+                                 sizeof(double) * 256 * 16});
   const int64_t tiles = (n + L::TR - 1) / L::TR;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * L::per_sm));
-  cudaFuncSetAttribute(sweep_stream<KP, TAB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  launch_pdl(sweep_stream<KP, TAB>, grid, L::TR, smem, st, G, alpha, Y, F, X, n, ymode, Gacc, Gout, Rf32,
-             counter, status);
+  auto kern = ymode == 2 ? sweep_stream<KP, TAB, true> : sweep_stream<KP, TAB, false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, L::TR, smem);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * (int64_t)std::max(1, occ)));
+  launch_pdl(kern, grid, L::TR, smem, st, G, alpha, Y, F, X, n, ymode, Gacc, Gout, Rf32, counter, status);
 }
 
 bool sweep_stream_supported(int k) { return k == 8 || k == 16 || k == 32; }
