@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(LT, 1) lai_sweep_fused(const float* __restrict
   for (int e = tid; e < LP * KP; e += LT) sM[e] = (e / KP < l) ? Mcur[e] : 0.f;
   for (int e = tid; e < KP * KP; e += LT) {
     const int i = e / KP, j = e - i * KP;
-    sG[e] = (i != j) ? (float)G[j * KP + i] : 0.f;
+    sG[e] = (i != j) ? -(float)G[j * KP + i] : 0.f;   // negated: the sweep is a chain of FMAs
   }
   for (int i = tid; i < KP; i += LT) {
     const double den = G[i * KP + i] + alpha;
@@ -147,32 +147,33 @@ __global__ void __launch_bounds__(LT, 1) lai_sweep_fused(const float* __restrict
     // ---- sweep of row tid (Gauss-Seidel over the KP columns), b read from sX, x -> sX and X
     if (tid < rows) {
       const int64_t r = r0 + tid;
-      float x[KP];
+      float2 x[KP / 2];   // column pairs (packed FFMA2)
       const float4* X4 = reinterpret_cast<const float4*>(X + r * KP);
 #pragma unroll
       for (int j = 0; j < KP; j += 4) {
         const float4 v = X4[j / 4];
-        x[j] = v.x; x[j + 1] = v.y; x[j + 2] = v.z; x[j + 3] = v.w;
+        x[j / 2] = make_float2(v.x, v.y); x[j / 2 + 1] = make_float2(v.z, v.w);
       }
       const float* brow = sX + tid * XS;
 #pragma unroll
       for (int i = 0; i < KP; ++i) {
-        float s0 = brow[i], s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        float2 s01 = make_float2(brow[i], 0.f), s23 = make_float2(0.f, 0.f);
 #pragma unroll
         for (int j = 0; j < KP; j += 4) {
           const float4 g = *reinterpret_cast<const float4*>(sG + i * KP + j);
-          s0 = fmaf(-x[j], g.x, s0);
-          s1 = fmaf(-x[j + 1], g.y, s1);
-          s2 = fmaf(-x[j + 2], g.z, s2);
-          s3 = fmaf(-x[j + 3], g.w, s3);
+          s01 = ffma2(x[j / 2], make_float2(g.x, g.y), s01);
+          s23 = ffma2(x[j / 2 + 1], make_float2(g.z, g.w), s23);
         }
-        const float sv = (s0 + s1) + (s2 + s3);
-        if (sOk[i]) x[i] = fmaxf(0.f, sv * sInv[i]);
+        const float sv = (s01.x + s01.y) + (s23.x + s23.y);
+        if (sOk[i]) {
+          const float v = fmaxf(0.f, sv * sInv[i]);
+          if (i & 1) x[i / 2].y = v; else x[i / 2].x = v;
+        }
       }
       float4* Xw = reinterpret_cast<float4*>(X + r * KP);
 #pragma unroll
       for (int j = 0; j < KP; j += 4) {
-        const float4 v = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
+        const float4 v = make_float4(x[j / 2].x, x[j / 2].y, x[j / 2 + 1].x, x[j / 2 + 1].y);
         Xw[j / 4] = v;
         *reinterpret_cast<float4*>(sX + tid * XS + j) = v;
       }
