@@ -56,8 +56,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // accumulators: NACC independent chains per buffer, each 2 NP columns ([.. X_hi | .. X_lo]);
   // two buffers.  NACC = 4: {A_hi, A_lo} x {even, odd K=8 step}; 2: {A_hi, A_lo}; 1: shared.
   constexpr int NACC = NP <= 32 ? 4 : NP <= 64 ? 2 : 1;
+  // NP > 64 (the c5 range finder, NP = 80): A_hi [X_hi | X_lo] (N = 2 NP) and A_lo X_hi (N = NP) into
+  // two independent accumulators per buffer (3 NP columns) instead of one chain of two N = 2 NP MMAs,
+  // whose A_lo X_lo quarter of the tensor work is dropped (it is below the 3xTF32 error anyway)
+  constexpr bool SPLIT2 = NP > 64 && 6 * NP <= 512;
   constexpr uint32_t ACC_COLS = 2 * NP;
-  constexpr uint32_t BUF_COLS = NACC * ACC_COLS;
+  constexpr uint32_t BUF_COLS = SPLIT2 ? 3 * NP : NACC * ACC_COLS;
+  constexpr uint32_t IDESC_LO = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) |
+                                ((uint32_t)(TC_BM >> 4) << 24);
   constexpr uint32_t TMEM_COLS = 2 * BUF_COLS <= 128 ? 128 : 2 * BUF_COLS <= 256 ? 256 : 512;
   constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)((2 * NP) >> 3) << 17) |
                              ((uint32_t)(TC_BM >> 4) << 24);
@@ -117,6 +123,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t a_hi = smem_u32(sm + s * STAGE), a_lo = a_hi + A_BYTES;
         const uint32_t b_hi = a_hi + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
         const uint32_t td = tmem + (uint32_t)b * BUF_COLS;
+        if constexpr (SPLIT2) {
+#pragma unroll
+          for (int kk = 0; kk < TC_BK / 8; ++kk) {
+            const uint32_t off = kk * 32;
+            const uint32_t acc0 = ((i % TC_DRAIN) != 0 || kk > 0) ? 1u : 0u;
+            mma_tf32(td, smem_desc_k128(a_hi + off), smem_desc_k128(b_hi + off), IDESC, acc0);
+            mma_tf32(td + 2 * NP, smem_desc_k128(a_lo + off), smem_desc_k128(b_hi + off), IDESC_LO, acc0);
+          }
+        } else
 #pragma unroll
         for (int kk = 0; kk < TC_BK / 8; ++kk) {
           const uint32_t off = kk * 32;   // 8 tf32 = 32 bytes along the swizzled row
@@ -165,7 +180,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_wait_sleep(acc_full + b, (c >> 1) & 1);
       tc_fence_after();
 #pragma unroll
-      for (int cc = 0; cc < NACC * 2 * NP; cc += 16) {
+      for (int cc = 0; cc < (int)BUF_COLS; cc += 16) {
         const int c0 = cc % NP;   // column block of Y; the NACC x {X_hi, X_lo} partial sums add up
         uint32_t r[16];
         const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)b * BUF_COLS + (uint32_t)cc;
