@@ -32,6 +32,10 @@ UNIT = "iters/s"
 SLEEP_CYCLES = 400_000   # ~0.2 ms: keeps the GPU busy while the host enqueues, so events time the device
 TF32_OVER_BF16 = 0.5     # nominal dense tf32 / bf16 ratio (B200_PROFILING.md: 1.1 vs 2.25 PFLOP/s)
 ALU_BOUND = {"lai_fused"}   # kernels whose roofline is fp32 SIMT arithmetic
+# Measured ceiling of global float reductions into random 128-byte rows of an L2-resident range on this
+# pool's B200 (tools/red_bench.cu, profiles/r2_red_bench.txt: 49.2 G rows/s = 6.3 TB/s of atomic payload,
+# the same for red.v4 and red.v2, 1965 MHz): what bounds the sampled CSR scatter, whose DRAM is ~20% busy.
+L2_ATOMIC_ROWS_PER_S = 49.2e9
 
 
 def parse():
@@ -382,6 +386,11 @@ def run_ours(args, ws, rank, local, pg):
         if by:
             roof["achieved"] = by / (dom_ms * 1e-3) / 1e9
             roof["frac"] = roof["achieved"] / pk["hbm_gbs"]
+    if dom == "sampled_ah_csr" and nnz_u and k == 32:   # one 128 B row of atomics per sampled nonzero
+        rows_s = nnz_u / (dom_ms * 1e-3)
+        roof["l2_atomic"] = {"achieved": rows_s / 1e9, "peak": L2_ATOMIC_ROWS_PER_S / 1e9, "unit": "G row-adds/s",
+                             "frac": rows_s / L2_ATOMIC_ROWS_PER_S,
+                             "peak_source": "tools/red_bench.cu on B200 (profiles/r2_red_bench.txt)"}
     if dom in ("gemm_3xtf32",) and fl:
         tf32 = pk.get("bf16_tflops", 1590.0) * TF32_OVER_BF16 / 3.0
         roof["tensor_3xtf32_tflops"] = {"achieved": fl / (dom_ms * 1e-3) / 1e12, "peak": tf32,

@@ -122,6 +122,9 @@ typedef struct {
  *                                  pass (default 86 MB, so each pass's slice of Y stays in L2).
  *   SYMNMF_SCATTER_SPLIT=<w>       sampled CSR scatter product: warps per sampled row and pass (each
  *                                  takes a contiguous part of the row's in-range nonzeros; default 4).
+ *   SYMNMF_SCATTER_SHFL=0          sampled CSR scatter product (k in {16,32,64}): every lane group loads
+ *                                  its own entries (broadcast loads) instead of the warp loading 32
+ *                                  consecutive entries once, a batch ahead, and shuffling them.
  *   SYMNMF_YALPHA=0                LvS on CSR with the streaming sweep: re-zero Y for each scatter and
  *                                  read F in the sweep, instead of the scatter accumulating onto
  *                                  Y = alpha F left by the previous sweep (state kept across runs).
@@ -359,6 +362,16 @@ symnmf_status symnmf_plan_rows_scaled(const float* F, int64_t row0, int32_t k, c
 symnmf_status symnmf_sampled_ah_rows(const symnmf_matrix* A_block, int64_t n_total, const int32_t* uniq,
                                      const int64_t* n_uniq_dev, int64_t cap, const float* Z, int32_t k, float* Y,
                                      void* ws, size_t* ws_bytes, cudaStream_t st);
+/* LAI on row blocks (Eq. 3.1: A ~ U Lambda U^T, so A F ~ U (Lambda (U^T F))).  The l x k
+ * projection U^T F is a sum over rows: each shard forms its block's share
+ *   Z_b = U_b^T F_b   (fp64, l x k row-major; U_b, F_b = the block's n rows of U and F),
+ * the caller allreduces the shares into Z, and symnmf_lai_apply_rows writes the block's rows
+ *   Y_b = U_b (Lambda Z)   (fp32 n x k; lambda = the l eigenvalues, fp64).
+ * With one block the two calls compose to symnmf_lai_ah.  1 <= l <= 80, k as everywhere. */
+symnmf_status symnmf_lai_project_rows(const float* U, int64_t n, int32_t l, const float* F, int32_t k, double* Z,
+                                      void* ws, size_t* ws_bytes, cudaStream_t st);
+symnmf_status symnmf_lai_apply_rows(const float* U, const double* lambda, int64_t n, int32_t l, const double* Z,
+                                    int32_t k, float* Y, void* ws, size_t* ws_bytes, cudaStream_t st);
 
 /* Kernel and memset node counts of the captured per-iteration graph (host only). */
 symnmf_status symnmf_solver_graph_nodes(const symnmf_solver* solver, int32_t* kernels_host, int32_t* memsets_host);

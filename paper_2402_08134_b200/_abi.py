@@ -78,6 +78,8 @@ SIGNATURES = {
     "symnmf_hybrid_shard_plan": (I32, [P, I64, I64, I32, I64, F64, U64, U32, U32, U64, U64, I64, PP, P, PSZ, P]),
     "symnmf_plan_rows_scaled": (I32, [P, I64, I32, PP, P, P, P, PSZ, P]),
     "symnmf_sampled_ah_rows": (I32, [PM, I64, P, P, I64, P, I32, P, P, PSZ, P]),
+    "symnmf_lai_project_rows": (I32, [P, I64, I32, P, I32, P, P, PSZ, P]),
+    "symnmf_lai_apply_rows": (I32, [P, P, I64, I32, P, I32, P, P, PSZ, P]),
 }
 
 _lib = None

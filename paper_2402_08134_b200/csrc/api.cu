@@ -523,6 +523,44 @@ extern "C" symnmf_status symnmf_lai_ah(const float* U, const double* lambda, int
   return finish();
 }
 
+// NEXT-4: the two halves of symnmf_lai_ah for a row block (the l x k allreduce between them is the caller's).
+extern "C" symnmf_status symnmf_lai_project_rows(const float* U, int64_t n, int32_t l, const float* F, int32_t k,
+                                                 double* Z, void* ws, size_t* ws_bytes, cudaStream_t st) {
+  if (!U || !F || !Z || n < 1 || l < 1 || l > kMaxL || bad_k(k)) return SYMNMF_ERR_ARG;
+  const int grid = gram_grid(n);
+  Carver c(nullptr);
+  c.take<double>(gram_partial_doubles(l, k, false, grid));
+  bool q;
+  symnmf_status r = ws_protocol(ws, ws_bytes, c.bytes(), &q);
+  if (r != SYMNMF_OK || q) return r;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  double* part = w.take<double>(gram_partial_doubles(l, k, false, grid));
+  int32_t* status = ws_status(ws);
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
+  launch_cross_gram(U, l, l, F, k, k, false, n, nullptr, nullptr, nullptr, part, grid, Z, k, status, st);
+  return finish();
+}
+
+extern "C" symnmf_status symnmf_lai_apply_rows(const float* U, const double* lambda, int64_t n, int32_t l,
+                                               const double* Z, int32_t k, float* Y, void* ws, size_t* ws_bytes,
+                                               cudaStream_t st) {
+  if (!U || !lambda || !Z || !Y || n < 1 || l < 1 || l > kMaxL || bad_k(k)) return SYMNMF_ERR_ARG;
+  Carver c(nullptr);
+  c.take<float>((size_t)l * k);
+  bool q;
+  symnmf_status r = ws_protocol(ws, ws_bytes, c.bytes(), &q);
+  if (r != SYMNMF_OK || q) return r;
+  if (!device_ok()) return SYMNMF_ERR_UNSUPPORTED;
+  Carver w(ws);
+  float* M = w.take<float>((size_t)l * k);
+  int32_t* status = ws_status(ws);
+  SYMNMF_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(int32_t), st));
+  launch_scale_rows(Z, l, k, lambda, M, status, st);
+  launch_rowapply32(U, l, n, l, M, k, Y, k, status, st);
+  return finish();
+}
+
 // ---------------------------------------------------------------- (a11)
 extern "C" symnmf_status symnmf_hals_sweep(const double* G, const float* Y, const float* F, float* X, int64_t n,
                                            int32_t k, double alpha, double* G_new, void* ws, size_t* ws_bytes,

@@ -11,6 +11,8 @@ One half-iteration (Alg. LvS-SymNMF; P:181 for EXACT):
            Y_s rows of the block as a pull over its CSR rows (no exchange of A)
            X_b <- sweep(G_s, Y_s,b, F_b, X_b)                                      (P:170-175)
     EXACT  F --allgather--> F_all;  Y_b = A_b F_all;  G = allreduce(G_b);  X_b <- sweep(G, Y_b, F_b, X_b)
+    LAI    Z_b = U_b^T F_b (l x k) --allreduce--> Z;  Y_b = U_b (Lambda Z);  G = allreduce(G_b);
+           X_b <- sweep(G, Y_b, F_b, X_b)                                          (Eq. 3.1, P:170-183)
 
 The collectives are plumbing: `LocalComm` holds P logical shards in one process (one device; sums in
 shard order, concatenation), `DistComm` one shard per rank over torch.distributed (NCCL for CUDA
@@ -94,18 +96,29 @@ class DistComm:
 
 
 class ShardedSolver:
-    """Row-sharded EXACT / LvS iterations on CSR A (the shards this process owns, per `comm`).
+    """Row-sharded EXACT / LvS iterations on CSR A, or LAI iterations on (U, lambda) (the shards this
+    process owns, per `comm`).
 
-    A: synth.CsrMatrix (host; each shard takes its rows), H0 (host n x k fp32), W0 = H0."""
+    A: synth.CsrMatrix (host; each shard takes its rows), H0 (host n x k fp32), W0 = H0.
+    mode="lai": A is None and lai=(U, lam) holds the range finder's factors (host or device, n x l
+    fp32 and l fp64; each shard takes its rows of U)."""
 
-    def __init__(self, A, H0, alpha: float, comm, mode="lvs", s=0, tau=1.0, seed=0, device="cuda"):
+    def __init__(self, A, H0, alpha: float, comm, mode="lvs", s=0, tau=1.0, seed=0, device="cuda", lai=None):
         self.comm, self.mode, self.alpha = comm, mode, float(alpha)
         self.s, self.tau, self.seed = int(s), float(tau), int(seed)
-        self.n, self.k = A.n, H0.shape[1]
-        self.blocks = row_blocks(A.n, comm.P)
-        self.M, self.W, self.H = [], [], []
+        self.n, self.k = H0.shape[0], H0.shape[1]
+        self.blocks = row_blocks(self.n, comm.P)
+        self.M, self.W, self.H, self.U = [], [], [], []
+        if mode == "lai":
+            U, lam = (torch.as_tensor(x) for x in lai)
+            self.lam = lam.to(device=device, dtype=torch.float64).contiguous()
         for p in comm.shards:
             r0, r1 = self.blocks[p]
+            if mode == "lai":
+                self.U.append(U[r0:r1].to(device=device, dtype=torch.float32).contiguous())
+                self.W.append(torch.from_numpy(np.ascontiguousarray(H0[r0:r1])).to(device))
+                self.H.append(torch.from_numpy(np.ascontiguousarray(H0[r0:r1])).to(device))
+                continue
             e0, e1 = int(A.rowptr[r0]), int(A.rowptr[r1])
             rp = torch.from_numpy((A.rowptr[r0:r1 + 1] - e0).astype(np.int64)).to(device)
             ci = torch.from_numpy(np.ascontiguousarray(A.colidx[e0:e1])).to(device)
@@ -120,6 +133,12 @@ class ShardedSolver:
         F = self.H if side == 0 else self.W
         X = self.W if side == 0 else self.H
         G = c.allreduce_sum([S.gram(f) for f in F])
+        if self.mode == "lai":   # Y_b = U_b (Lambda sum_b U_b^T F_b): one l x k allreduce (Eq. 3.1)
+            Z = c.allreduce_sum([S.lai_project_rows(u, f) for u, f in zip(self.U, F)])
+            for i in range(len(F)):
+                Y = S.lai_apply_rows(self.U[i], self.lam, Z[i])
+                S.hals_sweep(G[i], Y, F[i], X[i], self.alpha)
+            return
         if self.mode == "exact":
             F_all = c.allgather_cat(F)
             for i in range(len(F)):

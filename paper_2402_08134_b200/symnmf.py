@@ -274,6 +274,26 @@ def sampled_ah_rows(Mb: DeviceMatrix, n_total: int, uniq: torch.Tensor, Z: torch
     return Y
 
 
+def lai_project_rows(U: torch.Tensor, F: torch.Tensor) -> torch.Tensor:
+    """Z_b = U_b^T F_b (fp64 l x k) of a row block, symnmf_lai_project_rows."""
+    _cuda(U, torch.float32); _cuda(F, torch.float32)
+    n, l = U.shape
+    k = F.shape[1]
+    Z = torch.empty((l, k), dtype=torch.float64, device=F.device)
+    _call("symnmf_lai_project_rows", (_p(U), n, l, _p(F), k, _p(Z)), (_stream(),))
+    return Z
+
+
+def lai_apply_rows(U: torch.Tensor, lam: torch.Tensor, Z: torch.Tensor) -> torch.Tensor:
+    """Y_b = U_b (Lambda Z) (fp32 n_b x k) of a row block, symnmf_lai_apply_rows."""
+    _cuda(U, torch.float32); _cuda(lam, torch.float64); _cuda(Z, torch.float64)
+    n, l = U.shape
+    k = Z.shape[1]
+    Y = torch.empty((n, k), dtype=torch.float32, device=U.device)
+    _call("symnmf_lai_apply_rows", (_p(U), _p(lam), n, l, _p(Z), k, _p(Y)), (_stream(),))
+    return Y
+
+
 # ------------------------------------------------------------------ (a12, a13)
 def gaussian(n: int, l: int, seed: int, device="cuda") -> torch.Tensor:
     Om = torch.empty((n, l), dtype=torch.float32, device=device)

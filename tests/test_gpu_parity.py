@@ -219,8 +219,10 @@ def test_sampled_dense_all_rows_equals_exact():
     assert rel(Y.cpu().numpy(), O.ah(A, F)) < 1e-5
 
 
-@pytest.mark.parametrize("k", [3, 16, 32])
-def test_sampled_csr(c2small, k):
+@pytest.mark.parametrize("shfl", [False, True])
+@pytest.mark.parametrize("k", [3, 16, 32, 64])
+def test_sampled_csr(c2small, k, shfl, monkeypatch):
+    monkeypatch.setenv("SYMNMF_SCATTER_SHFL", "1" if shfl else "0")
     A = c2small["A"]
     F = random_factor(A.n, k, 9) ** 2
     plan, o = _plan_for(F, k, 1000, 1 / 1000, seed=5, it=3, side=1)
@@ -519,18 +521,21 @@ def test_csr_tile_exact_one_iteration(cfgname, n, k, tile, monkeypatch):
 
 
 @pytest.mark.parametrize("cfgname,n,k,s", [("c4", 40_000, 32, 800), ("c2", 20_000, 16, 400), ("c4", 40_000, 8, 2000)])
-@pytest.mark.parametrize("slice_mb", ["", "1", "stream", "stream1", "stream_zero"])
+@pytest.mark.parametrize("slice_mb", ["", "1", "stream", "stream1", "stream_zero", "noshfl", "stream1_noshfl"])
 def test_csr_lvs_solver_equals_abi_composition(cfgname, n, k, s, slice_mb, monkeypatch):
     """Solver LvS on CSR graphs with hubs (vector-atomic scatter of the sampled product, fused Gram)
     equals the composition of the ABI calls on the same device data; slice_mb = 1 forces several
     destination-range passes of the sampled scatter, "stream" the streaming sweep with G and R in
     the constant bank (the default from 2^20 rows), where the scatter accumulates onto the alpha F the
     previous sweep left in Y ("stream1": with several passes; "stream_zero": Y re-zeroed instead,
-    SYMNMF_YALPHA=0)."""
+    SYMNMF_YALPHA=0; "noshfl": the scatter with broadcast entry loads instead of the default
+    coalesced, shuffled ones, SYMNMF_SCATTER_SHFL=0, in the solver and the ABI call)."""
     if slice_mb.startswith("stream"):
         monkeypatch.setenv("SYMNMF_SWEEP", "stream")
-    if slice_mb in ("1", "stream1"):
+    if slice_mb in ("1", "stream1", "stream1_noshfl"):
         monkeypatch.setenv("SYMNMF_SCATTER_SLICE_MB", "1")
+    if slice_mb.endswith("noshfl"):
+        monkeypatch.setenv("SYMNMF_SCATTER_SHFL", "0")
     if slice_mb == "stream_zero":
         monkeypatch.setenv("SYMNMF_YALPHA", "0")
     A, H0, alpha = _csr_case(cfgname, n, k)

@@ -98,3 +98,34 @@ def test_sharded_lvs_half_matches_oracle_and_global_plan(cfgname, n, k, s, P):
     W, _ = sv.factors()
     Gs, Ys = O.sampled_products(A, H0, g["uniq_idx"], g["uniq_w"])
     assert rel(W.cpu().numpy(), O.hals_sweep(Gs, Ys, H0, H0, alpha)) < 1e-5
+
+
+@pytest.mark.parametrize("n,l,k,P", [(5_003, 20, 16, 1), (5_003, 20, 16, 3), (40_000, 74, 64, 2), (40_000, 74, 64, 4)])
+def test_sharded_lai_blocks_and_iteration_match_oracle(n, l, k, P):
+    """LAI on row blocks (Eq. 3.1): sum_b U_b^T F_b then U_b (Lambda Z) equals the oracle's
+    U (Lambda (U^T F)) (1e-5), with one block it equals symnmf_lai_ah, and two sharded iterations match
+    the oracle's fp64 LAI halves fed the GPU's own previous factors (per-half protocol, 1e-5)."""
+    r = np.random.default_rng(n + l + P)
+    U = np.linalg.qr(r.standard_normal((n, l)))[0].astype(np.float32)
+    lam = np.sort(r.random(l) * 50)[::-1].copy()
+    lam[-3:] *= -0.1                                   # Apx-EVD eigenvalues may be negative (P:228-235)
+    H0 = init_factor(n, k, 0.5, np.random.default_rng(5))
+    Ud, lamd = cu(U), cu(lam)
+    blocks = SH.row_blocks(n, P)
+    Hd = cu(H0)
+    Z = sum(S.lai_project_rows(Ud[r0:r1], Hd[r0:r1]) for r0, r1 in blocks)
+    assert rel(Z.cpu().numpy(), U.astype(np.float64).T @ H0.astype(np.float64)) < 1e-6
+    Y = torch.cat([S.lai_apply_rows(Ud[r0:r1], lamd, Z) for r0, r1 in blocks]).cpu().numpy()
+    assert rel(Y, O.lai_apply(U, lam, H0)) < 1e-5
+    if P == 1:
+        assert np.array_equal(Y, S.lai_ah(Ud, lamd, Hd).cpu().numpy())
+    alpha = 1.0                                        # any alpha >= 0 (the paper takes max(A), P:1103-1105)
+    sv = SH.ShardedSolver(None, H0, alpha, SH.LocalComm(P), mode="lai", lai=(U, lam))
+    for it in range(2):
+        for side in (0, 1):
+            W0, H0_ = (t.cpu().numpy().astype(np.float64) for t in sv.factors())
+            sv.half(it, side)
+            W, H = (t.cpu().numpy() for t in sv.factors())
+            Wr, Hr, _ = O.half_step(None, W0, H0_, alpha, it, side, "lai", U=U, lam=lam)
+            got, ref = (W, Wr) if side == 0 else (H, Hr)
+            assert rel(got, ref) < 1e-5, (it, side, rel(got, ref))
