@@ -36,6 +36,10 @@ ALU_BOUND = {"lai_fused"}   # kernels whose roofline is fp32 SIMT arithmetic (DE
 # pool's B200 (tools/red_bench.cu, profiles/r2_red_bench.txt: 49.2 G rows/s = 6.3 TB/s of atomic payload,
 # the same for red.v4 and red.v2, 1965 MHz): what bounds the sampled CSR scatter, whose DRAM is ~20% busy.
 L2_ATOMIC_ROWS_PER_S = 49.2e9
+# Same tool, "ld" lines: 1e8 gathers of random 128-byte rows run at 75 G rows/s (9.6 TB/s) from an L2-resident
+# range and 66.5 G rows/s (8.5 TB/s) from a 256 MB one -- the L2 slices' throughput, not HBM, caps the exact
+# CSR product's F gathers at k = 32 (one 128 B row of F per nonzero).
+L2_GATHER_ROWS_PER_S = 66.5e9
 
 
 def parse():
@@ -391,6 +395,11 @@ def run_ours(args, ws, rank, local, pg):
         roof["l2_atomic"] = {"achieved": rows_s / 1e9, "peak": L2_ATOMIC_ROWS_PER_S / 1e9, "unit": "G row-adds/s",
                              "frac": rows_s / L2_ATOMIC_ROWS_PER_S,
                              "peak_source": "tools/red_bench.cu on B200 (profiles/r2_red_bench.txt)"}
+    if dom == "spmm_csr" and k == 32 and 4 * n * k > (100 << 20):   # one 128 B row of F gathered per nonzero
+        rows_s = nnz / (dom_ms * 1e-3)
+        roof["l2_gather"] = {"achieved": rows_s / 1e9, "peak": L2_GATHER_ROWS_PER_S / 1e9, "unit": "G row-gathers/s",
+                             "frac": rows_s / L2_GATHER_ROWS_PER_S,
+                             "peak_source": "tools/red_bench.cu on B200 (profiles/r2_red_bench.txt, 256 MB range)"}
     if dom in ("gemm_3xtf32",) and fl:
         tf32 = pk.get("bf16_tflops", 1590.0) * TF32_OVER_BF16 / 3.0
         roof["tensor_3xtf32_tflops"] = {"achieved": fl / (dom_ms * 1e-3) / 1e12, "peak": tf32,

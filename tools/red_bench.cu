@@ -3,6 +3,8 @@
 // (spmm.cu: sampled_csr_v4).  Each "row op" adds 32 floats (k = 32) into one random 128 B row:
 //   v4: 8 lanes x red.global.add.v4.f32, v2: 16 lanes x .v2.f32, v1: 32 lanes x .f32,
 //   st: the same rows written with plain 16 B stores (the LSU/L2 cost without the atomic ALU).
+//   ld: the same rows gathered with 16 B loads and summed in registers -- the access pattern of the
+//       exact CSR product's F gathers (spmm_nnz.cu), 1e8 row gathers like c4's nonzeros.
 // Prints row ops/s and lane-instructions per clock per SM (at the SM clock nvidia-smi reports).
 // Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a tools/red_bench.cu -o /tmp/red_bench
 #include <cstdint>
@@ -43,6 +45,46 @@ __global__ void __launch_bounds__(256) red_kernel(float* __restrict__ Y, uint32_
   }
 }
 
+// Row gathers: 8 lanes x 16 B per random row, UNR independent rows in flight per lane group.
+template <int UNR>
+__global__ void __launch_bounds__(256) gather_kernel(const float4* __restrict__ F, uint32_t nrows, int64_t ops,
+                                                     uint32_t seed, float4* __restrict__ out) {
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / 8;
+  const int li = threadIdx.x % 8;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t o = gtid / 8; o < ops; o += ngroups * UNR) {
+    float4 v[UNR];
+#pragma unroll
+    for (int j = 0; j < UNR; ++j) {
+      const int64_t oj = o + j * ngroups;
+      const uint32_t r = mix((uint32_t)oj * 2654435761u + seed) % nrows;
+      v[j] = oj < ops ? __ldg(F + (int64_t)r * 8 + li) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < UNR; ++j) { acc.x += v[j].x; acc.y += v[j].y; acc.z += v[j].z; acc.w += v[j].w; }
+  }
+  if (acc.x == 123.456f) out[gtid] = acc;   // keep the loads
+}
+
+static void run_gather(const float* Y, uint32_t nrows, int64_t ops, int sms, float* out) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const int grid = sms * 8;
+  float best = 1e30f;
+  for (int it = 0; it < 4; ++it) {
+    cudaEventRecord(e0);
+    gather_kernel<8><<<grid, 256>>>(reinterpret_cast<const float4*>(Y), nrows, ops, 5u + it,
+                                    reinterpret_cast<float4*>(out));
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    if (it > 0 && ms < best) best = ms;
+  }
+  printf("ld  rows=%9u (%6.1f MB) ops=%lld  %.3f ms  %.2f G row-gathers/s  %.2f TB/s gathered\n", nrows,
+         nrows * 128.0 / 1e6, (long long)ops, best, ops / (best * 1e-3) / 1e9, ops / (best * 1e-3) * 128 / 1e12);
+}
+
 template <int MODE>
 static void run(const char* name, float* Y, uint32_t nrows, int64_t ops, int sms, double mhz) {
   cudaEvent_t e0, e1;
@@ -81,6 +123,10 @@ int main(int argc, char** argv) {
     run<1>("v1", Y, nrows, ops, sms, mhz);
     run<0>("st", Y, nrows, ops, sms, mhz);
   }
+  float* out; cudaMalloc(&out, (size_t)sms * 8 * 256 * 16);
+  const uint32_t gsizes[] = {1u << 14, 500000u, 1000000u, 2000000u};   // 2 MB, 64 MB, 128 MB, 256 MB (c4's F)
+  for (uint32_t nrows : gsizes) run_gather(Y, nrows, 100 * 1000 * 1000, sms, out);
+  cudaFree(out);
   cudaFree(Y);
   return cudaGetLastError() != cudaSuccess;
 }
