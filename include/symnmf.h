@@ -119,12 +119,16 @@ typedef struct {
  *                                  instead of the constant bank (a solver holds one of 4 constant
  *                                  slots; beyond 4 live solvers the shared-memory form is used).
  *   SYMNMF_SCATTER_SLICE_MB=<mb>   sampled CSR scatter product: rows of Y per destination-range
- *                                  pass (default 86 MB, so each pass's slice of Y stays in L2).
+ *                                  pass, so each pass's slice of Y stays in L2 (default 52 MB when the
+ *                                  passes are merged into one launch, k in {16,32,64}; else 86 MB).
  *   SYMNMF_SCATTER_SPLIT=<w>       sampled CSR scatter product: warps per sampled row and pass (each
- *                                  takes a contiguous part of the row's in-range nonzeros; default 4).
+ *                                  takes a contiguous part of the row's in-range nonzeros; default 2
+ *                                  with merged passes, else 4).
  *   SYMNMF_SCATTER_SHFL=0          sampled CSR scatter product (k in {16,32,64}): every lane group loads
  *                                  its own entries (broadcast loads) instead of the warp loading 32
  *                                  consecutive entries once, a batch ahead, and shuffling them.
+ *   SYMNMF_SCATTER_MERGE=0         sampled CSR scatter product: one launch per destination-range pass instead
+ *                                  of one launch whose block range p works on pass p.
  *   SYMNMF_YALPHA=0                LvS on CSR with the streaming sweep: re-zero Y for each scatter and
  *                                  read F in the sweep, instead of the scatter accumulating onto
  *                                  Y = alpha F left by the previous sweep (state kept across runs).

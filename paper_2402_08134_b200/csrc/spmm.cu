@@ -75,18 +75,28 @@ __global__ void __launch_bounds__(256) spmm_csr_scalar(const int64_t* __restrict
 // Measured on c4 (Y = 256 MB), LvS it/s by slice: 48 MB 425, 64 MB 433, 86 MB 435, 128 MB 427,
 // 256 MB (one pass) 400 -- every pass rescans the sampled nonzeros, so fewer passes win until the
 // slice stops fitting in L2 next to the streamed rows of A.
-static int64_t scatter_slice_bytes() {
+static bool scatter_shfl();
+static bool scatter_merge();
+// Rows of Y per destination-range pass.  Passes launched one by one: 86 MB (43/64/86/128 MB: 0.47/0.35/
+// 0.35/0.39 ms per c4 half).  Passes merged into one launch (k in {16, 32, 64}): 52 MB -- two adjacent
+// slices fit L2 while the tail of a pass overlaps the head of the next (86/64/52/43/32 MB:
+// 0.309/0.291/0.287/0.290/0.309 ms).
+static int64_t scatter_slice_bytes(int k) {
   const char* e = getenv("SYMNMF_SCATTER_SLICE_MB");
   const int64_t mb = e ? atoll(e) : 0;
-  return mb > 0 ? (mb << 20) : (86ll << 20);
+  if (mb > 0) return mb << 20;
+  const bool merged = (k == 16 || k == 32 || k == 64) && scatter_shfl() && scatter_merge();
+  return (merged ? 52ll : 86ll) << 20;
 }
 
 // Warps per sampled row of the scatter; SYMNMF_SCATTER_SPLIT overrides (symnmf.h).
-static int scatter_split() {
+static int scatter_split(int k) {
   const char* e = getenv("SYMNMF_SCATTER_SPLIT");
   const int v = e ? atoi(e) : 0;
-  // c4 LvS it/s by split (pass bounds precomputed): 1 565, 2 583, 4 614, 8 598, 16 545
-  return v > 0 ? std::min(v, 64) : 4;
+  // c4 LvS it/s by split, three 86 MB passes launched one by one: 1 565, 2 583, 4 614, 8 598, 16 545;
+  // five merged 52 MB passes (a row's per-pass segment is shorter): 1 728, 2 738, 3 738, 4 731, 8 653
+  if (v > 0) return std::min(v, 64);
+  return (k == 16 || k == 32 || k == 64) && scatter_shfl() && scatter_merge() ? 2 : 4;
 }
 
 // Coalesced + shuffled entry loads in the scatter (sampled_csr_v4s, the default for k in {16, 32, 64}
@@ -94,6 +104,13 @@ static int scatter_split() {
 // broadcast loads.  c4 LvS: 662 / 664 vs 675 / 675 it/s (scatter 0.350-0.360 vs 0.345-0.347 ms per half).
 static bool scatter_shfl() {
   const char* e = getenv("SYMNMF_SCATTER_SHFL");
+  return !e || atoi(e) != 0;
+}
+
+// All destination passes of the shuffled scatter in one launch (block range p = pass p), the default;
+// SYMNMF_SCATTER_MERGE=0 launches them one by one.  c4: scatter 0.345 -> 0.308 ms per half, LvS 675 -> 711 it/s.
+static bool scatter_merge() {
+  const char* e = getenv("SYMNMF_SCATTER_MERGE");
   return !e || atoi(e) != 0;
 }
 
@@ -190,13 +207,19 @@ __global__ void __launch_bounds__(256) sampled_csr_v4s(
     const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, const float* __restrict__ val,
     const float4* __restrict__ F4, const int32_t* __restrict__ uniq, const double* __restrict__ w,
     const int64_t* __restrict__ n_uniq_dev, float4* __restrict__ Y4, int split, const int32_t* __restrict__ ppos,
-    int pass, int64_t n, const int32_t* __restrict__ status) {
+    int pass, int merged, int64_t n, const int32_t* __restrict__ status) {
   if (dev_failed(status)) return;
   constexpr int NPW = 32 / LPR;   // nonzeros per warp step
   const int lane = threadIdx.x & 31, sub = lane / LPR, li = lane % LPR;
   const int64_t nu = *n_uniq_dev;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nu * split; t += nw) {
+  // merged > 1: one launch for all `merged` destination passes, block range p of the grid working on
+  // pass p -- CTAs are dispatched in block order, so the passes still run one after the other (each
+  // slice of Y L2-resident while its atomics land), but the tail of a pass overlaps the head of the next
+  const int gpp = merged > 1 ? gridDim.x / merged : gridDim.x;
+  if (merged > 1) pass = blockIdx.x / gpp;
+  const int64_t nw = ((int64_t)gpp * blockDim.x) >> 5;
+  for (int64_t t = ((int64_t)(blockIdx.x - pass * (merged > 1 ? gpp : 0)) * blockDim.x + threadIdx.x) >> 5;
+       t < nu * split; t += nw) {
     const int64_t u = t / split;
     const int part = (int)(t - u * split);
     const int64_t i = uniq[u];
@@ -264,7 +287,7 @@ void launch_sampled_csr(const symnmf_matrix& A, const float* F, int k, const int
 // Destination-range passes of the scatter for this A and k (>= 1).
 int sampled_csr_passes(int64_t n, int k) {
   const int64_t ybytes = (int64_t)sizeof(float) * n * k;
-  const int64_t slice = scatter_slice_bytes();
+  const int64_t slice = scatter_slice_bytes(k);
   return (int)std::max<int64_t>(1, (ybytes + slice - 1) / slice);
 }
 
@@ -304,16 +327,19 @@ void launch_sampled_csr_nozero(const symnmf_matrix& A, const float* F, int k, co
     // small enough to stay resident in L2 (126 MB) while the pass's vector atomics land on it,
     // instead of read-modify-writes of random 128-byte lines of a Y larger than L2.
     const int passes = sampled_csr_passes(A.n, k);
-    const int split = scatter_split();
+    const int split = scatter_split(k);
     const bool shfl = scatter_shfl();
     for (int p = 0; p < passes; ++p) {
       const int32_t lo = (int32_t)(A.n * p / passes), hi = (int32_t)(A.n * (p + 1) / passes);
       const int ranged = passes > 1;
       if (shfl && (!ranged || ppos) && (k == 16 || k == 32 || k == 64)) {
         const int32_t* pp = ranged ? ppos : nullptr;
-        if (k == 16) launch_pdl(sampled_csr_v4s<4>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, split, pp, p, A.n, status);
-        else if (k == 32) launch_pdl(sampled_csr_v4s<8>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, split, pp, p, A.n, status);
-        else launch_pdl(sampled_csr_v4s<16>, grid, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, split, pp, p, A.n, status);
+        const int merged = ranged && scatter_merge() ? passes : 1;
+        const int g = grid * merged;   // 6 / 8 / 12 / 16 CTAs per SM and pass: 0.297 / 0.290 / 0.288 / 0.288 ms
+        if (k == 16) launch_pdl(sampled_csr_v4s<4>, g, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, split, pp, p, merged, A.n, status);
+        else if (k == 32) launch_pdl(sampled_csr_v4s<8>, g, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, split, pp, p, merged, A.n, status);
+        else launch_pdl(sampled_csr_v4s<16>, g, 256, 0, st, A.rowptr, A.colidx, A.val, F4, uniq, w, n_uniq_dev, Y4, split, pp, p, merged, A.n, status);
+        if (merged > 1) break;
         continue;
       }
       switch (k / 4) {

@@ -521,7 +521,7 @@ def test_csr_tile_exact_one_iteration(cfgname, n, k, tile, monkeypatch):
 
 
 @pytest.mark.parametrize("cfgname,n,k,s", [("c4", 40_000, 32, 800), ("c2", 20_000, 16, 400), ("c4", 40_000, 8, 2000)])
-@pytest.mark.parametrize("slice_mb", ["", "1", "stream", "stream1", "stream_zero", "noshfl", "stream1_noshfl"])
+@pytest.mark.parametrize("slice_mb", ["", "1", "stream", "stream1", "stream_zero", "noshfl", "stream1_noshfl", "stream1_nomerge"])
 def test_csr_lvs_solver_equals_abi_composition(cfgname, n, k, s, slice_mb, monkeypatch):
     """Solver LvS on CSR graphs with hubs (vector-atomic scatter of the sampled product, fused Gram)
     equals the composition of the ABI calls on the same device data; slice_mb = 1 forces several
@@ -532,10 +532,12 @@ def test_csr_lvs_solver_equals_abi_composition(cfgname, n, k, s, slice_mb, monke
     coalesced, shuffled ones, SYMNMF_SCATTER_SHFL=0, in the solver and the ABI call)."""
     if slice_mb.startswith("stream"):
         monkeypatch.setenv("SYMNMF_SWEEP", "stream")
-    if slice_mb in ("1", "stream1", "stream1_noshfl"):
+    if slice_mb in ("1", "stream1", "stream1_noshfl", "stream1_nomerge"):
         monkeypatch.setenv("SYMNMF_SCATTER_SLICE_MB", "1")
     if slice_mb.endswith("noshfl"):
         monkeypatch.setenv("SYMNMF_SCATTER_SHFL", "0")
+    if slice_mb.endswith("nomerge"):
+        monkeypatch.setenv("SYMNMF_SCATTER_MERGE", "0")
     if slice_mb == "stream_zero":
         monkeypatch.setenv("SYMNMF_YALPHA", "0")
     A, H0, alpha = _csr_case(cfgname, n, k)
