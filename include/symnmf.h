@@ -129,6 +129,9 @@ typedef struct {
  *                                  consecutive entries once, a batch ahead, and shuffling them.
  *   SYMNMF_SCATTER_MERGE=0         sampled CSR scatter product: one launch per destination-range pass instead
  *                                  of one launch whose block range p works on pass p.
+ *   SYMNMF_PDL=0|1                 programmatic dependent launch between the kernels of a call / of the
+ *                                  solver's graph: forced off / on (default: on only in solver graphs
+ *                                  below 2^15 rows).
  *   SYMNMF_YALPHA=0                LvS on CSR with the streaming sweep: re-zero Y for each scatter and
  *                                  read F in the sweep, instead of the scatter accumulating onto
  *                                  Y = alpha F left by the previous sweep (state kept across runs).

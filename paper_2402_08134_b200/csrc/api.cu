@@ -1131,7 +1131,10 @@ extern "C" symnmf_status symnmf_solver_create(symnmf_solver** out, const symnmf_
     if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
       rs = SYMNMF_ERR_CUDA;
     } else {
-      ok = enqueue_iteration(S, cs);
+      {
+        pdl_scope pdl(S.n < (1ll << 15));   // common.cuh: PDL edges pay only for the small problems
+        ok = enqueue_iteration(S, cs);
+      }
       ce = cudaStreamEndCapture(cs, &g);
       if (!ok) rs = SYMNMF_ERR_UNSUPPORTED;
       else if (ce != cudaSuccess || !g) rs = SYMNMF_ERR_CUDA;

@@ -5,6 +5,7 @@
 #include <stdint.h>
 #include <stddef.h>
 #include <algorithm>
+#include <cstdlib>
 #include <utility>
 #include "symnmf.h"
 
@@ -22,6 +23,25 @@ constexpr int kWsHeader = 256;  // bytes reserved at the head of every workspace
 // their own dependents launch at once (launch_dependents) and wait for the predecessor's
 // completion and memory flush (griddepcontrol.wait) before touching its outputs.  Both
 // are no-ops for a kernel launched without the attribute.
+// Whether the attribute is set: SYMNMF_PDL=0|1 forces it off / on; otherwise the solver enables it
+// for the graph it captures only below 2^15 rows (pdl_scope) and the plain ABI calls leave it off.
+// Measured it/s with / without it (B200, graph replay): c1 LvS 11.77k / 11.63k, c3 LvS 1710 / 1697,
+// c1 / c3 EXACT equal; c2 LvS 8.14k / 8.40k, c2 EXACT 11.88k / 11.98k, c5 LAI 3.33k / 3.38k, c4 LvS
+// 737 / 747 and c4 EXACT 184 / 245 -- behind the large grids the early-resident dependents cost
+// more than the launch latency they hide.
+inline int& pdl_mode() {   // -1: default (off), 0 / 1: set by the capturing solver
+  static thread_local int m = -1;
+  return m;
+}
+struct pdl_scope {
+  int saved;
+  explicit pdl_scope(bool on) : saved(pdl_mode()) { pdl_mode() = on ? 1 : 0; }
+  ~pdl_scope() { pdl_mode() = saved; }
+};
+inline bool pdl_enabled() {
+  static const int env = [] { const char* e = getenv("SYMNMF_PDL"); return e ? (e[0] != '0' ? 1 : 0) : -1; }();
+  return env >= 0 ? env == 1 : pdl_mode() == 1;
+}
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
@@ -37,7 +57,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
