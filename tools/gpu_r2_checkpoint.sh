@@ -28,7 +28,7 @@ prof() {  # name cfg mode regex count
   echo "$1 ncu rc=$?"
 }
 prof c4_lvs c4 lvs "sampled_csr|sweep_stream|leverage_fused" 5
-prof c4_exact c4 exact "spmm_nnz<" 1
+prof c4_exact c4 exact "^spmm_nnz$" 1
 prof c3_lvs c3 lvs "tc_sampled" 1
 prof c3_exact c3 exact "tc_gemm" 1
 prof c2_lvs c2 lvs "sweep_fused|leverage_fused|sampled_csr" 3
