@@ -1,5 +1,5 @@
 #!/bin/bash
-# A/B of one environment knob on a bench config: tools/gpu_ab.sh <tag> <ENV_NAME> "<v1> <v2> ..." [bench args]
+# A/B of one environment knob on the default bench (c4 LvS) or the config given in the bench args:
 # (each value twice, interleaved; prints it/s and the per-kernel ms).  Runs the knob's parity tests first.
 set -u
 TAG=$1; VAR=$2; VALS=$3; shift 3
