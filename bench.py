@@ -197,7 +197,7 @@ def config_dict(args, d, ws):
             "rule": args.rule, "precision": precision_of(d), "s": cfg.s if lvs else None,
             "tau": cfg.tau if lvs else None, "l": cfg.l or None, "q": cfg.q or None,
             "l2": "flushed (256 MiB write) before every timed step", "parallelism": f"replicas{ws}",
-            "graph": "per-iteration CUDA graph replay (PDL edges)"}
+            "graph": "per-iteration CUDA graph replay (PDL edges only below 2^15 rows)"}
 
 
 # ------------------------------------------------------------------ reference arm: the oracle on host cores
