@@ -119,7 +119,7 @@ typedef struct {
  *                                  instead of the constant bank (a solver holds one of 4 constant
  *                                  slots; beyond 4 live solvers the shared-memory form is used).
  *   SYMNMF_SCATTER_SLICE_MB=<mb>   sampled CSR scatter product: rows of Y per destination-range
- *                                  pass, so each pass's slice of Y stays in L2 (default 52 MB when the
+ *                                  pass, so each pass's slice of Y stays in L2 (default 48 MB when the
  *                                  passes are merged into one launch, k in {16,32,64}; else 86 MB).
  *   SYMNMF_SCATTER_SPLIT=<w>       sampled CSR scatter product: warps per sampled row and pass (each
  *                                  takes a contiguous part of the row's in-range nonzeros; default 2

@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(256) spmm_csr_scalar(const int64_t* __restrict
 static bool scatter_shfl();
 static bool scatter_merge();
 // Rows of Y per destination-range pass.  Passes launched one by one: 86 MB (43/64/86/128 MB: 0.47/0.35/
-// 0.35/0.39 ms per c4 half).  Passes merged into one launch (k in {16, 32, 64}): 52 MB -- two adjacent
+// 0.35/0.39 ms per c4 half).  Passes merged into one launch (k in {16, 32, 64}): 48 MB -- two adjacent
 // slices fit L2 while the tail of a pass overlaps the head of the next (86/64/52/43/32 MB:
 // 0.309/0.291/0.287/0.290/0.309 ms).
 static int64_t scatter_slice_bytes(int k) {
@@ -86,7 +86,7 @@ static int64_t scatter_slice_bytes(int k) {
   const int64_t mb = e ? atoll(e) : 0;
   if (mb > 0) return mb << 20;
   const bool merged = (k == 16 || k == 32 || k == 64) && scatter_shfl() && scatter_merge();
-  return (merged ? 52ll : 86ll) << 20;
+  return (merged ? 48ll : 86ll) << 20;   // c4 with 2 warps per row and pass: 48 MB (6 passes) 0.276, 52-60 MB (5) 0.282 ms
 }
 
 // Warps per sampled row of the scatter; SYMNMF_SCATTER_SPLIT overrides (symnmf.h).
